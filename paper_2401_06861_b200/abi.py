@@ -1,0 +1,422 @@
+"""ctypes binding of the C ABI (include/naqs_b200.h).
+
+This is the reference-side binding a Python host would add:
+plain pointers and sizes, no torch types.  The library is the in-tree
+``libnaqs_b200.so`` built by ``__graft_entry__.build()``; importing this module
+fails loudly when it is missing -- there is no fallback implementation.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Iterable, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnaqs_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the CUDA core first (python -c 'import __graft_entry__ as g; g.build()')"
+    )
+
+lib = C.CDLL(LIB_PATH)
+
+# Gate kinds: ordinals of naqs::GateKind (proj/include/naqs/circuit.hpp:15-37).
+KINDS = [
+    "x", "y", "z", "h", "s", "sdg", "t", "tdg", "id",
+    "rx", "ry", "rz", "u1", "u2", "u3",
+    "cx", "cz", "swap", "ccx", "measure", "barrier",
+]
+KIND = {k: i for i, k in enumerate(KINDS)}
+ARITY = {k: (2 if k in ("cx", "cz", "swap") else 3 if k == "ccx" else 1) for k in KINDS}
+NPARAMS = {k: (1 if k in ("rx", "ry", "rz", "u1") else 2 if k == "u2" else 3 if k == "u3" else 0) for k in KINDS}
+
+OP_DTYPE = np.dtype(
+    [("kind", "<i4"), ("nqubits", "<i4"), ("qubits", "<i4", (3,)), ("reserved", "<i4"), ("params", "<f8", (3,))],
+    align=True,
+)
+assert OP_DTYPE.itemsize == 48
+SCHED_DTYPE = np.dtype(
+    [("type", "<i4"), ("nkraus", "<i4"), ("kraus_offset", "<i8"), ("op", OP_DTYPE)], align=True
+)
+assert SCHED_DTYPE.itemsize == 64
+
+
+class nq_opts(C.Structure):
+    _fields_ = [("device", C.c_int32), ("max_qubits", C.c_int32), ("tile_qubits", C.c_int32), ("fuse", C.c_int32)]
+
+
+NQ_OK, NQ_ERR_CONTRACT = 0, 1
+
+
+class NaqsError(RuntimeError):
+    """Any non-OK status (naqs::Error)."""
+
+
+class ContractError(NaqsError):
+    """NQ_ERR_CONTRACT (naqs::ContractError)."""
+
+
+_p = C.c_void_p
+_pp = C.POINTER(C.c_void_p)
+_dp = C.POINTER(C.c_double)
+_u64p = C.POINTER(C.c_uint64)
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_ucp = C.POINTER(C.c_ubyte)
+
+# name -> argtypes (restype is nq_status = int for all but the first two)
+SIGNATURES = {
+    "nq_last_error": ([], C.c_char_p),
+    "nq_abi_version": ([], C.c_int),
+    "nq_device_count": ([C.POINTER(C.c_int)], C.c_int),
+    "nq_default_opts": ([C.POINTER(nq_opts)], C.c_int),
+    "nq_sv_create": ([C.c_int, C.POINTER(nq_opts), _pp], C.c_int),
+    "nq_sv_destroy": ([_p], C.c_int),
+    "nq_sv_clone": ([_p, _pp], C.c_int),
+    "nq_sv_reset": ([_p], C.c_int),
+    "nq_sv_num_qubits": ([_p, C.POINTER(C.c_int)], C.c_int),
+    "nq_sv_apply_ops": ([_p, _p, C.c_int64], C.c_int),
+    "nq_sv_apply_matrix": ([_p, _i32p, C.c_int, _dp], C.c_int),
+    "nq_sv_scale": ([_p, C.c_double], C.c_int),
+    "nq_sv_flush": ([_p], C.c_int),
+    "nq_sv_norm_sq": ([_p, _dp], C.c_int),
+    "nq_sv_expectation_batch": ([_p, _u64p, _u64p, _i32p, _dp, C.c_int, _dp], C.c_int),
+    "nq_sv_probabilities": ([_p, _dp], C.c_int),
+    "nq_sv_sample_sorted": ([_p, _dp, C.c_uint64, _u64p, _u64p, _u64p], C.c_int),
+    "nq_sv_kraus_weights": ([_p, _i32p, C.c_int, C.c_int, _dp, _dp], C.c_int),
+    "nq_sv_get_amplitudes": ([_p, C.c_uint64, C.c_uint64, _dp], C.c_int),
+    "nq_sv_set_amplitudes": ([_p, C.c_uint64, C.c_uint64, _dp], C.c_int),
+    "nq_sv_device_ptr": ([_p, _pp], C.c_int),
+    "nq_sv_last_stats": ([_p, _i64p, _i64p, _i64p, _i64p], C.c_int),
+    "nq_sv_synchronize": ([_p], C.c_int),
+    "nq_dm_create": ([C.c_int, C.POINTER(nq_opts), _pp], C.c_int),
+    "nq_dm_destroy": ([_p], C.c_int),
+    "nq_dm_clone": ([_p, _pp], C.c_int),
+    "nq_dm_reset": ([_p], C.c_int),
+    "nq_dm_num_qubits": ([_p, C.POINTER(C.c_int)], C.c_int),
+    "nq_dm_apply_ops": ([_p, _p, C.c_int64], C.c_int),
+    "nq_dm_apply_channel": ([_p, _i32p, C.c_int, C.c_int, _dp], C.c_int),
+    "nq_dm_apply_schedule": ([_p, _p, C.c_int64, _dp], C.c_int),
+    "nq_dm_flush": ([_p], C.c_int),
+    "nq_dm_trace": ([_p, _dp], C.c_int),
+    "nq_dm_purity": ([_p, _dp], C.c_int),
+    "nq_dm_hermiticity_residual": ([_p, _dp], C.c_int),
+    "nq_dm_expectation_batch": ([_p, _u64p, _u64p, _i32p, _dp, C.c_int, _dp, _dp], C.c_int),
+    "nq_dm_probabilities": ([_p, _dp], C.c_int),
+    "nq_dm_get_entries": ([_p, C.c_uint64, C.c_uint64, _dp], C.c_int),
+    "nq_dm_set_entries": ([_p, C.c_uint64, C.c_uint64, _dp], C.c_int),
+    "nq_dm_last_stats": ([_p, _i64p, _i64p, _i64p, _i64p], C.c_int),
+    "nq_dm_synchronize": ([_p], C.c_int),
+    "nq_readout_apply_dist": ([_dp, C.c_int, _dp, _dp, _dp], C.c_int),
+    "nq_sample_dist_sorted": ([_dp, C.c_uint64, _dp, C.c_uint64, _u64p, _u64p, _u64p], C.c_int),
+    "nq_comm_unique_id": ([_ucp], C.c_int),
+    "nq_sv_create_sharded": ([C.c_int, C.c_int, C.c_int, _ucp, C.POINTER(nq_opts), _pp], C.c_int),
+    "nq_sv_comm_stats": ([_p, _i64p, _i64p], C.c_int),
+    "nq_plan_debug": ([C.c_int, _p, C.c_int64, C.c_int, C.c_int, _ucp, C.c_int64, _i64p], C.c_int),
+}
+
+for _name, (_args, _res) in SIGNATURES.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+
+def check(status: int) -> None:
+    if status == NQ_OK:
+        return
+    msg = lib.nq_last_error().decode()
+    if status == NQ_ERR_CONTRACT:
+        raise ContractError(msg)
+    raise NaqsError(f"status {status}: {msg}")
+
+
+def _ptr(a: np.ndarray, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+def make_ops(ops: Iterable[Sequence]) -> np.ndarray:
+    """[(name, qubits, params), ...] -> packed nq_op array."""
+    ops = list(ops)
+    arr = np.zeros(len(ops), dtype=OP_DTYPE)
+    for i, op in enumerate(ops):
+        name, qubits = op[0], op[1]
+        params = op[2] if len(op) > 2 else ()
+        arr[i]["kind"] = KIND[name]
+        arr[i]["nqubits"] = len(qubits)
+        for j, q in enumerate(qubits):
+            arr[i]["qubits"][j] = q
+        for j, p in enumerate(params):
+            arr[i]["params"][j] = p
+    return arr
+
+
+def opts(device: int = -1, max_qubits: int = 0, tile_qubits: int = 0, fuse: bool = True) -> nq_opts:
+    o = nq_opts()
+    check(lib.nq_default_opts(C.byref(o)))
+    o.device, o.max_qubits, o.tile_qubits, o.fuse = device, max_qubits, tile_qubits, 1 if fuse else 0
+    return o
+
+
+def pauli_masks(letters: str):
+    flip = signs = ny = 0
+    for i, L in enumerate(letters):
+        if L in "XY":
+            flip |= 1 << i
+        if L in "YZ":
+            signs |= 1 << i
+        if L == "Y":
+            ny += 1
+    return flip, signs, ny
+
+
+class SV:
+    """Thin owner of an nq_sv handle (C ABI)."""
+
+    def __init__(self, n: int, *, handle=None, **kw):
+        self.n = n
+        if handle is not None:
+            self.h = handle
+        else:
+            self.h = C.c_void_p()
+            check(lib.nq_sv_create(n, C.byref(opts(**kw)), C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            check(lib.nq_sv_destroy(self.h))
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def clone(self) -> "SV":
+        h = C.c_void_p()
+        check(lib.nq_sv_clone(self.h, C.byref(h)))
+        return SV(self.n, handle=h)
+
+    def reset(self):
+        check(lib.nq_sv_reset(self.h))
+
+    def apply(self, ops) -> "SV":
+        arr = ops if isinstance(ops, np.ndarray) else make_ops(ops)
+        check(lib.nq_sv_apply_ops(self.h, arr.ctypes.data, len(arr)))
+        return self
+
+    def apply_matrix(self, qubits, mat):
+        q = np.asarray(qubits, dtype=np.int32)
+        m = np.ascontiguousarray(np.asarray(mat, dtype=np.complex128))
+        check(lib.nq_sv_apply_matrix(self.h, _ptr(q, C.c_int32), len(q), m.view(np.float64).ctypes.data_as(_dp)))
+
+    def scale(self, f: float):
+        check(lib.nq_sv_scale(self.h, f))
+
+    def flush(self):
+        check(lib.nq_sv_flush(self.h))
+
+    def synchronize(self):
+        check(lib.nq_sv_synchronize(self.h))
+
+    def amplitudes(self, offset: int = 0, count: int | None = None) -> np.ndarray:
+        count = (1 << self.n) - offset if count is None else count
+        out = np.empty(count, dtype=np.complex128)
+        check(lib.nq_sv_get_amplitudes(self.h, offset, count, out.view(np.float64).ctypes.data_as(_dp)))
+        return out
+
+    def set_amplitudes(self, amps, offset: int = 0):
+        a = np.ascontiguousarray(np.asarray(amps, dtype=np.complex128))
+        check(lib.nq_sv_set_amplitudes(self.h, offset, len(a), a.view(np.float64).ctypes.data_as(_dp)))
+
+    def norm_sq(self) -> float:
+        v = C.c_double()
+        check(lib.nq_sv_norm_sq(self.h, C.byref(v)))
+        return v.value
+
+    def expectations(self, terms) -> np.ndarray:
+        """terms: [(letters, coeff), ...] with letters[i] acting on qubit i."""
+        flip = np.array([pauli_masks(t[0])[0] for t in terms], dtype=np.uint64)
+        signs = np.array([pauli_masks(t[0])[1] for t in terms], dtype=np.uint64)
+        ny = np.array([pauli_masks(t[0])[2] for t in terms], dtype=np.int32)
+        coeff = np.array([t[1] for t in terms], dtype=np.float64)
+        out = np.zeros(len(terms))
+        check(lib.nq_sv_expectation_batch(self.h, _ptr(flip, C.c_uint64), _ptr(signs, C.c_uint64),
+                                          _ptr(ny, C.c_int32), _ptr(coeff, C.c_double), len(terms),
+                                          _ptr(out, C.c_double)))
+        return out
+
+    def probabilities(self) -> np.ndarray:
+        out = np.empty(1 << self.n)
+        check(lib.nq_sv_probabilities(self.h, _ptr(out, C.c_double)))
+        return out
+
+    def sample_sorted(self, sorted_u: np.ndarray):
+        u = np.ascontiguousarray(sorted_u, dtype=np.float64)
+        idx = np.zeros(max(len(u), 1), dtype=np.uint64)
+        cnt = np.zeros(max(len(u), 1), dtype=np.uint64)
+        k = C.c_uint64()
+        check(lib.nq_sv_sample_sorted(self.h, _ptr(u, C.c_double), len(u), _ptr(idx, C.c_uint64),
+                                      _ptr(cnt, C.c_uint64), C.byref(k)))
+        return idx[: k.value].copy(), cnt[: k.value].copy()
+
+    def kraus_weights(self, qubits, kraus) -> np.ndarray:
+        q = np.asarray(qubits, dtype=np.int32)
+        ks = np.ascontiguousarray(np.asarray(kraus, dtype=np.complex128))
+        out = np.zeros(len(ks))
+        check(lib.nq_sv_kraus_weights(self.h, _ptr(q, C.c_int32), len(q), len(ks),
+                                      ks.view(np.float64).ctypes.data_as(_dp), _ptr(out, C.c_double)))
+        return out
+
+    def stats(self):
+        v = [C.c_int64() for _ in range(4)]
+        check(lib.nq_sv_last_stats(self.h, *[C.byref(x) for x in v]))
+        return {"passes": v[0].value, "microops": v[1].value, "source_ops": v[2].value, "launches": v[3].value}
+
+
+class DM:
+    """Thin owner of an nq_dm handle (C ABI)."""
+
+    def __init__(self, n: int, *, handle=None, **kw):
+        self.n = n
+        if handle is not None:
+            self.h = handle
+        else:
+            self.h = C.c_void_p()
+            check(lib.nq_dm_create(n, C.byref(opts(**kw)), C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            check(lib.nq_dm_destroy(self.h))
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def apply(self, ops) -> "DM":
+        arr = ops if isinstance(ops, np.ndarray) else make_ops(ops)
+        check(lib.nq_dm_apply_ops(self.h, arr.ctypes.data, len(arr)))
+        return self
+
+    def apply_channel(self, qubits, kraus):
+        q = np.asarray(qubits, dtype=np.int32)
+        ks = np.ascontiguousarray(np.asarray(kraus, dtype=np.complex128))
+        check(lib.nq_dm_apply_channel(self.h, _ptr(q, C.c_int32), len(q), len(ks),
+                                      ks.view(np.float64).ctypes.data_as(_dp)))
+
+    def apply_schedule(self, items):
+        """items: [("gate", (name, qubits, params)) | ("channel", qubits, kraus_list)]."""
+        arr = np.zeros(len(items), dtype=SCHED_DTYPE)
+        pool = []
+        off = 0
+        for i, it in enumerate(items):
+            if it[0] == "gate":
+                arr[i]["type"] = 0
+                arr[i]["op"] = make_ops([it[1]])[0]
+            else:
+                qubits, kraus = it[1], np.asarray(it[2], dtype=np.complex128)
+                arr[i]["type"] = 1
+                arr[i]["nkraus"] = len(kraus)
+                arr[i]["kraus_offset"] = off
+                arr[i]["op"]["nqubits"] = len(qubits)
+                for j, q in enumerate(qubits):
+                    arr[i]["op"]["qubits"][j] = q
+                pool.append(kraus.reshape(-1))
+                off += kraus.size
+        p = np.ascontiguousarray(np.concatenate(pool) if pool else np.zeros(1, dtype=np.complex128))
+        check(lib.nq_dm_apply_schedule(self.h, arr.ctypes.data, len(arr), p.view(np.float64).ctypes.data_as(_dp)))
+
+    def flush(self):
+        check(lib.nq_dm_flush(self.h))
+
+    def synchronize(self):
+        check(lib.nq_dm_synchronize(self.h))
+
+    def rho(self) -> np.ndarray:
+        d = 1 << self.n
+        out = np.empty(d * d, dtype=np.complex128)
+        check(lib.nq_dm_get_entries(self.h, 0, d * d, out.view(np.float64).ctypes.data_as(_dp)))
+        return out.reshape(d, d)
+
+    def set_rho(self, rho):
+        a = np.ascontiguousarray(np.asarray(rho, dtype=np.complex128).reshape(-1))
+        check(lib.nq_dm_set_entries(self.h, 0, len(a), a.view(np.float64).ctypes.data_as(_dp)))
+
+    def _scalar(self, fn) -> float:
+        v = C.c_double()
+        check(fn(self.h, C.byref(v)))
+        return v.value
+
+    def trace(self):
+        return self._scalar(lib.nq_dm_trace)
+
+    def purity(self):
+        return self._scalar(lib.nq_dm_purity)
+
+    def hermiticity_residual(self):
+        return self._scalar(lib.nq_dm_hermiticity_residual)
+
+    def expectations(self, terms):
+        flip = np.array([pauli_masks(t[0])[0] for t in terms], dtype=np.uint64)
+        signs = np.array([pauli_masks(t[0])[1] for t in terms], dtype=np.uint64)
+        ny = np.array([pauli_masks(t[0])[2] for t in terms], dtype=np.int32)
+        coeff = np.array([t[1] for t in terms], dtype=np.float64)
+        re = np.zeros(len(terms))
+        im = np.zeros(len(terms))
+        check(lib.nq_dm_expectation_batch(self.h, _ptr(flip, C.c_uint64), _ptr(signs, C.c_uint64),
+                                          _ptr(ny, C.c_int32), _ptr(coeff, C.c_double), len(terms),
+                                          _ptr(re, C.c_double), _ptr(im, C.c_double)))
+        return re, im
+
+    def probabilities(self):
+        out = np.empty(1 << self.n)
+        check(lib.nq_dm_probabilities(self.h, _ptr(out, C.c_double)))
+        return out
+
+    def stats(self):
+        v = [C.c_int64() for _ in range(4)]
+        check(lib.nq_dm_last_stats(self.h, *[C.byref(x) for x in v]))
+        return {"passes": v[0].value, "microops": v[1].value, "source_ops": v[2].value, "launches": v[3].value}
+
+
+def readout_apply_dist(dist, p01, p10) -> np.ndarray:
+    d = np.ascontiguousarray(dist, dtype=np.float64)
+    n = int(np.log2(len(d)))
+    a = np.ascontiguousarray(p01, dtype=np.float64)
+    b = np.ascontiguousarray(p10, dtype=np.float64)
+    out = np.empty_like(d)
+    check(lib.nq_readout_apply_dist(_ptr(d, C.c_double), n, _ptr(a, C.c_double), _ptr(b, C.c_double),
+                                    _ptr(out, C.c_double)))
+    return out
+
+
+def sample_dist_sorted(dist, sorted_u):
+    d = np.ascontiguousarray(dist, dtype=np.float64)
+    u = np.ascontiguousarray(sorted_u, dtype=np.float64)
+    idx = np.zeros(max(len(u), 1), dtype=np.uint64)
+    cnt = np.zeros(max(len(u), 1), dtype=np.uint64)
+    k = C.c_uint64()
+    check(lib.nq_sample_dist_sorted(_ptr(d, C.c_double), len(d), _ptr(u, C.c_double), len(u),
+                                    _ptr(idx, C.c_uint64), _ptr(cnt, C.c_uint64), C.byref(k)))
+    return idx[: k.value].copy(), cnt[: k.value].copy()
+
+
+def plan_debug(n: int, ops, tile_qubits: int = 0, fuse: bool = True) -> bytes:
+    arr = ops if isinstance(ops, np.ndarray) else make_ops(ops)
+    size = C.c_int64()
+    check(lib.nq_plan_debug(n, arr.ctypes.data, len(arr), tile_qubits, 1 if fuse else 0, None, 0, C.byref(size)))
+    buf = (C.c_ubyte * max(size.value, 1))()
+    check(lib.nq_plan_debug(n, arr.ctypes.data, len(arr), tile_qubits, 1 if fuse else 0, buf, size.value,
+                            C.byref(size)))
+    return bytes(buf)[: size.value]
+
+
+def device_count() -> int:
+    n = C.c_int()
+    st = lib.nq_device_count(C.byref(n))
+    return n.value if st == NQ_OK else 0

@@ -1,0 +1,908 @@
+// C ABI of the B200 simulation core (include/naqs_b200.h).
+//
+// Each function validates its preconditions with the reference's wording
+// (proj/src/statevector.cpp, proj/src/densitymatrix.cpp, proj/src/noise.cpp),
+// queues work, and runs it on the device's stream.  There is no host
+// execution path: every amplitude update, reduction and readout map runs in
+// kernels.cu.
+#include "../../include/naqs_b200.h"
+
+#include "engine.hpp"
+#include "kernels.hpp"
+#include "lower.hpp"
+#include "state.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+using namespace nqe;
+
+namespace nqe {
+
+thread_local std::string g_last_error;
+
+DeviceCtx& ctx_for(int dev) {
+    static std::mutex mu;
+    static std::map<int, std::unique_ptr<DeviceCtx>> ctxs;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = ctxs.find(dev);
+    if (it != ctxs.end()) return *it->second;
+    auto c = std::make_unique<DeviceCtx>();
+    c->dev = dev;
+    CUDA_TRY(cudaSetDevice(dev));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->stage_ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&c->h_small), 64 * 1024));
+    DeviceCtx& ref = *c;
+    ctxs[dev] = std::move(c);
+    return ref;
+}
+
+void DeviceCtx::ensure_scratch(size_t doubles) {
+    if (doubles <= scratch_cap) return;
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    if (d_scratch) CUDA_TRY(cudaFree(d_scratch));
+    d_scratch = nullptr;
+    const size_t cap = std::max<size_t>(doubles, 1 << 16);
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&d_scratch), cap * sizeof(double)));
+    scratch_cap = cap;
+}
+
+void DeviceCtx::stage(const unsigned char* src, size_t bytes) {
+    if (stage_pending) {
+        CUDA_TRY(cudaEventSynchronize(stage_ev));
+        stage_pending = false;
+    }
+    if (bytes > h_stage_cap) {
+        if (h_stage) CUDA_TRY(cudaFreeHost(h_stage));
+        h_stage = nullptr;
+        const size_t cap = std::max<size_t>(bytes * 2, 1 << 20);
+        CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&h_stage), cap));
+        h_stage_cap = cap;
+    }
+    if (bytes > d_ops_cap) {
+        CUDA_TRY(cudaStreamSynchronize(stream));
+        if (d_ops) CUDA_TRY(cudaFree(d_ops));
+        d_ops = nullptr;
+        const size_t cap = std::max<size_t>(bytes * 2, 1 << 20);
+        CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&d_ops), cap));
+        d_ops_cap = cap;
+    }
+    std::memcpy(h_stage, src, bytes);
+    CUDA_TRY(cudaMemcpyAsync(d_ops, h_stage, bytes, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaEventRecord(stage_ev, stream));
+    stage_pending = true;
+}
+
+// ---- state lifecycle ---------------------------------------------------------
+void state_init(State& s, int n, bool dm, const nq_opts* opts) {
+    nq_opts o;
+    nq_default_opts(&o);
+    if (opts) o = *opts;
+    const int guard = o.max_qubits > 0 ? o.max_qubits : (dm ? 14 : 30);
+    if (n < 1 || n > guard) {
+        throw NqError{NQ_ERR_CONTRACT, std::string(dm ? "density matrix" : "state vector") +
+                                           " qubit count must be in [1, " + std::to_string(guard) +
+                                           "], got " + std::to_string(n)};
+    }
+    int dev = o.device;
+    if (dev < 0) CUDA_TRY(cudaGetDevice(&dev));
+    s.dev = dev;
+    s.n = n;
+    s.dm = dm;
+    s.nbits = dm ? 2 * n : n;
+    s.nloc = s.nbits;
+    s.count = uint64_t(1) << s.nloc;
+    s.popt.nbits = s.nbits;
+    s.popt.nloc = s.nloc;
+    s.popt.tile_bits = o.tile_qubits > 0 ? std::min(o.tile_qubits, kMaxTileBits) : 12;
+    s.popt.low_bits = 4;
+    s.popt.fuse = o.fuse != 0;
+    configure_caps(s.popt);
+    DeviceCtx& c = ctx_for(dev);
+    CUDA_TRY(cudaSetDevice(dev));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s.d), s.count * sizeof(double2), c.stream));
+    launch_init_basis(s.d, s.count, 0, c.stream);
+    CUDA_TRY(cudaGetLastError());
+}
+
+void configure_caps(PlanOptions& p) {
+    const int m = std::min(p.tile_bits, p.nloc);
+    if (m <= 10) {
+        p.max_ops_per_pass = 1024;
+        p.max_pool_per_pass = 6144;
+    } else {
+        p.max_ops_per_pass = 192;
+        p.max_pool_per_pass = 1536;
+    }
+}
+
+void state_free(State& s) {
+    if (!s.d) return;
+    DeviceCtx& c = ctx_for(s.dev);
+    cudaSetDevice(s.dev);
+    cudaFreeAsync(s.d, c.stream);
+    s.d = nullptr;
+    shard_free(s);
+}
+
+void state_flush(State& s) {
+    if (s.queue.empty()) return;
+    if (s.world > 1) {
+        shard_flush(s);
+        return;
+    }
+    DeviceCtx& c = ctx_for(s.dev);
+    CUDA_TRY(cudaSetDevice(s.dev));
+    PlanStats st;
+    std::vector<PlannedPass> passes = plan_passes(s.queue, s.popt, &st);
+    s.queue.clear();
+    std::vector<size_t> offs;
+    std::vector<unsigned char> buf = serialize_passes(passes, s.nloc, &offs);
+    s.last_passes = st.passes;
+    s.last_microops = st.microops;
+    s.last_source_ops = st.source_ops;
+    s.last_launches = int64_t(passes.size());
+    if (buf.empty()) return;
+    c.stage(buf.data(), buf.size());
+    for (size_t i = 0; i < passes.size(); ++i) {
+        PassHdr h;
+        std::memcpy(&h, buf.data() + offs[i], sizeof(h));
+        launch_pass(s.d, c.d_ops + offs[i], h, 0, c.stream);
+    }
+    CUDA_TRY(cudaGetLastError());
+}
+
+double* result_slot(DeviceCtx& c, int i) { return c.d_scratch + i; }
+
+// Copy `count` doubles from device to the pinned small buffer and wait.
+void fetch(DeviceCtx& c, const double* dsrc, size_t count, double* host) {
+    CUDA_TRY(cudaMemcpyAsync(c.h_small, dsrc, count * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
+    std::memcpy(host, c.h_small, count * sizeof(double));
+}
+
+}  // namespace nqe
+
+namespace {
+
+void check_op_shape(const nq_op& op) {
+    if (op.kind < 0 || op.kind > NQ_BARRIER)
+        throw NqError{NQ_ERR_CONTRACT, "unknown gate kind " + std::to_string(op.kind)};
+    const int arity = kind_arity(op.kind);
+    if (op.nqubits != arity)
+        throw NqError{NQ_ERR_CONTRACT, "gate expects " + std::to_string(arity) + " qubit(s), got " +
+                                           std::to_string(op.nqubits)};
+    for (int i = 0; i < arity; ++i)
+        for (int j = i + 1; j < arity; ++j)
+            if (op.qubits[i] == op.qubits[j])
+                throw NqError{NQ_ERR_CONTRACT, "duplicate qubit index " + std::to_string(op.qubits[i])};
+}
+
+void check_range(const int32_t* q, int k, int n) {
+    for (int j = 0; j < k; ++j)
+        if (q[j] < 0 || q[j] >= n)
+            throw NqError{NQ_ERR_CONTRACT, "qubit index " + std::to_string(q[j]) + " out of range"};
+}
+
+template <class T>
+State& st(T* h) {
+    if (!h) throw NqError{NQ_ERR_CONTRACT, "null handle"};
+    return h->s;
+}
+
+bool is_identity_kraus(int k, int nkraus, const cplx* kr) {
+    if (nkraus != 1) return false;
+    const int d = 1 << k;
+    for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c)
+            if (std::abs(kr[r * d + c] - cplx(r == c ? 1.0 : 0.0, 0.0)) > 1e-14) return false;
+    return true;
+}
+
+void pauli_groups(const uint64_t* flip, int nterms, std::map<uint64_t, std::vector<int>>& groups) {
+    for (int t = 0; t < nterms; ++t) groups[flip[t]].push_back(t);
+}
+
+const cplx kIPow[4] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
+
+}  // namespace
+
+extern "C" {
+
+struct nq_sv {
+    State s;
+};
+struct nq_dm {
+    State s;
+};
+
+const char* nq_last_error(void) { return g_last_error.c_str(); }
+int nq_abi_version(void) { return NAQS_B200_ABI_VERSION; }
+
+nq_status nq_device_count(int* out) {
+    return guard([&] {
+        int n = 0;
+        CUDA_TRY(cudaGetDeviceCount(&n));
+        *out = n;
+    });
+}
+
+nq_status nq_default_opts(nq_opts* out) {
+    if (!out) return NQ_ERR_CONTRACT;
+    out->device = -1;
+    out->max_qubits = 0;
+    out->tile_qubits = 0;
+    out->fuse = 1;
+    return NQ_OK;
+}
+
+// ---- state vector --------------------------------------------------------------
+nq_status nq_sv_create(int n, const nq_opts* opts, nq_sv** out) {
+    return guard([&] {
+        auto h = std::make_unique<nq_sv>();
+        state_init(h->s, n, false, opts);
+        *out = h.release();
+    });
+}
+
+nq_status nq_sv_destroy(nq_sv* h) {
+    return guard([&] {
+        if (!h) return;
+        state_free(h->s);
+        delete h;
+    });
+}
+
+nq_status nq_sv_clone(const nq_sv* h, nq_sv** out) {
+    return guard([&] {
+        State& src = const_cast<nq_sv*>(h)->s;
+        if (src.world > 1) throw NqError{NQ_ERR_CONTRACT, "clone of a sharded state is not supported"};
+        state_flush(src);
+        auto c = std::make_unique<nq_sv>();
+        c->s.dev = src.dev;
+        c->s.n = src.n;
+        c->s.dm = src.dm;
+        c->s.nbits = src.nbits;
+        c->s.nloc = src.nloc;
+        c->s.count = src.count;
+        c->s.popt = src.popt;
+        DeviceCtx& cx = ctx_for(src.dev);
+        CUDA_TRY(cudaSetDevice(src.dev));
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&c->s.d), src.count * sizeof(double2), cx.stream));
+        CUDA_TRY(cudaMemcpyAsync(c->s.d, src.d, src.count * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                 cx.stream));
+        *out = c.release();
+    });
+}
+
+nq_status nq_sv_reset(nq_sv* h) {
+    return guard([&] {
+        State& s = st(h);
+        s.queue.clear();
+        DeviceCtx& c = ctx_for(s.dev);
+        CUDA_TRY(cudaSetDevice(s.dev));
+        const uint64_t one_at = (s.world > 1 && s.rank != 0) ? UINT64_MAX : 0;
+        launch_init_basis(s.d, s.count, one_at, c.stream);
+        shard_reset(s);
+        CUDA_TRY(cudaGetLastError());
+    });
+}
+
+nq_status nq_sv_num_qubits(const nq_sv* h, int* out) {
+    return guard([&] { *out = st(const_cast<nq_sv*>(h)).n; });
+}
+
+nq_status nq_sv_apply_ops(nq_sv* h, const nq_op* ops, int64_t count) {
+    return guard([&] {
+        State& s = st(h);
+        // Validate everything first so a failing call leaves the queue untouched.
+        for (int64_t i = 0; i < count; ++i) {
+            const nq_op& op = ops[i];
+            if (op.kind == NQ_MEASURE)
+                throw NqError{NQ_ERR_CONTRACT, "MEASURE has no state-vector kernel; use sample()"};
+            check_op_shape(op);
+            if (op.kind == NQ_BARRIER) continue;
+            check_range(op.qubits, op.nqubits, s.n);
+        }
+        for (int64_t i = 0; i < count; ++i) lower_sv_op(ops[i], s.queue);
+    });
+}
+
+nq_status nq_sv_apply_matrix(nq_sv* h, const int32_t* qubits, int k, const double* mat) {
+    return guard([&] {
+        State& s = st(h);
+        if (k < 1 || k > 4) throw NqError{NQ_ERR_CONTRACT, "matrix arity must be in [1, 4]"};
+        check_range(qubits, k, s.n);
+        for (int i = 0; i < k; ++i)
+            for (int j = i + 1; j < k; ++j)
+                if (qubits[i] == qubits[j]) throw NqError{NQ_ERR_CONTRACT, "duplicate qubit index"};
+        int q[4];
+        for (int j = 0; j < k; ++j) q[j] = qubits[j];
+        s.queue.push_back(sv_matrix_op(q, k, reinterpret_cast<const cplx*>(mat)));
+    });
+}
+
+nq_status nq_sv_scale(nq_sv* h, double factor) {
+    return guard([&] {
+        State& s = st(h);
+        EOp e;
+        e.type = E_DIAG;
+        e.k = 0;
+        e.mat = {cplx(factor, 0.0)};
+        e.src = 0;
+        s.queue.push_back(std::move(e));
+    });
+}
+
+nq_status nq_sv_flush(nq_sv* h) {
+    return guard([&] { state_flush(st(h)); });
+}
+
+nq_status nq_sv_norm_sq(nq_sv* h, double* out) {
+    return guard([&] {
+        State& s = st(h);
+        state_flush(s);
+        if (s.world > 1) {
+            *out = shard_norm_sq(s);
+            return;
+        }
+        DeviceCtx& c = ctx_for(s.dev);
+        c.ensure_scratch(scratch_doubles_needed(s.count) + 64);
+        launch_sumsq(s.d, s.count, c.d_scratch + 64, result_slot(c, 0), c.stream);
+        CUDA_TRY(cudaGetLastError());
+        fetch(c, result_slot(c, 0), 1, out);
+    });
+}
+
+nq_status nq_sv_expectation_batch(nq_sv* h, const uint64_t* flip, const uint64_t* signs,
+                                  const int32_t* ny, const double* coeff, int nterms, double* out) {
+    return guard([&] {
+        State& s = st(h);
+        const uint64_t lim = (s.n >= 64) ? ~uint64_t(0) : ((uint64_t(1) << s.n) - 1);
+        for (int t = 0; t < nterms; ++t)
+            if ((flip[t] & ~lim) || (signs[t] & ~lim))
+                throw NqError{NQ_ERR_CONTRACT, "Pauli mask exceeds the state's qubit count"};
+        state_flush(s);
+        if (s.world > 1) {
+            shard_expectation(s, flip, signs, ny, coeff, nterms, out);
+            return;
+        }
+        DeviceCtx& c = ctx_for(s.dev);
+        std::map<uint64_t, std::vector<int>> groups;
+        pauli_groups(flip, nterms, groups);
+        const int tpl = terms_per_launch();
+        int launches = 0;
+        for (auto& g : groups) launches += int((g.second.size() + tpl - 1) / tpl);
+        const size_t part = scratch_doubles_needed(s.count);
+        c.ensure_scratch(part + size_t(launches) * tpl + 64);
+        double* results = c.d_scratch + part;
+        std::vector<std::pair<int, int>> slot_of{static_cast<size_t>(nterms)};  // (launch, index)
+        std::vector<int> eps(size_t(nterms), 0);
+        int li = 0;
+        for (auto& g : groups) {
+            const uint64_t F = g.first;
+            const auto& terms = g.second;
+            for (size_t b = 0; b < terms.size(); b += size_t(tpl)) {
+                uint64_t sg[64];
+                int ep[64];
+                const int nt = int(std::min(terms.size() - b, size_t(tpl)));
+                for (int j = 0; j < nt; ++j) {
+                    const int t = terms[b + size_t(j)];
+                    sg[j] = signs[t];
+                    ep[j] = (F != 0 && (__builtin_popcountll(F & signs[t]) & 1)) ? 1 : 0;
+                    eps[size_t(t)] = ep[j];
+                    slot_of[size_t(t)] = {li, j};
+                }
+                launch_expect_sv(s.d, s.nloc, F, sg, ep, nt, c.d_scratch, results + size_t(li) * tpl,
+                                 c.stream);
+                ++li;
+            }
+        }
+        CUDA_TRY(cudaGetLastError());
+        std::vector<double> host(size_t(launches) * tpl);
+        if (!host.empty()) {
+            CUDA_TRY(cudaMemcpyAsync(host.data(), results, host.size() * sizeof(double),
+                                     cudaMemcpyDeviceToHost, c.stream));
+        }
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        for (int t = 0; t < nterms; ++t) {
+            const double acc = host[size_t(slot_of[size_t(t)].first) * tpl + size_t(slot_of[size_t(t)].second)];
+            cplx total;
+            if (flip[t] == 0) total = cplx(acc, 0.0);
+            else total = eps[size_t(t)] ? cplx(0.0, 2.0 * acc) : cplx(2.0 * acc, 0.0);
+            total *= kIPow[ny[t] & 3];
+            out[t] = coeff[t] * total.real();
+        }
+    });
+}
+
+nq_status nq_sv_probabilities(nq_sv* h, double* host_out) {
+    return guard([&] {
+        State& s = st(h);
+        state_flush(s);
+        if (s.world > 1) throw NqError{NQ_ERR_CONTRACT, "probabilities() of a sharded state: use sample"};
+        DeviceCtx& c = ctx_for(s.dev);
+        const uint64_t chunk = std::min<uint64_t>(s.count, uint64_t(1) << 26);
+        double* tmp = nullptr;
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&tmp), chunk * sizeof(double), c.stream));
+        for (uint64_t off = 0; off < s.count; off += chunk) {
+            const uint64_t len = std::min(chunk, s.count - off);
+            launch_probs(s.d + off, len, tmp, c.stream);
+            CUDA_TRY(cudaMemcpyAsync(host_out + off, tmp, len * sizeof(double), cudaMemcpyDeviceToHost,
+                                     c.stream));
+        }
+        CUDA_TRY(cudaFreeAsync(tmp, c.stream));
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+    });
+}
+
+nq_status nq_sv_sample_sorted(nq_sv* h, const double* sorted_u, uint64_t shots, uint64_t* idx_out,
+                              uint64_t* count_out, uint64_t* nout) {
+    return guard([&] {
+        State& s = st(h);
+        state_flush(s);
+        if (s.world > 1) {
+            shard_sample(s, sorted_u, shots, idx_out, count_out, nout);
+            return;
+        }
+        DeviceCtx& c = ctx_for(s.dev);
+        sample_sweep(c, s.d, nullptr, s.count, sorted_u, shots, idx_out, count_out, nout);
+    });
+}
+
+nq_status nq_sv_kraus_weights(nq_sv* h, const int32_t* qubits, int k, int nkraus, const double* kraus,
+                              double* weights_out) {
+    return guard([&] {
+        State& s = st(h);
+        if (k < 1 || k > 3) throw NqError{NQ_ERR_CONTRACT, "Kraus arity must be in [1, 3]"};
+        if (nkraus < 1 || nkraus > 16) throw NqError{NQ_ERR_CONTRACT, "1..16 Kraus operators supported"};
+        check_range(qubits, k, s.n);
+        state_flush(s);
+        if (s.world > 1) throw NqError{NQ_ERR_CONTRACT, "trajectories on a sharded state are not supported"};
+        DeviceCtx& c = ctx_for(s.dev);
+        const size_t D = size_t(1) << k;
+        double2* dm = nullptr;
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dm), size_t(nkraus) * D * D * sizeof(double2),
+                                 c.stream));
+        CUDA_TRY(cudaMemcpyAsync(dm, kraus, size_t(nkraus) * D * D * sizeof(double2), cudaMemcpyHostToDevice,
+                                 c.stream));
+        c.ensure_scratch(size_t(16) * 2048 + 64 + 16);
+        int q[3] = {qubits[0], k > 1 ? qubits[1] : 0, k > 2 ? qubits[2] : 0};
+        launch_kraus_weights(s.d, s.nloc, q, k, nkraus, dm, c.d_scratch + 64, result_slot(c, 0), c.stream);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaFreeAsync(dm, c.stream));
+        double w[16];
+        fetch(c, result_slot(c, 0), 16, w);
+        for (int i = 0; i < nkraus; ++i) weights_out[i] = w[i];
+    });
+}
+
+nq_status nq_sv_get_amplitudes(nq_sv* h, uint64_t offset, uint64_t count, double* host_out) {
+    return guard([&] {
+        State& s = st(h);
+        state_flush(s);
+        if (s.world > 1) {
+            shard_get_amplitudes(s, offset, count, host_out);
+            return;
+        }
+        if (offset > s.count || count > s.count - offset)
+            throw NqError{NQ_ERR_CONTRACT, "amplitude range out of bounds"};
+        DeviceCtx& c = ctx_for(s.dev);
+        if (count == 0) return;
+        CUDA_TRY(cudaMemcpyAsync(host_out, s.d + offset, count * sizeof(double2), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+    });
+}
+
+nq_status nq_sv_set_amplitudes(nq_sv* h, uint64_t offset, uint64_t count, const double* host_in) {
+    return guard([&] {
+        State& s = st(h);
+        state_flush(s);
+        if (s.world > 1) throw NqError{NQ_ERR_CONTRACT, "set_amplitudes on a sharded state is not supported"};
+        if (offset > s.count || count > s.count - offset)
+            throw NqError{NQ_ERR_CONTRACT, "amplitude range out of bounds"};
+        DeviceCtx& c = ctx_for(s.dev);
+        if (count == 0) return;
+        CUDA_TRY(cudaMemcpyAsync(s.d + offset, host_in, count * sizeof(double2), cudaMemcpyHostToDevice,
+                                 c.stream));
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+    });
+}
+
+nq_status nq_sv_device_ptr(nq_sv* h, void** out) {
+    return guard([&] {
+        State& s = st(h);
+        state_flush(s);
+        *out = s.d;
+    });
+}
+
+nq_status nq_sv_last_stats(const nq_sv* h, int64_t* passes, int64_t* microops, int64_t* source_ops,
+                           int64_t* launches) {
+    return guard([&] {
+        const State& s = const_cast<nq_sv*>(h)->s;
+        if (passes) *passes = s.last_passes;
+        if (microops) *microops = s.last_microops;
+        if (source_ops) *source_ops = s.last_source_ops;
+        if (launches) *launches = s.last_launches;
+    });
+}
+
+nq_status nq_sv_synchronize(nq_sv* h) {
+    return guard([&] {
+        State& s = st(h);
+        CUDA_TRY(cudaSetDevice(s.dev));
+        CUDA_TRY(cudaStreamSynchronize(ctx_for(s.dev).stream));
+    });
+}
+
+// ---- density matrix ----------------------------------------------------------------
+nq_status nq_dm_create(int n, const nq_opts* opts, nq_dm** out) {
+    return guard([&] {
+        auto h = std::make_unique<nq_dm>();
+        state_init(h->s, n, true, opts);
+        *out = h.release();
+    });
+}
+
+nq_status nq_dm_destroy(nq_dm* h) {
+    return guard([&] {
+        if (!h) return;
+        state_free(h->s);
+        delete h;
+    });
+}
+
+nq_status nq_dm_clone(const nq_dm* h, nq_dm** out) {
+    return guard([&] {
+        State& src = const_cast<nq_dm*>(h)->s;
+        state_flush(src);
+        auto c = std::make_unique<nq_dm>();
+        c->s.dev = src.dev;
+        c->s.n = src.n;
+        c->s.dm = true;
+        c->s.nbits = src.nbits;
+        c->s.nloc = src.nloc;
+        c->s.count = src.count;
+        c->s.popt = src.popt;
+        DeviceCtx& cx = ctx_for(src.dev);
+        CUDA_TRY(cudaSetDevice(src.dev));
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&c->s.d), src.count * sizeof(double2), cx.stream));
+        CUDA_TRY(cudaMemcpyAsync(c->s.d, src.d, src.count * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                 cx.stream));
+        *out = c.release();
+    });
+}
+
+nq_status nq_dm_reset(nq_dm* h) {
+    return guard([&] {
+        State& s = st(h);
+        s.queue.clear();
+        DeviceCtx& c = ctx_for(s.dev);
+        CUDA_TRY(cudaSetDevice(s.dev));
+        launch_init_basis(s.d, s.count, 0, c.stream);
+        CUDA_TRY(cudaGetLastError());
+    });
+}
+
+nq_status nq_dm_num_qubits(const nq_dm* h, int* out) {
+    return guard([&] { *out = st(const_cast<nq_dm*>(h)).n; });
+}
+
+static void dm_validate_gate(const State& s, const nq_op& op) {
+    if (op.kind == NQ_MEASURE)
+        throw NqError{NQ_ERR_CONTRACT, "MEASURE has no density-matrix kernel; use probabilities()"};
+    check_op_shape(op);
+    if (op.kind == NQ_BARRIER || op.kind == NQ_ID) return;
+    check_range(op.qubits, op.nqubits, s.n);
+}
+
+nq_status nq_dm_apply_ops(nq_dm* h, const nq_op* ops, int64_t count) {
+    return guard([&] {
+        State& s = st(h);
+        for (int64_t i = 0; i < count; ++i) dm_validate_gate(s, ops[i]);
+        for (int64_t i = 0; i < count; ++i) {
+            if (ops[i].kind == NQ_BARRIER || ops[i].kind == NQ_ID) {
+                if (ops[i].kind == NQ_ID) {
+                    EOp e;  // counted, no work (densitymatrix.cpp:115)
+                    s.queue.push_back(e);
+                }
+                continue;
+            }
+            lower_dm_op(ops[i], s.n, s.queue);
+        }
+    });
+}
+
+static void dm_channel(State& s, const int32_t* qubits, int k, int nkraus, const double* kraus) {
+    if (k != 1 && k != 2)
+        throw NqError{NQ_ERR_CONTRACT, "channel arity must be 1 or 2, got " + std::to_string(k)};
+    if (nkraus < 1) throw NqError{NQ_ERR_CONTRACT, "channel needs at least one Kraus operator"};
+    check_range(qubits, k, s.n);
+    if (k == 2 && qubits[0] == qubits[1]) throw NqError{NQ_ERR_CONTRACT, "duplicate qubit index"};
+    const cplx* kr = reinterpret_cast<const cplx*>(kraus);
+    if (is_identity_kraus(k, nkraus, kr)) return;  // densitymatrix.cpp:138
+    int q[2] = {qubits[0], k > 1 ? qubits[1] : 0};
+    s.queue.push_back(dm_channel_op(q, k, nkraus, kr, s.n));
+}
+
+nq_status nq_dm_apply_channel(nq_dm* h, const int32_t* qubits, int k, int nkraus, const double* kraus) {
+    return guard([&] { dm_channel(st(h), qubits, k, nkraus, kraus); });
+}
+
+nq_status nq_dm_apply_schedule(nq_dm* h, const nq_sched_item* items, int64_t count, const double* pool) {
+    return guard([&] {
+        State& s = st(h);
+        // validate all first (reference run_schedule validates item by item and
+        // throws mid-way; we reject the whole schedule before touching rho)
+        for (int64_t i = 0; i < count; ++i) {
+            const nq_sched_item& it = items[i];
+            if (it.type == 0) {
+                if (it.op.kind == NQ_MEASURE || it.op.kind == NQ_BARRIER) continue;
+                dm_validate_gate(s, it.op);
+            } else {
+                if (it.op.nqubits != 1 && it.op.nqubits != 2)
+                    throw NqError{NQ_ERR_CONTRACT, "channel arity must be 1 or 2"};
+                check_range(it.op.qubits, it.op.nqubits, s.n);
+            }
+        }
+        for (int64_t i = 0; i < count; ++i) {
+            const nq_sched_item& it = items[i];
+            if (it.type == 0) {
+                if (it.op.kind == NQ_MEASURE || it.op.kind == NQ_BARRIER) continue;
+                if (it.op.kind == NQ_ID) {
+                    s.queue.push_back(EOp{});
+                    continue;
+                }
+                lower_dm_op(it.op, s.n, s.queue);
+            } else {
+                dm_channel(s, it.op.qubits, it.op.nqubits, it.nkraus, pool + 2 * it.kraus_offset);
+            }
+        }
+    });
+}
+
+nq_status nq_dm_flush(nq_dm* h) {
+    return guard([&] { state_flush(st(h)); });
+}
+
+nq_status nq_dm_trace(nq_dm* h, double* out) {
+    return guard([&] {
+        State& s = st(h);
+        state_flush(s);
+        DeviceCtx& c = ctx_for(s.dev);
+        const uint64_t dim = uint64_t(1) << s.n;
+        c.ensure_scratch(scratch_doubles_needed(dim) + 64);
+        launch_trace(s.d, dim, c.d_scratch + 64, result_slot(c, 0), c.stream);
+        CUDA_TRY(cudaGetLastError());
+        fetch(c, result_slot(c, 0), 1, out);
+    });
+}
+
+nq_status nq_dm_purity(nq_dm* h, double* out) {
+    return guard([&] {
+        State& s = st(h);
+        state_flush(s);
+        DeviceCtx& c = ctx_for(s.dev);
+        c.ensure_scratch(scratch_doubles_needed(s.count) + 64);
+        launch_sumsq(s.d, s.count, c.d_scratch + 64, result_slot(c, 0), c.stream);
+        CUDA_TRY(cudaGetLastError());
+        fetch(c, result_slot(c, 0), 1, out);
+    });
+}
+
+nq_status nq_dm_hermiticity_residual(nq_dm* h, double* out) {
+    return guard([&] {
+        State& s = st(h);
+        state_flush(s);
+        DeviceCtx& c = ctx_for(s.dev);
+        c.ensure_scratch(2048 + 64);
+        launch_herm(s.d, uint64_t(1) << s.n, c.d_scratch + 64, result_slot(c, 0), c.stream);
+        CUDA_TRY(cudaGetLastError());
+        fetch(c, result_slot(c, 0), 1, out);
+    });
+}
+
+nq_status nq_dm_expectation_batch(nq_dm* h, const uint64_t* flip, const uint64_t* signs, const int32_t* ny,
+                                  const double* coeff, int nterms, double* out_re, double* out_im) {
+    return guard([&] {
+        State& s = st(h);
+        const uint64_t lim = (uint64_t(1) << s.n) - 1;
+        for (int t = 0; t < nterms; ++t)
+            if ((flip[t] & ~lim) || (signs[t] & ~lim))
+                throw NqError{NQ_ERR_CONTRACT, "Pauli mask exceeds the state's qubit count"};
+        state_flush(s);
+        DeviceCtx& c = ctx_for(s.dev);
+        const uint64_t dim = uint64_t(1) << s.n;
+        std::map<uint64_t, std::vector<int>> groups;
+        pauli_groups(flip, nterms, groups);
+        const int tpl = terms_per_launch();
+        int launches = 0;
+        for (auto& g : groups) launches += int((g.second.size() + tpl - 1) / tpl);
+        const size_t part = scratch_doubles_needed(dim);
+        c.ensure_scratch(part + size_t(launches) * 2 * tpl + 64);
+        double* results = c.d_scratch + part;
+        std::vector<std::pair<int, int>> slot_of{static_cast<size_t>(nterms)};
+        int li = 0;
+        for (auto& g : groups) {
+            const auto& terms = g.second;
+            for (size_t b = 0; b < terms.size(); b += size_t(tpl)) {
+                uint64_t sg[64];
+                const int nt = int(std::min(terms.size() - b, size_t(tpl)));
+                for (int j = 0; j < nt; ++j) {
+                    sg[j] = signs[terms[b + size_t(j)]];
+                    slot_of[size_t(terms[b + size_t(j)])] = {li, j};
+                }
+                launch_expect_dm(s.d, s.n, g.first, sg, nt, c.d_scratch, results + size_t(li) * 2 * tpl,
+                                 c.stream);
+                ++li;
+            }
+        }
+        CUDA_TRY(cudaGetLastError());
+        std::vector<double> host(size_t(launches) * 2 * tpl);
+        if (!host.empty())
+            CUDA_TRY(cudaMemcpyAsync(host.data(), results, host.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                     c.stream));
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        for (int t = 0; t < nterms; ++t) {
+            const size_t base = size_t(slot_of[size_t(t)].first) * 2 * tpl + 2 * size_t(slot_of[size_t(t)].second);
+            cplx total(host[base], host[base + 1]);
+            total *= kIPow[ny[t] & 3];
+            out_re[t] = coeff[t] * total.real();
+            if (out_im) out_im[t] = total.imag();
+        }
+    });
+}
+
+nq_status nq_dm_probabilities(nq_dm* h, double* host_out) {
+    return guard([&] {
+        State& s = st(h);
+        state_flush(s);
+        DeviceCtx& c = ctx_for(s.dev);
+        const uint64_t dim = uint64_t(1) << s.n;
+        c.ensure_scratch(scratch_doubles_needed(dim) + 64);
+        double* p = nullptr;
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p), dim * sizeof(double), c.stream));
+        launch_dm_probs(s.d, dim, p, c.d_scratch, c.stream);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(host_out, p, dim * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        CUDA_TRY(cudaFreeAsync(p, c.stream));
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+    });
+}
+
+nq_status nq_dm_get_entries(nq_dm* h, uint64_t offset, uint64_t count, double* host_out) {
+    return guard([&] {
+        State& s = st(h);
+        state_flush(s);
+        if (offset > s.count || count > s.count - offset)
+            throw NqError{NQ_ERR_CONTRACT, "entry range out of bounds"};
+        if (count == 0) return;
+        DeviceCtx& c = ctx_for(s.dev);
+        CUDA_TRY(cudaMemcpyAsync(host_out, s.d + offset, count * sizeof(double2), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+    });
+}
+
+nq_status nq_dm_set_entries(nq_dm* h, uint64_t offset, uint64_t count, const double* host_in) {
+    return guard([&] {
+        State& s = st(h);
+        state_flush(s);
+        if (offset > s.count || count > s.count - offset)
+            throw NqError{NQ_ERR_CONTRACT, "entry range out of bounds"};
+        if (count == 0) return;
+        DeviceCtx& c = ctx_for(s.dev);
+        CUDA_TRY(cudaMemcpyAsync(s.d + offset, host_in, count * sizeof(double2), cudaMemcpyHostToDevice,
+                                 c.stream));
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+    });
+}
+
+nq_status nq_dm_last_stats(const nq_dm* h, int64_t* passes, int64_t* microops, int64_t* source_ops,
+                           int64_t* launches) {
+    return guard([&] {
+        const State& s = const_cast<nq_dm*>(h)->s;
+        if (passes) *passes = s.last_passes;
+        if (microops) *microops = s.last_microops;
+        if (source_ops) *source_ops = s.last_source_ops;
+        if (launches) *launches = s.last_launches;
+    });
+}
+
+nq_status nq_dm_synchronize(nq_dm* h) {
+    return guard([&] {
+        State& s = st(h);
+        CUDA_TRY(cudaSetDevice(s.dev));
+        CUDA_TRY(cudaStreamSynchronize(ctx_for(s.dev).stream));
+    });
+}
+
+// ---- readout -------------------------------------------------------------------------
+nq_status nq_readout_apply_dist(const double* dist_in, int n, const double* p01, const double* p10,
+                                double* dist_out) {
+    return guard([&] {
+        if (n < 0 || n > 40) throw NqError{NQ_ERR_CONTRACT, "readout qubit count out of range"};
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        DeviceCtx& c = ctx_for(dev);
+        const uint64_t len = uint64_t(1) << n;
+        double* d = nullptr;
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d), len * sizeof(double), c.stream));
+        CUDA_TRY(cudaMemcpyAsync(d, dist_in, len * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+        c.ensure_scratch(scratch_doubles_needed(len) + 64);
+        launch_sum_real(d, len, c.d_scratch + 64, result_slot(c, 0), c.stream);
+        double sum = 0.0;
+        fetch(c, result_slot(c, 0), 1, &sum);
+        if (std::abs(sum - 1.0) > 1e-9) {
+            cudaFreeAsync(d, c.stream);
+            throw NqError{NQ_ERR_CONTRACT, "distribution sums to " + std::to_string(sum) + ", expected 1"};
+        }
+        for (int q = 0; q < n; ++q) {
+            if (p01[q] == 0.0 && p10[q] == 0.0) continue;
+            launch_readout(d, n, q, p01[q], p10[q], c.stream);
+        }
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(dist_out, d, len * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        CUDA_TRY(cudaFreeAsync(d, c.stream));
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+    });
+}
+
+// ---- planner introspection -------------------------------------------------------------
+nq_status nq_plan_debug(int n, const nq_op* ops, int64_t count, int tile_qubits, int fuse, unsigned char* buf,
+                        int64_t cap, int64_t* size) {
+    return guard([&] {
+        if (n < 1 || n > kMaxStateBits) throw NqError{NQ_ERR_CONTRACT, "qubit count out of range"};
+        std::vector<EOp> q;
+        for (int64_t i = 0; i < count; ++i) {
+            if (ops[i].kind == NQ_MEASURE) throw NqError{NQ_ERR_CONTRACT, "MEASURE in plan"};
+            check_op_shape(ops[i]);
+            if (ops[i].kind != NQ_BARRIER) check_range(ops[i].qubits, ops[i].nqubits, n);
+            lower_sv_op(ops[i], q);
+        }
+        PlanOptions p;
+        p.nbits = n;
+        p.nloc = n;
+        p.tile_bits = tile_qubits > 0 ? std::min(tile_qubits, kMaxTileBits) : 12;
+        p.fuse = fuse != 0;
+        configure_caps(p);
+        PlanStats stt;
+        auto passes = plan_passes(q, p, &stt);
+        std::vector<size_t> offs;
+        auto bytes = serialize_passes(passes, n, &offs);
+        *size = int64_t(bytes.size());
+        if (buf && cap > 0) std::memcpy(buf, bytes.data(), size_t(std::min<int64_t>(cap, int64_t(bytes.size()))));
+    });
+}
+
+}  // extern "C"
+
+extern "C" nq_status nq_sample_dist_sorted(const double* dist, uint64_t len, const double* sorted_u,
+                                           uint64_t shots, uint64_t* idx_out, uint64_t* count_out,
+                                           uint64_t* nout) {
+    return guard([&] {
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        DeviceCtx& c = ctx_for(dev);
+        double* d = nullptr;
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d), len * sizeof(double), c.stream));
+        CUDA_TRY(cudaMemcpyAsync(d, dist, len * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+        try {
+            sample_sweep(c, nullptr, d, len, sorted_u, shots, idx_out, count_out, nout);
+        } catch (...) {
+            cudaFreeAsync(d, c.stream);
+            throw;
+        }
+        CUDA_TRY(cudaFreeAsync(d, c.stream));
+    });
+}

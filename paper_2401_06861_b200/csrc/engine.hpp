@@ -1,0 +1,115 @@
+// Internal engine structures shared by the planner (host C++), the kernels
+// (CUDA) and the C ABI.  Nothing here crosses the public boundary.
+//
+// Design: a state of `nbits` bits (SV: n qubits; DM: vec(rho),
+// 2n bits, column bits low) is processed by PASSES.  A pass picks a set Q of
+// m "tile bits"; each CTA stages the 2^m amplitudes that share one value of
+// the remaining bits in shared memory, applies every micro-op of the pass
+// there, and writes the tile back: one HBM read + one write of the state per
+// pass, whatever the number of gates fused into it.
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace nqe {
+
+using cplx = std::complex<double>;
+
+constexpr int kMaxTileBits = 13;   // 2^13 * 16 B = 128 KiB of shared memory
+constexpr int kMaxStateBits = 48;
+constexpr int kMaxOpK = 4;         // dense micro-ops act on <= 4 tile bits
+
+// ---- device micro-ops ------------------------------------------------------
+enum MOpType : uint8_t {
+    MOP_DENSE = 0,  // 2^k x 2^k complex matrix on tile bits pos[0..k)
+    MOP_DIAG = 1,   // 2^k diagonal; bit j from tile bit pos[j] or full-index bit gq[j]
+    MOP_XPERM = 2,  // X on tile bit pos[0], controlled by cmask_tile / cmask_glob
+    MOP_SWAP = 3,   // swap tile bits pos[0], pos[1]
+    MOP_DEPOL = 4,  // x[c,r] -> a x[c,r] + b d_{c,r} sum_l x[l,l] on k col + k row bits
+};
+
+struct MOp {
+    uint8_t type;
+    uint8_t k;            // number of operator bits (DEPOL: 2 or 4)
+    int8_t pos[4];        // tile bit positions (DIAG: -1 = not in tile)
+    uint8_t gq[4];        // DIAG: full-index bit when pos[j] == -1
+    uint16_t pad0;
+    uint32_t mat;         // offset into the pass's complex pool
+    uint32_t cmask_tile;  // controls on tile bits (XPERM / DENSE)
+    uint64_t cmask_glob;  // controls on full-index bits outside the tile
+};
+static_assert(sizeof(MOp) == 32, "MOp layout");
+
+struct PassHdr {
+    int32_t m;          // tile bits
+    int32_t nops;
+    int32_t nloc;       // local state bits (device array has 2^nloc amplitudes)
+    int32_t nrest;      // number of non-tile local bits
+    int64_t ntiles;     // 2^(nloc - m)
+    uint32_t op_off;    // byte offset of MOp[nops] from the pass header
+    uint32_t pool_off;  // byte offset of the complex pool from the pass header
+    uint32_t pool_n;    // complex entries in the pool
+    uint32_t bytes;     // total bytes of this pass record (header+ops+pool, 16B aligned)
+    int8_t q[16];       // tile bit i <-> state bit q[i] (ascending)
+    int8_t rest[56];    // non-tile state bits, ascending
+};
+static_assert(sizeof(PassHdr) % 16 == 0, "PassHdr alignment");
+
+// ---- elementary ops (planner input) ----------------------------------------
+enum EOpType : uint8_t {
+    E_DENSE = 0,  // matrix on bits[0..k) (local bit j = bits[j])
+    E_DIAG = 1,   // diagonal on bits[0..k)
+    E_XPERM = 2,  // X on bits[0], controls in ctrl
+    E_SWAP = 3,   // swap bits[0], bits[1]
+    E_DEPOL = 4,  // depolarizing in Liouville form: bits = [cols..., rows...]; mat = {a, b}
+    E_NOP = 5,    // counted but does nothing (ID)
+};
+
+struct EOp {
+    EOpType type = E_NOP;
+    int k = 0;
+    int bits[4] = {0, 0, 0, 0};
+    uint64_t ctrl = 0;
+    std::vector<cplx> mat;  // DENSE: 4^k, DIAG: 2^k, DEPOL: 2
+    int64_t src = 1;        // source (reference) ops this elementary op accounts for
+};
+
+struct PlanOptions {
+    int nbits = 0;        // state bits seen by the planner (local + global)
+    int nloc = 0;         // local bits (== nbits on one device)
+    int tile_bits = 12;   // m
+    int low_bits = 4;     // minimum contiguous low bits in every tile (coalescing)
+    bool fuse = true;
+    int max_ops_per_pass = 192;
+    int max_pool_per_pass = 1536;  // complex entries
+};
+
+struct PlannedPass {
+    std::vector<int> q;     // tile bits
+    std::vector<MOp> ops;
+    std::vector<cplx> pool;
+};
+
+struct PlanStats {
+    int64_t passes = 0;
+    int64_t microops = 0;
+    int64_t source_ops = 0;
+};
+
+// Plan a sequence of elementary ops (all on local bits < nloc for the
+// non-diagonal targets; diagonal/control bits may be >= nloc).
+std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops, const PlanOptions& opt,
+                                     PlanStats* stats);
+
+// Serialise passes into one contiguous buffer of PassHdr records.
+std::vector<unsigned char> serialize_passes(const std::vector<PlannedPass>& passes, int nloc,
+                                            std::vector<size_t>* offsets);
+
+// Helpers shared by SV/DM lowering.
+void gate_matrix_2x2(int kind, const double* params, cplx out[4]);
+bool gate_is_diagonal(int kind);
+
+}  // namespace nqe

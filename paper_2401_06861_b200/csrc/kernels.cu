@@ -1,0 +1,989 @@
+// sm_100a kernels of the SV/DM simulation core.
+//
+//  pass_kernel<M>   one fused pass over the state: persistent
+//                   CTAs stage 2^M-amplitude tiles in shared memory with
+//                   streaming 16-byte loads, run the pass's micro-ops there,
+//                   and stream the tile back.  Replaces the per-gate sweeps
+//                   K1-K8 of proj/src/statevector.cpp:50-180 and the blockwise
+//                   Kraus sums K14 of proj/src/densitymatrix.cpp:60-110.
+//  reductions       fixed-grid, fixed-order (bit-reproducible) sums:
+//                   norm/purity (K9/K15), Pauli expectations (K10/K16),
+//                   probabilities (K11/K17), Kraus weights (K13).
+//  sampling         block sums + per-block sequential sweeps (K12).
+//  readout          per-qubit 2x2 stochastic maps (K18).
+#include "kernels.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+namespace nqe {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a*b + c
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
+    return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+__device__ __forceinline__ uint32_t ins0(uint32_t w, int b) {
+    return ((w >> b) << (b + 1)) | (w & ((1u << b) - 1u));
+}
+__device__ __forceinline__ uint64_t ins0_64(uint64_t w, int b) {
+    return ((w >> b) << (b + 1)) | (w & ((uint64_t(1) << b) - 1u));
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_stream(double2* p, double2 v) {
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// micro-op application on the shared-memory tile
+// ---------------------------------------------------------------------------
+template <int M, int T>
+__device__ __forceinline__ void op_dense1(const MOp& op, double2* tile, const double2* pool, int tid) {
+    const int b = op.pos[0];
+    const uint32_t bit = 1u << b;
+    const double2 u00 = pool[op.mat], u01 = pool[op.mat + 1], u10 = pool[op.mat + 2],
+                  u11 = pool[op.mat + 3];
+    constexpr int HALF = 1 << (M - 1);
+#pragma unroll 4
+    for (int w = tid; w < HALF; w += T) {
+        const uint32_t e0 = ins0(uint32_t(w), b), e1 = e0 | bit;
+        const double2 a0 = tile[e0], a1 = tile[e1];
+        tile[e0] = cfma(u00, a0, cmul(u01, a1));
+        tile[e1] = cfma(u10, a0, cmul(u11, a1));
+    }
+}
+
+template <int M, int T>
+__device__ __forceinline__ void op_dense2(const MOp& op, double2* tile, const double2* pool, int tid) {
+    const int p0 = op.pos[0], p1 = op.pos[1];
+    const int lo = min(p0, p1), hi = max(p0, p1);
+    const uint32_t b0 = 1u << p0, b1 = 1u << p1;
+    double2 u[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) u[i] = pool[op.mat + i];
+    constexpr int Q4 = 1 << (M - 2);
+#pragma unroll 2
+    for (int w = tid; w < Q4; w += T) {
+        const uint32_t e = ins0(ins0(uint32_t(w), lo), hi);
+        const uint32_t idx[4] = {e, e | b0, e | b1, e | b0 | b1};
+        double2 v[4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) v[l] = tile[idx[l]];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            double2 acc = cmul(u[r * 4], v[0]);
+#pragma unroll
+            for (int c = 1; c < 4; ++c) acc = cfma(u[r * 4 + c], v[c], acc);
+            tile[idx[r]] = acc;
+        }
+    }
+}
+
+template <int M, int T, int K>
+__device__ __forceinline__ void op_denseK(const MOp& op, double2* tile, const double2* pool, int tid) {
+    constexpr int D = 1 << K;
+    int sp[K];
+    uint32_t offs[D];
+#pragma unroll
+    for (int j = 0; j < K; ++j) sp[j] = op.pos[j];
+    // sort positions ascending (K <= 4, tiny insertion sort)
+#pragma unroll
+    for (int i = 1; i < K; ++i)
+#pragma unroll
+        for (int j = i; j > 0; --j)
+            if (sp[j - 1] > sp[j]) {
+                const int t = sp[j - 1];
+                sp[j - 1] = sp[j];
+                sp[j] = t;
+            }
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+        uint32_t o = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if ((l >> j) & 1) o |= 1u << op.pos[j];
+        offs[l] = o;
+    }
+    const double2* mat = pool + op.mat;
+    constexpr int G = 1 << (M - K);
+    for (int w = tid; w < G; w += T) {
+        uint32_t e = uint32_t(w);
+#pragma unroll
+        for (int j = 0; j < K; ++j) e = ins0(e, sp[j]);
+        double2 v[D];
+#pragma unroll
+        for (int l = 0; l < D; ++l) v[l] = tile[e | offs[l]];
+#pragma unroll 1
+        for (int r = 0; r < D; ++r) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc = cfma(mat[r * D + c], v[c], acc);
+            tile[e | offs[r]] = acc;
+        }
+    }
+}
+
+template <int M, int T>
+__device__ __forceinline__ void op_diag(const MOp& op, double2* tile, const double2* pool, int tid,
+                                        uint64_t full) {
+    const int k = op.k;
+    uint32_t gpart = 0;
+    int tpos[4];
+    int ntile = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        tpos[j] = -1;
+        if (j < k) {
+            if (op.pos[j] >= 0) {
+                tpos[j] = op.pos[j];
+                ++ntile;
+            } else {
+                gpart |= uint32_t((full >> op.gq[j]) & 1u) << j;
+            }
+        }
+    }
+    const double2* tab = pool + op.mat;
+    constexpr int SIZE = 1 << M;
+    if (ntile == 0) {
+        const double2 f = tab[gpart];
+        if (f.x == 1.0 && f.y == 0.0) return;
+#pragma unroll 4
+        for (int e = tid; e < SIZE; e += T) tile[e] = cmul(f, tile[e]);
+        return;
+    }
+    if (k == 1) {
+        const int b = tpos[0];
+        const double2 d0 = tab[0], d1 = tab[1];
+        if (d0.x == 1.0 && d0.y == 0.0) {
+            constexpr int HALF = SIZE / 2;
+#pragma unroll 4
+            for (int w = tid; w < HALF; w += T) {
+                const uint32_t e = ins0(uint32_t(w), b) | (1u << b);
+                tile[e] = cmul(d1, tile[e]);
+            }
+        } else {
+#pragma unroll 4
+            for (int e = tid; e < SIZE; e += T) tile[e] = cmul(((e >> b) & 1) ? d1 : d0, tile[e]);
+        }
+        return;
+    }
+#pragma unroll 4
+    for (int e = tid; e < SIZE; e += T) {
+        uint32_t idx = gpart;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (tpos[j] >= 0) idx |= uint32_t((e >> tpos[j]) & 1) << j;
+        const double2 f = tab[idx];
+        if (!(f.x == 1.0 && f.y == 0.0)) tile[e] = cmul(f, tile[e]);
+    }
+}
+
+template <int M, int T>
+__device__ __forceinline__ void op_xperm(const MOp& op, double2* tile, int tid, uint64_t full) {
+    if ((full & op.cmask_glob) != op.cmask_glob) return;
+    const int t = op.pos[0];
+    const uint32_t cm = op.cmask_tile;
+    // positions to insert: target + tile controls, ascending
+    int sp[4];
+    int ns = 0;
+    uint32_t all = cm | (1u << t);
+    for (int b = 0; b < M && ns < 4; ++b)
+        if ((all >> b) & 1) sp[ns++] = b;
+    const int work = (1 << M) >> ns;
+    const uint32_t tb = 1u << t;
+    for (int w = tid; w < work; w += T) {
+        uint32_t e = uint32_t(w);
+        for (int j = 0; j < ns; ++j) e = ins0(e, sp[j]);
+        e |= cm;
+        const double2 a = tile[e], b = tile[e | tb];
+        tile[e] = b;
+        tile[e | tb] = a;
+    }
+}
+
+template <int M, int T>
+__device__ __forceinline__ void op_swap(const MOp& op, double2* tile, int tid) {
+    const int p0 = op.pos[0], p1 = op.pos[1];
+    const int lo = min(p0, p1), hi = max(p0, p1);
+    const uint32_t b0 = 1u << p0, b1 = 1u << p1;
+    constexpr int Q4 = 1 << (M - 2);
+#pragma unroll 4
+    for (int w = tid; w < Q4; w += T) {
+        const uint32_t e = ins0(ins0(uint32_t(w), lo), hi);
+        const double2 a = tile[e | b0], b = tile[e | b1];
+        tile[e | b0] = b;
+        tile[e | b1] = a;
+    }
+}
+
+template <int M, int T>
+__device__ __forceinline__ void op_depol2(const MOp& op, double2* tile, const double2* pool, int tid) {
+    const double a = pool[op.mat].x, bcoef = pool[op.mat + 1].x;
+    {
+        const int pc = op.pos[0], pr = op.pos[1];
+        const int lo = min(pc, pr), hi = max(pc, pr);
+        const uint32_t bc = 1u << pc, br = 1u << pr;
+        constexpr int G = 1 << (M - 2);
+        for (int w = tid; w < G; w += T) {
+            const uint32_t e = ins0(ins0(uint32_t(w), lo), hi);
+            const double2 x0 = tile[e], x1 = tile[e | bc], x2 = tile[e | br], x3 = tile[e | bc | br];
+            const double tr_re = x0.x + x3.x, tr_im = x0.y + x3.y;
+            tile[e] = make_double2(fma(a, x0.x, bcoef * tr_re), fma(a, x0.y, bcoef * tr_im));
+            tile[e | bc] = make_double2(a * x1.x, a * x1.y);
+            tile[e | br] = make_double2(a * x2.x, a * x2.y);
+            tile[e | bc | br] = make_double2(fma(a, x3.x, bcoef * tr_re), fma(a, x3.y, bcoef * tr_im));
+        }
+    }
+}
+
+template <int M, int T>
+__device__ __forceinline__ void op_depol4(const MOp& op, double2* tile, const double2* pool, int tid) {
+    const double a = pool[op.mat].x, bcoef = pool[op.mat + 1].x;
+    // cols pos[0..2), rows pos[2..4); diagonal entries l = c + 4c
+    int sp[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sp[j] = op.pos[j];
+#pragma unroll
+    for (int i = 1; i < 4; ++i)
+#pragma unroll
+        for (int j = i; j > 0; --j)
+            if (sp[j - 1] > sp[j]) {
+                const int t = sp[j - 1];
+                sp[j - 1] = sp[j];
+                sp[j] = t;
+            }
+    uint32_t offs[16];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        uint32_t o = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if ((l >> j) & 1) o |= 1u << op.pos[j];
+        offs[l] = o;
+    }
+    constexpr int G = 1 << (M - 4);
+    for (int w = tid; w < G; w += T) {
+        uint32_t e = uint32_t(w);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) e = ins0(e, sp[j]);
+        double tr_re = 0.0, tr_im = 0.0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const double2 x = tile[e | offs[c + 4 * c]];
+            tr_re += x.x;
+            tr_im += x.y;
+        }
+#pragma unroll
+        for (int l = 0; l < 16; ++l) {
+            const double2 x = tile[e | offs[l]];
+            const bool diag = (l & 3) == (l >> 2);
+            tile[e | offs[l]] = diag ? make_double2(fma(a, x.x, bcoef * tr_re), fma(a, x.y, bcoef * tr_im))
+                                     : make_double2(a * x.x, a * x.y);
+        }
+    }
+}
+
+__device__ __forceinline__ uint64_t deposit(uint64_t v, const int8_t* pos, int cnt) {
+    uint64_t r = 0;
+    for (int j = 0; j < cnt; ++j)
+        if ((v >> j) & 1) r |= uint64_t(1) << pos[j];
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// the fused pass kernel
+// ---------------------------------------------------------------------------
+template <int M>
+__global__ void __launch_bounds__((1 << M) < kThreads ? (1 << M) : kThreads)
+    pass_kernel(double2* __restrict__ st, const unsigned char* __restrict__ rec, uint64_t rankbase) {
+    constexpr int SIZE = 1 << M;
+    constexpr int T = SIZE < kThreads ? SIZE : kThreads;
+    constexpr int EPT = SIZE / T;
+    constexpr int BATCH = EPT < 16 ? EPT : 16;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int8_t s_q[16];
+    __shared__ int8_t s_rest[56];
+    __shared__ uint64_t s_offj[EPT];
+
+    const PassHdr* h = reinterpret_cast<const PassHdr*>(rec);
+    const int tid = threadIdx.x;
+    const int nops = h->nops;
+    const int pool_n = int(h->pool_n);
+    double2* tile = reinterpret_cast<double2*>(smem_raw);
+    double2* pool = tile + SIZE;
+    MOp* ops = reinterpret_cast<MOp*>(pool + pool_n);
+
+    const double2* gpool = reinterpret_cast<const double2*>(rec + h->pool_off);
+    for (int i = tid; i < pool_n; i += T) pool[i] = gpool[i];
+    const uint4* gops = reinterpret_cast<const uint4*>(rec + h->op_off);
+    uint4* sops = reinterpret_cast<uint4*>(ops);
+    for (int i = tid; i < nops * 2; i += T) sops[i] = gops[i];
+    if (tid < 16) s_q[tid] = h->q[tid];
+    if (tid < 56) s_rest[tid] = h->rest[tid];
+    __syncthreads();
+    for (int j = tid; j < EPT; j += T) s_offj[j] = deposit(uint64_t(j) * T, s_q, M);
+    const uint64_t off_tid = deposit(uint64_t(tid), s_q, M);
+    const int nrest = h->nrest;
+    const int64_t ntiles = h->ntiles;
+    __syncthreads();
+
+    for (int64_t r = blockIdx.x; r < ntiles; r += gridDim.x) {
+        const uint64_t base = deposit(uint64_t(r), s_rest, nrest);
+        const double2* src = st + base + off_tid;
+#pragma unroll
+        for (int j0 = 0; j0 < EPT; j0 += BATCH) {
+            double2 v[BATCH];
+#pragma unroll
+            for (int j = 0; j < BATCH; ++j) v[j] = ld_stream(src + s_offj[j0 + j]);
+#pragma unroll
+            for (int j = 0; j < BATCH; ++j) tile[tid + (j0 + j) * T] = v[j];
+        }
+        __syncthreads();
+        const uint64_t full = rankbase | base;
+        for (int o = 0; o < nops; ++o) {
+            const MOp op = ops[o];
+            switch (op.type) {
+            case MOP_DENSE:
+                if (op.k == 1) op_dense1<M, T>(op, tile, pool, tid);
+                else if (op.k == 2) { if constexpr (M >= 2) op_dense2<M, T>(op, tile, pool, tid); }
+                else if (op.k == 3) { if constexpr (M >= 3) op_denseK<M, T, 3>(op, tile, pool, tid); }
+                else { if constexpr (M >= 4) op_denseK<M, T, 4>(op, tile, pool, tid); }
+                break;
+            case MOP_DIAG:
+                op_diag<M, T>(op, tile, pool, tid, full);
+                break;
+            case MOP_XPERM:
+                op_xperm<M, T>(op, tile, tid, full);
+                break;
+            case MOP_SWAP:
+                if constexpr (M >= 2) op_swap<M, T>(op, tile, tid);
+                break;
+            case MOP_DEPOL:
+                if (op.k == 2) { if constexpr (M >= 2) op_depol2<M, T>(op, tile, pool, tid); }
+                else { if constexpr (M >= 4) op_depol4<M, T>(op, tile, pool, tid); }
+                break;
+            default:
+                break;
+            }
+            __syncthreads();
+        }
+        double2* dst = st + base + off_tid;
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) st_stream(dst + s_offj[j], tile[tid + j * T]);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// reductions (fixed grid -> per-block partials -> one-block final combine)
+// ---------------------------------------------------------------------------
+template <int NT>
+__device__ __forceinline__ void block_reduce_store(double (&acc)[NT], double* out, int stride) {
+    __shared__ double red[kThreads / 32][NT > 0 ? NT : 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        double v = acc[t];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[warp][t] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NT) {
+        double s = 0.0;
+        for (int w = 0; w < int(blockDim.x / 32); ++w) s += red[w][threadIdx.x];
+        out[size_t(blockIdx.x) * stride + threadIdx.x] = s;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_sumsq(const double2* __restrict__ a, uint64_t n,
+                                                   uint64_t chunk, double* __restrict__ part) {
+    const uint64_t lo = uint64_t(blockIdx.x) * chunk;
+    const uint64_t hi = min(n, lo + chunk);
+    double acc[1] = {0.0};
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double2 v = a[i];
+        acc[0] = fma(v.x, v.x, fma(v.y, v.y, acc[0]));
+    }
+    block_reduce_store<1>(acc, part, 1);
+}
+
+// sum of Re(a[i * stride]) for i < n (DM trace)
+__global__ void __launch_bounds__(kThreads) k_strided_re(const double2* __restrict__ a, uint64_t n,
+                                                        uint64_t stride, uint64_t chunk,
+                                                        double* __restrict__ part) {
+    const uint64_t lo = uint64_t(blockIdx.x) * chunk;
+    const uint64_t hi = min(n, lo + chunk);
+    double acc[1] = {0.0};
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) acc[0] += a[i * stride].x;
+    block_reduce_store<1>(acc, part, 1);
+}
+
+// Sum NT columns of per-block partials (nblk rows) in a fixed order.
+__global__ void k_final(const double* __restrict__ part, int nblk, int nt, double* __restrict__ out) {
+    __shared__ double sh[kThreads];
+    for (int t = 0; t < nt; ++t) {
+        double s = 0.0;
+        for (int b = threadIdx.x; b < nblk; b += blockDim.x) s += part[size_t(b) * nt + t];
+        sh[threadIdx.x] = s;
+        __syncthreads();
+        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+            if (int(threadIdx.x) < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out[t] = sh[0];
+        __syncthreads();
+    }
+}
+
+constexpr int kTermsPerLaunch = 16;
+
+struct TermBatch {
+    uint64_t signs[kTermsPerLaunch];
+    int eps_im[kTermsPerLaunch];  // 1: accumulate Im(conj(a[y^F]) a[y]) instead of Re
+    int nt;
+};
+
+// SV Pauli expectations sharing one flip mask F.
+//  F == 0: acc_t = sum_y s_t(y) |a_y|^2
+//  F != 0: y ranges over indices with bit f0 = 0, v = conj(a[y^F]) a[y];
+//          acc_t = sum_y s_t(y) * (eps_t ? Im v : Re v)   (see abi.cpp)
+__global__ void __launch_bounds__(kThreads) k_expect(const double2* __restrict__ a, uint64_t nwork,
+                                                    uint64_t flip, int f0, uint64_t chunk,
+                                                    TermBatch tb, double* __restrict__ part) {
+    double acc[kTermsPerLaunch];
+#pragma unroll
+    for (int t = 0; t < kTermsPerLaunch; ++t) acc[t] = 0.0;
+    const uint64_t lo = uint64_t(blockIdx.x) * chunk;
+    const uint64_t hi = min(nwork, lo + chunk);
+    for (uint64_t w = lo + threadIdx.x; w < hi; w += blockDim.x) {
+        uint64_t y;
+        double re, im;
+        if (flip == 0) {
+            y = w;
+            const double2 v = a[y];
+            re = fma(v.x, v.x, v.y * v.y);
+            im = 0.0;
+        } else {
+            y = ins0_64(w, f0);
+            const double2 ay = a[y], az = a[y ^ flip];
+            re = fma(az.x, ay.x, az.y * ay.y);
+            im = fma(az.x, ay.y, -az.y * ay.x);
+        }
+#pragma unroll
+        for (int t = 0; t < kTermsPerLaunch; ++t) {
+            if (t < tb.nt) {
+                const double v = tb.eps_im[t] ? im : re;
+                acc[t] += (__popcll(y & tb.signs[t]) & 1) ? -v : v;
+            }
+        }
+    }
+    block_reduce_store<kTermsPerLaunch>(acc, part, kTermsPerLaunch);
+}
+
+// DM Pauli expectations: sum_y s(y) rho[y, y^F] (complex), dim = 2^n.
+__global__ void __launch_bounds__(kThreads) k_dm_expect(const double2* __restrict__ rho, uint64_t dim,
+                                                       uint64_t flip, uint64_t chunk, TermBatch tb,
+                                                       double* __restrict__ part) {
+    double acc[2 * kTermsPerLaunch];
+#pragma unroll
+    for (int t = 0; t < 2 * kTermsPerLaunch; ++t) acc[t] = 0.0;
+    const uint64_t lo = uint64_t(blockIdx.x) * chunk;
+    const uint64_t hi = min(dim, lo + chunk);
+    for (uint64_t y = lo + threadIdx.x; y < hi; y += blockDim.x) {
+        const double2 v = rho[y * dim + (y ^ flip)];
+#pragma unroll
+        for (int t = 0; t < kTermsPerLaunch; ++t) {
+            if (t < tb.nt) {
+                const bool neg = (__popcll(y & tb.signs[t]) & 1) != 0;
+                acc[2 * t] += neg ? -v.x : v.x;
+                acc[2 * t + 1] += neg ? -v.y : v.y;
+            }
+        }
+    }
+    block_reduce_store<2 * kTermsPerLaunch>(acc, part, 2 * kTermsPerLaunch);
+}
+
+__global__ void k_probs(const double2* __restrict__ a, uint64_t n, double* __restrict__ p) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double2 v = a[i];
+        p[i] = fma(v.x, v.x, v.y * v.y);
+    }
+}
+
+// DM diagonal: max(0, Re rho_ii)
+__global__ void k_dm_diag(const double2* __restrict__ rho, uint64_t dim, double* __restrict__ p) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < dim;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        p[i] = fmax(0.0, rho[i * dim + i].x);
+}
+
+__global__ void k_sum_real(const double* __restrict__ x, uint64_t n, uint64_t chunk,
+                           double* __restrict__ part) {
+    const uint64_t lo = uint64_t(blockIdx.x) * chunk;
+    const uint64_t hi = min(n, lo + chunk);
+    double acc[1] = {0.0};
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) acc[0] += x[i];
+    block_reduce_store<1>(acc, part, 1);
+}
+
+__global__ void k_scale_real(double* __restrict__ x, uint64_t n, const double* __restrict__ denom) {
+    const double d = *denom;
+    if (!(d > 0.0)) return;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        x[i] /= d;
+}
+
+// max_{r,c} |rho[r,c] - conj(rho[c,r])| via 32x32 smem transposes; per-block max.
+__global__ void k_herm(const double2* __restrict__ rho, uint64_t dim, double* __restrict__ part) {
+    __shared__ double2 t[32][33];
+    const uint64_t tiles_per_row = (dim + 31) / 32;
+    const uint64_t ntiles = tiles_per_row * tiles_per_row;
+    double worst = 0.0;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t tr = tile / tiles_per_row, tc = tile % tiles_per_row;
+        if (tc < tr) continue;  // upper triangle of tiles (incl. diagonal)
+        const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+        for (int yy = ty; yy < 32; yy += 8) {
+            const uint64_t r = tc * 32 + yy, c = tr * 32 + tx;  // transposed tile
+            t[yy][tx] = (r < dim && c < dim) ? rho[r * dim + c] : make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+        for (int yy = ty; yy < 32; yy += 8) {
+            const uint64_t r = tr * 32 + yy, c = tc * 32 + tx;
+            if (r < dim && c < dim) {
+                const double2 a = rho[r * dim + c];
+                const double2 b = t[tx][yy];  // rho[c, r]
+                const double dx = a.x - b.x, dy = a.y + b.y;
+                worst = fmax(worst, sqrt(dx * dx + dy * dy));
+            }
+        }
+        __syncthreads();
+    }
+    __shared__ double red[kThreads];
+    red[threadIdx.x] = worst;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (int(threadIdx.x) < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void k_final_max(const double* __restrict__ part, int nblk, double* __restrict__ out) {
+    __shared__ double sh[kThreads];
+    double s = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += blockDim.x) s = fmax(s, part[b]);
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (int(threadIdx.x) < w) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+// ---- Kraus branch weights (K13): w_i = sum_groups sum_row |(K_i v)_row|^2 ----
+struct KrausBatch {
+    int k;
+    int nk;
+    int sp[3];        // sorted positions
+    uint32_t off[8];  // local offsets (bit j <-> qubits[j])
+};
+
+__global__ void __launch_bounds__(kThreads) k_kraus_w(const double2* __restrict__ a, uint64_t ngroups,
+                                                     uint64_t chunk, KrausBatch kb,
+                                                     const double2* __restrict__ mats,
+                                                     double* __restrict__ part) {
+    double acc[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) acc[t] = 0.0;
+    const int D = 1 << kb.k;
+    const uint64_t lo = uint64_t(blockIdx.x) * chunk;
+    const uint64_t hi = min(ngroups, lo + chunk);
+    for (uint64_t w = lo + threadIdx.x; w < hi; w += blockDim.x) {
+        uint64_t e = w;
+        for (int j = 0; j < kb.k; ++j) e = ins0_64(e, kb.sp[j]);
+        double2 v[8];
+        for (int l = 0; l < D; ++l) v[l] = a[e + kb.off[l]];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            if (i < kb.nk) {
+                const double2* K = mats + size_t(i) * D * D;
+                double s = 0.0;
+                for (int r = 0; r < D; ++r) {
+                    double2 z = make_double2(0.0, 0.0);
+                    for (int c = 0; c < D; ++c) z = cfma(K[r * D + c], v[c], z);
+                    s = fma(z.x, z.x, fma(z.y, z.y, s));
+                }
+                acc[i] += s;
+            }
+        }
+    }
+    block_reduce_store<16>(acc, part, 16);
+}
+
+// ---- sampling (K12) ----
+// Per-block probability sums over fixed blocks of kSampleBlock elements.
+__global__ void k_block_psum(const double2* __restrict__ a, const double* __restrict__ p, uint64_t n,
+                             uint64_t bs, double* __restrict__ out) {
+    // one block of threads per sample block; fixed-order tree
+    const uint64_t lo = uint64_t(blockIdx.x) * bs;
+    const uint64_t hi = min(n, lo + bs);
+    double acc[1] = {0.0};
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        if (a) {
+            const double2 v = a[i];
+            acc[0] += fma(v.x, v.x, v.y * v.y);
+        } else {
+            acc[0] += p[i];
+        }
+    }
+    block_reduce_store<1>(acc, out, 1);
+}
+
+// One thread per block that owns uniforms: sequential cumulative sweep from
+// the host-computed block start, exactly like proj/src/statevector.cpp:311-320.
+__global__ void k_block_sweep(const double2* __restrict__ a, const double* __restrict__ p, uint64_t n,
+                              uint64_t bs, const int64_t* __restrict__ blk, const double* __restrict__ cum0,
+                              const int64_t* __restrict__ ulo, const int64_t* __restrict__ uhi,
+                              const double* __restrict__ u, int nb, uint64_t* __restrict__ idx_out,
+                              uint64_t* __restrict__ cnt_out, int64_t* __restrict__ npairs) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nb) return;
+    const uint64_t lo = uint64_t(blk[t]) * bs;
+    const uint64_t hi = min(n, lo + bs);
+    double cum = cum0[t];
+    int64_t next = ulo[t];
+    const int64_t end = uhi[t];
+    int64_t slot = ulo[t];
+    uint64_t last_nz = UINT64_MAX;
+    for (uint64_t i = lo; i < hi && next < end; ++i) {
+        double pi;
+        if (a) {
+            const double2 v = a[i];
+            pi = v.x * v.x + v.y * v.y;
+        } else {
+            pi = p[i];
+        }
+        cum += pi;
+        if (pi > 0.0) last_nz = i;
+        uint64_t here = 0;
+        while (next < end && u[next] < cum) {
+            ++here;
+            ++next;
+        }
+        if (here > 0) {
+            idx_out[slot] = i;
+            cnt_out[slot] = here;
+            ++slot;
+        }
+    }
+    if (next < end) {
+        // rounding between the host block prefix and this sweep: the remaining
+        // uniforms belong to this block; give them to its last nonzero entry.
+        for (uint64_t i = hi; i-- > lo;) {
+            double pi;
+            if (a) {
+                const double2 v = a[i];
+                pi = v.x * v.x + v.y * v.y;
+            } else {
+                pi = p[i];
+            }
+            if (pi > 0.0) {
+                last_nz = i;
+                break;
+            }
+        }
+        if (last_nz != UINT64_MAX) {
+            if (slot > ulo[t] && idx_out[slot - 1] == last_nz) {
+                cnt_out[slot - 1] += uint64_t(end - next);
+            } else {
+                idx_out[slot] = last_nz;
+                cnt_out[slot] = uint64_t(end - next);
+                ++slot;
+            }
+        }
+    }
+    npairs[t] = slot - ulo[t];
+}
+
+// Last index with p > 0 inside one block (for leftover uniforms).
+__global__ void k_last_nonzero(const double2* __restrict__ a, const double* __restrict__ p, uint64_t lo,
+                               uint64_t hi, uint64_t* __restrict__ out) {
+    __shared__ unsigned long long best;
+    if (threadIdx.x == 0) best = 0;
+    __syncthreads();
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        double pi;
+        if (a) {
+            const double2 v = a[i];
+            pi = v.x * v.x + v.y * v.y;
+        } else {
+            pi = p[i];
+        }
+        if (pi > 0.0) atomicMax(&best, (unsigned long long)(i + 1));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *out = uint64_t(best);
+}
+
+// ---- readout confusion (K18): one qubit per launch, pairs (idx, idx|bit) ----
+__global__ void k_readout(double* __restrict__ d, uint64_t half, int q, double p01, double p10) {
+    for (uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < half;
+         w += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i0 = ins0_64(w, q), i1 = i0 | (uint64_t(1) << q);
+        const double v0 = d[i0], v1 = d[i1];
+        d[i0] = (1.0 - p10) * v0 + p01 * v1;
+        d[i1] = p10 * v0 + (1.0 - p01) * v1;
+    }
+}
+
+__global__ void k_init_basis(double2* a, uint64_t n, uint64_t one_at) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        a[i] = make_double2(i == one_at ? 1.0 : 0.0, 0.0);
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+struct DevInfo {
+    int sms = 148;
+};
+
+DevInfo dev_info() {
+    static std::mutex mu;
+    static std::map<int, DevInfo> cache;
+    int d = 0;
+    cudaGetDevice(&d);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(d);
+    if (it != cache.end()) return it->second;
+    DevInfo info;
+    cudaDeviceGetAttribute(&info.sms, cudaDevAttrMultiProcessorCount, d);
+    cache[d] = info;
+    return info;
+}
+
+int grid_for(uint64_t n, int per_thread = 4) {
+    const uint64_t want = (n + uint64_t(kThreads) * per_thread - 1) / (uint64_t(kThreads) * per_thread);
+    const int sms = dev_info().sms;
+    return int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(sms) * 16)));
+}
+
+// Fixed reduction geometry: chunk and block count depend only on n, never on
+// the device, so results are bit-identical on any GPU / any run.
+void reduction_geometry(uint64_t n, uint64_t* chunk, int* nblk) {
+    const uint64_t target_blocks = 2048;
+    uint64_t c = (n + target_blocks - 1) / target_blocks;
+    c = std::max<uint64_t>(c, 1024);
+    c = (c + kThreads - 1) / kThreads * kThreads;
+    *chunk = c;
+    *nblk = int((n + c - 1) / c);
+    if (*nblk < 1) *nblk = 1;
+}
+
+template <int M>
+void launch_pass_m(double2* state, const unsigned char* rec, const PassHdr& h, uint64_t rankbase,
+                   cudaStream_t s) {
+    constexpr int SIZE = 1 << M;
+    constexpr int T = SIZE < kThreads ? SIZE : kThreads;
+    const size_t smem = size_t(SIZE) * 16 + size_t(h.pool_n) * 16 + size_t(h.nops) * sizeof(MOp);
+    static std::mutex mu;
+    static std::map<std::pair<int, size_t>, int> occ_cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int occ = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto key = std::make_pair(dev, smem);
+        auto it = occ_cache.find(key);
+        if (it == occ_cache.end()) {
+            cudaFuncSetAttribute(pass_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass_kernel<M>, T, smem);
+            if (occ < 1) occ = 1;
+            occ_cache[key] = occ;
+        } else {
+            occ = it->second;
+        }
+    }
+    const int64_t grid = std::min<int64_t>(h.ntiles, int64_t(dev_info().sms) * occ);
+    pass_kernel<M><<<unsigned(grid), T, smem, s>>>(state, rec, rankbase);
+}
+
+}  // namespace
+
+void launch_pass(double2* state, const unsigned char* dev_rec, const PassHdr& h, uint64_t rankbase,
+                 cudaStream_t s) {
+    switch (h.m) {
+    case 1: launch_pass_m<1>(state, dev_rec, h, rankbase, s); break;
+    case 2: launch_pass_m<2>(state, dev_rec, h, rankbase, s); break;
+    case 3: launch_pass_m<3>(state, dev_rec, h, rankbase, s); break;
+    case 4: launch_pass_m<4>(state, dev_rec, h, rankbase, s); break;
+    case 5: launch_pass_m<5>(state, dev_rec, h, rankbase, s); break;
+    case 6: launch_pass_m<6>(state, dev_rec, h, rankbase, s); break;
+    case 7: launch_pass_m<7>(state, dev_rec, h, rankbase, s); break;
+    case 8: launch_pass_m<8>(state, dev_rec, h, rankbase, s); break;
+    case 9: launch_pass_m<9>(state, dev_rec, h, rankbase, s); break;
+    case 10: launch_pass_m<10>(state, dev_rec, h, rankbase, s); break;
+    case 11: launch_pass_m<11>(state, dev_rec, h, rankbase, s); break;
+    case 12: launch_pass_m<12>(state, dev_rec, h, rankbase, s); break;
+    case 13: launch_pass_m<13>(state, dev_rec, h, rankbase, s); break;
+    default: throw std::logic_error("launch_pass: unsupported tile size " + std::to_string(h.m));
+    }
+}
+
+void launch_init_basis(double2* a, uint64_t n, uint64_t one_at, cudaStream_t s) {
+    k_init_basis<<<grid_for(n), kThreads, 0, s>>>(a, n, one_at);
+}
+
+void launch_sumsq(const double2* a, uint64_t n, double* scratch, double* out, cudaStream_t s) {
+    uint64_t chunk;
+    int nblk;
+    reduction_geometry(n, &chunk, &nblk);
+    k_sumsq<<<nblk, kThreads, 0, s>>>(a, n, chunk, scratch);
+    k_final<<<1, kThreads, 0, s>>>(scratch, nblk, 1, out);
+}
+
+void launch_trace(const double2* rho, uint64_t dim, double* scratch, double* out, cudaStream_t s) {
+    uint64_t chunk;
+    int nblk;
+    reduction_geometry(dim, &chunk, &nblk);
+    k_strided_re<<<nblk, kThreads, 0, s>>>(rho, dim, dim + 1, chunk, scratch);
+    k_final<<<1, kThreads, 0, s>>>(scratch, nblk, 1, out);
+}
+
+size_t scratch_doubles_needed(uint64_t n) {
+    uint64_t chunk;
+    int nblk;
+    reduction_geometry(n, &chunk, &nblk);
+    return size_t(nblk) * 2 * kTermsPerLaunch + 64;
+}
+
+int terms_per_launch() { return kTermsPerLaunch; }
+
+void launch_expect_sv(const double2* a, int nbits, uint64_t flip, const uint64_t* signs,
+                      const int* eps_im, int nt, double* scratch, double* out, cudaStream_t s) {
+    TermBatch tb{};
+    tb.nt = nt;
+    for (int t = 0; t < nt; ++t) {
+        tb.signs[t] = signs[t];
+        tb.eps_im[t] = eps_im[t];
+    }
+    const uint64_t n = uint64_t(1) << nbits;
+    const uint64_t nwork = flip ? n / 2 : n;
+    const int f0 = flip ? __builtin_ctzll(flip) : 0;
+    uint64_t chunk;
+    int nblk;
+    reduction_geometry(nwork, &chunk, &nblk);
+    k_expect<<<nblk, kThreads, 0, s>>>(a, nwork, flip, f0, chunk, tb, scratch);
+    k_final<<<1, kThreads, 0, s>>>(scratch, nblk, kTermsPerLaunch, out);
+}
+
+void launch_expect_dm(const double2* rho, int n, uint64_t flip, const uint64_t* signs, int nt,
+                      double* scratch, double* out, cudaStream_t s) {
+    TermBatch tb{};
+    tb.nt = nt;
+    for (int t = 0; t < nt; ++t) tb.signs[t] = signs[t];
+    const uint64_t dim = uint64_t(1) << n;
+    uint64_t chunk;
+    int nblk;
+    reduction_geometry(dim, &chunk, &nblk);
+    k_dm_expect<<<nblk, kThreads, 0, s>>>(rho, dim, flip, chunk, tb, scratch);
+    k_final<<<1, kThreads, 0, s>>>(scratch, nblk, 2 * kTermsPerLaunch, out);
+}
+
+void launch_probs(const double2* a, uint64_t n, double* p, cudaStream_t s) {
+    k_probs<<<grid_for(n), kThreads, 0, s>>>(a, n, p);
+}
+
+void launch_dm_probs(const double2* rho, uint64_t dim, double* p, double* scratch, cudaStream_t s) {
+    k_dm_diag<<<grid_for(dim), kThreads, 0, s>>>(rho, dim, p);
+    uint64_t chunk;
+    int nblk;
+    reduction_geometry(dim, &chunk, &nblk);
+    k_sum_real<<<nblk, kThreads, 0, s>>>(p, dim, chunk, scratch + 1);
+    k_final<<<1, kThreads, 0, s>>>(scratch + 1, nblk, 1, scratch);
+    k_scale_real<<<grid_for(dim), kThreads, 0, s>>>(p, dim, scratch);
+}
+
+void launch_sum_real(const double* x, uint64_t n, double* scratch, double* out, cudaStream_t s) {
+    uint64_t chunk;
+    int nblk;
+    reduction_geometry(n, &chunk, &nblk);
+    k_sum_real<<<nblk, kThreads, 0, s>>>(x, n, chunk, scratch);
+    k_final<<<1, kThreads, 0, s>>>(scratch, nblk, 1, out);
+}
+
+void launch_herm(const double2* rho, uint64_t dim, double* scratch, double* out, cudaStream_t s) {
+    const uint64_t tpr = (dim + 31) / 32;
+    const int nblk = int(std::min<uint64_t>(tpr * tpr, 2048));
+    k_herm<<<nblk, kThreads, 0, s>>>(rho, dim, scratch);
+    k_final_max<<<1, kThreads, 0, s>>>(scratch, nblk, out);
+}
+
+void launch_kraus_weights(const double2* a, int nbits, const int* qubits, int k, int nk,
+                          const double2* dev_mats, double* scratch, double* out, cudaStream_t s) {
+    KrausBatch kb{};
+    kb.k = k;
+    kb.nk = nk;
+    int sp[3] = {qubits[0], k > 1 ? qubits[1] : 0, k > 2 ? qubits[2] : 0};
+    std::sort(sp, sp + k);
+    for (int j = 0; j < k; ++j) kb.sp[j] = sp[j];
+    for (int l = 0; l < (1 << k); ++l) {
+        uint32_t o = 0;
+        for (int j = 0; j < k; ++j)
+            if ((l >> j) & 1) o |= 1u << qubits[j];
+        kb.off[l] = o;
+    }
+    const uint64_t ng = (uint64_t(1) << nbits) >> k;
+    uint64_t chunk;
+    int nblk;
+    reduction_geometry(ng, &chunk, &nblk);
+    k_kraus_w<<<nblk, kThreads, 0, s>>>(a, ng, chunk, kb, dev_mats, scratch);
+    k_final<<<1, kThreads, 0, s>>>(scratch, nblk, 16, out);
+}
+
+void launch_block_psum(const double2* a, const double* p, uint64_t n, uint64_t bs, double* out,
+                       cudaStream_t s) {
+    const uint64_t nb = (n + bs - 1) / bs;
+    k_block_psum<<<unsigned(nb), kThreads, 0, s>>>(a, p, n, bs, out);
+}
+
+void launch_block_sweep(const double2* a, const double* p, uint64_t n, uint64_t bs, const int64_t* blk,
+                        const double* cum0, const int64_t* ulo, const int64_t* uhi, const double* u,
+                        int nb, uint64_t* idx_out, uint64_t* cnt_out, int64_t* npairs, cudaStream_t s) {
+    if (nb <= 0) return;
+    k_block_sweep<<<(nb + 127) / 128, 128, 0, s>>>(a, p, n, bs, blk, cum0, ulo, uhi, u, nb, idx_out,
+                                                   cnt_out, npairs);
+}
+
+void launch_last_nonzero(const double2* a, const double* p, uint64_t lo, uint64_t hi, uint64_t* out,
+                         cudaStream_t s) {
+    k_last_nonzero<<<1, kThreads, 0, s>>>(a, p, lo, hi, out);
+}
+
+void launch_readout(double* d, int n, int q, double p01, double p10, cudaStream_t s) {
+    const uint64_t half = (uint64_t(1) << n) / 2;
+    k_readout<<<grid_for(half), kThreads, 0, s>>>(d, half, q, p01, p10);
+}
+
+}  // namespace nqe

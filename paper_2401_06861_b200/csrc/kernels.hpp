@@ -1,0 +1,40 @@
+// Host-side launchers of the sm_100a kernels (kernels.cu).
+#pragma once
+
+#include "engine.hpp"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace nqe {
+
+void launch_pass(double2* state, const unsigned char* dev_rec, const PassHdr& h, uint64_t rankbase,
+                 cudaStream_t s);
+void launch_init_basis(double2* a, uint64_t n, uint64_t one_at, cudaStream_t s);
+
+size_t scratch_doubles_needed(uint64_t n);
+int terms_per_launch();
+
+void launch_sumsq(const double2* a, uint64_t n, double* scratch, double* out, cudaStream_t s);
+void launch_trace(const double2* rho, uint64_t dim, double* scratch, double* out, cudaStream_t s);
+void launch_expect_sv(const double2* a, int nbits, uint64_t flip, const uint64_t* signs,
+                      const int* eps_im, int nt, double* scratch, double* out, cudaStream_t s);
+void launch_expect_dm(const double2* rho, int n, uint64_t flip, const uint64_t* signs, int nt,
+                      double* scratch, double* out, cudaStream_t s);
+void launch_probs(const double2* a, uint64_t n, double* p, cudaStream_t s);
+void launch_dm_probs(const double2* rho, uint64_t dim, double* p, double* scratch, cudaStream_t s);
+void launch_sum_real(const double* x, uint64_t n, double* scratch, double* out, cudaStream_t s);
+void launch_herm(const double2* rho, uint64_t dim, double* scratch, double* out, cudaStream_t s);
+void launch_kraus_weights(const double2* a, int nbits, const int* qubits, int k, int nk,
+                          const double2* dev_mats, double* scratch, double* out, cudaStream_t s);
+void launch_block_psum(const double2* a, const double* p, uint64_t n, uint64_t bs, double* out,
+                       cudaStream_t s);
+void launch_block_sweep(const double2* a, const double* p, uint64_t n, uint64_t bs, const int64_t* blk,
+                        const double* cum0, const int64_t* ulo, const int64_t* uhi, const double* u,
+                        int nb, uint64_t* idx_out, uint64_t* cnt_out, int64_t* npairs, cudaStream_t s);
+void launch_last_nonzero(const double2* a, const double* p, uint64_t lo, uint64_t hi, uint64_t* out,
+                         cudaStream_t s);
+void launch_readout(double* d, int n, int q, double p01, double p10, cudaStream_t s);
+
+}  // namespace nqe

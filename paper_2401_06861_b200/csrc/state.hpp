@@ -1,0 +1,111 @@
+// Device context and state objects behind the C ABI handles.
+#pragma once
+
+#include "../../include/naqs_b200.h"
+#include "engine.hpp"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <new>
+#include <string>
+#include <vector>
+
+namespace nqe {
+
+struct NqError {
+    nq_status code;
+    std::string msg;
+};
+
+#define CUDA_TRY(expr)                                                                         \
+    do {                                                                                       \
+        cudaError_t cuda_try_e_ = (expr);                                                      \
+        if (cuda_try_e_ != cudaSuccess) {                                                      \
+            throw ::nqe::NqError{cuda_try_e_ == cudaErrorMemoryAllocation ? NQ_ERR_OOM         \
+                                                                          : NQ_ERR_CUDA,       \
+                                 std::string(#expr) + ": " + cudaGetErrorString(cuda_try_e_)}; \
+        }                                                                                      \
+    } while (0)
+
+extern thread_local std::string g_last_error;
+
+template <class F>
+nq_status guard(F&& f) {
+    try {
+        f();
+        return NQ_OK;
+    } catch (const NqError& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return NQ_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return NQ_ERR_INTERNAL;
+    }
+}
+
+// One per CUDA device: the stream every state on that device runs on, the
+// pinned staging buffer for pass records, and reduction scratch.
+struct DeviceCtx {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t stage_ev = nullptr;
+    bool stage_pending = false;
+    unsigned char* h_stage = nullptr;
+    size_t h_stage_cap = 0;
+    unsigned char* d_ops = nullptr;
+    size_t d_ops_cap = 0;
+    double* d_scratch = nullptr;
+    size_t scratch_cap = 0;
+    double* h_small = nullptr;
+
+    void ensure_scratch(size_t doubles);
+    void stage(const unsigned char* src, size_t bytes);
+};
+
+DeviceCtx& ctx_for(int dev);
+
+struct ShardComm;  // shard.cpp
+
+struct State {
+    int n = 0;       // qubits
+    int nbits = 0;   // state bits (SV n, DM 2n)
+    int nloc = 0;    // bits held on this device
+    bool dm = false;
+    int dev = 0;
+    double2* d = nullptr;
+    uint64_t count = 0;  // 2^nloc
+    std::vector<EOp> queue;
+    PlanOptions popt;
+    int64_t last_passes = 0, last_microops = 0, last_source_ops = 0, last_launches = 0;
+    // sharded states (world > 1)
+    int rank = 0, world = 1;
+    ShardComm* comm = nullptr;
+};
+
+void state_init(State& s, int n, bool dm, const nq_opts* opts);
+void state_free(State& s);
+void state_flush(State& s);
+void configure_caps(PlanOptions& p);
+double* result_slot(DeviceCtx& c, int i);
+void fetch(DeviceCtx& c, const double* dsrc, size_t count, double* host);
+
+// sampling (sample.cpp): either amplitudes `a` or probabilities `p` (one is null)
+void sample_sweep(DeviceCtx& c, const double2* a, const double* p, uint64_t n, const double* sorted_u,
+                  uint64_t shots, uint64_t* idx_out, uint64_t* count_out, uint64_t* nout);
+
+// multi-GPU (shard.cpp)
+void shard_free(State& s);
+void shard_reset(State& s);
+void shard_flush(State& s);
+double shard_norm_sq(State& s);
+void shard_expectation(State& s, const uint64_t* flip, const uint64_t* signs, const int32_t* ny,
+                       const double* coeff, int nterms, double* out);
+void shard_sample(State& s, const double* sorted_u, uint64_t shots, uint64_t* idx_out, uint64_t* count_out,
+                  uint64_t* nout);
+void shard_get_amplitudes(State& s, uint64_t offset, uint64_t count, double* host_out);
+
+}  // namespace nqe

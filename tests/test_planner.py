@@ -1,0 +1,126 @@
+"""Host-side fusion planner, CPU only (no GPU needed).
+
+The planner's output (pass records, nq_plan_debug) is executed here by a
+numpy emulator of the micro-op semantics documented in csrc/engine.hpp and
+compared with the oracle.  This validates pass windows (commutation-safe
+deferral), tile bit selection, fusion and serialisation independently of the
+kernels; the GPU tests then validate the kernels on the same plans.
+"""
+import numpy as np
+import pytest
+
+from paper_2401_06861_b200 import abi, plan_format
+
+
+def ins0(w, b):
+    return ((w >> b) << (b + 1)) | (w & ((1 << b) - 1))
+
+
+def deposit(v, pos):
+    r = 0
+    for j, p in enumerate(pos):
+        if (v >> j) & 1:
+            r |= 1 << p
+    return r
+
+
+def run_plan(n, passes, amps):
+    a = amps.copy()
+    for p in passes:
+        size = 1 << p.m
+        offs = np.array([deposit(e, p.q) for e in range(size)], dtype=np.int64)
+        for r in range(p.ntiles):
+            base = deposit(r, p.rest)
+            t = a[base + offs].copy()
+            for op in p.ops:
+                apply_mop(op, t, p.pool, base, p.m)
+            a[base + offs] = t
+    return a
+
+
+def apply_mop(op, t, pool, full, m):
+    size = 1 << m
+    e = np.arange(size)
+    if op.type == "dense":
+        k = op.k
+        D = 1 << k
+        U = pool[op.mat:op.mat + D * D].reshape(D, D)
+        mask = sum(1 << op.pos[j] for j in range(k))
+        bases = e[(e & mask) == 0]
+        idx = np.stack([bases | deposit(l, op.pos[:k]) for l in range(D)])  # D x G
+        t[idx] = U @ t[idx]
+    elif op.type == "diag":
+        k = op.k
+        tab = pool[op.mat:op.mat + (1 << k)]
+        idx = np.zeros(size, dtype=np.int64)
+        for j in range(k):
+            if op.pos[j] >= 0:
+                idx |= ((e >> op.pos[j]) & 1) << j
+            else:
+                idx |= ((full >> op.gq[j]) & 1) << j
+        t *= tab[idx]
+    elif op.type == "xperm":
+        if (full & op.cmask_glob) != op.cmask_glob:
+            return
+        b = 1 << op.pos[0]
+        sel = e[((e & b) == 0) & ((e & op.cmask_tile) == op.cmask_tile)]
+        t[sel], t[sel | b] = t[sel | b].copy(), t[sel].copy()
+    elif op.type == "swap":
+        b0, b1 = 1 << op.pos[0], 1 << op.pos[1]
+        sel = e[((e & b0) != 0) & ((e & b1) == 0)]
+        other = (sel & ~b0) | b1
+        t[sel], t[other] = t[other].copy(), t[sel].copy()
+    else:
+        raise AssertionError(op.type)
+
+
+@pytest.mark.parametrize("n,tile", [(3, 12), (6, 4), (8, 5), (10, 6), (12, 8), (12, 12)])
+@pytest.mark.parametrize("fuse", [True, False])
+def test_plan_emulation_matches_oracle(port, n, tile, fuse):
+    for seed in range(3):
+        ops = port.random_circuit(5000 + 10 * n + seed, n, 150)
+        passes = plan_format.decode(abi.plan_debug(n, ops, tile_qubits=tile, fuse=fuse))
+        a0 = np.zeros(1 << n, dtype=complex)
+        a0[0] = 1
+        got = run_plan(n, passes, a0)
+        np.testing.assert_allclose(got, port.sv_run(n, ops), atol=1e-10, rtol=0)
+
+
+def test_tile_sets_respect_coalescing_and_capacity(port):
+    n, tile = 20, 10
+    ops = port.random_circuit(1, n, 300)
+    passes = plan_format.decode(abi.plan_debug(n, ops, tile_qubits=tile))
+    for p in passes:
+        assert p.m == tile
+        assert p.q[:4] == [0, 1, 2, 3]  # >= 4 contiguous low bits: 256-byte runs
+        assert sorted(p.q) == p.q and len(set(p.q)) == tile
+        assert set(p.q).isdisjoint(p.rest) and len(p.q) + len(p.rest) == n
+        for op in p.ops:
+            if op.type in ("dense", "xperm", "swap"):
+                assert all(0 <= x < tile for x in op.pos[: op.k])
+
+
+def test_fusion_reduces_passes_and_microops(port):
+    n = 24
+    ops = port.random_circuit(2024, n, 200)
+    fused = plan_format.decode(abi.plan_debug(n, ops, tile_qubits=12, fuse=True))
+    unfused = plan_format.decode(abi.plan_debug(n, ops, tile_qubits=12, fuse=False))
+    assert len(fused) == len(unfused)
+    assert sum(len(p.ops) for p in fused) < sum(len(p.ops) for p in unfused)
+    assert len(fused) < 200 / 5  # far fewer state sweeps than gates
+
+
+def test_diagonals_never_force_tile_bits():
+    # a run of RZ/CZ on high qubits fits in one pass with only low tile bits
+    n = 20
+    ops = [("rz", [q], [0.1 * q]) for q in range(n)] + [("cz", [q, (q + 7) % n]) for q in range(n)]
+    passes = plan_format.decode(abi.plan_debug(n, ops, tile_qubits=8))
+    assert len(passes) == 1
+    assert passes[0].q == list(range(8))
+
+
+def test_plan_rejects_bad_ops():
+    with pytest.raises(abi.ContractError):
+        abi.plan_debug(4, [("cx", [0, 4])])
+    with pytest.raises(abi.ContractError):
+        abi.plan_debug(4, [("measure", [0])])
