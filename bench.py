@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SV/DM simulation core (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Headline workload: the reference's seeded random circuit
+(proj/tests/test_util.hpp generator, Rng(2024)), 30 qubits, depth 200, on one
+B200.  One step = the whole circuit applied to the HBM-resident 2^30-amplitude
+state through the C ABI (fusion planning + fused passes).  Metric: source
+gates per second (whole job), plus achieved HBM GB/s.
+
+* value     device time of K steps (CUDA events on the library's stream),
+            barrier + synchronize on both sides, max over ranks.
+* e2e       the same steps through the reference-facing C ABI with host
+            buffers: each step copies its op list host->device (pinned
+            staging) and reads a <Z_0> expectation back device->host; timed
+            on the host clock around synchronised steps, max over ranks.
+* roofline  the fused-pass kernel: algorithmic bytes per launch (32 * 2^n:
+            every amplitude read and written once) / its average CUDA-event
+            duration inside the timed region, against MEASURED_PEAKS.json.
+* cpu_baseline  the reference engine compiled from its own sources
+            (oracle/_ref, kind "reference"; the C restatement "port" if that
+            build is absent), on the host cores, on a bounded prefix of the
+            same circuit.
+For N > 1 (torchrun) every rank simulates its own 30-qubit state (weak
+scaling, no data-path collective); see DESIGN.md §6 for the sharded path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--qubits", type=int, default=30)
+    ap.add_argument("--depth", type=int, default=200)
+    ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--cpu-ops", type=int, default=12, help="ops of the circuit prefix timed on the CPU")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as td
+
+        torch.cuda.set_device(local)
+        td.init_process_group("nccl")
+        dist = td
+    return world, rank, local, dist
+
+
+def barrier(dist, local):
+    if dist is not None:
+        import torch
+
+        dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+
+def max_over_ranks(dist, local, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+
+    t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def traffic_from_profiles():
+    """dram bytes per pass launch from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def host_mem_gib() -> float:
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable:"):
+                    return int(ln.split()[1]) / (1 << 20)
+    except OSError:
+        pass
+    return 0.0
+
+
+def cpu_reference_rate(n: int, ops, n_ops: int, reps: int):
+    """Gates/s of the reference engine on the host: `reps` timed runs of the
+    first `n_ops` ops on one persistent n-qubit state (all host threads)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    from oracle import Port, Ref, list_to_ops  # checker / baseline only
+
+    need = (16 << n) / (1 << 30) * 1.3 + 2
+    if host_mem_gib() < need:
+        return None, f"host RAM {host_mem_gib():.0f} GiB < {need:.0f} GiB needed for n={n}"
+    arr = list_to_ops(ops[:n_ops])
+    cores = cpu_threads()
+    if Ref.available():
+        ref = Ref()
+        ref.set_threads(cores)
+        h = ref.sv_new(n)
+        try:
+            times = [ref.sv_run_timed(h, arr) for _ in range(reps)]
+        finally:
+            ref.sv_free(h)
+        kind = "reference"
+    else:
+        port = Port()
+        amps = np.zeros(1 << n, dtype=np.complex128)
+        amps[0] = 1
+        times = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            port.sv_apply(amps, arr)
+            times.append((time.perf_counter() - t0) * 1e3)
+        kind, cores = "port", 1
+    ms = statistics.median(times)
+    return {"value": n_ops / (ms / 1e3), "unit": "gates/s", "cores": cores, "kind": kind,
+            "sample": f"first {n_ops} ops of random_circuit(Rng(2024), n={n}, depth=200) on one persistent "
+                      f"2^{n} state, median of {reps} runs, OMP threads={cores}",
+            "ms_per_run": ms}, None
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return 0
+    from paper_2401_06861_b200 import workloads
+
+    ops = workloads.random_circuit(args.seed, args.qubits, args.depth)
+    k = max(1, min(args.cpu_ops, len(ops)))
+    total_steps = args.warmup + args.steps
+    res, why = cpu_reference_rate(args.qubits, ops, k, total_steps)
+    base = {"metric": "SV gates/s (random circuit, depth 200)", "unit": "gates/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "config": {"workload": f"random_circuit(Rng({args.seed})) n={args.qubits} depth={args.depth}",
+                       "qubits": args.qubits}}
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": why}))
+        return 0
+    base.update({"value": res["value"], "ms_per_step": res["ms_per_run"], "dtype": "c128",
+                 "data": "synthetic", "scaling": "weak",
+                 "cpu_baseline": {k2: res[k2] for k2 in ("value", "unit", "cores", "kind", "sample")},
+                 "e2e": {"value": res["value"], "unit": "gates/s", "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0}})
+    print(json.dumps(base))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def secondary_workloads(abi, workloads, device):
+    """Quick numbers for the other BASELINE.json configurations (device time)."""
+    out = {}
+    # C2b: QFT-30
+    n = 30
+    ops = abi.make_ops(workloads.qft(n))
+    sv = abi.SV(n, device=device)
+    sv.apply(ops).flush()
+    abi.jit_wait()
+    sv.apply(ops).flush()
+    sv.synchronize()
+    abi.profile_begin(device, per_pass_events=False)
+    reps = 2
+    for _ in range(reps):
+        sv.apply(ops).flush()
+    p = abi.profile_end(device)
+    st = sv.stats()
+    out["qft30"] = {"gates_per_s": reps * len(ops) / (p["region_ms"] / 1e3), "ms_per_circuit": p["region_ms"] / reps,
+                    "gates": len(ops), "passes_per_circuit": st["passes"]}
+    sv.close()
+    # C4: noisy TFIM, DM n=14 (synthetic calibration), wall time of the schedule
+    from paper_2401_06861_b200 import naqs
+
+    nd = 14
+    cal = {"name": "synthetic", "qubits": [{"t1_us": 60.0, "t2_us": 40.0, "readout_p01": 0.02, "readout_p10": 0.02}] * nd,
+           "default_1q": {"error": 0.001, "duration_ns": 50.0}, "default_2q": {"error": 0.01, "duration_ns": 300.0}}
+    model = naqs.load_calibration(json.dumps(cal))
+    circ = naqs.Circuit(nd)
+    for name, qs, ps in workloads.tfim_trotter(nd, 1.0, steps=10):
+        circ.add(name, qs, ps)
+    naqs.density_expectation(circ, "Z" + "I" * (nd - 1), model)  # warm: plan + queue kernels
+    abi.jit_wait()
+    naqs.density_expectation(circ, "Z" + "I" * (nd - 1), model)
+    t0 = time.perf_counter()
+    z = naqs.density_expectation(circ, "Z" + "I" * (nd - 1), model)
+    dt = time.perf_counter() - t0
+    out["dm_noisy_tfim14"] = {"wall_s": dt, "items": len(circ) * 3 + sum(1 for o in circ.ops() if len(o[1]) == 2),
+                              "z0": z, "note": "end-to-end via naqs.density_expectation: attach_noise, superoperator "
+                                               "compile, fused passes, expectation"}
+    # C5: VQE n=28 energy evaluations (exact, 193 gates + 55 terms)
+    nv, layers = 28, 3
+    params = workloads.vqe_initial_params(nv, layers)
+    vops = abi.make_ops(workloads.vqe_ansatz(nv, layers, params))
+    terms = workloads.tfim_hamiltonian(nv)
+    sv = abi.SV(nv, device=device)
+    sv.apply(vops)
+    e = float(sum(sv.expectations(terms)))
+    abi.jit_wait()
+    sv.reset()
+    sv.apply(vops)
+    e = float(sum(sv.expectations(terms)))
+    reps = 3
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        sv.reset()
+        sv.apply(vops)
+        e = float(sum(sv.expectations(terms)))
+    dt = (time.perf_counter() - t0) / reps
+    out["vqe28"] = {"evals_per_s": 1.0 / dt, "ms_per_eval": dt * 1e3, "energy": e, "terms": len(terms),
+                    "gates": len(vops)}
+    sv.close()
+    return out
+
+
+def main():
+    args = parse_args()
+    world, rank, local, dist = dist_setup(args)
+    if args.impl == "reference":
+        return run_reference_arm(args, world, rank)
+
+    from paper_2401_06861_b200 import abi, workloads
+
+    if abi.device_count() < 1:
+        raise SystemExit("bench.py: no CUDA device")
+    dev = local
+    n, depth = args.qubits, args.depth
+    ops_list = workloads.random_circuit(args.seed, n, depth)
+    ops = abi.make_ops(ops_list)
+    sv = abi.SV(n, device=dev, tile_qubits=args.tile, max_qubits=max(30, n))
+
+    # warm-up: the first step plans the passes and queues their specialised
+    # kernels for compilation (jit.cpp); wait for them, then warm the rest
+    sv.apply(ops).flush()
+    abi.jit_wait()
+    for _ in range(max(args.warmup, 3) - 1):
+        sv.apply(ops).flush()
+    sv.synchronize()
+    jit = abi.jit_stats()
+    stats = sv.stats()
+
+    # ---- value: device time of K steps
+    barrier(dist, local)
+    sv.synchronize()
+    with ClockSampler(dev) as clk:
+        abi.profile_begin(dev, per_pass_events=True)
+        for _ in range(args.steps):
+            sv.apply(ops).flush()
+        prof = abi.profile_end(dev)
+    barrier(dist, local)
+    ms = max_over_ranks(dist, local, prof["region_ms"])
+    gates_total = args.steps * depth * world
+    value = gates_total / (ms / 1e3)
+    pass_avg_ms = prof["pass_ms"] / max(prof["pass_launches"], 1)
+    bytes_per_launch = prof["pass_bytes"] / max(prof["pass_launches"], 1)
+    achieved = bytes_per_launch / (pass_avg_ms / 1e3) / 1e9
+    peak, peak_kind = measured_peaks()
+    step_gbs = prof["pass_bytes"] / (prof["region_ms"] / 1e3) / 1e9
+
+    # ---- e2e: host buffers in, result out, every step
+    barrier(dist, local)
+    sv.synchronize()
+    abi.profile_begin(dev, per_pass_events=False)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sv.apply(ops)  # host op array -> planner -> pinned staging -> H2D
+        sv.expectations([("Z" + "I" * (n - 1), 1.0)])  # D2H of the step's result
+    t_e2e = time.perf_counter() - t0
+    prof_e2e = abi.profile_end(dev)
+    t_e2e = max_over_ranks(dist, local, t_e2e)
+    e2e = {"value": gates_total / t_e2e, "unit": "gates/s",
+           "h2d_bytes_per_step": int(prof_e2e["h2d_bytes"] / args.steps),
+           "d2h_bytes_per_step": int(prof_e2e["d2h_bytes"] / args.steps)}
+
+    out = None
+    if rank == 0:
+        out = {
+            "metric": "SV gates/s (random circuit, depth 200)",
+            "value": value,
+            "unit": "gates/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "c128",
+            "data": "synthetic",
+            "config": {"workload": f"random_circuit(Rng({args.seed})) n={n} depth={depth} "
+                                   f"(proj/tests/test_util.hpp generator)",
+                       "qubits": n, "depth": depth, "state_bytes": 16 << n,
+                       "parallelism": "single" if world == 1 else f"replicas x{world}",
+                       "l2": "state (16 GiB) >> L2 (126 MB): every pass streams from HBM"},
+            "hbm_gbs": step_gbs,
+            "hbm_frac_step": step_gbs / peak,
+            "passes_per_step": stats["passes"],
+            "microops_per_step": stats["microops"],
+            "gpu_launches": prof["kernel_launches"],
+            "jit": jit,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic_from_profiles(),
+                         "kernel": "pass_kernel<12>", "bytes_per_launch": bytes_per_launch,
+                         "avg_launch_ms": pass_avg_ms, "launches": prof["pass_launches"],
+                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
+            "clocks": clk.summary(),
+            "e2e": e2e,
+        }
+    sv.close()
+    if rank == 0 and not args.no_secondary:
+        try:
+            out["secondary"] = secondary_workloads(abi, workloads, dev)
+        except Exception as exc:  # secondary numbers never hide the headline
+            out["secondary"] = {"error": repr(exc)}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res, why = cpu_reference_rate(n, ops_list, args.cpu_ops, 3)
+        out["cpu_baseline"] = (
+            {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")} if res else {"unavailable": why})
+    if rank == 0:
+        print(json.dumps(out))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -208,6 +208,31 @@ nq_status nq_sv_create_sharded(int num_qubits, int rank, int world, const unsign
 /* Number of global-qubit exchanges performed so far and bytes sent. */
 nq_status nq_sv_comm_stats(const nq_sv* s, int64_t* exchanges, int64_t* bytes_sent);
 
+/* ---- measurement (bench.py) -------------------------------------------- */
+typedef struct nq_profile {
+    double region_ms;        /* device time between begin and end: CUDA events on the device stream */
+    double pass_ms;          /* summed device time of the fused-pass kernel launches in the region  */
+    int64_t pass_launches;
+    double pass_bytes;       /* algorithmic bytes of those launches: 32 * 2^nloc each (read+write)  */
+    int64_t kernel_launches; /* every kernel this library launched in the region                     */
+    int64_t h2d_bytes;       /* bytes this library copied host->device in the region                 */
+    int64_t d2h_bytes;       /* bytes copied device->host                                            */
+} nq_profile;
+/* Start a measured region on `device`'s stream; with per_pass_events != 0
+ * every pass launch is bracketed by CUDA events (pass_ms / pass_launches). */
+nq_status nq_profile_begin(int device, int per_pass_events);
+/* Synchronise and report the region. */
+nq_status nq_profile_end(int device, nq_profile* out);
+
+/* Run-time specialised pass kernels (NVRTC, cached per pass structure;
+ * policy NQ_JIT=off|auto|sync).  Wait for queued compilations / counters. */
+nq_status nq_jit_wait(void);
+nq_status nq_jit_stats(int64_t* compiled, int64_t* failed, int64_t* misses, int64_t* launches);
+/* Generated source of pass `pass_index` of an SV plan, optionally compiled
+ * with NVRTC (no device needed); *compiled_ok = 1/0, or -1 when not compiled. */
+nq_status nq_jit_debug(int num_qubits, const nq_op* ops, int64_t count, int tile_qubits, int pass_index,
+                       int compile, char* src_out, int64_t cap, int64_t* size, int* compiled_ok);
+
 /* ---- planner introspection (host logic, CPU-testable) ------------------ */
 /* Compile `ops` on an n-qubit state into the pass plan without executing it
  * and serialise it (see paper_2401_06861_b200/plan_format.py).  Writes

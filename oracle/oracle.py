@@ -377,6 +377,24 @@ class Ref:
         self._chk(self.lib.ref_sv_time_noreset(n, arr.ctypes.data, C.c_int64(len(arr)), reps, _d(ms), C.byref(ez)))
         return ms, ez.value
 
+    def sv_new(self, n):
+        self.lib.ref_sv_new.restype = C.c_void_p
+        h = self.lib.ref_sv_new(n)
+        if not h:
+            raise MemoryError(self.lib.ref_last_error().decode())
+        return C.c_void_p(h)
+
+    def sv_free(self, h):
+        self.lib.ref_sv_free.argtypes = [C.c_void_p]
+        self.lib.ref_sv_free(h)
+
+    def sv_run_timed(self, h, ops) -> float:
+        arr = ops if isinstance(ops, np.ndarray) else list_to_ops(ops)
+        ms = C.c_double()
+        self.lib.ref_sv_run_timed.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, _dp]
+        self._chk(self.lib.ref_sv_run_timed(h, arr.ctypes.data, len(arr), C.byref(ms)))
+        return ms.value
+
     def dm_time_noisy(self, n, ops, noise: NoiseSpec, reps):
         arr = ops if isinstance(ops, np.ndarray) else list_to_ops(ops)
         ms = np.zeros(reps)

@@ -313,4 +313,28 @@ int ref_dm_time_noisy(int n, const RefOp* ops, int64_t nops, const double* t1, c
     });
 }
 
+// Persistent state for CPU timing (bench.py cpu_baseline / --impl reference):
+// allocation and |0..0> fill happen once, outside the timed runs.
+void* ref_sv_new(int n) {
+    try {
+        return new StateVector(n);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+void ref_sv_free(void* h) { delete static_cast<StateVector*>(h); }
+
+int ref_sv_run_timed(void* h, const RefOp* ops, int64_t nops, double* ms) {
+    return wrap([&] {
+        auto* s = static_cast<StateVector*>(h);
+        const Circuit c = to_circuit(s->num_qubits(), ops, nops);
+        const auto t0 = std::chrono::steady_clock::now();
+        s->run(c);
+        const auto t1 = std::chrono::steady_clock::now();
+        *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    });
+}
+
 } // extern "C"

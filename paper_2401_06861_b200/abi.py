@@ -44,6 +44,12 @@ SCHED_DTYPE = np.dtype(
 assert SCHED_DTYPE.itemsize == 64
 
 
+class nq_profile(C.Structure):
+    _fields_ = [("region_ms", C.c_double), ("pass_ms", C.c_double), ("pass_launches", C.c_int64),
+                ("pass_bytes", C.c_double), ("kernel_launches", C.c_int64), ("h2d_bytes", C.c_int64),
+                ("d2h_bytes", C.c_int64)]
+
+
 class nq_opts(C.Structure):
     _fields_ = [("device", C.c_int32), ("max_qubits", C.c_int32), ("tile_qubits", C.c_int32), ("fuse", C.c_int32)]
 
@@ -115,6 +121,12 @@ SIGNATURES = {
     "nq_comm_unique_id": ([_ucp], C.c_int),
     "nq_sv_create_sharded": ([C.c_int, C.c_int, C.c_int, _ucp, C.POINTER(nq_opts), _pp], C.c_int),
     "nq_sv_comm_stats": ([_p, _i64p, _i64p], C.c_int),
+    "nq_profile_begin": ([C.c_int, C.c_int], C.c_int),
+    "nq_profile_end": ([C.c_int, C.POINTER(nq_profile)], C.c_int),
+    "nq_jit_wait": ([], C.c_int),
+    "nq_jit_stats": ([_i64p, _i64p, _i64p, _i64p], C.c_int),
+    "nq_jit_debug": ([C.c_int, _p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int64, _i64p,
+                      C.POINTER(C.c_int)], C.c_int),
     "nq_plan_debug": ([C.c_int, _p, C.c_int64, C.c_int, C.c_int, _ucp, C.c_int64, _i64p], C.c_int),
 }
 
@@ -414,6 +426,38 @@ def plan_debug(n: int, ops, tile_qubits: int = 0, fuse: bool = True) -> bytes:
     check(lib.nq_plan_debug(n, arr.ctypes.data, len(arr), tile_qubits, 1 if fuse else 0, buf, size.value,
                             C.byref(size)))
     return bytes(buf)[: size.value]
+
+
+def profile_begin(device: int = -1, per_pass_events: bool = True) -> None:
+    check(lib.nq_profile_begin(device, 1 if per_pass_events else 0))
+
+
+def profile_end(device: int = -1) -> dict:
+    p = nq_profile()
+    check(lib.nq_profile_end(device, C.byref(p)))
+    return {k: getattr(p, k) for k, _ in nq_profile._fields_}
+
+
+def jit_wait() -> None:
+    check(lib.nq_jit_wait())
+
+
+def jit_stats() -> dict:
+    v = [C.c_int64() for _ in range(4)]
+    check(lib.nq_jit_stats(*[C.byref(x) for x in v]))
+    return dict(zip(("compiled", "failed", "misses", "launches"), (x.value for x in v)))
+
+
+def jit_debug(n: int, ops, pass_index: int, tile_qubits: int = 0, compile: bool = True):
+    arr = ops if isinstance(ops, np.ndarray) else make_ops(ops)
+    size = C.c_int64()
+    ok = C.c_int()
+    check(lib.nq_jit_debug(n, arr.ctypes.data, len(arr), tile_qubits, pass_index, 0, None, 0, C.byref(size),
+                           C.byref(ok)))
+    buf = C.create_string_buffer(size.value + 1 << 16)
+    check(lib.nq_jit_debug(n, arr.ctypes.data, len(arr), tile_qubits, pass_index, 1 if compile else 0, buf,
+                           len(buf), C.byref(size), C.byref(ok)))
+    return buf.raw[: size.value].decode(), ok.value
 
 
 def device_count() -> int:

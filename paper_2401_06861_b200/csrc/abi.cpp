@@ -8,6 +8,7 @@
 #include "../../include/naqs_b200.h"
 
 #include "engine.hpp"
+#include "jit.hpp"
 #include "kernels.hpp"
 #include "lower.hpp"
 #include "state.hpp"
@@ -76,6 +77,7 @@ void DeviceCtx::stage(const unsigned char* src, size_t bytes) {
         d_ops_cap = cap;
     }
     std::memcpy(h_stage, src, bytes);
+    h2d_bytes += int64_t(bytes);
     CUDA_TRY(cudaMemcpyAsync(d_ops, h_stage, bytes, cudaMemcpyHostToDevice, stream));
     CUDA_TRY(cudaEventRecord(stage_ev, stream));
     stage_pending = true;
@@ -155,15 +157,33 @@ void state_flush(State& s) {
     for (size_t i = 0; i < passes.size(); ++i) {
         PassHdr h;
         std::memcpy(&h, buf.data() + offs[i], sizeof(h));
-        launch_pass(s.d, c.d_ops + offs[i], h, 0, c.stream);
+        std::pair<cudaEvent_t, cudaEvent_t>* ev = c.prof_pass ? prof_slot(c) : nullptr;
+        if (ev) CUDA_TRY(cudaEventRecord(ev->first, c.stream));
+        const unsigned char* rec = buf.data() + offs[i];
+        if (!jit_launch(s.d, c.d_ops + offs[i], h, reinterpret_cast<const MOp*>(rec + h.op_off),
+                        reinterpret_cast<const cplx*>(rec + h.pool_off), 0, c.stream, s.dev))
+            launch_pass(s.d, c.d_ops + offs[i], h, 0, c.stream);
+        if (ev) CUDA_TRY(cudaEventRecord(ev->second, c.stream));
+        if (c.prof) c.prof_pass_bytes += 32.0 * double(s.count);
     }
     CUDA_TRY(cudaGetLastError());
 }
 
 double* result_slot(DeviceCtx& c, int i) { return c.d_scratch + i; }
 
+std::pair<cudaEvent_t, cudaEvent_t>* prof_slot(DeviceCtx& c) {
+    if (c.prof_used == c.prof_ev.size()) {
+        std::pair<cudaEvent_t, cudaEvent_t> p;
+        CUDA_TRY(cudaEventCreate(&p.first));
+        CUDA_TRY(cudaEventCreate(&p.second));
+        c.prof_ev.push_back(p);
+    }
+    return &c.prof_ev[c.prof_used++];
+}
+
 // Copy `count` doubles from device to the pinned small buffer and wait.
 void fetch(DeviceCtx& c, const double* dsrc, size_t count, double* host) {
+    c.d2h_bytes += int64_t(count * sizeof(double));
     CUDA_TRY(cudaMemcpyAsync(c.h_small, dsrc, count * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     CUDA_TRY(cudaStreamSynchronize(c.stream));
     std::memcpy(host, c.h_small, count * sizeof(double));
@@ -408,6 +428,7 @@ nq_status nq_sv_expectation_batch(nq_sv* h, const uint64_t* flip, const uint64_t
         }
         CUDA_TRY(cudaGetLastError());
         std::vector<double> host(size_t(launches) * tpl);
+        c.d2h_bytes += int64_t(host.size() * sizeof(double));
         if (!host.empty()) {
             CUDA_TRY(cudaMemcpyAsync(host.data(), results, host.size() * sizeof(double),
                                      cudaMemcpyDeviceToHost, c.stream));
@@ -497,6 +518,7 @@ nq_status nq_sv_get_amplitudes(nq_sv* h, uint64_t offset, uint64_t count, double
             throw NqError{NQ_ERR_CONTRACT, "amplitude range out of bounds"};
         DeviceCtx& c = ctx_for(s.dev);
         if (count == 0) return;
+        c.d2h_bytes += int64_t(count * sizeof(double2));
         CUDA_TRY(cudaMemcpyAsync(host_out, s.d + offset, count * sizeof(double2), cudaMemcpyDeviceToHost,
                                  c.stream));
         CUDA_TRY(cudaStreamSynchronize(c.stream));
@@ -855,6 +877,102 @@ nq_status nq_readout_apply_dist(const double* dist_in, int n, const double* p01,
         CUDA_TRY(cudaMemcpyAsync(dist_out, d, len * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
         CUDA_TRY(cudaFreeAsync(d, c.stream));
         CUDA_TRY(cudaStreamSynchronize(c.stream));
+    });
+}
+
+// ---- measurement ----------------------------------------------------------------------
+nq_status nq_profile_begin(int device, int per_pass_events) {
+    return guard([&] {
+        int dev = device;
+        if (dev < 0) CUDA_TRY(cudaGetDevice(&dev));
+        CUDA_TRY(cudaSetDevice(dev));
+        DeviceCtx& c = ctx_for(dev);
+        if (!c.prof_t0) {
+            CUDA_TRY(cudaEventCreate(&c.prof_t0));
+            CUDA_TRY(cudaEventCreate(&c.prof_t1));
+        }
+        c.prof = true;
+        c.prof_pass = per_pass_events != 0;
+        c.prof_used = 0;
+        c.prof_pass_bytes = 0.0;
+        c.h2d_bytes = c.d2h_bytes = 0;
+        c.prof_launch0 = g_kernel_launches.load();
+        CUDA_TRY(cudaEventRecord(c.prof_t0, c.stream));
+    });
+}
+
+nq_status nq_profile_end(int device, nq_profile* out) {
+    return guard([&] {
+        int dev = device;
+        if (dev < 0) CUDA_TRY(cudaGetDevice(&dev));
+        CUDA_TRY(cudaSetDevice(dev));
+        DeviceCtx& c = ctx_for(dev);
+        if (!c.prof) throw NqError{NQ_ERR_CONTRACT, "nq_profile_end without nq_profile_begin"};
+        CUDA_TRY(cudaEventRecord(c.prof_t1, c.stream));
+        CUDA_TRY(cudaEventSynchronize(c.prof_t1));
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, c.prof_t0, c.prof_t1));
+        nq_profile p{};
+        p.region_ms = ms;
+        double pass = 0.0;
+        for (size_t i = 0; i < c.prof_used; ++i) {
+            float m = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&m, c.prof_ev[i].first, c.prof_ev[i].second));
+            pass += m;
+        }
+        p.pass_ms = pass;
+        p.pass_launches = int64_t(c.prof_used);
+        p.pass_bytes = c.prof_pass_bytes;
+        p.kernel_launches = g_kernel_launches.load() - c.prof_launch0;
+        p.h2d_bytes = c.h2d_bytes;
+        p.d2h_bytes = c.d2h_bytes;
+        c.prof = c.prof_pass = false;
+        *out = p;
+    });
+}
+
+nq_status nq_jit_wait(void) {
+    return guard([&] { jit_wait(); });
+}
+
+nq_status nq_jit_stats(int64_t* compiled, int64_t* failed, int64_t* misses, int64_t* launches) {
+    return guard([&] {
+        const JitStats j = jit_stats();
+        if (compiled) *compiled = j.compiled;
+        if (failed) *failed = j.failed;
+        if (misses) *misses = j.misses;
+        if (launches) *launches = j.launches;
+    });
+}
+
+nq_status nq_jit_debug(int n, const nq_op* ops, int64_t count, int tile_qubits, int pass_index, int compile,
+                       char* src_out, int64_t cap, int64_t* size, int* compiled_ok) {
+    return guard([&] {
+        std::vector<EOp> q;
+        for (int64_t i = 0; i < count; ++i) {
+            check_op_shape(ops[i]);
+            if (ops[i].kind != NQ_BARRIER) check_range(ops[i].qubits, ops[i].nqubits, n);
+            lower_sv_op(ops[i], q);
+        }
+        PlanOptions p;
+        p.nbits = n;
+        p.nloc = n;
+        p.tile_bits = tile_qubits > 0 ? std::min(tile_qubits, kMaxTileBits) : 12;
+        configure_caps(p);
+        auto passes = plan_passes(q, p, nullptr);
+        if (pass_index < 0 || pass_index >= int(passes.size())) throw NqError{NQ_ERR_CONTRACT, "no such pass"};
+        std::vector<size_t> offs;
+        auto bytes = serialize_passes(passes, n, &offs);
+        const unsigned char* rec = bytes.data() + offs[size_t(pass_index)];
+        PassHdr h;
+        std::memcpy(&h, rec, sizeof(h));
+        std::string src = jit_source(h, reinterpret_cast<const MOp*>(rec + h.op_off),
+                                     reinterpret_cast<const cplx*>(rec + h.pool_off));
+        std::string log;
+        if (compiled_ok) *compiled_ok = compile ? int(jit_compile_only(src, &log)) : -1;
+        if (!log.empty()) src += "\n/* NVRTC LOG\n" + log + "\n*/\n";
+        *size = int64_t(src.size());
+        if (src_out && cap > 0) std::memcpy(src_out, src.data(), size_t(std::min<int64_t>(cap, *size)));
     });
 }
 

@@ -21,24 +21,29 @@ using cplx = std::complex<double>;
 constexpr int kMaxTileBits = 13;   // 2^13 * 16 B = 128 KiB of shared memory
 constexpr int kMaxStateBits = 48;
 constexpr int kMaxOpK = 4;         // dense micro-ops act on <= 4 tile bits
+constexpr int kMaxDiagK = 6;       // diagonal micro-ops act on <= 6 bits (64-entry table)
 
 // ---- device micro-ops ------------------------------------------------------
 enum MOpType : uint8_t {
     MOP_DENSE = 0,  // 2^k x 2^k complex matrix on tile bits pos[0..k)
-    MOP_DIAG = 1,   // 2^k diagonal; bit j from tile bit pos[j] or full-index bit gq[j]
+    MOP_DIAG = 1,   // 2^k diagonal; pos[j] >= 0: tile bit, else full-index bit -1-pos[j]
     MOP_XPERM = 2,  // X on tile bit pos[0], controlled by cmask_tile / cmask_glob
     MOP_SWAP = 3,   // swap tile bits pos[0], pos[1]
     MOP_DEPOL = 4,  // x[c,r] -> a x[c,r] + b d_{c,r} sum_l x[l,l] on k col + k row bits
+    MOP_LAYOUT = 5, // register layout: slot j <-> tile bit pos[j] (j < k)
 };
+// Encoding of register-slot ops (everything but DIAG and LAYOUT): pos[] holds
+// register SLOTS (0..3), not tile bits; matrices are permuted by the planner so
+// that local operator bit j is the j-th smallest slot (DEPOL: pos = slots of
+// [col bits..., row bits...]).  DIAG keeps tile bits / full-index bits.
 
 struct MOp {
     uint8_t type;
     uint8_t k;            // number of operator bits (DEPOL: 2 or 4)
-    int8_t pos[4];        // tile bit positions (DIAG: -1 = not in tile)
-    uint8_t gq[4];        // DIAG: full-index bit when pos[j] == -1
+    int8_t pos[8];        // tile bit positions (DIAG: negative = full-index bit)
     uint16_t pad0;
     uint32_t mat;         // offset into the pass's complex pool
-    uint32_t cmask_tile;  // controls on tile bits (XPERM / DENSE)
+    uint32_t cmask_tile;  // controls on tile bits (XPERM)
     uint64_t cmask_glob;  // controls on full-index bits outside the tile
 };
 static_assert(sizeof(MOp) == 32, "MOp layout");

@@ -1,0 +1,489 @@
+// Pass-specialised kernels, generated and compiled at run time (NVRTC).
+//
+// The interpreter kernel (pass_kernel.cu) decodes micro-ops at run time; its
+// per-op dispatch costs about as many instructions as the op itself.  A pass
+// record fully determines a straight-line program: tile bits, register
+// layouts, slots, controls and which diagonal entries are exactly 1 are all
+// compile-time here, so the generated kernel is pure loads, FP64 math,
+// register moves and relayouts.  Operator matrices stay in the pass's pool
+// (shared memory), so re-running the same circuit structure with new angles
+// (VQE, Trotter sweeps, repeated benchmark steps) reuses the compiled kernel.
+//
+// Compilation is asynchronous: the first time a structure is seen the
+// interpreter runs it while a worker thread compiles; later flushes use the
+// specialised kernel.  NQ_JIT=off|auto|sync selects the policy.
+#include "jit.hpp"
+
+#include "kernels.hpp"
+#include "state.hpp"
+
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+namespace nqe {
+
+namespace {
+
+const char* kPassOpsSrc =
+#include "pass_ops_src.inc"
+    ;
+
+struct Entry {
+    std::atomic<int> state{0};  // 0 pending, 1 ready, 2 failed
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t kern = nullptr;
+    int threads = 0;
+    size_t smem = 0;
+    std::map<int, int> occ;  // device -> blocks per SM
+    std::string log;
+};
+
+struct Jit {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::unordered_map<std::string, std::shared_ptr<Entry>> cache;
+    std::deque<std::pair<std::string, std::shared_ptr<Entry>>> queue;
+    int busy = 0;
+    std::thread worker;
+    bool started = false;
+    int device = 0;
+    JitStats stats;
+};
+
+Jit& jit() {
+    static Jit* j = new Jit();  // leaked on purpose: no teardown-order issues with the worker
+    return *j;
+}
+
+JitMode mode_from_env() {
+    const char* e = std::getenv("NQ_JIT");
+    if (!e) return JitMode::Auto;
+    const std::string s(e);
+    if (s == "off" || s == "0") return JitMode::Off;
+    if (s == "sync") return JitMode::Sync;
+    return JitMode::Auto;
+}
+
+// ---- code generation ----------------------------------------------------------
+std::string hex64(unsigned long long v) {
+    char b[32];
+    std::snprintf(b, sizeof b, "0x%llxull", v);
+    return b;
+}
+
+// deposit bits of `src` (low bits first) into the ascending positions `pos`,
+// as an expression built from runs of consecutive positions.
+std::string deposit_expr(const std::string& src, const std::vector<int>& pos, bool wide) {
+    std::ostringstream o;
+    const char* one = wide ? "1ull" : "1u";
+    bool first = true;
+    size_t k = 0;
+    while (k < pos.size()) {
+        size_t e = k;
+        while (e + 1 < pos.size() && pos[e + 1] == pos[e] + 1) ++e;
+        const size_t len = e - k + 1;
+        if (!first) o << " | ";
+        first = false;
+        o << "(((" << src << " >> " << k << ") & ((" << one << " << " << len << ") - " << one << ")) << " << pos[k]
+          << ")";
+        k = e + 1;
+    }
+    if (first) o << (wide ? "0ull" : "0u");
+    return o.str();
+}
+
+struct Layout {
+    int rp[4];
+    int r = 4;
+    std::vector<int> nonr;  // ascending tile bits that are thread bits
+    unsigned rconst(int l) const {
+        unsigned c = 0;
+        for (int j = 0; j < r; ++j)
+            if ((l >> j) & 1) c |= 1u << rp[j];
+        return c;
+    }
+};
+
+unsigned swz_host(unsigned e) { return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7u); }
+
+Layout layout_of(const MOp& op, int m) {
+    Layout L;
+    L.r = op.k;
+    unsigned rm = 0;
+    for (int j = 0; j < L.r; ++j) {
+        L.rp[j] = op.pos[j];
+        rm |= 1u << op.pos[j];
+    }
+    for (int b = 0; b < m; ++b)
+        if (!((rm >> b) & 1u)) L.nonr.push_back(b);
+    return L;
+}
+
+}  // namespace
+
+std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
+    const int m = h.m;
+    const int E = 16;
+    const int T = (1 << m) / E;
+    std::vector<int> q(h.q, h.q + m), rest(h.rest, h.rest + h.nrest);
+    std::ostringstream s;
+    s << "#include \"pass_ops.cuh\"\n"
+      << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << (T >= 256 ? 512 / T : 1) << ")\n"
+      << "nqjit(double2* __restrict__ st, const double2* __restrict__ gpool, unsigned long long rankbase,"
+         " long long ntiles) {\n"
+      << "  using namespace nq;\n"
+      << "  extern __shared__ __align__(16) unsigned char smem[];\n"
+      << "  double2* tile = reinterpret_cast<double2*>(smem);\n"
+      << "  double2* pool = tile + " << (1 << m) << ";\n"
+      << "  const unsigned tid = threadIdx.x;\n"
+      << "  for (unsigned i = tid; i < " << h.pool_n << "u; i += " << T << "u) pool[i] = gpool[i];\n"
+      << "  __syncthreads();\n";
+    // layouts
+    std::vector<Layout> lays;
+    std::vector<int> lay_of_op(size_t(h.nops), 0);
+    for (int i = 0; i < h.nops; ++i) {
+        if (ops[i].type == MOP_LAYOUT) lays.push_back(layout_of(ops[i], m));
+        lay_of_op[size_t(i)] = int(lays.size()) - 1;
+    }
+    for (size_t k = 0; k < lays.size(); ++k) {
+        s << "  const unsigned tb" << k << " = " << deposit_expr("tid", lays[k].nonr, false) << ";\n";
+        s << "  const unsigned sw" << k << " = swz(tb" << k << ");\n";
+    }
+    auto state_off = [&](const std::string& tbname, const Layout& L) {
+        // state offset of the thread part: tile bit b -> state bit q[b]
+        std::ostringstream o;
+        bool first = true;
+        for (int b : L.nonr) {
+            if (!first) o << " | ";
+            first = false;
+            o << "((unsigned long long)((" << tbname << " >> " << b << ") & 1u) << " << q[size_t(b)] << ")";
+        }
+        if (first) o << "0ull";
+        return o.str();
+    };
+    auto reg_off = [&](const Layout& L, int l) {
+        unsigned long long c = 0;
+        for (int j = 0; j < L.r; ++j)
+            if ((l >> j) & 1) c |= 1ull << q[size_t(L.rp[j])];
+        return c;
+    };
+    const Layout& L0 = lays.front();
+    const Layout& LN = lays.back();
+    s << "  const unsigned long long toff_ld = " << state_off("tb0", L0) << ";\n";
+    s << "  const unsigned long long toff_st = " << state_off("tb" + std::to_string(lays.size() - 1), LN) << ";\n";
+    s << "  for (long long r = blockIdx.x; r < ntiles; r += gridDim.x) {\n"
+      << "    const unsigned long long base = " << deposit_expr("(unsigned long long)r", rest, true) << ";\n"
+      << "    const unsigned long long full = rankbase | base;\n"
+      << "    (void)full;\n"
+      << "    double2 a[16];\n"
+      << "    { const double2* src = st + base + toff_ld;\n";
+    for (int l = 0; l < E; ++l) s << "      a[" << l << "] = ld_stream(src + " << hex64(reg_off(L0, l)) << ");\n";
+    s << "    }\n";
+    bool any_relayout = false;
+    for (int i = 1; i < h.nops; ++i) {
+        const MOp& op = ops[i];
+        const int li = lay_of_op[size_t(i)];
+        const Layout& L = lays[size_t(li)];
+        const std::string tbn = "tb" + std::to_string(li);
+        const std::string P = "pool + " + std::to_string(op.mat);
+        switch (op.type) {
+        case MOP_LAYOUT: {
+            any_relayout = true;
+            const Layout& A = lays[size_t(li - 1)];
+            s << "    __syncthreads();\n";
+            for (int l = 0; l < E; ++l)
+                s << "    tile[sw" << (li - 1) << " ^ " << swz_host(A.rconst(l)) << "u] = a[" << l << "];\n";
+            s << "    __syncthreads();\n";
+            for (int l = 0; l < E; ++l)
+                s << "    a[" << l << "] = tile[sw" << li << " ^ " << swz_host(L.rconst(l)) << "u];\n";
+            break;
+        }
+        case MOP_DENSE:
+            if (op.k == 1) {
+                s << "    d1<16, " << int(op.pos[0]) << ">(a, " << P << ");\n";
+            } else if (op.k == 2) {
+                s << "    d2<16, " << int(op.pos[0]) << ", " << int(op.pos[1]) << ">(a, " << P << ");\n";
+            } else if (op.k == 3) {
+                s << "    d3<16, " << (6 - op.pos[0] - op.pos[1] - op.pos[2]) << ">(a, " << P << ");\n";
+            } else {
+                any_relayout = true;
+                s << "    __syncthreads();\n    d4<16>(a, " << P << ", tile + tid * 16u);\n";
+            }
+            break;
+        case MOP_SWAP:
+            s << "    swp<16, " << int(op.pos[0]) << ", " << int(op.pos[1]) << ">(a);\n";
+            break;
+        case MOP_DEPOL:
+            if (op.k == 2) {
+                const int a0 = std::min(op.pos[0], op.pos[1]), a1 = std::max(op.pos[0], op.pos[1]);
+                s << "    dep2<16, " << a0 << ", " << a1 << ">(a, lds(" << P << ").x, lds(" << P << " + 1).x);\n";
+            } else {
+                const int p0 = op.pos[0] == 0   ? op.pos[2]
+                               : op.pos[2] == 0 ? op.pos[0]
+                               : op.pos[1] == 0 ? op.pos[3]
+                                                : op.pos[1];
+                s << "    dep4<16, " << p0 << ">(a, lds(" << P << ").x, lds(" << P << " + 1).x);\n";
+            }
+            break;
+        case MOP_XPERM: {
+            unsigned cmL = 0, cmT = 0;
+            for (int p = 0; p < m; ++p) {
+                if (!((op.cmask_tile >> p) & 1u)) continue;
+                int slot = -1;
+                for (int j = 0; j < L.r; ++j)
+                    if (L.rp[j] == p) slot = j;
+                if (slot >= 0) cmL |= 1u << slot;
+                else cmT |= 1u << p;
+            }
+            s << "    if (((full & " << hex64(op.cmask_glob) << ") == " << hex64(op.cmask_glob) << ") && ((" << tbn
+              << " & " << cmT << "u) == " << cmT << "u)) xperm<16, " << int(op.pos[0]) << ">(a, " << cmL << "u);\n";
+            break;
+        }
+        case MOP_DIAG: {
+            // table index: register-slot bits (compile-time per l) | thread bits | global bits
+            std::ostringstream g;
+            g << "0u";
+            unsigned slotc[4] = {0, 0, 0, 0};
+            bool anyreg = false;
+            for (int j = 0; j < op.k; ++j) {
+                const int p = op.pos[j];
+                if (p < 0) {
+                    g << " | ((unsigned)((full >> " << (-1 - p) << ") & 1ull) << " << j << ")";
+                    continue;
+                }
+                int slot = -1;
+                for (int t = 0; t < L.r; ++t)
+                    if (L.rp[t] == p) slot = t;
+                if (slot >= 0) {
+                    slotc[slot] |= 1u << j;
+                    anyreg = true;
+                } else {
+                    g << " | (((" << tbn << " >> " << p << ") & 1u) << " << j << ")";
+                }
+            }
+            const cplx* tab = pool + op.mat;
+            s << "    { const unsigned g = " << g.str() << "; const double2* D = " << P << " + g;\n";
+            if (!anyreg) {
+                s << "      const double2 f = lds(D); if (!is_one(f)) {\n";
+                for (int l = 0; l < E; ++l) s << "      a[" << l << "] = cmul(f, a[" << l << "]);\n";
+                s << "      } }\n";
+            } else {
+                for (int l = 0; l < E; ++l) {
+                    unsigned c = 0;
+                    for (int t = 0; t < 4; ++t)
+                        if ((l >> t) & 1) c |= slotc[t];
+                    // entries that are exactly 1 for every thread/global choice are skipped
+                    bool all_one = true;
+                    for (int gi = 0; gi < (1 << op.k) && all_one; ++gi) {
+                        if ((unsigned(gi) & (slotc[0] | slotc[1] | slotc[2] | slotc[3])) != c) continue;
+                        all_one = tab[gi] == cplx(1.0, 0.0);
+                    }
+                    if (all_one) continue;
+                    s << "      a[" << l << "] = dmul(a[" << l << "], lds(D + " << c << "u));\n";
+                }
+                s << "    }\n";
+            }
+            break;
+        }
+        default:
+            break;
+        }
+    }
+    s << "    { double2* dst = st + base + toff_st;\n";
+    for (int l = 0; l < E; ++l) s << "      st_stream(dst + " << hex64(reg_off(LN, l)) << ", a[" << l << "]);\n";
+    s << "    }\n";
+    if (any_relayout) s << "    __syncthreads();\n";
+    s << "  }\n}\n";
+    return s.str();
+}
+
+namespace {
+
+bool compile_entry(const std::string& src, Entry& e, int device) {
+    nvrtcProgram prog;
+    const char* hdrs[1] = {kPassOpsSrc};
+    const char* names[1] = {"pass_ops.cuh"};
+    if (nvrtcCreateProgram(&prog, src.c_str(), "nqjit.cu", 1, hdrs, names) != NVRTC_SUCCESS) {
+        e.log = "nvrtcCreateProgram failed";
+        return false;
+    }
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "--extra-device-vectorization"};
+    const nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
+    size_t logn = 0;
+    nvrtcGetProgramLogSize(prog, &logn);
+    if (logn > 1) {
+        e.log.resize(logn);
+        nvrtcGetProgramLog(prog, &e.log[0]);
+    }
+    if (rc != NVRTC_SUCCESS) {
+        nvrtcDestroyProgram(&prog);
+        return false;
+    }
+    size_t n = 0;
+    nvrtcGetCUBINSize(prog, &n);
+    std::vector<char> cubin(n);
+    nvrtcGetCUBIN(prog, cubin.data());
+    nvrtcDestroyProgram(&prog);
+    cudaSetDevice(device);
+    if (cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess) {
+        e.log += " cudaLibraryLoadData failed";
+        cudaGetLastError();
+        return false;
+    }
+    if (cudaLibraryGetKernel(&e.kern, e.lib, "nqjit") != cudaSuccess) {
+        e.log += " cudaLibraryGetKernel failed";
+        cudaGetLastError();
+        return false;
+    }
+    return true;
+}
+
+void worker_loop() {
+    Jit& J = jit();
+    for (;;) {
+        std::pair<std::string, std::shared_ptr<Entry>> job;
+        {
+            std::unique_lock<std::mutex> lk(J.mu);
+            J.cv.wait(lk, [&] { return !J.queue.empty(); });
+            job = std::move(J.queue.front());
+            J.queue.pop_front();
+            ++J.busy;
+        }
+        const bool ok = compile_entry(job.first, *job.second, J.device);
+        job.second->state.store(ok ? 1 : 2);
+        {
+            std::lock_guard<std::mutex> lk(J.mu);
+            --J.busy;
+            if (ok) ++J.stats.compiled;
+            else ++J.stats.failed;
+        }
+        J.cv.notify_all();
+    }
+}
+
+}  // namespace
+
+JitMode jit_mode() {
+    static const JitMode m = mode_from_env();
+    return m;
+}
+
+bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,
+                uint64_t rankbase, cudaStream_t s, int device) {
+    const JitMode mode = jit_mode();
+    if (mode == JitMode::Off || h.m < 8 || h.m > 13) return false;
+    if (mode == JitMode::Auto && h.nloc < 18) return false;  // interpreter is fine for small states
+    std::string src = jit_source(h, ops, pool);
+    Jit& J = jit();
+    std::shared_ptr<Entry> e;
+    {
+        std::unique_lock<std::mutex> lk(J.mu);
+        auto it = J.cache.find(src);
+        if (it == J.cache.end()) {
+            e = std::make_shared<Entry>();
+            J.cache.emplace(src, e);
+            if (mode == JitMode::Sync) {
+                lk.unlock();
+                const bool ok = compile_entry(src, *e, device);
+                e->state.store(ok ? 1 : 2);
+                lk.lock();
+                if (ok) ++J.stats.compiled;
+                else ++J.stats.failed;
+            } else {
+                J.device = device;
+                if (!J.started) {
+                    // NVRTC compiles are independent: a small pool of workers
+                    const unsigned hw = std::thread::hardware_concurrency();
+                    const unsigned nw = std::max(1u, std::min(8u, hw / 2));
+                    for (unsigned w = 0; w < nw; ++w) std::thread(worker_loop).detach();
+                    J.started = true;
+                }
+                J.queue.emplace_back(src, e);
+                J.cv.notify_all();
+                ++J.stats.misses;
+                return false;
+            }
+        } else {
+            e = it->second;
+        }
+    }
+    if (e->state.load() != 1) {
+        ++J.stats.misses;
+        return false;
+    }
+    const int T = (1 << h.m) / 16;
+    const size_t smem = (size_t(1) << h.m) * 16 + size_t(h.pool_n) * 16;
+    int occ = 0;
+    {
+        std::lock_guard<std::mutex> lk(J.mu);
+        auto it = e->occ.find(device);
+        if (it == e->occ.end()) {
+            cudaFuncSetAttribute(reinterpret_cast<const void*>(e->kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(e->kern), T, smem);
+            if (occ < 1) occ = 1;
+            e->occ[device] = occ;
+        } else {
+            occ = it->second;
+        }
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const long long grid = std::min<long long>(h.ntiles, (long long)sms * occ);
+    const double2* gpool = reinterpret_cast<const double2*>(dev_rec + h.pool_off);
+    unsigned long long rb = rankbase;
+    long long nt = h.ntiles;
+    void* args[] = {&state, &gpool, &rb, &nt};
+    if (cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(unsigned(grid)), dim3(unsigned(T)), args, smem,
+                         s) != cudaSuccess) {
+        return false;
+    }
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+    ++J.stats.launches;
+    return true;
+}
+
+bool jit_compile_only(const std::string& src, std::string* log) {
+    nvrtcProgram prog;
+    const char* hdrs[1] = {kPassOpsSrc};
+    const char* names[1] = {"pass_ops.cuh"};
+    if (nvrtcCreateProgram(&prog, src.c_str(), "nqjit.cu", 1, hdrs, names) != NVRTC_SUCCESS) return false;
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17"};
+    const nvrtcResult rc = nvrtcCompileProgram(prog, 2, opts);
+    size_t logn = 0;
+    nvrtcGetProgramLogSize(prog, &logn);
+    if (log && logn > 1) {
+        log->resize(logn);
+        nvrtcGetProgramLog(prog, &(*log)[0]);
+    }
+    nvrtcDestroyProgram(&prog);
+    return rc == NVRTC_SUCCESS;
+}
+
+void jit_wait() {
+    Jit& J = jit();
+    std::unique_lock<std::mutex> lk(J.mu);
+    J.cv.wait(lk, [&] { return J.queue.empty() && J.busy == 0; });
+}
+
+JitStats jit_stats() {
+    Jit& J = jit();
+    std::lock_guard<std::mutex> lk(J.mu);
+    return J.stats;
+}
+
+}  // namespace nqe

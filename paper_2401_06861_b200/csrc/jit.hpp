@@ -1,0 +1,41 @@
+// Run-time specialised pass kernels (jit.cpp).
+#pragma once
+
+#include "engine.hpp"
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+
+namespace nqe {
+
+enum class JitMode { Off, Auto, Sync };
+
+struct JitStats {
+    int64_t compiled = 0;
+    int64_t failed = 0;
+    int64_t misses = 0;
+    int64_t launches = 0;
+};
+
+JitMode jit_mode();
+
+// CUDA source of the kernel specialised to one pass record.
+std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool);
+
+// Launch the specialised kernel for this pass if it is compiled (queueing the
+// compilation otherwise, or compiling inline under NQ_JIT=sync).  Returns
+// false when the caller must run the interpreter kernel instead.
+bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,
+                uint64_t rankbase, cudaStream_t s, int device);
+
+// NVRTC compile without loading (CPU-testable); false + log on failure.
+bool jit_compile_only(const std::string& src, std::string* log);
+
+// Block until every queued compilation has finished.
+void jit_wait();
+JitStats jit_stats();
+
+}  // namespace nqe

@@ -5,9 +5,13 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 namespace nqe {
+
+// Every kernel launched by this library (for the bench's gpu_launches claim).
+extern std::atomic<int64_t> g_kernel_launches;
 
 void launch_pass(double2* state, const unsigned char* dev_rec, const PassHdr& h, uint64_t rankbase,
                  cudaStream_t s);

@@ -1,0 +1,181 @@
+// Register-resident micro-op building blocks of the fused pass kernel.
+//
+// Shared by the interpreter kernel (pass_kernel.cu) and the pass-specialised
+// kernels generated at run time (jit.cpp compiles this header with NVRTC).
+// Self-contained: no includes, only CUDA built-ins.
+//
+// A thread holds E = 2^R amplitudes a[l]; bit j of l is register slot j.
+// Every operator takes its slots as template arguments, so amplitudes stay in
+// registers; operator matrices are read from shared memory at the point of use.
+#pragma once
+
+namespace nq {
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a*b + c
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
+    return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+__device__ __forceinline__ bool is_one(double2 f) { return f.x == 1.0 && f.y == 0.0; }
+
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_stream(double2* p, double2 v) {
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+// Shared-memory load the compiler may not hoist: matrices are re-read (one
+// broadcast LDS per entry) instead of occupying registers.
+__device__ __forceinline__ double2 lds(const double2* p) {
+    double2 v;
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+
+// Swizzle of the relayout buffer: conflict-free LDS/STS.128 when the three
+// lowest thread bits of a layout have distinct residues mod 3.
+__device__ __forceinline__ unsigned swz(unsigned e) { return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7u); }
+
+// a <- diag factor f, skipping exact ones (d0 = 1 diagonals touch half the amplitudes)
+__device__ __forceinline__ double2 dmul(double2 a, double2 f) { return is_one(f) ? a : cmul(f, a); }
+
+template <int E, int J>
+__device__ __forceinline__ void d1(double2 (&a)[E], const double2* u) {
+    const double2 u00 = lds(u), u01 = lds(u + 1), u10 = lds(u + 2), u11 = lds(u + 3);
+#pragma unroll
+    for (int l = 0; l < E; ++l) {
+        if ((l >> J) & 1) continue;
+        const int h = l | (1 << J);
+        const double2 x0 = a[l], x1 = a[h];
+        a[l] = cfma(u00, x0, cmul(u01, x1));
+        a[h] = cfma(u10, x0, cmul(u11, x1));
+    }
+}
+
+template <int E, int J0, int J1>
+__device__ __forceinline__ void d2(double2 (&a)[E], const double2* u) {
+#pragma unroll
+    for (int l = 0; l < E; ++l) {
+        if (((l >> J0) & 1) || ((l >> J1) & 1)) continue;
+        const int i0 = l, i1 = l | (1 << J0), i2 = l | (1 << J1), i3 = l | (1 << J0) | (1 << J1);
+        const double2 x0 = a[i0], x1 = a[i1], x2 = a[i2], x3 = a[i3];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            double2 acc = cmul(lds(u + 4 * r), x0);
+            acc = cfma(lds(u + 4 * r + 1), x1, acc);
+            acc = cfma(lds(u + 4 * r + 2), x2, acc);
+            acc = cfma(lds(u + 4 * r + 3), x3, acc);
+            a[r == 0 ? i0 : r == 1 ? i1 : r == 2 ? i2 : i3] = acc;
+        }
+    }
+}
+
+// k = 3 on all slots except `Skip` (local bit order = ascending slots).
+template <int E, int Skip>
+__device__ __forceinline__ void d3(double2 (&a)[E], const double2* u) {
+    constexpr int J0 = Skip == 0 ? 1 : 0;
+    constexpr int J1 = Skip <= 1 ? 2 : 1;
+    constexpr int J2 = Skip <= 2 ? 3 : 2;
+#pragma unroll
+    for (int l = 0; l < E; ++l) {
+        if ((l >> J0) & 1 || (l >> J1) & 1 || (l >> J2) & 1) continue;
+        double2 x[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) x[c] = a[l | ((c & 1) << J0) | (((c >> 1) & 1) << J1) | (((c >> 2) & 1) << J2)];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            double2 acc = cmul(lds(u + 8 * r), x[0]);
+#pragma unroll
+            for (int c = 1; c < 8; ++c) acc = cfma(lds(u + 8 * r + c), x[c], acc);
+            a[l | ((r & 1) << J0) | (((r >> 1) & 1) << J1) | (((r >> 2) & 1) << J2)] = acc;
+        }
+    }
+}
+
+// k = 4 on all slots: inputs parked in this thread's private scratch row.
+template <int E>
+__device__ __forceinline__ void d4(double2 (&a)[E], const double2* u, double2* scratch) {
+    if constexpr (E == 16) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) scratch[c] = a[c];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            double2 acc = cmul(lds(u + 16 * r), lds(scratch));
+#pragma unroll
+            for (int c = 1; c < 16; ++c) acc = cfma(lds(u + 16 * r + c), lds(scratch + c), acc);
+            a[r] = acc;
+        }
+    }
+}
+
+// X on slot J for the amplitudes whose register-slot controls CML are set.
+template <int E, int J>
+__device__ __forceinline__ void xperm(double2 (&a)[E], unsigned cmL) {
+#pragma unroll
+    for (int l = 0; l < E; ++l) {
+        if ((l >> J) & 1) continue;
+        if ((unsigned(l) & cmL) == cmL) {
+            const double2 t = a[l];
+            a[l] = a[l | (1 << J)];
+            a[l | (1 << J)] = t;
+        }
+    }
+}
+
+template <int E, int J0, int J1>
+__device__ __forceinline__ void swp(double2 (&a)[E]) {
+#pragma unroll
+    for (int l = 0; l < E; ++l) {
+        if (((l >> J0) & 1) && !((l >> J1) & 1)) {
+            const int o = (l & ~(1 << J0)) | (1 << J1);
+            const double2 t = a[l];
+            a[l] = a[o];
+            a[o] = t;
+        }
+    }
+}
+
+// 1-qubit depolarizing in Liouville form on slots {J0, J1} (column, row bit).
+template <int E, int J0, int J1>
+__device__ __forceinline__ void dep2(double2 (&a)[E], double al, double be) {
+#pragma unroll
+    for (int l = 0; l < E; ++l) {
+        if (((l >> J0) & 1) || ((l >> J1) & 1)) continue;
+        const int d = l | (1 << J0) | (1 << J1);
+        const double tr = a[l].x + a[d].x, ti = a[l].y + a[d].y;
+        a[l] = make_double2(fma(al, a[l].x, be * tr), fma(al, a[l].y, be * ti));
+        a[d] = make_double2(fma(al, a[d].x, be * tr), fma(al, a[d].y, be * ti));
+        a[l | (1 << J0)] = make_double2(al * a[l | (1 << J0)].x, al * a[l | (1 << J0)].y);
+        a[l | (1 << J1)] = make_double2(al * a[l | (1 << J1)].x, al * a[l | (1 << J1)].y);
+    }
+}
+
+// 2-qubit depolarizing on all 4 slots; slot 0 is paired with slot P (1..3).
+template <int E, int P>
+__device__ __forceinline__ void dep4(double2 (&a)[E], double al, double be) {
+    if constexpr (E == 16) {
+        constexpr int Q0 = P == 1 ? 2 : 1;
+        constexpr int Q1 = P == 3 ? 2 : 3;
+        double tr = 0.0, ti = 0.0;
+#pragma unroll
+        for (int l = 0; l < 16; ++l) {
+            if ((((l >> 0) & 1) == ((l >> P) & 1)) && (((l >> Q0) & 1) == ((l >> Q1) & 1))) {
+                tr += a[l].x;
+                ti += a[l].y;
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < 16; ++l) {
+            const bool dg = (((l >> 0) & 1) == ((l >> P) & 1)) && (((l >> Q0) & 1) == ((l >> Q1) & 1));
+            a[l] = dg ? make_double2(fma(al, a[l].x, be * tr), fma(al, a[l].y, be * ti))
+                      : make_double2(al * a[l].x, al * a[l].y);
+        }
+    }
+}
+
+}  // namespace nq

@@ -8,11 +8,20 @@
 //     pass's m-bit tile set Q and none of the bits it touches is "blocked" by an
 //     earlier deferred op.  Deferred ops block every bit they touch, so an op
 //     is only ever moved ahead of ops it is disjoint from (they commute).
-//  2. Micro-op fusion inside a pass.  Runs of dense/diagonal operators on the
-//     same bits are multiplied into one pending operator per bit group;
-//     diagonal operators may merge into one diagonal on up to 4 bits;
-//     permutations (X/CX/CCX/SWAP) and depolarizing maps flush the groups
-//     they touch and are emitted as cheap dedicated micro-ops.
+//  2. Micro-op fusion inside a pass (PassBuilder):
+//     - runs of dense/diagonal operators on the same bits are multiplied into
+//       one pending operator per bit group; diagonal groups merge up to
+//       kMaxDiagK bits;
+//     - diagonal groups commute with X/CX/CCX on their control bits, so they
+//       are not flushed by a permutation that only uses them as controls;
+//     - a permutation P = X_t (controlled by C) that meets the same P again with
+//       only diagonal work on t in between cancels: P D P = D o P is diagonal,
+//       so CX.RZ.CX (ZZ rotations of TFIM/QAOA) and the CX.U1.CX halves of the
+//       QFT's controlled phases become pure diagonals;
+//     - other permutations, SWAP and depolarizing maps are emitted as cheap
+//       dedicated micro-ops.
+//  Micro-ops are kept in state-bit form and mapped to tile positions when the
+//  pass is closed, so the pass caps apply to the fused (post-fusion) program.
 #include "engine.hpp"
 
 #include <algorithm>
@@ -23,9 +32,11 @@ namespace nqe {
 
 namespace {
 
+uint64_t bit(int b) { return uint64_t(1) << b; }
+
 uint64_t bitmask_of(const EOp& op, bool with_ctrl) {
     uint64_t m = 0;
-    for (int j = 0; j < op.k; ++j) m |= uint64_t(1) << op.bits[j];
+    for (int j = 0; j < op.k; ++j) m |= bit(op.bits[j]);
     if (with_ctrl) m |= op.ctrl;
     return m;
 }
@@ -38,7 +49,7 @@ uint64_t need_mask(const EOp& op) {
     case E_SWAP:
         return bitmask_of(op, false);
     case E_XPERM:
-        return uint64_t(1) << op.bits[0];
+        return bit(op.bits[0]);
     default:
         return 0;  // diagonal and no-op need no tile bits
     }
@@ -55,32 +66,33 @@ int pool_cost(const EOp& op) {
 
 int popcount64(uint64_t x) { return __builtin_popcountll(x); }
 
-// A pending (not yet emitted) fused operator on a small bit group.
-struct Pending {
+// A fused operator on a small bit group (pending or emitted).
+struct Group {
     int k = 0;
-    int bits[4];
+    int bits[kMaxDiagK];
     bool diag = true;
     std::vector<cplx> m;  // diag: 2^k; dense: 4^k row-major
     uint64_t mask() const {
         uint64_t r = 0;
-        for (int j = 0; j < k; ++j) r |= uint64_t(1) << bits[j];
+        for (int j = 0; j < k; ++j) r |= bit(bits[j]);
         return r;
+    }
+    int index_of(int b) const {
+        for (int t = 0; t < k; ++t)
+            if (bits[t] == b) return t;
+        return -1;
     }
 };
 
-// Local index (in group g's bit order) -> local index of `op` restricted to op's bits.
-int sub_index(int gi, const Pending& g, const EOp& op) {
+// Local index of `sub` (its bit order) from a local index of `g`.
+int sub_index(int gi, const Group& g, const int* sbits, int sk) {
     int oi = 0;
-    for (int j = 0; j < op.k; ++j) {
-        int pos = -1;
-        for (int t = 0; t < g.k; ++t)
-            if (g.bits[t] == op.bits[j]) pos = t;
-        if ((gi >> pos) & 1) oi |= 1 << j;
-    }
+    for (int j = 0; j < sk; ++j)
+        if ((gi >> g.index_of(sbits[j])) & 1) oi |= 1 << j;
     return oi;
 }
 
-void to_dense(Pending& g) {
+void to_dense(Group& g) {
     if (!g.diag) return;
     const int d = 1 << g.k;
     std::vector<cplx> m(size_t(d) * d, cplx(0.0, 0.0));
@@ -90,32 +102,29 @@ void to_dense(Pending& g) {
 }
 
 // g <- op * g, op's bits a subset of g's bits.
-void absorb(Pending& g, const EOp& op) {
+void absorb(Group& g, const int* obits, int ok, bool odiag, const std::vector<cplx>& om) {
     const int d = 1 << g.k;
-    if (op.type == E_DIAG) {
-        if (g.diag) {
-            for (int i = 0; i < d; ++i) g.m[size_t(i)] *= op.mat[size_t(sub_index(i, g, op))];
-        } else {
-            for (int i = 0; i < d; ++i) {
-                const cplx f = op.mat[size_t(sub_index(i, g, op))];
+    if (odiag) {
+        for (int i = 0; i < d; ++i) {
+            const cplx f = om[size_t(sub_index(i, g, obits, ok))];
+            if (g.diag) {
+                g.m[size_t(i)] *= f;
+            } else {
                 for (int c = 0; c < d; ++c) g.m[size_t(i) * d + c] *= f;
             }
         }
         return;
     }
-    // dense op
     to_dense(g);
-    const int od = 1 << op.k;
-    uint64_t opmask_local = 0;  // op bits in g-local positions
-    for (int j = 0; j < op.k; ++j)
-        for (int t = 0; t < g.k; ++t)
-            if (g.bits[t] == op.bits[j]) opmask_local |= uint64_t(1) << t;
+    const int od = 1 << ok;
+    uint64_t local = 0;
+    for (int j = 0; j < ok; ++j) local |= bit(g.index_of(obits[j]));
     std::vector<cplx> out(size_t(d) * d, cplx(0.0, 0.0));
     for (int i = 0; i < d; ++i) {
-        const int oi = sub_index(i, g, op);
+        const int oi = sub_index(i, g, obits, ok);
         for (int ip = 0; ip < d; ++ip) {
-            if ((uint64_t(i) & ~opmask_local) != (uint64_t(ip) & ~opmask_local)) continue;
-            const cplx e = op.mat[size_t(oi) * od + size_t(sub_index(ip, g, op))];
+            if ((uint64_t(i) & ~local) != (uint64_t(ip) & ~local)) continue;
+            const cplx e = om[size_t(oi) * od + size_t(sub_index(ip, g, obits, ok))];
             if (e == cplx(0.0, 0.0)) continue;
             for (int c = 0; c < d; ++c) out[size_t(i) * d + c] += e * g.m[size_t(ip) * d + c];
         }
@@ -123,8 +132,8 @@ void absorb(Pending& g, const EOp& op) {
     g.m = std::move(out);
 }
 
-Pending pending_from(const EOp& op) {
-    Pending g;
+Group group_from(const EOp& op) {
+    Group g;
     g.k = op.k;
     for (int j = 0; j < op.k; ++j) g.bits[j] = op.bits[j];
     g.diag = (op.type == E_DIAG);
@@ -132,113 +141,255 @@ Pending pending_from(const EOp& op) {
     return g;
 }
 
-// Merge diagonal groups (all diagonal) and a diagonal op into one group.
-Pending merge_diag(const std::vector<Pending*>& groups, const EOp& op) {
-    Pending out;
-    out.k = 0;
-    auto add_bit = [&](int b) {
-        for (int t = 0; t < out.k; ++t)
-            if (out.bits[t] == b) return;
-        out.bits[out.k++] = b;
-    };
-    for (auto* g : groups)
-        for (int j = 0; j < g->k; ++j) add_bit(g->bits[j]);
-    for (int j = 0; j < op.k; ++j) add_bit(op.bits[j]);
-    const int d = 1 << out.k;
-    out.diag = true;
-    out.m.assign(size_t(d), cplx(1.0, 0.0));
-    for (auto* g : groups) {
-        EOp as_op;
-        as_op.type = E_DIAG;
-        as_op.k = g->k;
-        for (int j = 0; j < g->k; ++j) as_op.bits[j] = g->bits[j];
-        as_op.mat = g->m;
-        absorb(out, as_op);
-    }
-    absorb(out, op);
-    return out;
+Group diag_identity_on(uint64_t mask) {
+    Group g;
+    g.k = 0;
+    for (int b = 0; b < 64; ++b)
+        if ((mask >> b) & 1) g.bits[g.k++] = b;
+    g.diag = true;
+    g.m.assign(size_t(1) << g.k, cplx(1.0, 0.0));
+    return g;
 }
 
-bool is_identity_diag(const Pending& g) {
+bool is_identity_diag(const Group& g) {
     for (const auto& v : g.m)
         if (v != cplx(1.0, 0.0)) return false;
     return true;
 }
 
+// D o P for P = X on bit t controlled by `ctrl`, D diagonal: entry for basis
+// state x is D(P x).  Result lives on D's bits plus the controls.
+Group conjugate_diag(const Group& D, int t, uint64_t ctrl) {
+    Group out = diag_identity_on(D.mask() | ctrl);
+    const int d = 1 << out.k;
+    const int tj = out.index_of(t);
+    uint64_t cl = 0;
+    for (int j = 0; j < out.k; ++j)
+        if ((ctrl >> out.bits[j]) & 1) cl |= bit(j);
+    for (int i = 0; i < d; ++i) {
+        int x = i;
+        if ((uint64_t(i) & cl) == cl) x ^= 1 << tj;
+        out.m[size_t(i)] = D.m[size_t(sub_index(x, out, D.bits, D.k))];
+    }
+    return out;
+}
+
+// A micro-op in state-bit form.
+struct BitOp {
+    MOpType type;
+    int k = 0;
+    int bits[kMaxDiagK];
+    uint64_t ctrl = 0;
+    std::vector<cplx> m;
+    bool alive = true;
+    uint64_t touch() const {
+        uint64_t r = ctrl;
+        for (int j = 0; j < k; ++j) r |= bit(bits[j]);
+        return r;
+    }
+};
+
 class PassBuilder {
   public:
-    PassBuilder(const std::vector<int>& q, int nloc) : q_(q) {
-        std::fill(std::begin(tpos_), std::end(tpos_), -1);
-        for (size_t i = 0; i < q.size(); ++i) tpos_[q[i]] = int(i);
-        (void)nloc;
+    explicit PassBuilder(bool fuse) : fuse_(fuse) {}
+
+    size_t microops() const { return live_ + pend_.size(); }
+    size_t pool() const {
+        size_t p = pool_;
+        for (const auto& g : pend_) p += g.m.size();
+        return p;
     }
 
-    void emit_pending(const Pending& g) {
-        if (g.diag && is_identity_diag(g)) return;
-        MOp op{};
-        op.k = uint8_t(g.k);
-        op.mat = uint32_t(pass_.pool.size());
-        if (g.diag) {
-            op.type = MOP_DIAG;
-            for (int j = 0; j < g.k; ++j) {
-                op.pos[j] = int8_t(tpos_[g.bits[j]]);
-                op.gq[j] = uint8_t(g.bits[j]);
-            }
-        } else {
-            op.type = MOP_DENSE;
-            for (int j = 0; j < g.k; ++j) {
-                if (tpos_[g.bits[j]] < 0) throw std::logic_error("planner: dense bit outside tile");
-                op.pos[j] = int8_t(tpos_[g.bits[j]]);
-            }
+    void add(const EOp& e) {
+        if (e.type == E_NOP) return;
+        if (!fuse_) {
+            if (e.type == E_DENSE || e.type == E_DIAG)
+                emit_group(group_from(e));
+            else
+                emit_direct(e);
+            return;
         }
-        pass_.pool.insert(pass_.pool.end(), g.m.begin(), g.m.end());
-        pass_.ops.push_back(op);
+        switch (e.type) {
+        case E_DENSE:
+        case E_DIAG:
+            add_matrix(e);
+            return;
+        case E_XPERM:
+            add_xperm(e);
+            return;
+        default:
+            flush_overlapping(bitmask_of(e, true), false);
+            emit_direct(e);
+        }
+    }
+
+    // Close the pass: map state bits to tile bits, split the micro-op program
+    // into register-layout stages and encode register slots.
+    PlannedPass finish(const std::vector<int>& q) {
+        for (const auto& g : pend_) emit_group(g);
+        pend_.clear();
+        const int m = int(q.size());
+        const int rsz = std::min(4, m);
+        int tpos[kMaxStateBits];
+        std::fill(std::begin(tpos), std::end(tpos), -1);
+        for (size_t i = 0; i < q.size(); ++i) tpos[q[i]] = int(i);
+
+        std::vector<const BitOp*> live;
+        for (const auto& b : ops_)
+            if (b.alive) live.push_back(&b);
+        // tile bits that must be register-resident for each op
+        auto need = [&](const BitOp& b) -> uint32_t {
+            if (b.type == MOP_DIAG) return 0;
+            const int cnt = b.type == MOP_XPERM ? 1 : b.k;
+            uint32_t r = 0;
+            for (int j = 0; j < cnt; ++j) {
+                if (tpos[b.bits[j]] < 0) throw std::logic_error("planner: target bit outside tile");
+                r |= 1u << tpos[b.bits[j]];
+            }
+            return r;
+        };
+        // fill a register set up to rsz bits with the highest free tile bits
+        auto fill = [&](uint32_t r) {
+            for (int t = m - 1; t >= 0 && popcount64(r) < rsz; --t) r |= 1u << t;
+            return r;
+        };
+        std::vector<uint32_t> stage_of(live.size(), 0);
+        uint32_t cur = 0;
+        bool have = false;
+        for (size_t i = 0; i < live.size(); ++i) {
+            const uint32_t nd = need(*live[i]);
+            if (nd == 0 || (have && (nd & ~cur) == 0)) {
+                stage_of[i] = cur;
+                continue;
+            }
+            uint32_t r = nd;
+            for (size_t j = i + 1; j < live.size(); ++j) {
+                const uint32_t nj = need(*live[j]);
+                if (popcount64(r | nj) > rsz) break;
+                r |= nj;
+            }
+            cur = fill(r);
+            if (!have) {  // ops before the first register-bound op share its layout
+                for (size_t j = 0; j < i; ++j) stage_of[j] = cur;
+            }
+            have = true;
+            stage_of[i] = cur;
+        }
+        if (!have) {
+            cur = fill(0);
+            for (auto& s : stage_of) s = cur;
+        }
+
+        PlannedPass p;
+        p.q = q;
+        auto layout_op = [&](uint32_t r) {
+            MOp op{};
+            op.type = MOP_LAYOUT;
+            op.k = uint8_t(rsz);
+            int k = 0;
+            for (int t = 0; t < m; ++t)
+                if ((r >> t) & 1u) op.pos[k++] = int8_t(t);
+            return op;
+        };
+        uint32_t lay = stage_of.empty() ? fill(0) : stage_of[0];
+        p.ops.push_back(layout_op(lay));
+        for (size_t i = 0; i < live.size(); ++i) {
+            if (stage_of[i] != lay) {
+                lay = stage_of[i];
+                p.ops.push_back(layout_op(lay));
+            }
+            const BitOp& b = *live[i];
+            int slot_of_t[32];
+            {
+                int k = 0;
+                for (int t = 0; t < m; ++t) slot_of_t[t] = ((lay >> t) & 1u) ? k++ : -1;
+            }
+            MOp op{};
+            op.type = uint8_t(b.type);
+            op.k = uint8_t(b.k);
+            op.mat = uint32_t(p.pool.size());
+            for (int bb = 0; bb < 64; ++bb) {
+                if (!((b.ctrl >> bb) & 1)) continue;
+                if (bb < kMaxStateBits && tpos[bb] >= 0)
+                    op.cmask_tile |= uint32_t(1) << tpos[bb];
+                else
+                    op.cmask_glob |= bit(bb);
+            }
+            if (b.type == MOP_DIAG) {
+                for (int j = 0; j < b.k; ++j)
+                    op.pos[j] = int8_t(tpos[b.bits[j]] >= 0 ? tpos[b.bits[j]] : -1 - b.bits[j]);
+                p.pool.insert(p.pool.end(), b.m.begin(), b.m.end());
+            } else if (b.type == MOP_DENSE) {
+                // local bit i of the stored matrix = i-th smallest slot
+                int slots[4], order[4];
+                for (int j = 0; j < b.k; ++j) {
+                    slots[j] = slot_of_t[tpos[b.bits[j]]];
+                    order[j] = j;
+                }
+                std::sort(order, order + b.k, [&](int x, int y) { return slots[x] < slots[y]; });
+                for (int i2 = 0; i2 < b.k; ++i2) op.pos[i2] = int8_t(slots[order[i2]]);
+                const int d = 1 << b.k;
+                auto old_index = [&](int xn) {
+                    int xo = 0;
+                    for (int i2 = 0; i2 < b.k; ++i2)
+                        if ((xn >> i2) & 1) xo |= 1 << order[i2];
+                    return xo;
+                };
+                for (int r = 0; r < d; ++r)
+                    for (int c = 0; c < d; ++c) p.pool.push_back(b.m[size_t(old_index(r)) * d + size_t(old_index(c))]);
+            } else {
+                for (int j = 0; j < b.k; ++j) op.pos[j] = int8_t(slot_of_t[tpos[b.bits[j]]]);
+                if (b.type == MOP_SWAP && op.pos[0] > op.pos[1]) std::swap(op.pos[0], op.pos[1]);
+                p.pool.insert(p.pool.end(), b.m.begin(), b.m.end());
+            }
+            p.ops.push_back(op);
+        }
+        return p;
+    }
+
+  private:
+    void emit_group(const Group& g) {
+        if (g.diag && is_identity_diag(g)) return;
+        BitOp b;
+        b.type = g.diag ? MOP_DIAG : MOP_DENSE;
+        b.k = g.k;
+        for (int j = 0; j < g.k; ++j) b.bits[j] = g.bits[j];
+        b.m = g.m;
+        push(std::move(b));
     }
 
     void emit_direct(const EOp& e) {
-        MOp op{};
-        op.k = uint8_t(e.k);
-        op.mat = uint32_t(pass_.pool.size());
+        BitOp b;
+        b.k = e.k;
+        for (int j = 0; j < e.k; ++j) b.bits[j] = e.bits[j];
+        b.ctrl = e.ctrl;
         switch (e.type) {
-        case E_XPERM:
-            op.type = MOP_XPERM;
-            op.pos[0] = int8_t(tpos_[e.bits[0]]);
-            for (int b = 0; b < 64; ++b) {
-                if (!((e.ctrl >> b) & 1)) continue;
-                if (b < kMaxStateBits && tpos_[b] >= 0)
-                    op.cmask_tile |= uint32_t(1) << tpos_[b];
-                else
-                    op.cmask_glob |= uint64_t(1) << b;
-            }
-            break;
-        case E_SWAP:
-            op.type = MOP_SWAP;
-            op.pos[0] = int8_t(tpos_[e.bits[0]]);
-            op.pos[1] = int8_t(tpos_[e.bits[1]]);
-            break;
+        case E_XPERM: b.type = MOP_XPERM; break;
+        case E_SWAP: b.type = MOP_SWAP; break;
         case E_DEPOL:
-            op.type = MOP_DEPOL;
-            for (int j = 0; j < e.k; ++j) op.pos[j] = int8_t(tpos_[e.bits[j]]);
-            pass_.pool.push_back(e.mat[0]);
-            pass_.pool.push_back(e.mat[1]);
+            b.type = MOP_DEPOL;
+            b.m = e.mat;
             break;
-        case E_DENSE:
-        case E_DIAG:
-            emit_pending(pending_from(e));
-            return;
-        default:
-            return;
+        default: throw std::logic_error("planner: unexpected direct op");
         }
-        for (int j = 0; j < e.k && e.type != E_XPERM; ++j)
-            if (op.pos[j] < 0) throw std::logic_error("planner: target bit outside tile");
-        if (op.pos[0] < 0) throw std::logic_error("planner: target bit outside tile");
-        pass_.ops.push_back(op);
+        push(std::move(b));
     }
 
-    void flush_overlapping(uint64_t mask) {
+    void push(BitOp&& b) {
+        pool_ += b.m.size();
+        ++live_;
+        ops_.push_back(std::move(b));
+    }
+
+    // Emit pending groups overlapping `mask`; with keep_diag_ctrl, diagonal
+    // groups that only overlap control bits are kept (they commute).
+    void flush_overlapping(uint64_t mask, bool keep_diag_ctrl, uint64_t target = 0) {
         for (size_t i = 0; i < pend_.size();) {
-            if (pend_[i].mask() & mask) {
-                emit_pending(pend_[i]);
+            const Group& g = pend_[i];
+            const bool over = (g.mask() & mask) != 0;
+            const bool commutes = keep_diag_ctrl && g.diag && !(g.mask() & target);
+            if (over && !commutes) {
+                emit_group(g);
                 pend_.erase(pend_.begin() + long(i));
             } else {
                 ++i;
@@ -246,84 +397,201 @@ class PassBuilder {
         }
     }
 
-    void add(const EOp& e, bool fuse) {
-        if (e.type == E_NOP) return;
-        if (!fuse) {
-            emit_direct(e);
-            return;
-        }
-        const uint64_t touched = bitmask_of(e, true);
-        if ((e.type == E_DENSE || e.type == E_DIAG) && e.ctrl == 0) {
-            std::vector<size_t> over;
-            for (size_t i = 0; i < pend_.size(); ++i)
-                if (pend_[i].mask() & touched) over.push_back(i);
-            const uint64_t emask = bitmask_of(e, false);
-            if (over.size() == 1) {
-                Pending& g = pend_[over[0]];
-                const bool subset = (emask & ~g.mask()) == 0;
-                if (subset) {
-                    if (!g.diag || e.type == E_DIAG) {
-                        absorb(g, e);
-                        return;
-                    }
-                    if (g.k == e.k) {  // diag group on exactly these bits, dense op
-                        absorb(g, e);
-                        return;
-                    }
-                }
+    void add_matrix(const EOp& e) {
+        const uint64_t emask = bitmask_of(e, false);
+        std::vector<size_t> over;
+        for (size_t i = 0; i < pend_.size(); ++i)
+            if (pend_[i].mask() & emask) over.push_back(i);
+        const bool ediag = e.type == E_DIAG;
+        if (over.size() == 1) {
+            Group& g = pend_[over[0]];
+            if ((emask & ~g.mask()) == 0 && (!g.diag || ediag || g.k == e.k)) {
+                absorb(g, e.bits, e.k, ediag, e.mat);
+                return;
             }
-            if (e.type == E_DIAG && !over.empty()) {
-                bool all_diag = true;
-                uint64_t uni = emask;
-                for (size_t i : over) {
-                    all_diag = all_diag && pend_[i].diag;
-                    uni |= pend_[i].mask();
-                }
-                if (all_diag && popcount64(uni) <= kMaxOpK) {
-                    std::vector<Pending*> gs;
-                    for (size_t i : over) gs.push_back(&pend_[i]);
-                    Pending merged = merge_diag(gs, e);
-                    for (size_t j = over.size(); j-- > 0;) pend_.erase(pend_.begin() + long(over[j]));
-                    pend_.push_back(std::move(merged));
-                    return;
-                }
-            }
-            flush_overlapping(touched);
-            pend_.push_back(pending_from(e));
-            return;
         }
-        flush_overlapping(touched);
+        if (ediag && !over.empty()) {
+            bool all_diag = true;
+            uint64_t uni = emask;
+            for (size_t i : over) {
+                all_diag = all_diag && pend_[i].diag;
+                uni |= pend_[i].mask();
+            }
+            if (all_diag && popcount64(uni) <= kMaxDiagK) {
+                Group mg = diag_identity_on(uni);
+                for (size_t i : over) absorb(mg, pend_[i].bits, pend_[i].k, true, pend_[i].m);
+                absorb(mg, e.bits, e.k, true, e.mat);
+                for (size_t j = over.size(); j-- > 0;) pend_.erase(pend_.begin() + long(over[j]));
+                pend_.push_back(std::move(mg));
+                return;
+            }
+        }
+        flush_overlapping(emask, false);
+        pend_.push_back(group_from(e));
+    }
+
+    void add_xperm(const EOp& e) {
+        const int t = e.bits[0];
+        const uint64_t touched = bit(t) | e.ctrl;
+        if (try_cancel(t, e.ctrl)) return;
+        // diagonal groups on control bits commute with the permutation
+        flush_overlapping(touched, true, bit(t));
         emit_direct(e);
     }
 
-    PlannedPass finish() {
-        for (const auto& g : pend_) emit_pending(g);
-        pend_.clear();
-        pass_.q = q_;
-        return std::move(pass_);
+    // P .. (diagonal work on t) .. P  ->  conjugated diagonal, both P removed.
+    bool try_cancel(int t, uint64_t ctrl) {
+        const uint64_t touched = bit(t) | ctrl;
+        // most recent emitted op touching t or the controls must be the same P
+        long idx = -1;
+        for (long i = long(ops_.size()) - 1; i >= 0; --i) {
+            const BitOp& b = ops_[size_t(i)];
+            if (!b.alive || !(b.touch() & touched)) continue;
+            // diagonal micro-ops on control bits only commute with P
+            if (b.type == MOP_DIAG && !((b.touch() >> t) & 1)) continue;
+            if (b.type == MOP_XPERM && b.bits[0] == t && b.ctrl == ctrl) idx = i;
+            break;
+        }
+        if (idx < 0) return false;
+        // pending groups involving t must be diagonal; conjugate and merge them
+        std::vector<size_t> on_t;
+        uint64_t uni = 0;
+        for (size_t i = 0; i < pend_.size(); ++i) {
+            if (!((pend_[i].mask() >> t) & 1)) continue;
+            if (!pend_[i].diag) return false;
+            on_t.push_back(i);
+            uni |= pend_[i].mask();
+        }
+        if (!on_t.empty()) {
+            uni |= ctrl;
+            // conjugated groups now also touch the controls: merge with any
+            // pending diagonal groups there
+            std::vector<size_t> merge = on_t;
+            for (size_t i = 0; i < pend_.size(); ++i) {
+                if (std::find(on_t.begin(), on_t.end(), i) != on_t.end()) continue;
+                if (pend_[i].mask() & ctrl) {
+                    if (!pend_[i].diag) return false;
+                    merge.push_back(i);
+                    uni |= pend_[i].mask();
+                }
+            }
+            if (popcount64(uni) > kMaxDiagK) return false;
+            Group mg = diag_identity_on(uni);
+            for (size_t i : merge) {
+                Group gi = pend_[i];
+                if ((gi.mask() >> t) & 1) gi = conjugate_diag(gi, t, ctrl);
+                absorb(mg, gi.bits, gi.k, true, gi.m);
+            }
+            std::sort(merge.begin(), merge.end());
+            for (size_t j = merge.size(); j-- > 0;) pend_.erase(pend_.begin() + long(merge[j]));
+            pend_.push_back(std::move(mg));
+        }
+        ops_[size_t(idx)].alive = false;
+        --live_;
+        return true;
     }
 
-  private:
-    std::vector<int> q_;
-    int tpos_[kMaxStateBits];
-    std::vector<Pending> pend_;
-    PlannedPass pass_;
+    bool fuse_;
+    std::vector<BitOp> ops_;
+    std::vector<Group> pend_;
+    size_t live_ = 0, pool_ = 0;
 };
+
+// P1..Pa  D1..Db  P1..Pa  ->  D1'..Db'  for mutually commuting X-type
+// permutations P and diagonal D (D' = D o P1..Pa).  Catches CX.RZ.CX (TFIM /
+// QAOA ZZ rotations), the CX.U1.CX halves of controlled phases (QFT) and, in
+// Liouville space, the row+column copies of those sandwiches.
+bool perms_commute(const EOp& a, const EOp& b) {
+    return !((a.ctrl >> b.bits[0]) & 1) && !((b.ctrl >> a.bits[0]) & 1);
+}
+
+std::vector<EOp> cancel_perm_sandwiches(const std::vector<EOp>& in) {
+    std::vector<EOp> out;
+    out.reserve(in.size());
+    size_t i = 0;
+    while (i < in.size()) {
+        if (in[i].type != E_XPERM) {
+            out.push_back(in[i++]);
+            continue;
+        }
+        // leading run of commuting permutations
+        size_t a = i;
+        while (a < in.size() && in[a].type == E_XPERM && a - i < 4) {
+            bool ok = true;
+            for (size_t p = i; p < a; ++p) ok = ok && perms_commute(in[p], in[a]);
+            if (!ok) break;
+            ++a;
+        }
+        const size_t na = a - i;
+        size_t d = a;
+        while (d < in.size() && (in[d].type == E_DIAG || in[d].type == E_NOP)) ++d;
+        bool match = d > a && d + na <= in.size();
+        std::vector<bool> used(na, false);
+        for (size_t t = 0; match && t < na; ++t) {
+            const EOp& q = in[d + t];
+            bool found = false;
+            for (size_t p = 0; p < na && !found; ++p) {
+                if (used[p] || q.type != E_XPERM) continue;
+                if (q.bits[0] == in[i + p].bits[0] && q.ctrl == in[i + p].ctrl) {
+                    used[p] = true;
+                    found = true;
+                }
+            }
+            match = found;
+        }
+        std::vector<EOp> conj;
+        if (match) {
+            for (size_t t = a; t < d && match; ++t) {
+                if (in[t].type == E_NOP) {
+                    conj.push_back(in[t]);
+                    continue;
+                }
+                Group g = group_from(in[t]);
+                for (size_t p = i; p < a; ++p) {
+                    const int tb = in[p].bits[0];
+                    if (!((g.mask() >> tb) & 1)) continue;
+                    if (popcount64(g.mask() | in[p].ctrl) > kMaxDiagK) {
+                        match = false;
+                        break;
+                    }
+                    g = conjugate_diag(g, tb, in[p].ctrl);
+                }
+                EOp e;
+                e.type = E_DIAG;
+                e.k = g.k;
+                for (int j = 0; j < g.k; ++j) e.bits[j] = g.bits[j];
+                e.mat = g.m;
+                e.src = in[t].src;
+                conj.push_back(std::move(e));
+            }
+        }
+        if (!match) {
+            out.push_back(in[i++]);
+            continue;
+        }
+        int64_t src = 0;
+        for (size_t p = 0; p < na; ++p) src += in[i + p].src + in[d + p].src;
+        conj.front().src += src;
+        for (auto& e : conj) out.push_back(std::move(e));
+        i = d + na;
+    }
+    return out;
+}
 
 }  // namespace
 
-std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops, const PlanOptions& opt,
+std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanOptions& opt,
                                      PlanStats* stats) {
+    const std::vector<EOp> ops = opt.fuse ? cancel_perm_sandwiches(ops_in) : ops_in;
     const int nloc = opt.nloc;
     const int m = std::min(opt.tile_bits, nloc);
     // A state no larger than one tile is processed whole: every bit is "low".
     // Otherwise keep >= low_bits contiguous low bits for coalescing, but always
     // leave room for one 4-bit operator among the high tile bits.
     const int lb = (nloc <= opt.tile_bits) ? m : std::max(0, std::min(opt.low_bits, m - kMaxOpK));
-    const uint64_t low_mask = (lb >= 64) ? ~uint64_t(0) : ((uint64_t(1) << lb) - 1);
-    const uint64_t all_mask =
-        (opt.nbits >= 64) ? ~uint64_t(0) : ((uint64_t(1) << opt.nbits) - 1);
-    const uint64_t loc_mask = (nloc >= 64) ? ~uint64_t(0) : ((uint64_t(1) << nloc) - 1);
+    const uint64_t low_mask = (lb >= 64) ? ~uint64_t(0) : (bit(lb) - 1);
+    const uint64_t all_mask = (opt.nbits >= 64) ? ~uint64_t(0) : (bit(opt.nbits) - 1);
+    const uint64_t loc_mask = (nloc >= 64) ? ~uint64_t(0) : (bit(nloc) - 1);
 
     std::vector<PlannedPass> passes;
     int64_t src_total = 0;
@@ -339,8 +607,9 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops, const PlanOpti
     while (!remaining.empty()) {
         uint64_t qhigh = 0;  // required tile bits >= lb
         uint64_t blocked = 0;
-        int nops = 0, pool = 0;
-        std::vector<const EOp*> in_pass, deferred;
+        PassBuilder pb(opt.fuse);
+        std::vector<const EOp*> deferred;
+        size_t taken = 0;
         size_t i = 0;
         for (; i < remaining.size(); ++i) {
             const EOp* e = remaining[i];
@@ -356,14 +625,13 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops, const PlanOpti
             }
             const uint64_t nh = qhigh | (need_mask(*e) & ~low_mask);
             const bool fits = popcount64(nh) <= m - lb;
-            const bool caps = (nops + 1 <= opt.max_ops_per_pass) &&
-                              (pool + pool_cost(*e) <= opt.max_pool_per_pass);
-            if (!caps) break;  // close the pass here; the rest goes to the next pass
+            const bool caps = (pb.microops() + 1 <= size_t(opt.max_ops_per_pass)) &&
+                              (pb.pool() + size_t(pool_cost(*e)) <= size_t(opt.max_pool_per_pass));
+            if (!caps && taken > 0) break;  // close the pass; the rest goes to the next one
             if (fits) {
                 qhigh = nh;
-                in_pass.push_back(e);
-                ++nops;
-                pool += pool_cost(*e);
+                pb.add(*e);
+                ++taken;
             } else {
                 deferred.push_back(e);
                 blocked |= touched;
@@ -375,27 +643,22 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops, const PlanOpti
         }
         std::vector<const EOp*> next = deferred;
         next.insert(next.end(), remaining.begin() + long(i), remaining.end());
-        if (in_pass.empty()) {
-            if (next.size() == remaining.size() && !next.empty()) {
-                // A single op must always fit (k <= 4 <= m - lb is guaranteed by callers);
-                // take it alone to guarantee progress.
-                in_pass.push_back(next.front());
-                qhigh = need_mask(*next.front()) & ~low_mask;
-                next.erase(next.begin());
-            }
+        if (taken == 0 && !next.empty()) {
+            // every op needs <= kMaxOpK <= m - lb high bits, so the first one always
+            // fits alone; take it to guarantee progress
+            qhigh = need_mask(*next.front()) & ~low_mask;
+            pb.add(*next.front());
+            next.erase(next.begin());
         }
         // Tile bit set: low bits, required high bits, then fill upward.
         uint64_t qmask = low_mask | qhigh;
-        for (int b = 0; b < nloc && popcount64(qmask) < m; ++b) qmask |= uint64_t(1) << b;
+        for (int b = 0; b < nloc && popcount64(qmask) < m; ++b) qmask |= bit(b);
         std::vector<int> q;
         for (int b = 0; b < nloc; ++b)
             if ((qmask >> b) & 1) q.push_back(b);
         if (int(q.size()) != m) throw std::logic_error("planner: tile size mismatch");
-
-        PassBuilder pb(q, nloc);
-        for (const EOp* e : in_pass) pb.add(*e, opt.fuse);
-        PlannedPass p = pb.finish();
-        if (!p.ops.empty()) passes.push_back(std::move(p));
+        PlannedPass p = pb.finish(q);
+        if (p.ops.size() > 1) passes.push_back(std::move(p));  // ops[0] is the load layout
         remaining.swap(next);
     }
     if (stats) {
@@ -421,7 +684,7 @@ std::vector<unsigned char> serialize_passes(const std::vector<PlannedPass>& pass
         for (size_t i = 0; i < p.q.size(); ++i) h.q[i] = int8_t(p.q[i]);
         int nr = 0;
         uint64_t qm = 0;
-        for (int b : p.q) qm |= uint64_t(1) << b;
+        for (int b : p.q) qm |= bit(b);
         for (int b = 0; b < nloc; ++b)
             if (!((qm >> b) & 1)) h.rest[nr++] = int8_t(b);
         h.nrest = nr;

@@ -1,11 +1,5 @@
-// sm_100a kernels of the SV/DM simulation core.
-//
-//  pass_kernel<M>   one fused pass over the state: persistent
-//                   CTAs stage 2^M-amplitude tiles in shared memory with
-//                   streaming 16-byte loads, run the pass's micro-ops there,
-//                   and stream the tile back.  Replaces the per-gate sweeps
-//                   K1-K8 of proj/src/statevector.cpp:50-180 and the blockwise
-//                   Kraus sums K14 of proj/src/densitymatrix.cpp:60-110.
+// sm_100a kernels of the SV/DM simulation core, other than the fused pass
+// kernel (pass_kernel.cu):
 //  reductions       fixed-grid, fixed-order (bit-reproducible) sums:
 //                   norm/purity (K9/K15), Pauli expectations (K10/K16),
 //                   probabilities (K11/K17), Kraus weights (K13).
@@ -16,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -47,346 +42,6 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
 }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) {
     asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
-}
-
-// ---------------------------------------------------------------------------
-// micro-op application on the shared-memory tile
-// ---------------------------------------------------------------------------
-template <int M, int T>
-__device__ __forceinline__ void op_dense1(const MOp& op, double2* tile, const double2* pool, int tid) {
-    const int b = op.pos[0];
-    const uint32_t bit = 1u << b;
-    const double2 u00 = pool[op.mat], u01 = pool[op.mat + 1], u10 = pool[op.mat + 2],
-                  u11 = pool[op.mat + 3];
-    constexpr int HALF = 1 << (M - 1);
-#pragma unroll 4
-    for (int w = tid; w < HALF; w += T) {
-        const uint32_t e0 = ins0(uint32_t(w), b), e1 = e0 | bit;
-        const double2 a0 = tile[e0], a1 = tile[e1];
-        tile[e0] = cfma(u00, a0, cmul(u01, a1));
-        tile[e1] = cfma(u10, a0, cmul(u11, a1));
-    }
-}
-
-template <int M, int T>
-__device__ __forceinline__ void op_dense2(const MOp& op, double2* tile, const double2* pool, int tid) {
-    const int p0 = op.pos[0], p1 = op.pos[1];
-    const int lo = min(p0, p1), hi = max(p0, p1);
-    const uint32_t b0 = 1u << p0, b1 = 1u << p1;
-    double2 u[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) u[i] = pool[op.mat + i];
-    constexpr int Q4 = 1 << (M - 2);
-#pragma unroll 2
-    for (int w = tid; w < Q4; w += T) {
-        const uint32_t e = ins0(ins0(uint32_t(w), lo), hi);
-        const uint32_t idx[4] = {e, e | b0, e | b1, e | b0 | b1};
-        double2 v[4];
-#pragma unroll
-        for (int l = 0; l < 4; ++l) v[l] = tile[idx[l]];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            double2 acc = cmul(u[r * 4], v[0]);
-#pragma unroll
-            for (int c = 1; c < 4; ++c) acc = cfma(u[r * 4 + c], v[c], acc);
-            tile[idx[r]] = acc;
-        }
-    }
-}
-
-template <int M, int T, int K>
-__device__ __forceinline__ void op_denseK(const MOp& op, double2* tile, const double2* pool, int tid) {
-    constexpr int D = 1 << K;
-    int sp[K];
-    uint32_t offs[D];
-#pragma unroll
-    for (int j = 0; j < K; ++j) sp[j] = op.pos[j];
-    // sort positions ascending (K <= 4, tiny insertion sort)
-#pragma unroll
-    for (int i = 1; i < K; ++i)
-#pragma unroll
-        for (int j = i; j > 0; --j)
-            if (sp[j - 1] > sp[j]) {
-                const int t = sp[j - 1];
-                sp[j - 1] = sp[j];
-                sp[j] = t;
-            }
-#pragma unroll
-    for (int l = 0; l < D; ++l) {
-        uint32_t o = 0;
-#pragma unroll
-        for (int j = 0; j < K; ++j)
-            if ((l >> j) & 1) o |= 1u << op.pos[j];
-        offs[l] = o;
-    }
-    const double2* mat = pool + op.mat;
-    constexpr int G = 1 << (M - K);
-    for (int w = tid; w < G; w += T) {
-        uint32_t e = uint32_t(w);
-#pragma unroll
-        for (int j = 0; j < K; ++j) e = ins0(e, sp[j]);
-        double2 v[D];
-#pragma unroll
-        for (int l = 0; l < D; ++l) v[l] = tile[e | offs[l]];
-#pragma unroll 1
-        for (int r = 0; r < D; ++r) {
-            double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int c = 0; c < D; ++c) acc = cfma(mat[r * D + c], v[c], acc);
-            tile[e | offs[r]] = acc;
-        }
-    }
-}
-
-template <int M, int T>
-__device__ __forceinline__ void op_diag(const MOp& op, double2* tile, const double2* pool, int tid,
-                                        uint64_t full) {
-    const int k = op.k;
-    uint32_t gpart = 0;
-    int tpos[4];
-    int ntile = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        tpos[j] = -1;
-        if (j < k) {
-            if (op.pos[j] >= 0) {
-                tpos[j] = op.pos[j];
-                ++ntile;
-            } else {
-                gpart |= uint32_t((full >> op.gq[j]) & 1u) << j;
-            }
-        }
-    }
-    const double2* tab = pool + op.mat;
-    constexpr int SIZE = 1 << M;
-    if (ntile == 0) {
-        const double2 f = tab[gpart];
-        if (f.x == 1.0 && f.y == 0.0) return;
-#pragma unroll 4
-        for (int e = tid; e < SIZE; e += T) tile[e] = cmul(f, tile[e]);
-        return;
-    }
-    if (k == 1) {
-        const int b = tpos[0];
-        const double2 d0 = tab[0], d1 = tab[1];
-        if (d0.x == 1.0 && d0.y == 0.0) {
-            constexpr int HALF = SIZE / 2;
-#pragma unroll 4
-            for (int w = tid; w < HALF; w += T) {
-                const uint32_t e = ins0(uint32_t(w), b) | (1u << b);
-                tile[e] = cmul(d1, tile[e]);
-            }
-        } else {
-#pragma unroll 4
-            for (int e = tid; e < SIZE; e += T) tile[e] = cmul(((e >> b) & 1) ? d1 : d0, tile[e]);
-        }
-        return;
-    }
-#pragma unroll 4
-    for (int e = tid; e < SIZE; e += T) {
-        uint32_t idx = gpart;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (tpos[j] >= 0) idx |= uint32_t((e >> tpos[j]) & 1) << j;
-        const double2 f = tab[idx];
-        if (!(f.x == 1.0 && f.y == 0.0)) tile[e] = cmul(f, tile[e]);
-    }
-}
-
-template <int M, int T>
-__device__ __forceinline__ void op_xperm(const MOp& op, double2* tile, int tid, uint64_t full) {
-    if ((full & op.cmask_glob) != op.cmask_glob) return;
-    const int t = op.pos[0];
-    const uint32_t cm = op.cmask_tile;
-    // positions to insert: target + tile controls, ascending
-    int sp[4];
-    int ns = 0;
-    uint32_t all = cm | (1u << t);
-    for (int b = 0; b < M && ns < 4; ++b)
-        if ((all >> b) & 1) sp[ns++] = b;
-    const int work = (1 << M) >> ns;
-    const uint32_t tb = 1u << t;
-    for (int w = tid; w < work; w += T) {
-        uint32_t e = uint32_t(w);
-        for (int j = 0; j < ns; ++j) e = ins0(e, sp[j]);
-        e |= cm;
-        const double2 a = tile[e], b = tile[e | tb];
-        tile[e] = b;
-        tile[e | tb] = a;
-    }
-}
-
-template <int M, int T>
-__device__ __forceinline__ void op_swap(const MOp& op, double2* tile, int tid) {
-    const int p0 = op.pos[0], p1 = op.pos[1];
-    const int lo = min(p0, p1), hi = max(p0, p1);
-    const uint32_t b0 = 1u << p0, b1 = 1u << p1;
-    constexpr int Q4 = 1 << (M - 2);
-#pragma unroll 4
-    for (int w = tid; w < Q4; w += T) {
-        const uint32_t e = ins0(ins0(uint32_t(w), lo), hi);
-        const double2 a = tile[e | b0], b = tile[e | b1];
-        tile[e | b0] = b;
-        tile[e | b1] = a;
-    }
-}
-
-template <int M, int T>
-__device__ __forceinline__ void op_depol2(const MOp& op, double2* tile, const double2* pool, int tid) {
-    const double a = pool[op.mat].x, bcoef = pool[op.mat + 1].x;
-    {
-        const int pc = op.pos[0], pr = op.pos[1];
-        const int lo = min(pc, pr), hi = max(pc, pr);
-        const uint32_t bc = 1u << pc, br = 1u << pr;
-        constexpr int G = 1 << (M - 2);
-        for (int w = tid; w < G; w += T) {
-            const uint32_t e = ins0(ins0(uint32_t(w), lo), hi);
-            const double2 x0 = tile[e], x1 = tile[e | bc], x2 = tile[e | br], x3 = tile[e | bc | br];
-            const double tr_re = x0.x + x3.x, tr_im = x0.y + x3.y;
-            tile[e] = make_double2(fma(a, x0.x, bcoef * tr_re), fma(a, x0.y, bcoef * tr_im));
-            tile[e | bc] = make_double2(a * x1.x, a * x1.y);
-            tile[e | br] = make_double2(a * x2.x, a * x2.y);
-            tile[e | bc | br] = make_double2(fma(a, x3.x, bcoef * tr_re), fma(a, x3.y, bcoef * tr_im));
-        }
-    }
-}
-
-template <int M, int T>
-__device__ __forceinline__ void op_depol4(const MOp& op, double2* tile, const double2* pool, int tid) {
-    const double a = pool[op.mat].x, bcoef = pool[op.mat + 1].x;
-    // cols pos[0..2), rows pos[2..4); diagonal entries l = c + 4c
-    int sp[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) sp[j] = op.pos[j];
-#pragma unroll
-    for (int i = 1; i < 4; ++i)
-#pragma unroll
-        for (int j = i; j > 0; --j)
-            if (sp[j - 1] > sp[j]) {
-                const int t = sp[j - 1];
-                sp[j - 1] = sp[j];
-                sp[j] = t;
-            }
-    uint32_t offs[16];
-#pragma unroll
-    for (int l = 0; l < 16; ++l) {
-        uint32_t o = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if ((l >> j) & 1) o |= 1u << op.pos[j];
-        offs[l] = o;
-    }
-    constexpr int G = 1 << (M - 4);
-    for (int w = tid; w < G; w += T) {
-        uint32_t e = uint32_t(w);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) e = ins0(e, sp[j]);
-        double tr_re = 0.0, tr_im = 0.0;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const double2 x = tile[e | offs[c + 4 * c]];
-            tr_re += x.x;
-            tr_im += x.y;
-        }
-#pragma unroll
-        for (int l = 0; l < 16; ++l) {
-            const double2 x = tile[e | offs[l]];
-            const bool diag = (l & 3) == (l >> 2);
-            tile[e | offs[l]] = diag ? make_double2(fma(a, x.x, bcoef * tr_re), fma(a, x.y, bcoef * tr_im))
-                                     : make_double2(a * x.x, a * x.y);
-        }
-    }
-}
-
-__device__ __forceinline__ uint64_t deposit(uint64_t v, const int8_t* pos, int cnt) {
-    uint64_t r = 0;
-    for (int j = 0; j < cnt; ++j)
-        if ((v >> j) & 1) r |= uint64_t(1) << pos[j];
-    return r;
-}
-
-// ---------------------------------------------------------------------------
-// the fused pass kernel
-// ---------------------------------------------------------------------------
-template <int M>
-__global__ void __launch_bounds__((1 << M) < kThreads ? (1 << M) : kThreads)
-    pass_kernel(double2* __restrict__ st, const unsigned char* __restrict__ rec, uint64_t rankbase) {
-    constexpr int SIZE = 1 << M;
-    constexpr int T = SIZE < kThreads ? SIZE : kThreads;
-    constexpr int EPT = SIZE / T;
-    constexpr int BATCH = EPT < 16 ? EPT : 16;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int8_t s_q[16];
-    __shared__ int8_t s_rest[56];
-    __shared__ uint64_t s_offj[EPT];
-
-    const PassHdr* h = reinterpret_cast<const PassHdr*>(rec);
-    const int tid = threadIdx.x;
-    const int nops = h->nops;
-    const int pool_n = int(h->pool_n);
-    double2* tile = reinterpret_cast<double2*>(smem_raw);
-    double2* pool = tile + SIZE;
-    MOp* ops = reinterpret_cast<MOp*>(pool + pool_n);
-
-    const double2* gpool = reinterpret_cast<const double2*>(rec + h->pool_off);
-    for (int i = tid; i < pool_n; i += T) pool[i] = gpool[i];
-    const uint4* gops = reinterpret_cast<const uint4*>(rec + h->op_off);
-    uint4* sops = reinterpret_cast<uint4*>(ops);
-    for (int i = tid; i < nops * 2; i += T) sops[i] = gops[i];
-    if (tid < 16) s_q[tid] = h->q[tid];
-    if (tid < 56) s_rest[tid] = h->rest[tid];
-    __syncthreads();
-    for (int j = tid; j < EPT; j += T) s_offj[j] = deposit(uint64_t(j) * T, s_q, M);
-    const uint64_t off_tid = deposit(uint64_t(tid), s_q, M);
-    const int nrest = h->nrest;
-    const int64_t ntiles = h->ntiles;
-    __syncthreads();
-
-    for (int64_t r = blockIdx.x; r < ntiles; r += gridDim.x) {
-        const uint64_t base = deposit(uint64_t(r), s_rest, nrest);
-        const double2* src = st + base + off_tid;
-#pragma unroll
-        for (int j0 = 0; j0 < EPT; j0 += BATCH) {
-            double2 v[BATCH];
-#pragma unroll
-            for (int j = 0; j < BATCH; ++j) v[j] = ld_stream(src + s_offj[j0 + j]);
-#pragma unroll
-            for (int j = 0; j < BATCH; ++j) tile[tid + (j0 + j) * T] = v[j];
-        }
-        __syncthreads();
-        const uint64_t full = rankbase | base;
-        for (int o = 0; o < nops; ++o) {
-            const MOp op = ops[o];
-            switch (op.type) {
-            case MOP_DENSE:
-                if (op.k == 1) op_dense1<M, T>(op, tile, pool, tid);
-                else if (op.k == 2) { if constexpr (M >= 2) op_dense2<M, T>(op, tile, pool, tid); }
-                else if (op.k == 3) { if constexpr (M >= 3) op_denseK<M, T, 3>(op, tile, pool, tid); }
-                else { if constexpr (M >= 4) op_denseK<M, T, 4>(op, tile, pool, tid); }
-                break;
-            case MOP_DIAG:
-                op_diag<M, T>(op, tile, pool, tid, full);
-                break;
-            case MOP_XPERM:
-                op_xperm<M, T>(op, tile, tid, full);
-                break;
-            case MOP_SWAP:
-                if constexpr (M >= 2) op_swap<M, T>(op, tile, tid);
-                break;
-            case MOP_DEPOL:
-                if (op.k == 2) { if constexpr (M >= 2) op_depol2<M, T>(op, tile, pool, tid); }
-                else { if constexpr (M >= 4) op_depol4<M, T>(op, tile, pool, tid); }
-                break;
-            default:
-                break;
-            }
-            __syncthreads();
-        }
-        double2* dst = st + base + off_tid;
-#pragma unroll
-        for (int j = 0; j < EPT; ++j) st_stream(dst + s_offj[j], tile[tid + j * T]);
-        __syncthreads();
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -801,58 +456,13 @@ void reduction_geometry(uint64_t n, uint64_t* chunk, int* nblk) {
     if (*nblk < 1) *nblk = 1;
 }
 
-template <int M>
-void launch_pass_m(double2* state, const unsigned char* rec, const PassHdr& h, uint64_t rankbase,
-                   cudaStream_t s) {
-    constexpr int SIZE = 1 << M;
-    constexpr int T = SIZE < kThreads ? SIZE : kThreads;
-    const size_t smem = size_t(SIZE) * 16 + size_t(h.pool_n) * 16 + size_t(h.nops) * sizeof(MOp);
-    static std::mutex mu;
-    static std::map<std::pair<int, size_t>, int> occ_cache;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int occ = 0;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        auto key = std::make_pair(dev, smem);
-        auto it = occ_cache.find(key);
-        if (it == occ_cache.end()) {
-            cudaFuncSetAttribute(pass_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass_kernel<M>, T, smem);
-            if (occ < 1) occ = 1;
-            occ_cache[key] = occ;
-        } else {
-            occ = it->second;
-        }
-    }
-    const int64_t grid = std::min<int64_t>(h.ntiles, int64_t(dev_info().sms) * occ);
-    pass_kernel<M><<<unsigned(grid), T, smem, s>>>(state, rec, rankbase);
-}
-
 }  // namespace
 
-void launch_pass(double2* state, const unsigned char* dev_rec, const PassHdr& h, uint64_t rankbase,
-                 cudaStream_t s) {
-    switch (h.m) {
-    case 1: launch_pass_m<1>(state, dev_rec, h, rankbase, s); break;
-    case 2: launch_pass_m<2>(state, dev_rec, h, rankbase, s); break;
-    case 3: launch_pass_m<3>(state, dev_rec, h, rankbase, s); break;
-    case 4: launch_pass_m<4>(state, dev_rec, h, rankbase, s); break;
-    case 5: launch_pass_m<5>(state, dev_rec, h, rankbase, s); break;
-    case 6: launch_pass_m<6>(state, dev_rec, h, rankbase, s); break;
-    case 7: launch_pass_m<7>(state, dev_rec, h, rankbase, s); break;
-    case 8: launch_pass_m<8>(state, dev_rec, h, rankbase, s); break;
-    case 9: launch_pass_m<9>(state, dev_rec, h, rankbase, s); break;
-    case 10: launch_pass_m<10>(state, dev_rec, h, rankbase, s); break;
-    case 11: launch_pass_m<11>(state, dev_rec, h, rankbase, s); break;
-    case 12: launch_pass_m<12>(state, dev_rec, h, rankbase, s); break;
-    case 13: launch_pass_m<13>(state, dev_rec, h, rankbase, s); break;
-    default: throw std::logic_error("launch_pass: unsupported tile size " + std::to_string(h.m));
-    }
-}
+std::atomic<int64_t> g_kernel_launches{0};
 
 void launch_init_basis(double2* a, uint64_t n, uint64_t one_at, cudaStream_t s) {
     k_init_basis<<<grid_for(n), kThreads, 0, s>>>(a, n, one_at);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch_sumsq(const double2* a, uint64_t n, double* scratch, double* out, cudaStream_t s) {
@@ -860,7 +470,9 @@ void launch_sumsq(const double2* a, uint64_t n, double* scratch, double* out, cu
     int nblk;
     reduction_geometry(n, &chunk, &nblk);
     k_sumsq<<<nblk, kThreads, 0, s>>>(a, n, chunk, scratch);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     k_final<<<1, kThreads, 0, s>>>(scratch, nblk, 1, out);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch_trace(const double2* rho, uint64_t dim, double* scratch, double* out, cudaStream_t s) {
@@ -868,7 +480,9 @@ void launch_trace(const double2* rho, uint64_t dim, double* scratch, double* out
     int nblk;
     reduction_geometry(dim, &chunk, &nblk);
     k_strided_re<<<nblk, kThreads, 0, s>>>(rho, dim, dim + 1, chunk, scratch);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     k_final<<<1, kThreads, 0, s>>>(scratch, nblk, 1, out);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 size_t scratch_doubles_needed(uint64_t n) {
@@ -895,7 +509,9 @@ void launch_expect_sv(const double2* a, int nbits, uint64_t flip, const uint64_t
     int nblk;
     reduction_geometry(nwork, &chunk, &nblk);
     k_expect<<<nblk, kThreads, 0, s>>>(a, nwork, flip, f0, chunk, tb, scratch);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     k_final<<<1, kThreads, 0, s>>>(scratch, nblk, kTermsPerLaunch, out);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch_expect_dm(const double2* rho, int n, uint64_t flip, const uint64_t* signs, int nt,
@@ -908,21 +524,28 @@ void launch_expect_dm(const double2* rho, int n, uint64_t flip, const uint64_t* 
     int nblk;
     reduction_geometry(dim, &chunk, &nblk);
     k_dm_expect<<<nblk, kThreads, 0, s>>>(rho, dim, flip, chunk, tb, scratch);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     k_final<<<1, kThreads, 0, s>>>(scratch, nblk, 2 * kTermsPerLaunch, out);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch_probs(const double2* a, uint64_t n, double* p, cudaStream_t s) {
     k_probs<<<grid_for(n), kThreads, 0, s>>>(a, n, p);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch_dm_probs(const double2* rho, uint64_t dim, double* p, double* scratch, cudaStream_t s) {
     k_dm_diag<<<grid_for(dim), kThreads, 0, s>>>(rho, dim, p);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     uint64_t chunk;
     int nblk;
     reduction_geometry(dim, &chunk, &nblk);
     k_sum_real<<<nblk, kThreads, 0, s>>>(p, dim, chunk, scratch + 1);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     k_final<<<1, kThreads, 0, s>>>(scratch + 1, nblk, 1, scratch);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     k_scale_real<<<grid_for(dim), kThreads, 0, s>>>(p, dim, scratch);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch_sum_real(const double* x, uint64_t n, double* scratch, double* out, cudaStream_t s) {
@@ -930,14 +553,18 @@ void launch_sum_real(const double* x, uint64_t n, double* scratch, double* out, 
     int nblk;
     reduction_geometry(n, &chunk, &nblk);
     k_sum_real<<<nblk, kThreads, 0, s>>>(x, n, chunk, scratch);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     k_final<<<1, kThreads, 0, s>>>(scratch, nblk, 1, out);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch_herm(const double2* rho, uint64_t dim, double* scratch, double* out, cudaStream_t s) {
     const uint64_t tpr = (dim + 31) / 32;
     const int nblk = int(std::min<uint64_t>(tpr * tpr, 2048));
     k_herm<<<nblk, kThreads, 0, s>>>(rho, dim, scratch);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     k_final_max<<<1, kThreads, 0, s>>>(scratch, nblk, out);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch_kraus_weights(const double2* a, int nbits, const int* qubits, int k, int nk,
@@ -959,13 +586,16 @@ void launch_kraus_weights(const double2* a, int nbits, const int* qubits, int k,
     int nblk;
     reduction_geometry(ng, &chunk, &nblk);
     k_kraus_w<<<nblk, kThreads, 0, s>>>(a, ng, chunk, kb, dev_mats, scratch);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     k_final<<<1, kThreads, 0, s>>>(scratch, nblk, 16, out);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch_block_psum(const double2* a, const double* p, uint64_t n, uint64_t bs, double* out,
                        cudaStream_t s) {
     const uint64_t nb = (n + bs - 1) / bs;
     k_block_psum<<<unsigned(nb), kThreads, 0, s>>>(a, p, n, bs, out);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch_block_sweep(const double2* a, const double* p, uint64_t n, uint64_t bs, const int64_t* blk,
@@ -974,16 +604,19 @@ void launch_block_sweep(const double2* a, const double* p, uint64_t n, uint64_t 
     if (nb <= 0) return;
     k_block_sweep<<<(nb + 127) / 128, 128, 0, s>>>(a, p, n, bs, blk, cum0, ulo, uhi, u, nb, idx_out,
                                                    cnt_out, npairs);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch_last_nonzero(const double2* a, const double* p, uint64_t lo, uint64_t hi, uint64_t* out,
                          cudaStream_t s) {
     k_last_nonzero<<<1, kThreads, 0, s>>>(a, p, lo, hi, out);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch_readout(double* d, int n, int q, double p01, double p10, cudaStream_t s) {
     const uint64_t half = (uint64_t(1) << n) / 2;
     k_readout<<<grid_for(half), kThreads, 0, s>>>(d, half, q, p01, p10);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 }  // namespace nqe

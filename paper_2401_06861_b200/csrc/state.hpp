@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <new>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace nqe {
@@ -61,12 +62,20 @@ struct DeviceCtx {
     double* d_scratch = nullptr;
     size_t scratch_cap = 0;
     double* h_small = nullptr;
+    // measured region (nq_profile_begin/end)
+    bool prof = false, prof_pass = false;
+    cudaEvent_t prof_t0 = nullptr, prof_t1 = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
+    size_t prof_used = 0;
+    double prof_pass_bytes = 0.0;
+    int64_t prof_launch0 = 0, h2d_bytes = 0, d2h_bytes = 0;
 
     void ensure_scratch(size_t doubles);
     void stage(const unsigned char* src, size_t bytes);
 };
 
 DeviceCtx& ctx_for(int dev);
+std::pair<cudaEvent_t, cudaEvent_t>* prof_slot(DeviceCtx& c);
 
 struct ShardComm;  // shard.cpp
 

@@ -12,10 +12,10 @@ from typing import List
 
 import numpy as np
 
-MOP_NAMES = {0: "dense", 1: "diag", 2: "xperm", 3: "swap", 4: "depol"}
+MOP_NAMES = {0: "dense", 1: "diag", 2: "xperm", 3: "swap", 4: "depol", 5: "layout"}
 HDR_FMT = "<iiiiqIIII16b56b"
 HDR_SIZE = struct.calcsize(HDR_FMT)
-MOP_FMT = "<BB4b4BHII4xQ"
+MOP_FMT = "<BB8bHII4xQ"
 MOP_SIZE = struct.calcsize(MOP_FMT)
 assert HDR_SIZE == 112 and MOP_SIZE == 32
 
@@ -52,10 +52,11 @@ def decode(buf: bytes) -> List[Pass]:
         rest = list(f[25:25 + 56])[:nrest]
         p = Pass(m=m, nloc=nloc, ntiles=ntiles, q=q, rest=rest)
         for i in range(nops):
-            t, k, p0, p1, p2, p3, g0, g1, g2, g3, _pad, mat, cmt, cmg = struct.unpack_from(
-                MOP_FMT, buf, at + op_off + i * MOP_SIZE)
-            p.ops.append(MicroOp(MOP_NAMES[t], k, [p0, p1, p2, p3][:max(k, 1)], [g0, g1, g2, g3][:max(k, 1)], mat,
-                                 cmt, cmg))
+            f2 = struct.unpack_from(MOP_FMT, buf, at + op_off + i * MOP_SIZE)
+            t, k = f2[0], f2[1]
+            pos = list(f2[2:10])
+            mat, cmt, cmg = f2[11], f2[12], f2[13]
+            p.ops.append(MicroOp(MOP_NAMES[t], k, pos[:max(k, 1)], [], mat, cmt, cmg))
         p.pool = np.frombuffer(buf, dtype=np.complex128, count=pool_n, offset=at + pool_off).copy()
         out.append(p)
         at += nbytes

@@ -1,0 +1,58 @@
+"""Run-time specialised pass kernels (jit.cpp) against the oracle.
+
+NQ_JIT is read once per process, so each case runs in a subprocess with
+NQ_JIT=sync (every pass of tile size >= 8 compiled and launched as a
+specialised kernel) and compares with the oracle there.
+"""
+import os
+import subprocess
+import sys
+import textwrap
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = textwrap.dedent(
+    """
+    import sys
+    sys.path[:0] = [{root!r}, {oracle!r}]
+    import numpy as np
+    from oracle import Port, NoiseSpec, ops_to_list
+    from paper_2401_06861_b200 import abi, naqs
+    port = Port()
+    worst = 0.0
+    for n, tile, seed in [(12, 8, 1), (14, 10, 2), (16, 12, 3), (18, 12, 4), (17, 9, 5), (20, 13, 6)]:
+        ops = port.random_circuit(seed, n, 250)
+        sv = abi.SV(n, tile_qubits=tile)
+        sv.apply(ops)
+        got = sv.amplitudes()
+        worst = max(worst, float(np.max(np.abs(got - port.sv_run(n, ops)))))
+        # a second run of the same structure reuses the compiled kernels
+        sv.reset()
+        sv.apply(ops)
+        assert np.array_equal(sv.amplitudes(), got)
+    # density matrix with noise (Liouville superoperators, depolarizing maps)
+    for n in (5, 6):
+        c = port.random_circuit(100 + n, n, 60, 2)
+        circ = naqs.Circuit(n)
+        for k, q, p in ops_to_list(c):
+            circ.add(k, q, p)
+        noise = NoiseSpec(n, e1=0.01, e2=0.05)
+        rho = naqs.run_density(circ, naqs.load_calibration(noise.calibration_json()))
+        worst = max(worst, float(np.max(np.abs(rho - port.dm_run_noisy(n, c, noise)))))
+    st = abi.jit_stats()
+    assert st["launches"] > 0 and st["failed"] == 0, st
+    print("WORST", worst, st)
+    assert worst <= 1e-10, worst
+    """
+)
+
+
+def test_specialised_kernels_match_oracle():
+    env = dict(os.environ, NQ_JIT="sync")
+    code = SCRIPT.format(root=ROOT, oracle=os.path.join(ROOT, "oracle"))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
+    assert "WORST" in r.stdout

@@ -25,29 +25,39 @@ def deposit(v, pos):
 
 
 def run_plan(n, passes, amps):
+    """Numpy emulator of the pass records (semantics of csrc/engine.hpp)."""
     a = amps.copy()
     for p in passes:
         size = 1 << p.m
         offs = np.array([deposit(e, p.q) for e in range(size)], dtype=np.int64)
+        assert p.ops[0].type == "layout"
         for r in range(p.ntiles):
             base = deposit(r, p.rest)
             t = a[base + offs].copy()
+            lay = None
             for op in p.ops:
-                apply_mop(op, t, p.pool, base, p.m)
+                if op.type == "layout":
+                    lay = op.pos[: op.k]
+                    assert lay == sorted(lay)
+                    continue
+                apply_mop(op, t, p.pool, base, p.m, lay)
             a[base + offs] = t
     return a
 
 
-def apply_mop(op, t, pool, full, m):
+def apply_mop(op, t, pool, full, m, lay):
     size = 1 << m
     e = np.arange(size)
+    # register-slot ops address tile bits through the current layout
+    tp = [lay[s] for s in op.pos[: op.k]] if op.type in ("dense", "xperm", "swap", "depol") else None
     if op.type == "dense":
+        assert op.pos[: op.k] == sorted(op.pos[: op.k])
         k = op.k
         D = 1 << k
         U = pool[op.mat:op.mat + D * D].reshape(D, D)
-        mask = sum(1 << op.pos[j] for j in range(k))
+        mask = sum(1 << b for b in tp)
         bases = e[(e & mask) == 0]
-        idx = np.stack([bases | deposit(l, op.pos[:k]) for l in range(D)])  # D x G
+        idx = np.stack([bases | deposit(l, tp) for l in range(D)])  # D x G
         t[idx] = U @ t[idx]
     elif op.type == "diag":
         k = op.k
@@ -57,16 +67,16 @@ def apply_mop(op, t, pool, full, m):
             if op.pos[j] >= 0:
                 idx |= ((e >> op.pos[j]) & 1) << j
             else:
-                idx |= ((full >> op.gq[j]) & 1) << j
+                idx |= ((full >> (-1 - op.pos[j])) & 1) << j
         t *= tab[idx]
     elif op.type == "xperm":
         if (full & op.cmask_glob) != op.cmask_glob:
             return
-        b = 1 << op.pos[0]
+        b = 1 << tp[0]
         sel = e[((e & b) == 0) & ((e & op.cmask_tile) == op.cmask_tile)]
         t[sel], t[sel | b] = t[sel | b].copy(), t[sel].copy()
     elif op.type == "swap":
-        b0, b1 = 1 << op.pos[0], 1 << op.pos[1]
+        b0, b1 = 1 << tp[0], 1 << tp[1]
         sel = e[((e & b0) != 0) & ((e & b1) == 0)]
         other = (sel & ~b0) | b1
         t[sel], t[other] = t[other].copy(), t[sel].copy()
