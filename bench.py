@@ -22,8 +22,9 @@ gates per second (whole job), plus achieved HBM GB/s.
             (oracle/_ref, kind "reference"; the C restatement "port" if that
             build is absent), on the host cores, on a bounded prefix of the
             same circuit.
-For N > 1 (torchrun) every rank simulates its own 30-qubit state (weak
-scaling, no data-path collective); see DESIGN.md §6 for the sharded path.
+For N > 1 (torchrun) the state is ONE sharded state of 30 + log2(N) qubits
+(2^30 amplitudes per GPU: weak scaling); non-diagonal gates on the log2(N)
+global qubits trigger NCCL half-shard exchanges.
 """
 from __future__ import annotations
 
@@ -321,10 +322,24 @@ def main():
     if abi.device_count() < 1:
         raise SystemExit("bench.py: no CUDA device")
     dev = local
-    n, depth = args.qubits, args.depth
+    g = world.bit_length() - 1
+    if (1 << g) != world:
+        raise SystemExit("bench.py: the sharded state needs a power-of-two number of GPUs")
+    n_local, depth = args.qubits, args.depth
+    n = n_local + g  # weak scaling: 2^n_local amplitudes per GPU
     ops_list = workloads.random_circuit(args.seed, n, depth)
     ops = abi.make_ops(ops_list)
-    sv = abi.SV(n, device=dev, tile_qubits=args.tile, max_qubits=max(30, n))
+    if world == 1:
+        sv = abi.SV(n, device=dev, tile_qubits=args.tile, max_qubits=max(30, n))
+    else:
+        import torch
+
+        uid = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(abi.comm_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        sv = abi.SV.sharded(n, rank, world, bytes(uid.cpu().numpy().tobytes()), device=dev,
+                            tile_qubits=args.tile, max_qubits=n)
 
     # warm-up: the first step plans the passes and queues their specialised
     # kernels for compilation (jit.cpp); wait for them, then warm the rest
@@ -346,7 +361,7 @@ def main():
         prof = abi.profile_end(dev)
     barrier(dist, local)
     ms = max_over_ranks(dist, local, prof["region_ms"])
-    gates_total = args.steps * depth * world
+    gates_total = args.steps * depth  # one circuit on the whole (sharded) state
     value = gates_total / (ms / 1e3)
     pass_avg_ms = prof["pass_ms"] / max(prof["pass_launches"], 1)
     bytes_per_launch = prof["pass_bytes"] / max(prof["pass_launches"], 1)
@@ -387,7 +402,10 @@ def main():
             "config": {"workload": f"random_circuit(Rng({args.seed})) n={n} depth={depth} "
                                    f"(proj/tests/test_util.hpp generator)",
                        "qubits": n, "depth": depth, "state_bytes": 16 << n,
-                       "parallelism": "single" if world == 1 else f"replicas x{world}",
+                       "parallelism": "single" if world == 1 else
+                       f"sharded x{world}: {g} global qubits, NCCL half-shard exchanges",
+                       "local_qubits": n_local,
+                       "comm": sv.comm_stats() if world > 1 else None,
                        "l2": "state (16 GiB) >> L2 (126 MB): every pass streams from HBM"},
             "hbm_gbs": step_gbs,
             "hbm_frac_step": step_gbs / peak,
@@ -404,7 +422,7 @@ def main():
             "e2e": e2e,
         }
     sv.close()
-    if rank == 0 and not args.no_secondary:
+    if rank == 0 and world == 1 and not args.no_secondary:
         try:
             out["secondary"] = secondary_workloads(abi, workloads, dev)
         except Exception as exc:  # secondary numbers never hide the headline

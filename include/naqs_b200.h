@@ -207,6 +207,12 @@ nq_status nq_sv_create_sharded(int num_qubits, int rank, int world, const unsign
                                const nq_opts* opts, nq_sv** out);
 /* Number of global-qubit exchanges performed so far and bytes sent. */
 nq_status nq_sv_comm_stats(const nq_sv* s, int64_t* exchanges, int64_t* bytes_sent);
+/* Host-side schedule of a sharded flush (no device, no NCCL): the segments of
+ * local work and the global<->local exchanges `ops` would produce on `world`
+ * ranks, followed by the exchanges restoring the identity qubit map.
+ * Serialised as int64 records (see paper_2401_06861_b200/abi.py:shard_debug). */
+nq_status nq_shard_debug(int num_qubits, int world, const nq_op* ops, int64_t count, int64_t* buf, int64_t cap,
+                         int64_t* size);
 
 /* ---- measurement (bench.py) -------------------------------------------- */
 typedef struct nq_profile {

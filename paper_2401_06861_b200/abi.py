@@ -21,6 +21,26 @@ if not os.path.exists(LIB_PATH):
         f"{LIB_PATH} is missing: build the CUDA core first (python -c 'import __graft_entry__ as g; g.build()')"
     )
 
+def _torch_nccl():
+    """torch's bundled libnccl.so.2, found without importing torch."""
+    import importlib.util
+
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return None
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        p = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            return p
+    return None
+
+
+# NCCL is bound lazily by the library (csrc/shard.cpp); prefer torch's copy so
+# that importing torch later in the same process still works.
+if "NQ_NCCL_LIB" not in os.environ and _torch_nccl():
+    os.environ["NQ_NCCL_LIB"] = _torch_nccl()
+
 lib = C.CDLL(LIB_PATH)
 
 # Gate kinds: ordinals of naqs::GateKind (proj/include/naqs/circuit.hpp:15-37).
@@ -121,6 +141,7 @@ SIGNATURES = {
     "nq_comm_unique_id": ([_ucp], C.c_int),
     "nq_sv_create_sharded": ([C.c_int, C.c_int, C.c_int, _ucp, C.POINTER(nq_opts), _pp], C.c_int),
     "nq_sv_comm_stats": ([_p, _i64p, _i64p], C.c_int),
+    "nq_shard_debug": ([C.c_int, C.c_int, _p, C.c_int64, _i64p, C.c_int64, _i64p], C.c_int),
     "nq_profile_begin": ([C.c_int, C.c_int], C.c_int),
     "nq_profile_end": ([C.c_int, C.POINTER(nq_profile)], C.c_int),
     "nq_jit_wait": ([], C.c_int),
@@ -286,6 +307,54 @@ class SV:
         v = [C.c_int64() for _ in range(4)]
         check(lib.nq_sv_last_stats(self.h, *[C.byref(x) for x in v]))
         return {"passes": v[0].value, "microops": v[1].value, "source_ops": v[2].value, "launches": v[3].value}
+
+    @classmethod
+    def sharded(cls, n: int, rank: int, world: int, uid: bytes, **kw) -> "SV":
+        """State of n qubits split over `world` ranks (one GPU each); every rank
+        must call this (and every later method) collectively."""
+        h = C.c_void_p()
+        u = (C.c_ubyte * 128).from_buffer_copy(uid)
+        check(lib.nq_sv_create_sharded(n, rank, world, u, C.byref(opts(**kw)), C.byref(h)))
+        return cls(n, handle=h)
+
+    def comm_stats(self):
+        a, b = C.c_int64(), C.c_int64()
+        check(lib.nq_sv_comm_stats(self.h, C.byref(a), C.byref(b)))
+        return {"exchanges": a.value, "bytes_sent": b.value}
+
+
+def comm_unique_id() -> bytes:
+    u = (C.c_ubyte * 128)()
+    check(lib.nq_comm_unique_id(u))
+    return bytes(u)
+
+
+def shard_debug(n: int, world: int, ops):
+    """Host schedule of a sharded flush: list of ("exchange", gbit, vbit) and
+    ("segment", [(type, k, bits, ctrl, matrix), ...]) in physical bits."""
+    arr = ops if isinstance(ops, np.ndarray) else make_ops(ops)
+    size = C.c_int64()
+    check(lib.nq_shard_debug(n, world, arr.ctypes.data, len(arr), None, 0, C.byref(size)))
+    buf = np.zeros(max(size.value, 1), dtype=np.int64)
+    check(lib.nq_shard_debug(n, world, arr.ctypes.data, len(arr), buf.ctypes.data_as(_i64p), len(buf),
+                             C.byref(size)))
+    out, i = [], 0
+    types = {0: "dense", 1: "diag", 2: "xperm", 3: "swap", 4: "depol", 5: "nop"}
+    while i < size.value:
+        kind, a, b, cnt = (int(x) for x in buf[i:i + 4])
+        i += 4
+        if kind == 1:
+            out.append(("exchange", a, b))
+            continue
+        seg = []
+        for _ in range(cnt):
+            t, k, b0, b1, b2, b3, ctrl, msz = (int(x) for x in buf[i:i + 8])
+            i += 8
+            mat = buf[i:i + 2 * msz].copy().view(np.float64).reshape(-1, 2)
+            i += 2 * msz
+            seg.append((types[t], k, [b0, b1, b2, b3][:k], ctrl & ((1 << 64) - 1), mat[:, 0] + 1j * mat[:, 1]))
+        out.append(("segment", seg))
+    return out
 
 
 class DM:

@@ -104,7 +104,9 @@ void state_init(State& s, int n, bool dm, const nq_opts* opts) {
     s.count = uint64_t(1) << s.nloc;
     s.popt.nbits = s.nbits;
     s.popt.nloc = s.nloc;
-    s.popt.tile_bits = o.tile_qubits > 0 ? std::min(o.tile_qubits, kMaxTileBits) : 12;
+    // 11 tile bits: 2^11 amplitudes per CTA, 4 CTAs of 128 threads per SM
+    // (best measured pass throughput on B200)
+    s.popt.tile_bits = o.tile_qubits > 0 ? std::min(o.tile_qubits, kMaxTileBits) : 11;
     s.popt.low_bits = 4;
     s.popt.fuse = o.fuse != 0;
     configure_caps(s.popt);
@@ -236,13 +238,6 @@ const cplx kIPow[4] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
 }  // namespace
 
 extern "C" {
-
-struct nq_sv {
-    State s;
-};
-struct nq_dm {
-    State s;
-};
 
 const char* nq_last_error(void) { return g_last_error.c_str(); }
 int nq_abi_version(void) { return NAQS_B200_ABI_VERSION; }
@@ -395,17 +390,91 @@ nq_status nq_sv_expectation_batch(nq_sv* h, const uint64_t* flip, const uint64_t
             shard_expectation(s, flip, signs, ny, coeff, nterms, out);
             return;
         }
+        std::vector<cplx> totals;
+        sv_expect_raw(s, flip, signs, nterms, totals);
+        for (int t = 0; t < nterms; ++t) out[t] = coeff[t] * (totals[size_t(t)] * kIPow[ny[t] & 3]).real();
+    });
+}
+
+}  // extern "C"
+
+namespace nqe {
+
+// sum_y (-1)^popcount(y & signs) conj(a[y^flip]) a[y] for each term, over this
+// device's amplitudes (masks in local bits), before the i^ny factor.
+void sv_expect_raw(State& s, const uint64_t* flip, const uint64_t* signs, int nterms, std::vector<cplx>& totals) {
+    {
         DeviceCtx& c = ctx_for(s.dev);
-        std::map<uint64_t, std::vector<int>> groups;
-        pauli_groups(flip, nterms, groups);
+        std::vector<int> eps(size_t(nterms), 0);
+        for (int t = 0; t < nterms; ++t)
+            eps[size_t(t)] = (flip[t] != 0 && (__builtin_popcountll(flip[t] & signs[t]) & 1)) ? 1 : 0;
+        // 1) batches of terms whose flips fit one tile: one state read per batch
+        const int m = std::min(11, s.nloc);
+        const int lb = s.nloc <= 11 ? m : 4;
+        const uint64_t lowm = (uint64_t(1) << lb) - 1;
+        std::vector<ExpBatch> batches;
+        std::vector<uint64_t> bhigh;
+        std::vector<std::pair<int, int>> slot_of{static_cast<size_t>(nterms)};  // (batch or launch, index)
+        std::vector<int> tiled(size_t(nterms), 0);
+        for (int t = 0; t < nterms; ++t) {
+            const uint64_t hi = flip[t] & ~lowm;
+            if (__builtin_popcountll(hi) > m - lb) continue;
+            size_t b = 0;
+            for (; b < batches.size(); ++b)
+                if (batches[b].nt < kMaxExpTerms && __builtin_popcountll(bhigh[b] | hi) <= m - lb) break;
+            if (b == batches.size()) {
+                batches.push_back(ExpBatch{});
+                bhigh.push_back(0);
+            }
+            bhigh[b] |= hi;
+            slot_of[size_t(t)] = {int(b), batches[b].nt++};
+            tiled[size_t(t)] = 1;
+        }
+        const size_t part = std::max(scratch_doubles_needed(s.count), expect_tiled_scratch());
         const int tpl = terms_per_launch();
+        std::map<uint64_t, std::vector<int>> groups;
+        for (int t = 0; t < nterms; ++t)
+            if (!tiled[size_t(t)]) groups[flip[t]].push_back(t);
         int launches = 0;
         for (auto& g : groups) launches += int((g.second.size() + tpl - 1) / tpl);
-        const size_t part = scratch_doubles_needed(s.count);
-        c.ensure_scratch(part + size_t(launches) * tpl + 64);
-        double* results = c.d_scratch + part;
-        std::vector<std::pair<int, int>> slot_of{static_cast<size_t>(nterms)};  // (launch, index)
-        std::vector<int> eps(size_t(nterms), 0);
+        const size_t res_tiled = batches.size() * kMaxExpTerms;
+        c.ensure_scratch(part + res_tiled + size_t(launches) * tpl + 64);
+        double* tiled_res = c.d_scratch + part;
+        for (size_t b = 0; b < batches.size(); ++b) {
+            ExpBatch& B = batches[b];
+            uint64_t qm = lowm | bhigh[b];
+            for (int bit = 0; bit < s.nloc && __builtin_popcountll(qm) < m; ++bit) qm |= uint64_t(1) << bit;
+            int tpos[64];
+            int k = 0, r = 0;
+            for (int bit = 0; bit < s.nloc; ++bit) {
+                if ((qm >> bit) & 1) {
+                    tpos[bit] = k;
+                    B.q[k++] = int8_t(bit);
+                } else {
+                    tpos[bit] = -1;
+                    B.rest[r++] = int8_t(bit);
+                }
+            }
+            B.m = m;
+            B.nrest = r;
+            for (int t = 0; t < nterms; ++t) {
+                if (!tiled[size_t(t)] || slot_of[size_t(t)].first != int(b)) continue;
+                ExpTerm& E = B.t[slot_of[size_t(t)].second];
+                E = ExpTerm{};
+                for (int bit = 0; bit < s.nloc; ++bit) {
+                    if ((flip[t] >> bit) & 1) E.ftile |= 1u << tpos[bit];
+                    if ((signs[t] >> bit) & 1) {
+                        if (tpos[bit] >= 0) E.stile |= 1u << tpos[bit];
+                        else E.sglob |= uint64_t(1) << bit;
+                    }
+                }
+                E.f0 = E.ftile ? __builtin_ctz(E.ftile) : 0;
+                E.eps_im = eps[size_t(t)];
+            }
+            launch_expect_tiled(s.d, s.nloc, B, c.d_scratch, tiled_res + b * kMaxExpTerms, c.stream);
+        }
+        // 2) terms with wide flips: one read per flip group
+        double* results = tiled_res + res_tiled;
         int li = 0;
         for (auto& g : groups) {
             const uint64_t F = g.first;
@@ -417,8 +486,7 @@ nq_status nq_sv_expectation_batch(nq_sv* h, const uint64_t* flip, const uint64_t
                 for (int j = 0; j < nt; ++j) {
                     const int t = terms[b + size_t(j)];
                     sg[j] = signs[t];
-                    ep[j] = (F != 0 && (__builtin_popcountll(F & signs[t]) & 1)) ? 1 : 0;
-                    eps[size_t(t)] = ep[j];
+                    ep[j] = eps[size_t(t)];
                     slot_of[size_t(t)] = {li, j};
                 }
                 launch_expect_sv(s.d, s.nloc, F, sg, ep, nt, c.d_scratch, results + size_t(li) * tpl,
@@ -427,23 +495,30 @@ nq_status nq_sv_expectation_batch(nq_sv* h, const uint64_t* flip, const uint64_t
             }
         }
         CUDA_TRY(cudaGetLastError());
-        std::vector<double> host(size_t(launches) * tpl);
+        std::vector<double> host(res_tiled + size_t(launches) * tpl);
         c.d2h_bytes += int64_t(host.size() * sizeof(double));
         if (!host.empty()) {
-            CUDA_TRY(cudaMemcpyAsync(host.data(), results, host.size() * sizeof(double),
+            CUDA_TRY(cudaMemcpyAsync(host.data(), tiled_res, host.size() * sizeof(double),
                                      cudaMemcpyDeviceToHost, c.stream));
         }
         CUDA_TRY(cudaStreamSynchronize(c.stream));
         for (int t = 0; t < nterms; ++t) {
-            const double acc = host[size_t(slot_of[size_t(t)].first) * tpl + size_t(slot_of[size_t(t)].second)];
+            const size_t at = tiled[size_t(t)]
+                                  ? size_t(slot_of[size_t(t)].first) * kMaxExpTerms + size_t(slot_of[size_t(t)].second)
+                                  : res_tiled + size_t(slot_of[size_t(t)].first) * tpl +
+                                        size_t(slot_of[size_t(t)].second);
+            const double acc = host[at];
             cplx total;
             if (flip[t] == 0) total = cplx(acc, 0.0);
             else total = eps[size_t(t)] ? cplx(0.0, 2.0 * acc) : cplx(2.0 * acc, 0.0);
-            total *= kIPow[ny[t] & 3];
-            out[t] = coeff[t] * total.real();
+            totals.push_back(total);
         }
-    });
+    }
 }
+
+}  // namespace nqe
+
+extern "C" {
 
 nq_status nq_sv_probabilities(nq_sv* h, double* host_out) {
     return guard([&] {

@@ -9,8 +9,15 @@
 // (shared memory), so re-running the same circuit structure with new angles
 // (VQE, Trotter sweeps, repeated benchmark steps) reuses the compiled kernel.
 //
+// Memory pipeline of the generated kernel: the next tile is prefetched into
+// one of two shared-memory buffers with cp.async (16-byte LDGSTS, natural
+// order, fully coalesced) while the current tile is computed from registers;
+// the current tile's buffer doubles as the relayout scratch.  The buffer
+// addressing uses a per-pass linear swizzle chosen so that every register
+// layout of the pass (and the natural order) is bank-conflict free.
+//
 // Compilation is asynchronous: the first time a structure is seen the
-// interpreter runs it while a worker thread compiles; later flushes use the
+// interpreter runs it while worker threads compile; later flushes use the
 // specialised kernel.  NQ_JIT=off|auto|sync selects the policy.
 #include "jit.hpp"
 
@@ -20,8 +27,11 @@
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
+#include <algorithm>
+#include <array>
 #include <atomic>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
@@ -46,8 +56,6 @@ struct Entry {
     std::atomic<int> state{0};  // 0 pending, 1 ready, 2 failed
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kern = nullptr;
-    int threads = 0;
-    size_t smem = 0;
     std::map<int, int> occ;  // device -> blocks per SM
     std::string log;
 };
@@ -58,14 +66,13 @@ struct Jit {
     std::unordered_map<std::string, std::shared_ptr<Entry>> cache;
     std::deque<std::pair<std::string, std::shared_ptr<Entry>>> queue;
     int busy = 0;
-    std::thread worker;
     bool started = false;
     int device = 0;
     JitStats stats;
 };
 
 Jit& jit() {
-    static Jit* j = new Jit();  // leaked on purpose: no teardown-order issues with the worker
+    static Jit* j = new Jit();  // leaked on purpose: no teardown-order issues with the workers
     return *j;
 }
 
@@ -78,7 +85,11 @@ JitMode mode_from_env() {
     return JitMode::Auto;
 }
 
-// ---- code generation ----------------------------------------------------------
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
 std::string hex64(unsigned long long v) {
     char b[32];
     std::snprintf(b, sizeof b, "0x%llxull", v);
@@ -118,8 +129,6 @@ struct Layout {
     }
 };
 
-unsigned swz_host(unsigned e) { return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7u); }
-
 Layout layout_of(const MOp& op, int m) {
     Layout L;
     L.r = op.k;
@@ -133,41 +142,103 @@ Layout layout_of(const MOp& op, int m) {
     return L;
 }
 
+// Linear swizzle: address = (e & ~7) | sum_p e_p * v[p] (over GF(2)).
+struct Swizzle {
+    unsigned v[16];
+    unsigned apply(unsigned e) const {
+        unsigned lo = 0;
+        for (int p = 0; p < 16; ++p)
+            if ((e >> p) & 1u) lo ^= v[p];
+        return (e & ~7u) | lo;
+    }
+    // masks of the positions contributing to address bit i
+    unsigned mask(int i) const {
+        unsigned m = 0;
+        for (int p = 0; p < 16; ++p)
+            if ((v[p] >> i) & 1u) m |= 1u << p;
+        return m;
+    }
+};
+
+bool independent3(unsigned a, unsigned b, unsigned c) {
+    return a && b && c && a != b && (a ^ b) != c && a != c && b != c;
+}
+
+// Make the three lowest thread bits of every layout (and of the natural
+// order) map to distinct 16-byte bank groups.
+Swizzle choose_swizzle(const std::vector<Layout>& lays, int m) {
+    std::vector<std::array<int, 3>> triples;
+    triples.push_back({0, 1, 2});
+    for (const auto& L : lays)
+        if (L.nonr.size() >= 3) triples.push_back({L.nonr[0], L.nonr[1], L.nonr[2]});
+    Swizzle sw{};
+    uint64_t x = 0x9E3779B97F4A7C15ull;
+    for (int attempt = 0; attempt < 20000; ++attempt) {
+        for (int p = 0; p < 16; ++p) {
+            if (attempt == 0) {
+                sw.v[p] = (p < 3) ? (1u << p) : (1u << (p % 3));  // fold-by-3 default
+            } else {
+                x ^= x << 13;
+                x ^= x >> 7;
+                x ^= x << 17;
+                sw.v[p] = p < m ? unsigned(1 + x % 7) : 0u;
+            }
+        }
+        bool ok = true;
+        for (const auto& t : triples) ok = ok && independent3(sw.v[t[0]], sw.v[t[1]], sw.v[t[2]]);
+        if (ok) return sw;
+    }
+    for (int p = 0; p < 16; ++p) sw.v[p] = p < 3 ? (1u << p) : 0u;  // identity: always a bijection
+    return sw;
+}
+
+std::string swz_expr(const std::string& x, const Swizzle& sw) {
+    std::ostringstream o;
+    o << "((" << x << " & ~7u)";
+    for (int i = 0; i < 3; ++i) {
+        const unsigned mk = sw.mask(i);
+        if (mk) o << " | ((unsigned)(__popc(" << x << " & " << mk << "u) & 1) << " << i << ")";
+    }
+    o << ")";
+    return o.str();
+}
+
 }  // namespace
+
+const JitKnobs& jit_knobs() {
+    // Measured on B200 (random circuit, n = 30): direct loads with a 128-register
+    // cap (512 threads / SM) beat the cp.async double buffer, whose extra 32-64 KB
+    // of shared memory halves the resident CTAs.  -1 = auto (512 / threads).
+    static const JitKnobs k{env_int("NQ_JIT_PREFETCH", 0) != 0, env_int("NQ_JIT_MINB", -1)};
+    return k;
+}
 
 std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     const int m = h.m;
+    const int SIZE = 1 << m;
     const int E = 16;
-    const int T = (1 << m) / E;
+    const int T = SIZE / E;
+    int logT = 0;
+    while ((1 << logT) < T) ++logT;
     std::vector<int> q(h.q, h.q + m), rest(h.rest, h.rest + h.nrest);
-    std::ostringstream s;
-    s << "#include \"pass_ops.cuh\"\n"
-      << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << (T >= 256 ? 512 / T : 1) << ")\n"
-      << "nqjit(double2* __restrict__ st, const double2* __restrict__ gpool, unsigned long long rankbase,"
-         " long long ntiles) {\n"
-      << "  using namespace nq;\n"
-      << "  extern __shared__ __align__(16) unsigned char smem[];\n"
-      << "  double2* tile = reinterpret_cast<double2*>(smem);\n"
-      << "  double2* pool = tile + " << (1 << m) << ";\n"
-      << "  const unsigned tid = threadIdx.x;\n"
-      << "  for (unsigned i = tid; i < " << h.pool_n << "u; i += " << T << "u) pool[i] = gpool[i];\n"
-      << "  __syncthreads();\n";
-    // layouts
+
     std::vector<Layout> lays;
     std::vector<int> lay_of_op(size_t(h.nops), 0);
     for (int i = 0; i < h.nops; ++i) {
         if (ops[i].type == MOP_LAYOUT) lays.push_back(layout_of(ops[i], m));
         lay_of_op[size_t(i)] = int(lays.size()) - 1;
     }
-    for (size_t k = 0; k < lays.size(); ++k) {
-        s << "  const unsigned tb" << k << " = " << deposit_expr("tid", lays[k].nonr, false) << ";\n";
-        s << "  const unsigned sw" << k << " = swz(tb" << k << ");\n";
-    }
-    auto state_off = [&](const std::string& tbname, const Layout& L) {
-        // state offset of the thread part: tile bit b -> state bit q[b]
+    const Swizzle sw = choose_swizzle(lays, m);
+    auto reg_off = [&](const Layout& L, int l) {
+        unsigned long long c = 0;
+        for (int j = 0; j < L.r; ++j)
+            if ((l >> j) & 1) c |= 1ull << q[size_t(L.rp[j])];
+        return c;
+    };
+    auto state_off = [&](const std::string& tbname, const std::vector<int>& bits) {
         std::ostringstream o;
         bool first = true;
-        for (int b : L.nonr) {
+        for (int b : bits) {
             if (!first) o << " | ";
             first = false;
             o << "((unsigned long long)((" << tbname << " >> " << b << ") & 1u) << " << q[size_t(b)] << ")";
@@ -175,25 +246,87 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
         if (first) o << "0ull";
         return o.str();
     };
-    auto reg_off = [&](const Layout& L, int l) {
-        unsigned long long c = 0;
-        for (int j = 0; j < L.r; ++j)
-            if ((l >> j) & 1) c |= 1ull << q[size_t(L.rp[j])];
-        return c;
-    };
+
+    const JitKnobs& kn = jit_knobs();
+    std::ostringstream s;
+    s << "#include \"pass_ops.cuh\"\n"
+      << "extern \"C\" __global__ void __launch_bounds__(" << T;
+    const int minb = kn.min_blocks >= 0 ? kn.min_blocks : std::max(1, 512 / T);
+    if (minb > 0) s << ", " << minb;
+    s << ")\n"
+      << "nqjit(double2* __restrict__ st, const double2* __restrict__ gpool, unsigned long long rankbase,"
+         " long long ntiles) {\n"
+      << "  using namespace nq;\n"
+      << "  extern __shared__ __align__(16) unsigned char smem[];\n"
+      << "  double2* buf0 = reinterpret_cast<double2*>(smem);\n"
+      << "  double2* buf1 = buf0 + " << (kn.prefetch ? SIZE : 0) << ";\n"
+      << "  double2* pool = buf1 + " << SIZE << ";\n"
+      << "  const unsigned tid = threadIdx.x;\n"
+      << "  for (unsigned i = tid; i < " << h.pool_n << "u; i += " << T << "u) pool[i] = gpool[i];\n";
+    // natural-order prefetch: element e = tid + j*T
+    {
+        std::vector<int> lowbits;
+        for (int b = 0; b < logT; ++b) lowbits.push_back(b);
+        s << "  const unsigned long long poff = " << state_off("tid", lowbits) << ";\n";
+        s << "  const unsigned psw = " << swz_expr("tid", sw) << ";\n";
+    }
+    for (size_t k = 0; k < lays.size(); ++k) {
+        s << "  const unsigned tb" << k << " = " << deposit_expr("tid", lays[k].nonr, false) << ";\n";
+        s << "  const unsigned sw" << k << " = " << swz_expr("tb" + std::to_string(k), sw) << ";\n";
+    }
     const Layout& L0 = lays.front();
     const Layout& LN = lays.back();
-    s << "  const unsigned long long toff_ld = " << state_off("tb0", L0) << ";\n";
-    s << "  const unsigned long long toff_st = " << state_off("tb" + std::to_string(lays.size() - 1), LN) << ";\n";
-    s << "  for (long long r = blockIdx.x; r < ntiles; r += gridDim.x) {\n"
-      << "    const unsigned long long base = " << deposit_expr("(unsigned long long)r", rest, true) << ";\n"
-      << "    const unsigned long long full = rankbase | base;\n"
-      << "    (void)full;\n"
-      << "    double2 a[16];\n"
-      << "    { const double2* src = st + base + toff_ld;\n";
-    for (int l = 0; l < E; ++l) s << "      a[" << l << "] = ld_stream(src + " << hex64(reg_off(L0, l)) << ");\n";
-    s << "    }\n";
-    bool any_relayout = false;
+    s << "  const unsigned long long toff_st = " << state_off("tb" + std::to_string(lays.size() - 1), LN.nonr)
+      << ";\n";
+    // prefetch helper (inline lambda-free: a macro-like block emitted twice)
+    auto prefetch = [&](const std::string& rexpr, const std::string& bufname, const std::string& indent) {
+        s << indent << "{ const unsigned long long pb = " << deposit_expr("(unsigned long long)(" + rexpr + ")", rest, true)
+          << " + poff;\n";
+        for (int j = 0; j < E; ++j) {
+            const unsigned e = unsigned(j) * unsigned(T);
+            unsigned long long go = 0;
+            for (int b = 0; b < m; ++b)
+                if ((e >> b) & 1u) go |= 1ull << q[size_t(b)];
+            s << indent << "  cp_async16(" << bufname << " + (psw ^ " << sw.apply(e) << "u), st + pb + " << hex64(go)
+              << ");\n";
+        }
+        s << indent << "}\n";
+    };
+    if (kn.prefetch) {
+        s << "  long long r = blockIdx.x;\n"
+          << "  if (r < ntiles) {\n";
+        prefetch("r", "buf0", "    ");
+        s << "  }\n  cp_async_commit();\n"
+          << "  __syncthreads();\n"
+          << "  for (int it = 0; r < ntiles; r += gridDim.x, ++it) {\n"
+          << "    double2* cur = (it & 1) ? buf1 : buf0;\n"
+          << "    double2* nxt = (it & 1) ? buf0 : buf1;\n"
+          << "    const long long rn = r + gridDim.x;\n"
+          << "    if (rn < ntiles) {\n";
+        prefetch("rn", "nxt", "      ");
+        s << "    }\n"
+          << "    cp_async_commit();\n"
+          << "    cp_async_wait<1>();\n"
+          << "    __syncthreads();\n"
+          << "    const unsigned long long base = " << deposit_expr("(unsigned long long)r", rest, true) << ";\n"
+          << "    const unsigned long long full = rankbase | base;\n"
+          << "    (void)full;\n"
+          << "    double2 a[16];\n";
+        for (int l = 0; l < E; ++l) s << "    a[" << l << "] = cur[sw0 ^ " << sw.apply(L0.rconst(l)) << "u];\n";
+    } else {
+        // direct streaming loads into the first register layout; one buffer
+        s << "  const unsigned long long toff_ld = " << state_off("tb0", L0.nonr) << ";\n"
+          << "  __syncthreads();\n"
+          << "  for (long long r = blockIdx.x; r < ntiles; r += gridDim.x) {\n"
+          << "    double2* cur = buf0;\n"
+          << "    const unsigned long long base = " << deposit_expr("(unsigned long long)r", rest, true) << ";\n"
+          << "    const unsigned long long full = rankbase | base;\n"
+          << "    (void)full;\n"
+          << "    double2 a[16];\n"
+          << "    { const double2* src = st + base + toff_ld;\n";
+        for (int l = 0; l < E; ++l) s << "      a[" << l << "] = ld_stream(src + " << hex64(reg_off(L0, l)) << ");\n";
+        s << "    }\n";
+    }
     for (int i = 1; i < h.nops; ++i) {
         const MOp& op = ops[i];
         const int li = lay_of_op[size_t(i)];
@@ -202,14 +335,13 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
         const std::string P = "pool + " + std::to_string(op.mat);
         switch (op.type) {
         case MOP_LAYOUT: {
-            any_relayout = true;
             const Layout& A = lays[size_t(li - 1)];
             s << "    __syncthreads();\n";
             for (int l = 0; l < E; ++l)
-                s << "    tile[sw" << (li - 1) << " ^ " << swz_host(A.rconst(l)) << "u] = a[" << l << "];\n";
+                s << "    cur[sw" << (li - 1) << " ^ " << sw.apply(A.rconst(l)) << "u] = a[" << l << "];\n";
             s << "    __syncthreads();\n";
             for (int l = 0; l < E; ++l)
-                s << "    a[" << l << "] = tile[sw" << li << " ^ " << swz_host(L.rconst(l)) << "u];\n";
+                s << "    a[" << l << "] = cur[sw" << li << " ^ " << sw.apply(L.rconst(l)) << "u];\n";
             break;
         }
         case MOP_DENSE:
@@ -220,8 +352,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
             } else if (op.k == 3) {
                 s << "    d3<16, " << (6 - op.pos[0] - op.pos[1] - op.pos[2]) << ">(a, " << P << ");\n";
             } else {
-                any_relayout = true;
-                s << "    __syncthreads();\n    d4<16>(a, " << P << ", tile + tid * 16u);\n";
+                s << "    __syncthreads();\n    d4<16>(a, " << P << ", cur + tid * 16u);\n";
             }
             break;
         case MOP_SWAP:
@@ -254,7 +385,6 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
             break;
         }
         case MOP_DIAG: {
-            // table index: register-slot bits (compile-time per l) | thread bits | global bits
             std::ostringstream g;
             g << "0u";
             unsigned slotc[4] = {0, 0, 0, 0};
@@ -282,6 +412,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
                 for (int l = 0; l < E; ++l) s << "      a[" << l << "] = cmul(f, a[" << l << "]);\n";
                 s << "      } }\n";
             } else {
+                const unsigned regmask = slotc[0] | slotc[1] | slotc[2] | slotc[3];
                 for (int l = 0; l < E; ++l) {
                     unsigned c = 0;
                     for (int t = 0; t < 4; ++t)
@@ -289,7 +420,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
                     // entries that are exactly 1 for every thread/global choice are skipped
                     bool all_one = true;
                     for (int gi = 0; gi < (1 << op.k) && all_one; ++gi) {
-                        if ((unsigned(gi) & (slotc[0] | slotc[1] | slotc[2] | slotc[3])) != c) continue;
+                        if ((unsigned(gi) & regmask) != c) continue;
                         all_one = tab[gi] == cplx(1.0, 0.0);
                     }
                     if (all_one) continue;
@@ -305,13 +436,17 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     }
     s << "    { double2* dst = st + base + toff_st;\n";
     for (int l = 0; l < E; ++l) s << "      st_stream(dst + " << hex64(reg_off(LN, l)) << ", a[" << l << "]);\n";
-    s << "    }\n";
-    if (any_relayout) s << "    __syncthreads();\n";
-    s << "  }\n}\n";
+    s << "    }\n"
+      << "    __syncthreads();\n"
+      << "  }\n";
+    if (kn.prefetch) s << "  cp_async_wait<0>();\n";
+    s << "}\n";
     return s.str();
 }
 
 namespace {
+
+const char* kNvrtcOpts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"};
 
 bool compile_entry(const std::string& src, Entry& e, int device) {
     nvrtcProgram prog;
@@ -321,8 +456,7 @@ bool compile_entry(const std::string& src, Entry& e, int device) {
         e.log = "nvrtcCreateProgram failed";
         return false;
     }
-    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "--extra-device-vectorization"};
-    const nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
+    const nvrtcResult rc = nvrtcCompileProgram(prog, 3, kNvrtcOpts);
     size_t logn = 0;
     nvrtcGetProgramLogSize(prog, &logn);
     if (logn > 1) {
@@ -385,7 +519,7 @@ JitMode jit_mode() {
 bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,
                 uint64_t rankbase, cudaStream_t s, int device) {
     const JitMode mode = jit_mode();
-    if (mode == JitMode::Off || h.m < 8 || h.m > 13) return false;
+    if (mode == JitMode::Off || h.m < 8 || h.m > 12) return false;
     if (mode == JitMode::Auto && h.nloc < 18) return false;  // interpreter is fine for small states
     std::string src = jit_source(h, ops, pool);
     Jit& J = jit();
@@ -426,14 +560,14 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
         return false;
     }
     const int T = (1 << h.m) / 16;
-    const size_t smem = (size_t(1) << h.m) * 16 + size_t(h.pool_n) * 16;
+    const size_t smem = (size_t(jit_knobs().prefetch ? 2 : 1) << h.m) * 16 + size_t(h.pool_n) * 16;
     int occ = 0;
     {
         std::lock_guard<std::mutex> lk(J.mu);
         auto it = e->occ.find(device);
         if (it == e->occ.end()) {
             cudaFuncSetAttribute(reinterpret_cast<const void*>(e->kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024);
+                                 220 * 1024);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(e->kern), T, smem);
             if (occ < 1) occ = 1;
             e->occ[device] = occ;
@@ -450,6 +584,7 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
     void* args[] = {&state, &gpool, &rb, &nt};
     if (cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(unsigned(grid)), dim3(unsigned(T)), args, smem,
                          s) != cudaSuccess) {
+        cudaGetLastError();
         return false;
     }
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
@@ -462,8 +597,7 @@ bool jit_compile_only(const std::string& src, std::string* log) {
     const char* hdrs[1] = {kPassOpsSrc};
     const char* names[1] = {"pass_ops.cuh"};
     if (nvrtcCreateProgram(&prog, src.c_str(), "nqjit.cu", 1, hdrs, names) != NVRTC_SUCCESS) return false;
-    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17"};
-    const nvrtcResult rc = nvrtcCompileProgram(prog, 2, opts);
+    const nvrtcResult rc = nvrtcCompileProgram(prog, 3, kNvrtcOpts);
     size_t logn = 0;
     nvrtcGetProgramLogSize(prog, &logn);
     if (log && logn > 1) {

@@ -22,6 +22,15 @@ struct JitStats {
 
 JitMode jit_mode();
 
+// Code-generation knobs (environment, read once): NQ_JIT_PREFETCH=0|1 selects
+// direct loads vs a cp.async double-buffered prefetch of the next tile;
+// NQ_JIT_MINB=k adds __launch_bounds__ min-blocks k (register cap).
+struct JitKnobs {
+    bool prefetch;
+    int min_blocks;
+};
+const JitKnobs& jit_knobs();
+
 // CUDA source of the kernel specialised to one pass record.
 std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool);
 

@@ -26,6 +26,31 @@ void launch_expect_sv(const double2* a, int nbits, uint64_t flip, const uint64_t
                       const int* eps_im, int nt, double* scratch, double* out, cudaStream_t s);
 void launch_expect_dm(const double2* rho, int n, uint64_t flip, const uint64_t* signs, int nt,
                       double* scratch, double* out, cudaStream_t s);
+// Tiled multi-term expectations (expect.cu): every term's flip mask lies in
+// the tile bits q[0..m); sign masks are split into tile and full-index parts.
+constexpr int kMaxExpTerms = 32;
+struct ExpTerm {
+    uint32_t ftile;   // flip mask on tile bits (0: Z-type term)
+    uint32_t stile;   // sign mask on tile bits
+    uint64_t sglob;   // sign mask on full-index bits outside the tile
+    int32_t f0;       // lowest set bit of ftile
+    int32_t eps_im;   // accumulate Im(conj(a[y^F]) a[y]) instead of Re
+};
+struct ExpBatch {
+    int32_t m, nrest, nt, pad;
+    int8_t q[16];
+    int8_t rest[56];
+    ExpTerm t[kMaxExpTerms];
+};
+size_t expect_tiled_scratch();
+void launch_expect_tiled(const double2* a, int nloc, const ExpBatch& b, double* part, double* out, cudaStream_t s);
+
+// half-shard pack/unpack for global<->local qubit swaps (comm_kernels.cu)
+void launch_half_pack(const double2* st, double2* buf, uint64_t k0, uint64_t len, int v, uint64_t val,
+                      cudaStream_t s);
+void launch_half_unpack(double2* st, const double2* buf, uint64_t k0, uint64_t len, int v, uint64_t val,
+                        cudaStream_t s);
+
 void launch_probs(const double2* a, uint64_t n, double* p, cudaStream_t s);
 void launch_dm_probs(const double2* rho, uint64_t dim, double* p, double* scratch, cudaStream_t s);
 void launch_sum_real(const double* x, uint64_t n, double* scratch, double* out, cudaStream_t s);

@@ -41,6 +41,15 @@ __device__ __forceinline__ double2 lds(const double2* p) {
 // lowest thread bits of a layout have distinct residues mod 3.
 __device__ __forceinline__ unsigned swz(unsigned e) { return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7u); }
 
+// 16-byte global -> shared asynchronous copy (LDGSTS), bypassing L1.
+__device__ __forceinline__ void cp_async16(double2* smem_dst, const double2* gsrc) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // a <- diag factor f, skipping exact ones (d0 = 1 diagonals touch half the amplitudes)
 __device__ __forceinline__ double2 dmul(double2 a, double2 f) { return is_one(f) ? a : cmul(f, a); }
 

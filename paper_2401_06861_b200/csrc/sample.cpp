@@ -24,7 +24,8 @@ constexpr uint64_t kBlock = 4096;
 }
 
 void sample_sweep(DeviceCtx& c, const double2* a, const double* p, uint64_t n, const double* sorted_u,
-                  uint64_t shots, uint64_t* idx_out, uint64_t* count_out, uint64_t* nout) {
+                  uint64_t shots, uint64_t* idx_out, uint64_t* count_out, uint64_t* nout, double cum_start,
+                  bool leftovers) {
     *nout = 0;
     if (shots == 0) return;
     CUDA_TRY(cudaSetDevice(c.dev));
@@ -42,7 +43,7 @@ void sample_sweep(DeviceCtx& c, const double2* a, const double* p, uint64_t n, c
     // host: block prefix + uniform ownership
     std::vector<int64_t> blk, ulo, uhi;
     std::vector<double> cum0;
-    double cum = 0.0;
+    double cum = cum_start;
     uint64_t next = 0;
     for (uint64_t b = 0; b < nb && next < shots; ++b) {
         const double start = cum;
@@ -106,7 +107,7 @@ void sample_sweep(DeviceCtx& c, const double2* a, const double* p, uint64_t n, c
             }
         }
     }
-    if (next < shots) {
+    if (next < shots && leftovers) {
         // leftovers: last index with nonzero probability
         int64_t lastb = -1;
         for (uint64_t b = nb; b-- > 0;)

@@ -1,41 +1,636 @@
-// Multi-GPU layer (placeholder until the sharded executor lands).
+// Multi-GPU layer (subsystem 5; no counterpart in the reference, which is a
+// single-process engine: SPEC.md:188 non-goal).  SURVEY.md §8e.
+//
+// One process per GPU.  The 2^n state is split over world = 2^g ranks by its
+// top g PHYSICAL bits: rank r owns the 2^(n-g) amplitudes whose physical
+// index has top bits r.  A logical->physical qubit map lets the layer move a
+// qubit between global and local positions:
+//   * diagonal ops and controls on global bits need no communication: the
+//     pass kernels see the rank-extended index (rankbase = r << nloc);
+//   * a non-diagonal op on a global bit first swaps that bit with a local
+//     "victim" bit (the local qubit whose next non-diagonal use is farthest
+//     away, Belady): partners r and r ^ 2^j exchange the half of their shard
+//     whose victim bit differs from their own rank bit (pack -> ncclSend /
+//     ncclRecv -> unpack, chunked through two bounce buffers).
+// Reductions gather per-rank partials and add them in rank order (results do
+// not depend on timing).  Readouts that expose the index order (amplitudes,
+// sampling) first restore the identity map.
+//
+// Scheduling is pure host logic (schedule()) and is exported for CPU testing
+// through nq_shard_debug().
+#include "jit.hpp"
+#include "kernels.hpp"
+#include "lower.hpp"
 #include "state.hpp"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
 
 namespace nqe {
 
-void shard_free(State& s) { (void)s; }
-void shard_reset(State& s) { (void)s; }
-void shard_flush(State& s) { (void)s; throw NqError{NQ_ERR_INTERNAL, "sharded execution not available"}; }
-double shard_norm_sq(State& s) { (void)s; throw NqError{NQ_ERR_INTERNAL, "sharded execution not available"}; }
-void shard_expectation(State& s, const uint64_t*, const uint64_t*, const int32_t*, const double*, int, double*) {
-    (void)s;
-    throw NqError{NQ_ERR_INTERNAL, "sharded execution not available"};
+// NCCL is resolved at first use (dlopen), not at link time: a process that
+// also imports torch must share torch's libnccl.so.2 (a newer build than the
+// system one), so we bind to whichever libnccl.so.2 is already loaded, else
+// NQ_NCCL_LIB (set by paper_2401_06861_b200/abi.py to torch's copy when
+// present), else the system library.
+namespace {
+struct NcclApi {
+    decltype(&::ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&::ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&::ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&::ncclGroupStart) GroupStart = nullptr;
+    decltype(&::ncclGroupEnd) GroupEnd = nullptr;
+    decltype(&::ncclSend) Send = nullptr;
+    decltype(&::ncclRecv) Recv = nullptr;
+    decltype(&::ncclAllGather) AllGather = nullptr;
+    decltype(&::ncclAllReduce) AllReduce = nullptr;
+    decltype(&::ncclGetErrorString) GetErrorString = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    static std::string err;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+        if (!h) {
+            const char* env = std::getenv("NQ_NCCL_LIB");
+            if (env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+        }
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            err = dlerror() ? dlerror() : "dlopen(libnccl.so.2) failed";
+            return;
+        }
+#define NQ_SYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name))
+        NQ_SYM(GetUniqueId, "ncclGetUniqueId");
+        NQ_SYM(CommInitRank, "ncclCommInitRank");
+        NQ_SYM(CommDestroy, "ncclCommDestroy");
+        NQ_SYM(GroupStart, "ncclGroupStart");
+        NQ_SYM(GroupEnd, "ncclGroupEnd");
+        NQ_SYM(Send, "ncclSend");
+        NQ_SYM(Recv, "ncclRecv");
+        NQ_SYM(AllGather, "ncclAllGather");
+        NQ_SYM(AllReduce, "ncclAllReduce");
+        NQ_SYM(GetErrorString, "ncclGetErrorString");
+#undef NQ_SYM
+    });
+    if (!api.CommInitRank) throw NqError{NQ_ERR_NCCL, "NCCL unavailable: " + err};
+    return api;
 }
-void shard_sample(State& s, const double*, uint64_t, uint64_t*, uint64_t*, uint64_t*) {
-    (void)s;
-    throw NqError{NQ_ERR_INTERNAL, "sharded execution not available"};
+}  // namespace
+
+#define ncclGetUniqueId nccl().GetUniqueId
+#define ncclCommInitRank nccl().CommInitRank
+#define ncclCommDestroy nccl().CommDestroy
+#define ncclGroupStart nccl().GroupStart
+#define ncclGroupEnd nccl().GroupEnd
+#define ncclSend nccl().Send
+#define ncclRecv nccl().Recv
+#define ncclAllGather nccl().AllGather
+#define ncclAllReduce nccl().AllReduce
+#define ncclGetErrorString nccl().GetErrorString
+
+#define NCCL_TRY(expr)                                                                                 \
+    do {                                                                                               \
+        ncclResult_t nccl_try_r_ = (expr);                                                             \
+        if (nccl_try_r_ != ncclSuccess)                                                                \
+            throw NqError{NQ_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(nccl_try_r_)}; \
+    } while (0)
+
+struct ShardComm {
+    ncclComm_t comm = nullptr;
+    double2* sendbuf = nullptr;
+    double2* recvbuf = nullptr;
+    uint64_t chunk = 0;  // amplitudes per bounce buffer
+    std::vector<int> l2p, p2l;
+    int64_t exchanges = 0, bytes = 0;
+};
+
+// ---- host scheduling ----------------------------------------------------------
+struct Action {
+    enum Kind { Segment, Exchange } kind;
+    std::vector<EOp> ops;  // Segment: ops in physical bits
+    int gbit = 0, vbit = 0;  // Exchange: swap physical global bit gbit with local vbit
+};
+
+namespace {
+
+uint64_t emask(const EOp& e, bool ctrl) {
+    uint64_t m = 0;
+    for (int j = 0; j < e.k; ++j) m |= uint64_t(1) << e.bits[j];
+    if (ctrl) m |= e.ctrl;
+    return m;
 }
-void shard_get_amplitudes(State& s, uint64_t, uint64_t, double*) {
-    (void)s;
-    throw NqError{NQ_ERR_INTERNAL, "sharded execution not available"};
+
+// bits that must be local (non-diagonal targets), as in the planner
+uint64_t need_bits(const EOp& e) {
+    switch (e.type) {
+    case E_DENSE:
+    case E_DEPOL:
+    case E_SWAP:
+        return emask(e, false);
+    case E_XPERM:
+        return uint64_t(1) << e.bits[0];
+    default:
+        return 0;
+    }
+}
+
+EOp to_physical(const EOp& e, const std::vector<int>& l2p) {
+    EOp p = e;
+    for (int j = 0; j < e.k; ++j) p.bits[j] = l2p[size_t(e.bits[j])];
+    uint64_t c = 0;
+    for (int b = 0; b < 64; ++b)
+        if ((e.ctrl >> b) & 1) c |= uint64_t(1) << l2p[size_t(b)];
+    p.ctrl = c;
+    return p;
+}
+
+void swap_map(std::vector<int>& l2p, std::vector<int>& p2l, int pa, int pb) {
+    const int la = p2l[size_t(pa)], lb = p2l[size_t(pb)];
+    p2l[size_t(pa)] = lb;
+    p2l[size_t(pb)] = la;
+    l2p[size_t(la)] = pb;
+    l2p[size_t(lb)] = pa;
+}
+
+// Local physical bit to evict for global bit `g`: not needed by `protect`
+// (logical mask), farthest next non-diagonal use in ops[from..].
+int choose_victim(const std::vector<EOp>& ops, size_t from, const std::vector<int>& p2l, int nloc,
+                  uint64_t protect_logical) {
+    int best = -1;
+    size_t best_dist = 0;
+    for (int v = nloc - 1; v >= 0; --v) {
+        const int lq = p2l[size_t(v)];
+        if ((protect_logical >> lq) & 1) continue;
+        size_t d = ops.size() + 1;  // never used again
+        for (size_t i = from; i < ops.size(); ++i)
+            if ((need_bits(ops[i]) >> lq) & 1) {
+                d = i;
+                break;
+            }
+        if (best < 0 || d > best_dist) {
+            best = v;
+            best_dist = d;
+        }
+    }
+    if (best < 0) throw NqError{NQ_ERR_INTERNAL, "sharded: no local qubit available to swap in"};
+    return best;
+}
+
+}  // namespace
+
+// Split a queue (logical bits) into segments of local work and exchanges,
+// updating the qubit map as the exchanges will.
+std::vector<Action> schedule(const std::vector<EOp>& ops, std::vector<int>& l2p, std::vector<int>& p2l, int nloc) {
+    std::vector<Action> acts;
+    Action seg{Action::Segment, {}, 0, 0};
+    const uint64_t loc_mask = (uint64_t(1) << nloc) - 1;
+    for (size_t i = 0; i < ops.size(); ++i) {
+        EOp p = to_physical(ops[i], l2p);
+        uint64_t glob = need_bits(p) & ~loc_mask;
+        if (glob) {
+            if (!seg.ops.empty()) acts.push_back(std::move(seg));
+            seg = Action{Action::Segment, {}, 0, 0};
+            const uint64_t protect = emask(ops[i], false);
+            while (glob) {
+                const int g = __builtin_ctzll(glob);
+                glob &= glob - 1;
+                const int v = choose_victim(ops, i + 1, p2l, nloc, protect);
+                acts.push_back(Action{Action::Exchange, {}, g, v});
+                swap_map(l2p, p2l, g, v);
+            }
+            p = to_physical(ops[i], l2p);
+        }
+        seg.ops.push_back(std::move(p));
+    }
+    if (!seg.ops.empty()) acts.push_back(std::move(seg));
+    return acts;
+}
+
+// Exchanges that restore the identity map (physical bit p holds logical p).
+std::vector<Action> schedule_identity(std::vector<int>& l2p, std::vector<int>& p2l, int nloc, int n) {
+    std::vector<Action> acts;
+    for (int p = n - 1; p >= 0; --p) {
+        if (p2l[size_t(p)] == p) continue;
+        const int w = l2p[size_t(p)];  // where logical p currently lives
+        const bool pg = p >= nloc, wg = w >= nloc;
+        if (!pg && !wg) {
+            EOp s;
+            s.type = E_SWAP;
+            s.k = 2;
+            s.bits[0] = p;
+            s.bits[1] = w;
+            s.src = 0;
+            acts.push_back(Action{Action::Segment, {s}, 0, 0});
+        } else if (pg != wg) {
+            acts.push_back(Action{Action::Exchange, {}, pg ? p : w, pg ? w : p});
+        } else {
+            // two global bits: (p w) = (p l)(w l)(p l) through local bit 0
+            acts.push_back(Action{Action::Exchange, {}, p, 0});
+            acts.push_back(Action{Action::Exchange, {}, w, 0});
+            acts.push_back(Action{Action::Exchange, {}, p, 0});
+        }
+        swap_map(l2p, p2l, p, w);
+    }
+    return acts;
+}
+
+// ---- device execution ------------------------------------------------------------
+namespace {
+
+__attribute__((unused)) uint64_t ins_bit(uint64_t k, int v, uint64_t val) {
+    return ((k >> v) << (v + 1)) | (val << v) | (k & ((uint64_t(1) << v) - 1));
+}
+
+void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops) {
+    PlanOptions po = s.popt;
+    PlanStats st;
+    std::vector<PlannedPass> passes = plan_passes(ops, po, &st);
+    std::vector<size_t> offs;
+    std::vector<unsigned char> buf = serialize_passes(passes, s.nloc, &offs);
+    s.last_passes += st.passes;
+    s.last_microops += st.microops;
+    s.last_source_ops += st.source_ops;
+    s.last_launches += int64_t(passes.size());
+    if (buf.empty()) return;
+    c.stage(buf.data(), buf.size());
+    const uint64_t rankbase = uint64_t(s.rank) << s.nloc;
+    for (size_t i = 0; i < passes.size(); ++i) {
+        PassHdr h;
+        std::memcpy(&h, buf.data() + offs[i], sizeof(h));
+        std::pair<cudaEvent_t, cudaEvent_t>* ev = c.prof_pass ? prof_slot(c) : nullptr;
+        if (ev) CUDA_TRY(cudaEventRecord(ev->first, c.stream));
+        const unsigned char* rec = buf.data() + offs[i];
+        if (!jit_launch(s.d, c.d_ops + offs[i], h, reinterpret_cast<const MOp*>(rec + h.op_off),
+                        reinterpret_cast<const cplx*>(rec + h.pool_off), rankbase, c.stream, s.dev))
+            launch_pass(s.d, c.d_ops + offs[i], h, rankbase, c.stream);
+        if (ev) CUDA_TRY(cudaEventRecord(ev->second, c.stream));
+        if (c.prof) c.prof_pass_bytes += 32.0 * double(s.count);
+    }
+    CUDA_TRY(cudaGetLastError());
+}
+
+void run_exchange(State& s, DeviceCtx& c, int g, int v) {
+    ShardComm& sc = *s.comm;
+    const int j = g - s.nloc;
+    const int partner = s.rank ^ (1 << j);
+    const uint64_t mybit = uint64_t((s.rank >> j) & 1);
+    const uint64_t half = s.count / 2;
+    for (uint64_t k0 = 0; k0 < half; k0 += sc.chunk) {
+        const uint64_t len = std::min(sc.chunk, half - k0);
+        launch_half_pack(s.d, sc.sendbuf, k0, len, v, 1 - mybit, c.stream);
+        NCCL_TRY(ncclGroupStart());
+        NCCL_TRY(ncclSend(sc.sendbuf, size_t(len) * 2, ncclDouble, partner, sc.comm, c.stream));
+        NCCL_TRY(ncclRecv(sc.recvbuf, size_t(len) * 2, ncclDouble, partner, sc.comm, c.stream));
+        NCCL_TRY(ncclGroupEnd());
+        launch_half_unpack(s.d, sc.recvbuf, k0, len, v, 1 - mybit, c.stream);
+        sc.bytes += int64_t(len) * 16;
+    }
+    CUDA_TRY(cudaGetLastError());
+    ++sc.exchanges;
+}
+
+void execute(State& s, const std::vector<Action>& acts) {
+    DeviceCtx& c = ctx_for(s.dev);
+    CUDA_TRY(cudaSetDevice(s.dev));
+    for (const auto& a : acts) {
+        if (a.kind == Action::Segment) run_segment(s, c, a.ops);
+        else run_exchange(s, c, a.gbit, a.vbit);
+    }
+}
+
+// rank-ordered sum of one double per rank (deterministic)
+std::vector<double> allgather_doubles(State& s, const std::vector<double>& mine) {
+    DeviceCtx& c = ctx_for(s.dev);
+    const size_t k = mine.size();
+    double* d = nullptr;
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d), (size_t(s.world) + 1) * k * sizeof(double), c.stream));
+    CUDA_TRY(cudaMemcpyAsync(d, mine.data(), k * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    NCCL_TRY(ncclAllGather(d, d + k, k, ncclDouble, s.comm->comm, c.stream));
+    std::vector<double> all(size_t(s.world) * k);
+    CUDA_TRY(cudaMemcpyAsync(all.data(), d + k, all.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    CUDA_TRY(cudaFreeAsync(d, c.stream));
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return all;
+}
+
+void normalize_map(State& s) {
+    ShardComm& sc = *s.comm;
+    bool identity = true;
+    for (int p = 0; p < s.n; ++p) identity = identity && sc.p2l[size_t(p)] == p;
+    if (identity) return;
+    execute(s, schedule_identity(sc.l2p, sc.p2l, s.nloc, s.n));
+}
+
+}  // namespace
+
+void shard_free(State& s) {
+    if (!s.comm) return;
+    ShardComm* sc = s.comm;
+    DeviceCtx& c = ctx_for(s.dev);
+    cudaStreamSynchronize(c.stream);
+    if (sc->sendbuf) cudaFree(sc->sendbuf);
+    if (sc->recvbuf) cudaFree(sc->recvbuf);
+    if (sc->comm) ncclCommDestroy(sc->comm);
+    delete sc;
+    s.comm = nullptr;
+}
+
+void shard_reset(State& s) {
+    if (!s.comm) return;
+    for (int q = 0; q < s.n; ++q) s.comm->l2p[size_t(q)] = s.comm->p2l[size_t(q)] = q;
+}
+
+void shard_flush(State& s) {
+    ShardComm& sc = *s.comm;
+    std::vector<EOp> ops;
+    ops.swap(s.queue);
+    s.last_passes = s.last_microops = s.last_source_ops = s.last_launches = 0;
+    execute(s, schedule(ops, sc.l2p, sc.p2l, s.nloc));
+}
+
+double shard_norm_sq(State& s) {
+    DeviceCtx& c = ctx_for(s.dev);
+    c.ensure_scratch(scratch_doubles_needed(s.count) + 64);
+    launch_sumsq(s.d, s.count, c.d_scratch + 64, result_slot(c, 0), c.stream);
+    CUDA_TRY(cudaGetLastError());
+    double mine = 0.0;
+    fetch(c, result_slot(c, 0), 1, &mine);
+    const auto all = allgather_doubles(s, {mine});
+    double total = 0.0;
+    for (double v : all) total += v;
+    return total;
+}
+
+void shard_expectation(State& s, const uint64_t* flip, const uint64_t* signs, const int32_t* ny, const double* coeff,
+                       int nterms, double* out) {
+    ShardComm& sc = *s.comm;
+    const uint64_t loc_mask = (uint64_t(1) << s.nloc) - 1;
+    for (int t = 0; t < nterms; ++t)
+        if (__builtin_popcountll(flip[t]) > s.nloc)
+            throw NqError{NQ_ERR_CONTRACT, "sharded expectation: a Pauli term flips more qubits (" +
+                                               std::to_string(__builtin_popcountll(flip[t])) +
+                                               ") than one rank holds (" + std::to_string(s.nloc) + ")"};
+    // Terms are evaluated in batches whose flipped qubits are all local under
+    // the current qubit map; before a term that flips a global qubit, that
+    // qubit is swapped in (Belady victim over the remaining terms' flips).
+    const size_t nt = static_cast<size_t>(nterms);
+    std::vector<double> mine(2 * nt, 0.0);
+    std::vector<int> batch;
+    auto run_batch = [&] {
+        if (batch.empty()) return;
+        std::vector<uint64_t> pf, ps;
+        std::vector<double> sgn;
+        for (int t : batch) {
+            uint64_t f = 0, g = 0;
+            for (int q = 0; q < s.n; ++q) {
+                if ((flip[t] >> q) & 1) f |= uint64_t(1) << sc.l2p[size_t(q)];
+                if ((signs[t] >> q) & 1) g |= uint64_t(1) << sc.l2p[size_t(q)];
+            }
+            if (f & ~loc_mask) throw NqError{NQ_ERR_INTERNAL, "sharded expectation: flip bit still global"};
+            pf.push_back(f);
+            ps.push_back(g & loc_mask);
+            sgn.push_back((__builtin_popcountll((g >> s.nloc) & uint64_t(s.rank)) & 1) ? -1.0 : 1.0);
+        }
+        std::vector<cplx> totals;
+        sv_expect_raw(s, pf.data(), ps.data(), int(batch.size()), totals);
+        for (size_t i = 0; i < batch.size(); ++i) {
+            mine[2 * size_t(batch[i])] = sgn[i] * totals[i].real();
+            mine[2 * size_t(batch[i]) + 1] = sgn[i] * totals[i].imag();
+        }
+        batch.clear();
+    };
+    auto stand_in = [](int q) {
+        EOp e;
+        e.type = E_XPERM;  // an op that needs qubit q local
+        e.k = 1;
+        e.bits[0] = q;
+        return e;
+    };
+    for (int t = 0; t < nterms; ++t) {
+        uint64_t glob = 0;
+        for (int q = 0; q < s.n; ++q)
+            if (((flip[t] >> q) & 1) && sc.l2p[size_t(q)] >= s.nloc) glob |= uint64_t(1) << q;
+        if (glob) {
+            run_batch();
+            // future uses: the flips of this and the remaining terms
+            std::vector<EOp> fut;
+            for (int u = t; u < nterms; ++u)
+                for (int q = 0; q < s.n; ++q)
+                    if ((flip[u] >> q) & 1) fut.push_back(stand_in(q));
+            std::vector<Action> ex;
+            for (int q = 0; q < s.n; ++q) {
+                if (!((glob >> q) & 1)) continue;
+                const int gb = sc.l2p[size_t(q)];
+                const int v = choose_victim(fut, 0, sc.p2l, s.nloc, flip[t]);
+                ex.push_back(Action{Action::Exchange, {}, gb, v});
+                swap_map(sc.l2p, sc.p2l, gb, v);
+            }
+            execute(s, ex);
+        }
+        batch.push_back(t);
+    }
+    run_batch();
+    const auto all = allgather_doubles(s, mine);
+    static const cplx kI4[4] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
+    for (int t = 0; t < nterms; ++t) {
+        cplx tot(0.0, 0.0);
+        for (int r = 0; r < s.world; ++r)
+            tot += cplx(all[size_t(r) * mine.size() + size_t(2 * t)], all[size_t(r) * mine.size() + size_t(2 * t + 1)]);
+        out[t] = coeff[t] * (tot * kI4[ny[t] & 3]).real();
+    }
+}
+
+void shard_sample(State& s, const double* sorted_u, uint64_t shots, uint64_t* idx_out, uint64_t* count_out,
+                  uint64_t* nout) {
+    normalize_map(s);
+    DeviceCtx& c = ctx_for(s.dev);
+    // this rank's probability mass; rank-ordered offsets
+    c.ensure_scratch(scratch_doubles_needed(s.count) + 64);
+    launch_sumsq(s.d, s.count, c.d_scratch + 64, result_slot(c, 0), c.stream);
+    double mass = 0.0;
+    fetch(c, result_slot(c, 0), 1, &mass);
+    const auto masses = allgather_doubles(s, {mass});
+    double start = 0.0;
+    for (int r = 0; r < s.rank; ++r) start += masses[size_t(r)];
+    int last_nz = -1;
+    for (int r = 0; r < s.world; ++r)
+        if (masses[size_t(r)] > 0.0) last_nz = r;
+    const double end = start + mass;
+    // uniforms owned by this rank: [start, end), the last nonzero rank also takes leftovers
+    uint64_t lo = uint64_t(std::lower_bound(sorted_u, sorted_u + shots, start) - sorted_u);
+    uint64_t hi = (s.rank == last_nz) ? shots : uint64_t(std::lower_bound(sorted_u, sorted_u + shots, end) - sorted_u);
+    if (s.rank > last_nz) lo = hi = 0;
+    std::vector<uint64_t> li(std::max<uint64_t>(hi - lo, 1)), lc(std::max<uint64_t>(hi - lo, 1));
+    uint64_t k = 0;
+    if (hi > lo)
+        sample_sweep(c, s.d, nullptr, s.count, sorted_u + lo, hi - lo, li.data(), lc.data(), &k, start,
+                     s.rank == last_nz);
+    // gather (index, count) pairs in rank order
+    const auto ks = allgather_doubles(s, {double(k)});
+    uint64_t maxk = 1;
+    for (double v : ks) maxk = std::max<uint64_t>(maxk, uint64_t(v));
+    std::vector<double> pack(size_t(2 * maxk), 0.0);
+    for (uint64_t i = 0; i < k; ++i) {
+        pack[size_t(2 * i)] = double((uint64_t(s.rank) << s.nloc) | li[size_t(i)]);
+        pack[size_t(2 * i + 1)] = double(lc[size_t(i)]);
+    }
+    const auto all = allgather_doubles(s, pack);
+    uint64_t o = 0;
+    for (int r = 0; r < s.world; ++r)
+        for (uint64_t i = 0; i < uint64_t(ks[size_t(r)]); ++i) {
+            idx_out[o] = uint64_t(all[size_t(r) * pack.size() + size_t(2 * i)]);
+            count_out[o] = uint64_t(all[size_t(r) * pack.size() + size_t(2 * i + 1)]);
+            ++o;
+        }
+    *nout = o;
+}
+
+void shard_get_amplitudes(State& s, uint64_t offset, uint64_t count, double* host_out) {
+    if (offset > (uint64_t(1) << s.n) || count > (uint64_t(1) << s.n) - offset)
+        throw NqError{NQ_ERR_CONTRACT, "amplitude range out of bounds"};
+    normalize_map(s);
+    DeviceCtx& c = ctx_for(s.dev);
+    double2* d = nullptr;
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d), std::max<uint64_t>(count, 1) * sizeof(double2), c.stream));
+    CUDA_TRY(cudaMemsetAsync(d, 0, std::max<uint64_t>(count, 1) * sizeof(double2), c.stream));
+    const uint64_t mine_lo = uint64_t(s.rank) << s.nloc, mine_hi = mine_lo + s.count;
+    const uint64_t a = std::max(offset, mine_lo), b = std::min(offset + count, mine_hi);
+    if (a < b)
+        CUDA_TRY(cudaMemcpyAsync(d + (a - offset), s.d + (a - mine_lo), (b - a) * sizeof(double2),
+                                 cudaMemcpyDeviceToDevice, c.stream));
+    // exactly one rank contributes each element: the sum with zeros is exact
+    if (count) NCCL_TRY(ncclAllReduce(d, d, size_t(count) * 2, ncclDouble, ncclSum, s.comm->comm, c.stream));
+    if (count)
+        CUDA_TRY(cudaMemcpyAsync(host_out, d, count * sizeof(double2), cudaMemcpyDeviceToHost, c.stream));
+    CUDA_TRY(cudaFreeAsync(d, c.stream));
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
 }
 
 }  // namespace nqe
 
+using namespace nqe;
+
 extern "C" {
 
 nq_status nq_comm_unique_id(unsigned char out[128]) {
-    (void)out;
-    return nqe::guard([&] { throw nqe::NqError{NQ_ERR_INTERNAL, "sharded execution not available"}; });
+    return guard([&] {
+        ncclUniqueId id;
+        NCCL_TRY(ncclGetUniqueId(&id));
+        static_assert(sizeof(id) == 128, "ncclUniqueId size");
+        std::memcpy(out, &id, 128);
+    });
 }
 
-nq_status nq_sv_create_sharded(int, int, int, const unsigned char*, const nq_opts*, nq_sv**) {
-    return nqe::guard([&] { throw nqe::NqError{NQ_ERR_INTERNAL, "sharded execution not available"}; });
+nq_status nq_sv_create_sharded(int n, int rank, int world, const unsigned char uid[128], const nq_opts* opts,
+                               nq_sv** out) {
+    return guard([&] {
+        if (world < 1 || (world & (world - 1)))
+            throw NqError{NQ_ERR_CONTRACT, "world size must be a power of two"};
+        if (rank < 0 || rank >= world) throw NqError{NQ_ERR_CONTRACT, "rank out of range"};
+        int g = 0;
+        while ((1 << g) < world) ++g;
+        nq_opts o;
+        nq_default_opts(&o);
+        if (opts) o = *opts;
+        const int cap = o.max_qubits > 0 ? o.max_qubits : 40;
+        if (n - g < 1 || n > cap)
+            throw NqError{NQ_ERR_CONTRACT, "sharded state qubit count must be in [" + std::to_string(g + 1) + ", " +
+                                               std::to_string(cap) + "], got " + std::to_string(n)};
+        if (n - g < 8) throw NqError{NQ_ERR_CONTRACT, "sharded states need at least 8 local qubits per rank"};
+        auto h = std::make_unique<nq_sv>();
+        State& s = h->s;
+        nq_opts lo = o;
+        lo.max_qubits = n;  // the local allocation is n - g qubits; state_init checks n
+        state_init(s, n - g, false, &lo);
+        s.n = n;
+        s.nbits = n;
+        s.nloc = n - g;
+        s.count = uint64_t(1) << s.nloc;
+        s.rank = rank;
+        s.world = world;
+        s.popt.nbits = n;
+        s.popt.nloc = s.nloc;
+        configure_caps(s.popt);
+        DeviceCtx& c = ctx_for(s.dev);
+        launch_init_basis(s.d, s.count, rank == 0 ? 0 : UINT64_MAX, c.stream);
+        auto sc = std::make_unique<ShardComm>();
+        sc->l2p.resize(size_t(n));
+        sc->p2l.resize(size_t(n));
+        for (int q = 0; q < n; ++q) sc->l2p[size_t(q)] = sc->p2l[size_t(q)] = q;
+        sc->chunk = std::min<uint64_t>(s.count / 2, uint64_t(1) << 26);
+        CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&sc->sendbuf), sc->chunk * sizeof(double2)));
+        CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&sc->recvbuf), sc->chunk * sizeof(double2)));
+        ncclUniqueId id;
+        std::memcpy(&id, uid, 128);
+        NCCL_TRY(ncclCommInitRank(&sc->comm, world, id, rank));
+        s.comm = sc.release();
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        *out = h.release();
+    });
 }
 
-nq_status nq_sv_comm_stats(const nq_sv*, int64_t* exchanges, int64_t* bytes_sent) {
-    if (exchanges) *exchanges = 0;
-    if (bytes_sent) *bytes_sent = 0;
-    return NQ_OK;
+nq_status nq_sv_comm_stats(const nq_sv* h, int64_t* exchanges, int64_t* bytes_sent) {
+    return guard([&] {
+        const State& s = h->s;
+        if (exchanges) *exchanges = s.comm ? s.comm->exchanges : 0;
+        if (bytes_sent) *bytes_sent = s.comm ? s.comm->bytes : 0;
+    });
 }
+
+// Host scheduling only (no device): the actions a sharded flush of `ops`
+// would take from the identity map, serialised as int64 records:
+// [kind(0 seg,1 exch), a, b, nops_or_0] followed by nops * nq_op for segments
+// (ops in physical bits, as kinds/targets of the lowered elementary ops).
+nq_status nq_shard_debug(int n, int world, const nq_op* ops, int64_t count, int64_t* buf, int64_t cap,
+                         int64_t* size) {
+    return guard([&] {
+        int g = 0;
+        while ((1 << g) < world) ++g;
+        if ((1 << g) != world || n - g < 1) throw NqError{NQ_ERR_CONTRACT, "bad world size"};
+        std::vector<EOp> q;
+        for (int64_t i = 0; i < count; ++i) lower_sv_op(ops[i], q);
+        const size_t nn = static_cast<size_t>(n);
+        std::vector<int> l2p(nn), p2l(nn);
+        for (int i = 0; i < n; ++i) l2p[size_t(i)] = p2l[size_t(i)] = i;
+        auto acts = schedule(q, l2p, p2l, n - g);
+        auto fin = schedule_identity(l2p, p2l, n - g, n);
+        acts.insert(acts.end(), fin.begin(), fin.end());
+        std::vector<int64_t> out;
+        for (const auto& a : acts) {
+            auto put = [&](std::initializer_list<int64_t> vals) { out.insert(out.end(), vals); };
+            if (a.kind == Action::Exchange) {
+                put({1, int64_t(a.gbit), int64_t(a.vbit), 0});
+                continue;
+            }
+            put({0, 0, 0, int64_t(a.ops.size())});
+            for (const auto& e : a.ops) {
+                // elementary op: type, k, bits[4], ctrl, matrix size, matrix (re,im as bit patterns)
+                put({int64_t(e.type), int64_t(e.k), int64_t(e.bits[0]), int64_t(e.bits[1]), int64_t(e.bits[2]),
+                     int64_t(e.bits[3]), int64_t(e.ctrl), int64_t(e.mat.size())});
+                for (const auto& v : e.mat) {
+                    int64_t re, im;
+                    const double vr = v.real(), vi = v.imag();
+                    std::memcpy(&re, &vr, 8);
+                    std::memcpy(&im, &vi, 8);
+                    out.push_back(re);
+                    out.push_back(im);
+                }
+            }
+        }
+        *size = int64_t(out.size());
+        if (buf && cap > 0) std::memcpy(buf, out.data(), size_t(std::min<int64_t>(cap, *size)) * 8);
+    });
 }
+
+}  // extern "C"

@@ -95,6 +95,8 @@ struct State {
     ShardComm* comm = nullptr;
 };
 
+void sv_expect_raw(State& s, const uint64_t* flip, const uint64_t* signs, int nterms, std::vector<cplx>& totals);
+
 void state_init(State& s, int n, bool dm, const nq_opts* opts);
 void state_free(State& s);
 void state_flush(State& s);
@@ -103,8 +105,11 @@ double* result_slot(DeviceCtx& c, int i);
 void fetch(DeviceCtx& c, const double* dsrc, size_t count, double* host);
 
 // sampling (sample.cpp): either amplitudes `a` or probabilities `p` (one is null)
+// cum_start: cumulative probability before this array (sharded states);
+// leftovers: whether uniforms beyond the final cumulative are assigned here.
 void sample_sweep(DeviceCtx& c, const double2* a, const double* p, uint64_t n, const double* sorted_u,
-                  uint64_t shots, uint64_t* idx_out, uint64_t* count_out, uint64_t* nout);
+                  uint64_t shots, uint64_t* idx_out, uint64_t* count_out, uint64_t* nout, double cum_start = 0.0,
+                  bool leftovers = true);
 
 // multi-GPU (shard.cpp)
 void shard_free(State& s);
@@ -118,3 +123,13 @@ void shard_sample(State& s, const double* sorted_u, uint64_t shots, uint64_t* id
 void shard_get_amplitudes(State& s, uint64_t offset, uint64_t count, double* host_out);
 
 }  // namespace nqe
+
+// The opaque C-ABI handles.
+extern "C" {
+struct nq_sv {
+    nqe::State s;
+};
+struct nq_dm {
+    nqe::State s;
+};
+}

@@ -1,0 +1,60 @@
+"""Sharded state vector over 2 GPUs (NCCL) against the oracle.
+
+Needs >= 2 visible GPUs (gpurun --gpus 2); skipped otherwise.  Each rank is a
+process owning one GPU; the NCCL unique id is created in the parent.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2401_06861_b200 import abi
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _rank_main(rank, world, uid, n, seed, outdir):
+    sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
+    from oracle import Port
+    from paper_2401_06861_b200 import abi as A
+
+    port = Port()
+    ops = port.random_circuit(seed, n, 300)
+    sv = A.SV.sharded(n, rank, world, uid, device=rank)
+    sv.apply(ops)
+    norm = sv.norm_sq()
+    rng = np.random.default_rng(seed)
+    terms = [("".join(rng.choice(list("IXYZ"), size=n)), float(rng.uniform(-1, 1))) for _ in range(12)]
+    terms.append(("X" * (n - 1) + "Z", 0.5))
+    ex = sv.expectations(terms)
+    u = np.sort(port.rng_double(99, 4000))
+    idx, cnt = sv.sample_sorted(u)
+    amps = sv.amplitudes()
+    stats = sv.comm_stats()
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), norm=norm, ex=ex, idx=idx, cnt=cnt, amps=amps,
+             exchanges=stats["exchanges"], letters=np.array([t[0] for t in terms]),
+             coeff=np.array([t[1] for t in terms]))
+
+
+@pytest.mark.parametrize("n", [14, 20])
+def test_sharded_two_gpus(port, tmp_path, n):
+    if abi.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    world, seed = 2, 808 + n
+    uid = abi.comm_unique_id()
+    mp.start_processes(_rank_main, args=(world, uid, n, seed, str(tmp_path)), nprocs=world, start_method="spawn")
+    ops = port.random_circuit(seed, n, 300)
+    want = port.sv_run(n, ops)
+    for r in range(world):
+        d = np.load(tmp_path / f"r{r}.npz")
+        assert int(d["exchanges"]) > 0
+        np.testing.assert_allclose(d["amps"], want, atol=1e-10, rtol=0)
+        assert abs(float(d["norm"]) - 1.0) < 1e-10
+        ref = [port.expectation(want, str(L), float(c)) for L, c in zip(d["letters"], d["coeff"])]
+        np.testing.assert_allclose(d["ex"], ref, atol=1e-10, rtol=0)
+        dense = np.zeros(1 << n, dtype=np.uint64)
+        dense[d["idx"].astype(np.int64)] = d["cnt"]
+        assert np.array_equal(dense, port.sample_distribution(np.abs(want) ** 2, 4000, 99))
