@@ -25,6 +25,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -292,6 +293,14 @@ class PassBuilder {
             return op;
         };
         uint32_t lay = stage_of.empty() ? fill(0) : stage_of[0];
+        // Coalescing: HBM is read and written in the first / last layout.  If
+        // those hold any of the 5 lowest tile bits in registers, a warp's 32
+        // lanes do not cover 32 consecutive amplitudes; then load (store) in
+        // the layout of the 4 highest tile bits and relayout through shared
+        // memory instead.
+        const uint32_t lane_bits = m >= 9 ? 0x1Fu : 0u;
+        const uint32_t top = fill(0);
+        if (coalesce_ && (lay & lane_bits)) p.ops.push_back(layout_op(top));
         p.ops.push_back(layout_op(lay));
         for (size_t i = 0; i < live.size(); ++i) {
             if (stage_of[i] != lay) {
@@ -344,8 +353,11 @@ class PassBuilder {
             }
             p.ops.push_back(op);
         }
+        if (coalesce_ && (lay & lane_bits)) p.ops.push_back(layout_op(top));
         return p;
     }
+
+    void set_coalesce(bool c) { coalesce_ = c; }
 
   private:
     void emit_group(const Group& g) {
@@ -492,6 +504,7 @@ class PassBuilder {
     }
 
     bool fuse_;
+    bool coalesce_ = true;
     std::vector<BitOp> ops_;
     std::vector<Group> pend_;
     size_t live_ = 0, pool_ = 0;
@@ -501,6 +514,18 @@ class PassBuilder {
 // permutations P and diagonal D (D' = D o P1..Pa).  Catches CX.RZ.CX (TFIM /
 // QAOA ZZ rotations), the CX.U1.CX halves of controlled phases (QFT) and, in
 // Liouville space, the row+column copies of those sandwiches.
+// NQ_COALESCE=1 enables the load/store relayouts.  Off by default: measured on
+// B200 (random circuit n = 30, tile 11) the extra shared-memory round trips
+// cost more (8.08 ms/pass) than the partially coalesced accesses (7.43 ms/pass),
+// whose DRAM traffic stays exactly algorithmic (L2 merges the sectors).
+bool coalesce_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("NQ_COALESCE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 bool perms_commute(const EOp& a, const EOp& b) {
     return !((a.ctrl >> b.bits[0]) & 1) && !((b.ctrl >> a.bits[0]) & 1);
 }
@@ -608,6 +633,7 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
         uint64_t qhigh = 0;  // required tile bits >= lb
         uint64_t blocked = 0;
         PassBuilder pb(opt.fuse);
+        pb.set_coalesce(coalesce_enabled());
         std::vector<const EOp*> deferred;
         size_t taken = 0;
         size_t i = 0;

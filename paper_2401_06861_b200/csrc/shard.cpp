@@ -356,7 +356,13 @@ void shard_flush(State& s) {
     std::vector<EOp> ops;
     ops.swap(s.queue);
     s.last_passes = s.last_microops = s.last_source_ops = s.last_launches = 0;
-    execute(s, schedule(ops, sc.l2p, sc.p2l, s.nloc));
+    std::vector<Action> acts = schedule(ops, sc.l2p, sc.p2l, s.nloc);
+    // Restore the identity qubit map at the end of the flush: every flush of
+    // the same circuit then runs the same physical program (so its
+    // pass-specialised kernels are reused), and readouts need no remap.
+    std::vector<Action> back = schedule_identity(sc.l2p, sc.p2l, s.nloc, s.n);
+    acts.insert(acts.end(), back.begin(), back.end());
+    execute(s, acts);
 }
 
 double shard_norm_sq(State& s) {
