@@ -226,13 +226,17 @@ def run_reference_arm(args, world, rank):
         return 0
     from paper_2401_06861_b200 import workloads
 
-    ops = workloads.random_circuit(args.seed, args.qubits, args.depth)
-    k = max(1, min(args.cpu_ops, len(ops)))
+    # same workload as the b200 arm: 30 + log2(N) qubits for N GPUs
+    n = args.qubits + (world.bit_length() - 1)
+    ops = workloads.random_circuit(args.seed, n, args.depth)
+    # bounded sample: fewer ops per step as the state doubles (a few s per step)
+    k = max(1, min(args.cpu_ops >> max(0, n - 30), len(ops)))
     total_steps = args.warmup + args.steps
-    res, why = cpu_reference_rate(args.qubits, ops, k, total_steps)
+    res, why = cpu_reference_rate(n, ops, k, total_steps)
     base = {"metric": "SV gates/s (random circuit, depth 200)", "unit": "gates/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "config": {"workload": f"random_circuit(Rng({args.seed})) n={args.qubits} depth={args.depth}",
+            "config": {"workload": f"random_circuit(Rng({args.seed})) n={args.qubits} depth={args.depth} "
+                                   f"(proj/tests/test_util.hpp generator)",
                        "qubits": args.qubits}}
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": why}))

@@ -164,7 +164,8 @@ void state_flush(State& s) {
         const unsigned char* rec = buf.data() + offs[i];
         if (!jit_launch(s.d, c.d_ops + offs[i], h, reinterpret_cast<const MOp*>(rec + h.op_off),
                         reinterpret_cast<const cplx*>(rec + h.pool_off), 0, c.stream, s.dev))
-            launch_pass(s.d, c.d_ops + offs[i], h, 0, c.stream);
+            launch_pass(s.d, c.d_ops + offs[i], h, 0, c.stream,
+                        reinterpret_cast<const MOp*>(rec + h.op_off)[0].k);
         if (ev) CUDA_TRY(cudaEventRecord(ev->second, c.stream));
         if (c.prof) c.prof_pass_bytes += 32.0 * double(s.count);
     }

@@ -88,6 +88,7 @@ struct PlanOptions {
     int tile_bits = 12;   // m
     int low_bits = 4;     // minimum contiguous low bits in every tile (coalescing)
     bool fuse = true;
+    int reg_bits = 4;     // amplitudes per thread = 2^reg_bits (3 or 4)
     int max_ops_per_pass = 192;
     int max_pool_per_pass = 1536;  // complex entries
 };

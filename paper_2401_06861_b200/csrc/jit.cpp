@@ -216,7 +216,7 @@ const JitKnobs& jit_knobs() {
 std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     const int m = h.m;
     const int SIZE = 1 << m;
-    const int E = 16;
+    const int E = 1 << ops[0].k;  // ops[0] is the load layout: 3 or 4 register bits
     const int T = SIZE / E;
     int logT = 0;
     while ((1 << logT) < T) ++logT;
@@ -251,7 +251,8 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     std::ostringstream s;
     s << "#include \"pass_ops.cuh\"\n"
       << "extern \"C\" __global__ void __launch_bounds__(" << T;
-    const int minb = kn.min_blocks >= 0 ? kn.min_blocks : std::max(1, 512 / T);
+    // 8 amplitudes per thread need ~half the registers: aim for 768 threads/SM
+    const int minb = kn.min_blocks >= 0 ? kn.min_blocks : std::max(1, (E == 8 ? 768 : 512) / T);
     if (minb > 0) s << ", " << minb;
     s << ")\n"
       << "nqjit(double2* __restrict__ st, const double2* __restrict__ gpool, unsigned long long rankbase,"
@@ -311,7 +312,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
           << "    const unsigned long long base = " << deposit_expr("(unsigned long long)r", rest, true) << ";\n"
           << "    const unsigned long long full = rankbase | base;\n"
           << "    (void)full;\n"
-          << "    double2 a[16];\n";
+          << "    double2 a[" << E << "];\n";
         for (int l = 0; l < E; ++l) s << "    a[" << l << "] = cur[sw0 ^ " << sw.apply(L0.rconst(l)) << "u];\n";
     } else {
         // direct streaming loads into the first register layout; one buffer
@@ -322,7 +323,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
           << "    const unsigned long long base = " << deposit_expr("(unsigned long long)r", rest, true) << ";\n"
           << "    const unsigned long long full = rankbase | base;\n"
           << "    (void)full;\n"
-          << "    double2 a[16];\n"
+          << "    double2 a[" << E << "];\n"
           << "    { const double2* src = st + base + toff_ld;\n";
         for (int l = 0; l < E; ++l) s << "      a[" << l << "] = ld_stream(src + " << hex64(reg_off(L0, l)) << ");\n";
         s << "    }\n";
@@ -346,22 +347,22 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
         }
         case MOP_DENSE:
             if (op.k == 1) {
-                s << "    d1<16, " << int(op.pos[0]) << ">(a, " << P << ");\n";
+                s << "    d1<" << E << ", " << int(op.pos[0]) << ">(a, " << P << ");\n";
             } else if (op.k == 2) {
-                s << "    d2<16, " << int(op.pos[0]) << ", " << int(op.pos[1]) << ">(a, " << P << ");\n";
+                s << "    d2<" << E << ", " << int(op.pos[0]) << ", " << int(op.pos[1]) << ">(a, " << P << ");\n";
             } else if (op.k == 3) {
-                s << "    d3<16, " << (6 - op.pos[0] - op.pos[1] - op.pos[2]) << ">(a, " << P << ");\n";
+                s << "    d3<" << E << ", " << (6 - op.pos[0] - op.pos[1] - op.pos[2]) << ">(a, " << P << ");\n";
             } else {
                 s << "    __syncthreads();\n    d4<16>(a, " << P << ", cur + tid * 16u);\n";
             }
             break;
         case MOP_SWAP:
-            s << "    swp<16, " << int(op.pos[0]) << ", " << int(op.pos[1]) << ">(a);\n";
+            s << "    swp<" << E << ", " << int(op.pos[0]) << ", " << int(op.pos[1]) << ">(a);\n";
             break;
         case MOP_DEPOL:
             if (op.k == 2) {
                 const int a0 = std::min(op.pos[0], op.pos[1]), a1 = std::max(op.pos[0], op.pos[1]);
-                s << "    dep2<16, " << a0 << ", " << a1 << ">(a, lds(" << P << ").x, lds(" << P << " + 1).x);\n";
+                s << "    dep2<" << E << ", " << a0 << ", " << a1 << ">(a, lds(" << P << ").x, lds(" << P << " + 1).x);\n";
             } else {
                 const int p0 = op.pos[0] == 0   ? op.pos[2]
                                : op.pos[2] == 0 ? op.pos[0]
@@ -381,7 +382,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
                 else cmT |= 1u << p;
             }
             s << "    if (((full & " << hex64(op.cmask_glob) << ") == " << hex64(op.cmask_glob) << ") && ((" << tbn
-              << " & " << cmT << "u) == " << cmT << "u)) xperm<16, " << int(op.pos[0]) << ">(a, " << cmL << "u);\n";
+              << " & " << cmT << "u) == " << cmT << "u)) xperm<" << E << ", " << int(op.pos[0]) << ">(a, " << cmL << "u);\n";
             break;
         }
         case MOP_DIAG: {
@@ -413,20 +414,30 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
                 s << "      } }\n";
             } else {
                 const unsigned regmask = slotc[0] | slotc[1] | slotc[2] | slotc[3];
+                // one shared-memory load per distinct table entry, then a plain
+                // complex multiply per amplitude (exact ones skipped at compile time)
+                std::map<unsigned, int> fidx;
+                std::ostringstream body;
                 for (int l = 0; l < E; ++l) {
                     unsigned c = 0;
                     for (int t = 0; t < 4; ++t)
                         if ((l >> t) & 1) c |= slotc[t];
-                    // entries that are exactly 1 for every thread/global choice are skipped
                     bool all_one = true;
                     for (int gi = 0; gi < (1 << op.k) && all_one; ++gi) {
                         if ((unsigned(gi) & regmask) != c) continue;
                         all_one = tab[gi] == cplx(1.0, 0.0);
                     }
                     if (all_one) continue;
-                    s << "      a[" << l << "] = dmul(a[" << l << "], lds(D + " << c << "u));\n";
+                    auto it = fidx.find(c);
+                    if (it == fidx.end()) {
+                        const int id = int(fidx.size());
+                        fidx[c] = id;
+                        s << "      const double2 f" << id << " = lds(D + " << c << "u);\n";
+                        it = fidx.find(c);
+                    }
+                    body << "      a[" << l << "] = cmul(f" << it->second << ", a[" << l << "]);\n";
                 }
-                s << "    }\n";
+                s << body.str() << "    }\n";
             }
             break;
         }
@@ -559,7 +570,7 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
         ++J.stats.misses;
         return false;
     }
-    const int T = (1 << h.m) / 16;
+    const int T = (1 << h.m) / (1 << ops[0].k);
     const size_t smem = (size_t(jit_knobs().prefetch ? 2 : 1) << h.m) * 16 + size_t(h.pool_n) * 16;
     int occ = 0;
     {

@@ -13,8 +13,9 @@ namespace nqe {
 // Every kernel launched by this library (for the bench's gpu_launches claim).
 extern std::atomic<int64_t> g_kernel_launches;
 
+// rbits: register bits of the pass's layouts (its first MOP_LAYOUT's k: 3 or 4)
 void launch_pass(double2* state, const unsigned char* dev_rec, const PassHdr& h, uint64_t rankbase,
-                 cudaStream_t s);
+                 cudaStream_t s, int rbits);
 void launch_init_basis(double2* a, uint64_t n, uint64_t one_at, cudaStream_t s);
 
 size_t scratch_doubles_needed(uint64_t n);

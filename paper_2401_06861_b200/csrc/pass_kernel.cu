@@ -34,10 +34,10 @@ namespace {
 
 using namespace nq;
 
-template <int M>
+template <int M, int RR>
 struct Geo {
     static constexpr int SIZE = 1 << M;
-    static constexpr int R = M < 4 ? M : 4;  // register bits
+    static constexpr int R = M < RR ? M : RR;  // register bits
     static constexpr int E = 1 << R;         // amplitudes per thread
     static constexpr int T = SIZE / E;       // threads per CTA
 };
@@ -49,9 +49,9 @@ struct Lay {
     uint32_t tb;    // this thread's tile-index bits (thread bits deposited)
 };
 
-template <int M>
+template <int M, int RR>
 __device__ __forceinline__ void set_layout(Lay& L, const int8_t* pos, int tid) {
-    constexpr int R = Geo<M>::R;
+    constexpr int R = Geo<M, RR>::R;
     uint32_t rmask = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -82,10 +82,10 @@ __device__ __forceinline__ uint32_t rpart(const Lay& L, int l) {
 // Diagonal operator: table index bit j comes from a register slot, a thread
 // bit, or a full-index bit outside the tile.  Per amplitude: a compile-time
 // OR of per-slot contributions, one broadcast-friendly LDS, one cmul.
-template <int M>
-__device__ __forceinline__ void diag_op(double2 (&a)[Geo<M>::E], const Lay& L, const MOp& op, const double2* tab,
+template <int M, int RR>
+__device__ __forceinline__ void diag_op(double2 (&a)[Geo<M, RR>::E], const Lay& L, const MOp& op, const double2* tab,
                                         uint64_t full) {
-    constexpr int E = Geo<M>::E, R = Geo<M>::R;
+    constexpr int E = Geo<M, RR>::E, R = Geo<M, RR>::R;
     uint32_t base = 0;       // thread + global contributions
     uint32_t ms[4] = {0, 0, 0, 0};  // contribution of register slot s
     bool any_reg = false;
@@ -120,10 +120,10 @@ __device__ __forceinline__ void diag_op(double2 (&a)[Geo<M>::E], const Lay& L, c
     }
 }
 
-template <int M>
-__device__ __forceinline__ void dense_op(double2 (&a)[Geo<M>::E], const MOp& op, const double2* u,
+template <int M, int RR>
+__device__ __forceinline__ void dense_op(double2 (&a)[Geo<M, RR>::E], const MOp& op, const double2* u,
                                          double2* scratch) {
-    constexpr int E = Geo<M>::E, R = Geo<M>::R;
+    constexpr int E = Geo<M, RR>::E, R = Geo<M, RR>::R;
     if (op.k == 1) {
         switch (op.pos[0]) {
         case 0: d1<E, 0>(a, u); break;
@@ -158,9 +158,9 @@ __device__ __forceinline__ void dense_op(double2 (&a)[Geo<M>::E], const MOp& op,
     }
 }
 
-template <int M>
-__device__ __forceinline__ void xperm_op(double2 (&a)[Geo<M>::E], const Lay& L, const MOp& op, uint64_t full) {
-    constexpr int E = Geo<M>::E, R = Geo<M>::R;
+template <int M, int RR>
+__device__ __forceinline__ void xperm_op(double2 (&a)[Geo<M, RR>::E], const Lay& L, const MOp& op, uint64_t full) {
+    constexpr int E = Geo<M, RR>::E, R = Geo<M, RR>::R;
     if ((full & op.cmask_glob) != op.cmask_glob) return;
     // split tile controls into register-slot controls and thread-bit controls
     uint32_t cmL = 0, cmT = 0;
@@ -183,9 +183,9 @@ __device__ __forceinline__ void xperm_op(double2 (&a)[Geo<M>::E], const Lay& L, 
     }
 }
 
-template <int M>
-__device__ __forceinline__ void swap_op(double2 (&a)[Geo<M>::E], const MOp& op) {
-    constexpr int E = Geo<M>::E, R = Geo<M>::R;
+template <int M, int RR>
+__device__ __forceinline__ void swap_op(double2 (&a)[Geo<M, RR>::E], const MOp& op) {
+    constexpr int E = Geo<M, RR>::E, R = Geo<M, RR>::R;
     if constexpr (R >= 2) {
         switch (op.pos[0] * 4 + op.pos[1]) {
         case 1: swp<E, 0, 1>(a); break;
@@ -198,9 +198,9 @@ __device__ __forceinline__ void swap_op(double2 (&a)[Geo<M>::E], const MOp& op) 
     }
 }
 
-template <int M>
-__device__ __forceinline__ void depol_op(double2 (&a)[Geo<M>::E], const MOp& op, const double2* p) {
-    constexpr int E = Geo<M>::E, R = Geo<M>::R;
+template <int M, int RR>
+__device__ __forceinline__ void depol_op(double2 (&a)[Geo<M, RR>::E], const MOp& op, const double2* p) {
+    constexpr int E = Geo<M, RR>::E, R = Geo<M, RR>::R;
     const double al = lds(p).x, be = lds(p + 1).x;
     if (op.k == 2) {
         if constexpr (R >= 2) {
@@ -233,7 +233,7 @@ __device__ __forceinline__ uint64_t deposit(uint64_t v, const int8_t* pos, int c
 }
 
 // State offset of tile element e (tile bit i <-> state bit q[i]).
-template <int M>
+template <int M, int RR>
 __device__ __forceinline__ uint64_t tile_off(uint32_t e, const int8_t* q) {
     uint64_t r = 0;
 #pragma unroll
@@ -242,10 +242,10 @@ __device__ __forceinline__ uint64_t tile_off(uint32_t e, const int8_t* q) {
     return r;
 }
 
-template <int M>
-__global__ void __launch_bounds__(Geo<M>::T, (Geo<M>::T >= 256 ? 512 / Geo<M>::T : 1))
+template <int M, int RR>
+__global__ void __launch_bounds__(Geo<M, RR>::T, (Geo<M, RR>::T >= 256 ? 512 / Geo<M, RR>::T : 1))
     pass_kernel(double2* __restrict__ st, const unsigned char* __restrict__ rec, uint64_t rankbase) {
-    constexpr int SIZE = Geo<M>::SIZE, R = Geo<M>::R, E = Geo<M>::E, T = Geo<M>::T;
+    constexpr int SIZE = Geo<M, RR>::SIZE, R = Geo<M, RR>::R, E = Geo<M, RR>::E, T = Geo<M, RR>::T;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int8_t s_q[16];
     __shared__ int8_t s_rest[56];
@@ -269,10 +269,10 @@ __global__ void __launch_bounds__(Geo<M>::T, (Geo<M>::T >= 256 ? 512 / Geo<M>::T
 
     // ops[0] is the load layout
     Lay L0;
-    set_layout<M>(L0, ops[0].pos, tid);
+    set_layout<M, RR>(L0, ops[0].pos, tid);
     const int nrest = h->nrest;
     const int64_t ntiles = h->ntiles;
-    const uint64_t off0 = tile_off<M>(L0.tb, s_q);
+    const uint64_t off0 = tile_off<M, RR>(L0.tb, s_q);
     uint64_t roff0[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) roff0[j] = j < R ? uint64_t(1) << s_q[L0.rp[j]] : 0;
@@ -299,18 +299,18 @@ __global__ void __launch_bounds__(Geo<M>::T, (Geo<M>::T >= 256 ? 512 / Geo<M>::T
             switch (op.type) {
             case MOP_DENSE:
                 if (op.k == 4) __syncthreads();  // scratch rows alias the relayout buffer
-                dense_op<M>(a, op, pool + op.mat, scratch);
+                dense_op<M, RR>(a, op, pool + op.mat, scratch);
                 break;
-            case MOP_DIAG: diag_op<M>(a, L, op, pool + op.mat, full); break;
-            case MOP_XPERM: xperm_op<M>(a, L, op, full); break;
-            case MOP_SWAP: swap_op<M>(a, op); break;
-            case MOP_DEPOL: depol_op<M>(a, op, pool + op.mat); break;
+            case MOP_DIAG: diag_op<M, RR>(a, L, op, pool + op.mat, full); break;
+            case MOP_XPERM: xperm_op<M, RR>(a, L, op, full); break;
+            case MOP_SWAP: swap_op<M, RR>(a, op); break;
+            case MOP_DEPOL: depol_op<M, RR>(a, op, pool + op.mat); break;
             case MOP_LAYOUT:
                 if constexpr (R < M) {
                     __syncthreads();  // previous readers of the buffer are done
 #pragma unroll
                     for (int l = 0; l < E; ++l) tile[swz(L.tb | rpart<R>(L, l))] = a[l];
-                    set_layout<M>(L, op.pos, tid);
+                    set_layout<M, RR>(L, op.pos, tid);
                     __syncthreads();
 #pragma unroll
                     for (int l = 0; l < E; ++l) a[l] = tile[swz(L.tb | rpart<R>(L, l))];
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(Geo<M>::T, (Geo<M>::T >= 256 ? 512 / Geo<M>::T
             }
         }
         {
-            const uint64_t offs = tile_off<M>(L.tb, s_q);
+            const uint64_t offs = tile_off<M, RR>(L.tb, s_q);
             uint64_t ro[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) ro[j] = j < R ? uint64_t(1) << s_q[L.rp[j]] : 0;
@@ -351,9 +351,9 @@ int sm_count() {
     return s;
 }
 
-template <int M>
+template <int M, int RR>
 void launch_pass_m(double2* state, const unsigned char* rec, const PassHdr& h, uint64_t rankbase, cudaStream_t s) {
-    constexpr int SIZE = Geo<M>::SIZE, T = Geo<M>::T;
+    constexpr int SIZE = Geo<M, RR>::SIZE, T = Geo<M, RR>::T;
     const size_t smem = size_t(SIZE) * 16 + size_t(h.pool_n) * 16 + size_t(h.nops) * sizeof(MOp);
     static std::mutex mu;
     static std::map<std::pair<int, size_t>, int> occ_cache;
@@ -365,8 +365,8 @@ void launch_pass_m(double2* state, const unsigned char* rec, const PassHdr& h, u
         auto key = std::make_pair(dev, smem);
         auto it = occ_cache.find(key);
         if (it == occ_cache.end()) {
-            cudaFuncSetAttribute(pass_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass_kernel<M>, T, smem);
+            cudaFuncSetAttribute(pass_kernel<M, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass_kernel<M, RR>, T, smem);
             if (occ < 1) occ = 1;
             occ_cache[key] = occ;
         } else {
@@ -374,28 +374,40 @@ void launch_pass_m(double2* state, const unsigned char* rec, const PassHdr& h, u
         }
     }
     const int64_t grid = std::min<int64_t>(h.ntiles, int64_t(sm_count()) * occ);
-    pass_kernel<M><<<unsigned(grid), T, smem, s>>>(state, rec, rankbase);
+    pass_kernel<M, RR><<<unsigned(grid), T, smem, s>>>(state, rec, rankbase);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+template <int M>
+void launch_pass_r(double2* state, const unsigned char* rec, const PassHdr& h, uint64_t rankbase, cudaStream_t s,
+                   int rbits) {
+    if constexpr (M >= 5) {
+        if (rbits == 3) {
+            launch_pass_m<M, 3>(state, rec, h, rankbase, s);
+            return;
+        }
+    }
+    launch_pass_m<M, 4>(state, rec, h, rankbase, s);
 }
 
 }  // namespace
 
 void launch_pass(double2* state, const unsigned char* dev_rec, const PassHdr& h, uint64_t rankbase,
-                 cudaStream_t s) {
+                 cudaStream_t s, int rbits) {
     switch (h.m) {
-    case 1: launch_pass_m<1>(state, dev_rec, h, rankbase, s); break;
-    case 2: launch_pass_m<2>(state, dev_rec, h, rankbase, s); break;
-    case 3: launch_pass_m<3>(state, dev_rec, h, rankbase, s); break;
-    case 4: launch_pass_m<4>(state, dev_rec, h, rankbase, s); break;
-    case 5: launch_pass_m<5>(state, dev_rec, h, rankbase, s); break;
-    case 6: launch_pass_m<6>(state, dev_rec, h, rankbase, s); break;
-    case 7: launch_pass_m<7>(state, dev_rec, h, rankbase, s); break;
-    case 8: launch_pass_m<8>(state, dev_rec, h, rankbase, s); break;
-    case 9: launch_pass_m<9>(state, dev_rec, h, rankbase, s); break;
-    case 10: launch_pass_m<10>(state, dev_rec, h, rankbase, s); break;
-    case 11: launch_pass_m<11>(state, dev_rec, h, rankbase, s); break;
-    case 12: launch_pass_m<12>(state, dev_rec, h, rankbase, s); break;
-    case 13: launch_pass_m<13>(state, dev_rec, h, rankbase, s); break;
+    case 1: launch_pass_r<1>(state, dev_rec, h, rankbase, s, rbits); break;
+    case 2: launch_pass_r<2>(state, dev_rec, h, rankbase, s, rbits); break;
+    case 3: launch_pass_r<3>(state, dev_rec, h, rankbase, s, rbits); break;
+    case 4: launch_pass_r<4>(state, dev_rec, h, rankbase, s, rbits); break;
+    case 5: launch_pass_r<5>(state, dev_rec, h, rankbase, s, rbits); break;
+    case 6: launch_pass_r<6>(state, dev_rec, h, rankbase, s, rbits); break;
+    case 7: launch_pass_r<7>(state, dev_rec, h, rankbase, s, rbits); break;
+    case 8: launch_pass_r<8>(state, dev_rec, h, rankbase, s, rbits); break;
+    case 9: launch_pass_r<9>(state, dev_rec, h, rankbase, s, rbits); break;
+    case 10: launch_pass_r<10>(state, dev_rec, h, rankbase, s, rbits); break;
+    case 11: launch_pass_r<11>(state, dev_rec, h, rankbase, s, rbits); break;
+    case 12: launch_pass_r<12>(state, dev_rec, h, rankbase, s, rbits); break;
+    case 13: launch_pass_r<13>(state, dev_rec, h, rankbase, s, rbits); break;
     default: throw std::logic_error("launch_pass: unsupported tile size " + std::to_string(h.m));
     }
 }

@@ -230,7 +230,12 @@ class PassBuilder {
         for (const auto& g : pend_) emit_group(g);
         pend_.clear();
         const int m = int(q.size());
-        const int rsz = std::min(4, m);
+        // register bits per thread: reg_bits_ (3 or 4), but 4 whenever an op
+        // needs four register-resident bits (2-qubit superoperators)
+        bool need4 = false;
+        for (const auto& b : ops_)
+            if (b.alive && b.k == 4 && (b.type == MOP_DENSE || b.type == MOP_DEPOL)) need4 = true;
+        const int rsz = std::min(need4 ? 4 : reg_bits_, m);
         int tpos[kMaxStateBits];
         std::fill(std::begin(tpos), std::end(tpos), -1);
         for (size_t i = 0; i < q.size(); ++i) tpos[q[i]] = int(i);
@@ -358,6 +363,7 @@ class PassBuilder {
     }
 
     void set_coalesce(bool c) { coalesce_ = c; }
+    void set_reg_bits(int r) { reg_bits_ = r; }
 
   private:
     void emit_group(const Group& g) {
@@ -505,6 +511,7 @@ class PassBuilder {
 
     bool fuse_;
     bool coalesce_ = true;
+    int reg_bits_ = 4;
     std::vector<BitOp> ops_;
     std::vector<Group> pend_;
     size_t live_ = 0, pool_ = 0;
@@ -524,6 +531,15 @@ bool coalesce_enabled() {
         return e && e[0] == '1';
     }();
     return on;
+}
+
+// NQ_REGBITS=3|4 overrides PlanOptions::reg_bits (A/B measurements).
+int reg_bits_env(int dflt) {
+    static const int v = [] {
+        const char* e = std::getenv("NQ_REGBITS");
+        return e ? std::atoi(e) : 0;
+    }();
+    return (v == 3 || v == 4) ? v : dflt;
 }
 
 bool perms_commute(const EOp& a, const EOp& b) {
@@ -629,13 +645,21 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
         remaining.push_back(&e);
     }
 
-    while (!remaining.empty()) {
-        uint64_t qhigh = 0;  // required tile bits >= lb
-        uint64_t blocked = 0;
-        PassBuilder pb(opt.fuse);
-        pb.set_coalesce(coalesce_enabled());
-        std::vector<const EOp*> deferred;
+    struct Trial {
+        PassBuilder pb;
+        uint64_t qhigh = 0;
         size_t taken = 0;
+        std::vector<const EOp*> next;
+        explicit Trial(bool fuse) : pb(fuse) {}
+    };
+    // One pass from `remaining`, with the high tile bits optionally pre-seeded.
+    auto build = [&](uint64_t seed) {
+        Trial t(opt.fuse);
+        t.pb.set_coalesce(coalesce_enabled());
+        t.pb.set_reg_bits(reg_bits_env(opt.reg_bits));
+        t.qhigh = seed;
+        uint64_t blocked = 0;
+        std::vector<const EOp*> deferred;
         size_t i = 0;
         for (; i < remaining.size(); ++i) {
             const EOp* e = remaining[i];
@@ -649,15 +673,15 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
                 }
                 continue;
             }
-            const uint64_t nh = qhigh | (need_mask(*e) & ~low_mask);
+            const uint64_t nh = t.qhigh | (need_mask(*e) & ~low_mask);
             const bool fits = popcount64(nh) <= m - lb;
-            const bool caps = (pb.microops() + 1 <= size_t(opt.max_ops_per_pass)) &&
-                              (pb.pool() + size_t(pool_cost(*e)) <= size_t(opt.max_pool_per_pass));
-            if (!caps && taken > 0) break;  // close the pass; the rest goes to the next one
+            const bool caps = (t.pb.microops() + 1 <= size_t(opt.max_ops_per_pass)) &&
+                              (t.pb.pool() + size_t(pool_cost(*e)) <= size_t(opt.max_pool_per_pass));
+            if (!caps && t.taken > 0) break;  // close the pass; the rest goes to the next one
             if (fits) {
-                qhigh = nh;
-                pb.add(*e);
-                ++taken;
+                t.qhigh = nh;
+                t.pb.add(*e);
+                ++t.taken;
             } else {
                 deferred.push_back(e);
                 blocked |= touched;
@@ -667,8 +691,50 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
                 }
             }
         }
-        std::vector<const EOp*> next = deferred;
-        next.insert(next.end(), remaining.begin() + long(i), remaining.end());
+        t.next = deferred;
+        t.next.insert(t.next.end(), remaining.begin() + long(i), remaining.end());
+        return t;
+    };
+    // Seeds: the plain in-order greedy, and the high bits most needed by the
+    // next W ops (W = 24, 48, 96); keep the trial that takes the most ops.
+    auto freq_seed = [&](size_t w) {
+        int cnt[64] = {0};
+        for (size_t i = 0; i < remaining.size() && i < w; ++i) {
+            const uint64_t nm = need_mask(*remaining[i]) & ~low_mask;
+            for (int b = 0; b < 64; ++b)
+                if ((nm >> b) & 1) ++cnt[b];
+        }
+        uint64_t seed = 0;
+        for (int k = 0; k < m - lb; ++k) {
+            int best = -1;
+            for (int b = 0; b < 64; ++b)
+                if (cnt[b] > 0 && !((seed >> b) & 1) && (best < 0 || cnt[b] > cnt[best])) best = b;
+            if (best < 0) break;
+            seed |= bit(best);
+        }
+        return seed;
+    };
+    // Off by default: on the BASELINE workloads (random-30, QFT-30, TFIM-28,
+    // VQE-28) it found no plan with fewer passes than the plain greedy.
+    static const bool seeds_env = [] {
+        const char* e = std::getenv("NQ_PLAN_SEEDS");
+        return e && e[0] == '1';
+    }();
+    const bool multi_seed = seeds_env && opt.fuse && nloc > m;
+    while (!remaining.empty()) {
+        Trial t = build(0);
+        if (multi_seed) {
+            for (size_t w : {size_t(24), size_t(48), size_t(96)}) {
+                const uint64_t seed = freq_seed(w);
+                if (!seed) continue;
+                Trial c = build(seed);
+                if (c.taken > t.taken) t = std::move(c);
+            }
+        }
+        PassBuilder& pb = t.pb;
+        uint64_t qhigh = t.qhigh;
+        size_t taken = t.taken;
+        std::vector<const EOp*> next = std::move(t.next);
         if (taken == 0 && !next.empty()) {
             // every op needs <= kMaxOpK <= m - lb high bits, so the first one always
             // fits alone; take it to guarantee progress
