@@ -345,17 +345,21 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
                 s << "    a[" << l << "] = cur[sw" << li << " ^ " << sw.apply(L.rconst(l)) << "u];\n";
             break;
         }
-        case MOP_DENSE:
+        case MOP_DENSE: {
+            bool real = true;
+            for (size_t i = 0; i < (size_t(1) << (2 * op.k)) && real; ++i) real = pool[op.mat + i].imag() == 0.0;
+            const char* R = real ? ", true" : "";
             if (op.k == 1) {
-                s << "    d1<" << E << ", " << int(op.pos[0]) << ">(a, " << P << ");\n";
+                s << "    d1<" << E << ", " << int(op.pos[0]) << R << ">(a, " << P << ");\n";
             } else if (op.k == 2) {
-                s << "    d2<" << E << ", " << int(op.pos[0]) << ", " << int(op.pos[1]) << ">(a, " << P << ");\n";
+                s << "    d2<" << E << ", " << int(op.pos[0]) << ", " << int(op.pos[1]) << R << ">(a, " << P << ");\n";
             } else if (op.k == 3) {
-                s << "    d3<" << E << ", " << (6 - op.pos[0] - op.pos[1] - op.pos[2]) << ">(a, " << P << ");\n";
+                s << "    d3<" << E << ", " << (6 - op.pos[0] - op.pos[1] - op.pos[2]) << R << ">(a, " << P << ");\n";
             } else {
-                s << "    __syncthreads();\n    d4<16>(a, " << P << ", cur + tid * 16u);\n";
+                s << "    __syncthreads();\n    d4<16" << R << ">(a, " << P << ", cur + tid * 16u);\n";
             }
             break;
+        }
         case MOP_SWAP:
             s << "    swp<" << E << ", " << int(op.pos[0]) << ", " << int(op.pos[1]) << ">(a);\n";
             break;

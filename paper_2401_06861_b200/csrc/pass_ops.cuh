@@ -53,7 +53,20 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // a <- diag factor f, skipping exact ones (d0 = 1 diagonals touch half the amplitudes)
 __device__ __forceinline__ double2 dmul(double2 a, double2 f) { return is_one(f) ? a : cmul(f, a); }
 
-template <int E, int J>
+// Matrix-entry products; R = true when the pass compiler proved every entry of
+// the matrix real (H, RY and their products): half the FP64 work.
+template <bool R>
+__device__ __forceinline__ double2 mmul(double2 u, double2 x) {
+    if constexpr (R) return make_double2(u.x * x.x, u.x * x.y);
+    else return cmul(u, x);
+}
+template <bool R>
+__device__ __forceinline__ double2 mfma(double2 u, double2 x, double2 acc) {
+    if constexpr (R) return make_double2(fma(u.x, x.x, acc.x), fma(u.x, x.y, acc.y));
+    else return cfma(u, x, acc);
+}
+
+template <int E, int J, bool R = false>
 __device__ __forceinline__ void d1(double2 (&a)[E], const double2* u) {
     const double2 u00 = lds(u), u01 = lds(u + 1), u10 = lds(u + 2), u11 = lds(u + 3);
 #pragma unroll
@@ -61,12 +74,12 @@ __device__ __forceinline__ void d1(double2 (&a)[E], const double2* u) {
         if ((l >> J) & 1) continue;
         const int h = l | (1 << J);
         const double2 x0 = a[l], x1 = a[h];
-        a[l] = cfma(u00, x0, cmul(u01, x1));
-        a[h] = cfma(u10, x0, cmul(u11, x1));
+        a[l] = mfma<R>(u00, x0, mmul<R>(u01, x1));
+        a[h] = mfma<R>(u10, x0, mmul<R>(u11, x1));
     }
 }
 
-template <int E, int J0, int J1>
+template <int E, int J0, int J1, bool R = false>
 __device__ __forceinline__ void d2(double2 (&a)[E], const double2* u) {
 #pragma unroll
     for (int l = 0; l < E; ++l) {
@@ -75,17 +88,17 @@ __device__ __forceinline__ void d2(double2 (&a)[E], const double2* u) {
         const double2 x0 = a[i0], x1 = a[i1], x2 = a[i2], x3 = a[i3];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-            double2 acc = cmul(lds(u + 4 * r), x0);
-            acc = cfma(lds(u + 4 * r + 1), x1, acc);
-            acc = cfma(lds(u + 4 * r + 2), x2, acc);
-            acc = cfma(lds(u + 4 * r + 3), x3, acc);
+            double2 acc = mmul<R>(lds(u + 4 * r), x0);
+            acc = mfma<R>(lds(u + 4 * r + 1), x1, acc);
+            acc = mfma<R>(lds(u + 4 * r + 2), x2, acc);
+            acc = mfma<R>(lds(u + 4 * r + 3), x3, acc);
             a[r == 0 ? i0 : r == 1 ? i1 : r == 2 ? i2 : i3] = acc;
         }
     }
 }
 
 // k = 3 on all slots except `Skip` (local bit order = ascending slots).
-template <int E, int Skip>
+template <int E, int Skip, bool R = false>
 __device__ __forceinline__ void d3(double2 (&a)[E], const double2* u) {
     constexpr int J0 = Skip == 0 ? 1 : 0;
     constexpr int J1 = Skip <= 1 ? 2 : 1;
@@ -98,25 +111,25 @@ __device__ __forceinline__ void d3(double2 (&a)[E], const double2* u) {
         for (int c = 0; c < 8; ++c) x[c] = a[l | ((c & 1) << J0) | (((c >> 1) & 1) << J1) | (((c >> 2) & 1) << J2)];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            double2 acc = cmul(lds(u + 8 * r), x[0]);
+            double2 acc = mmul<R>(lds(u + 8 * r), x[0]);
 #pragma unroll
-            for (int c = 1; c < 8; ++c) acc = cfma(lds(u + 8 * r + c), x[c], acc);
+            for (int c = 1; c < 8; ++c) acc = mfma<R>(lds(u + 8 * r + c), x[c], acc);
             a[l | ((r & 1) << J0) | (((r >> 1) & 1) << J1) | (((r >> 2) & 1) << J2)] = acc;
         }
     }
 }
 
 // k = 4 on all slots: inputs parked in this thread's private scratch row.
-template <int E>
+template <int E, bool R = false>
 __device__ __forceinline__ void d4(double2 (&a)[E], const double2* u, double2* scratch) {
     if constexpr (E == 16) {
 #pragma unroll
         for (int c = 0; c < 16; ++c) scratch[c] = a[c];
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
-            double2 acc = cmul(lds(u + 16 * r), lds(scratch));
+            double2 acc = mmul<R>(lds(u + 16 * r), lds(scratch));
 #pragma unroll
-            for (int c = 1; c < 16; ++c) acc = cfma(lds(u + 16 * r + c), lds(scratch + c), acc);
+            for (int c = 1; c < 16; ++c) acc = mfma<R>(lds(u + 16 * r + c), lds(scratch + c), acc);
             a[r] = acc;
         }
     }

@@ -619,6 +619,53 @@ std::vector<EOp> cancel_perm_sandwiches(const std::vector<EOp>& in) {
     return out;
 }
 
+// Global phase hoisting.  A diagonal table t acts as t[0] * (t / t[0]); the
+// scalar t[0] commutes with everything, so it is multiplied into one dense
+// micro-op instead (a dense op touches every amplitude exactly once).  The
+// rescaled table has an exact 1 in entry 0, which the JIT turns into skipped
+// complex multiplies (RZ(theta) -> diag(1, e^{i theta}) halves its FP64 work).
+// Controlled micro-ops are left alone; a complex dense op is preferred as the
+// carrier so real matrices keep their cheaper real form.
+bool mat_is_real(const std::vector<cplx>& pool, uint32_t off, size_t n) {
+    for (size_t i = 0; i < n; ++i)
+        if (pool[off + i].imag() != 0.0) return false;
+    return true;
+}
+
+void hoist_global_phase(std::vector<PlannedPass>& passes) {
+    PlannedPass* cp = nullptr;
+    const MOp* carrier = nullptr;
+    for (auto& p : passes) {
+        for (const auto& op : p.ops) {
+            if (op.type != MOP_DENSE || op.cmask_tile || op.cmask_glob) continue;
+            const size_t n = size_t(1) << (2 * op.k);
+            if (!carrier || (mat_is_real(cp->pool, carrier->mat, size_t(1) << (2 * carrier->k)) &&
+                             !mat_is_real(p.pool, op.mat, n))) {
+                carrier = &op;
+                cp = &p;
+            }
+        }
+    }
+    if (!carrier) return;
+    cplx phase(1.0, 0.0);
+    for (auto& p : passes) {
+        for (const auto& op : p.ops) {
+            if (op.type != MOP_DIAG || op.cmask_tile || op.cmask_glob || op.k == 0) continue;
+            const cplx f = p.pool[op.mat];
+            if (f == cplx(1.0, 0.0)) continue;
+            const double af = std::abs(f);
+            if (!(af > 0.5 && af < 2.0)) continue;
+            const cplx inv = std::conj(f) / (af * af);
+            for (size_t i = 1; i < (size_t(1) << op.k); ++i) p.pool[op.mat + i] *= inv;
+            p.pool[op.mat] = cplx(1.0, 0.0);
+            phase *= f;
+        }
+    }
+    if (phase == cplx(1.0, 0.0)) return;
+    const size_t n = size_t(1) << (2 * carrier->k);
+    for (size_t i = 0; i < n; ++i) cp->pool[carrier->mat + i] *= phase;
+}
+
 }  // namespace
 
 std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanOptions& opt,
@@ -753,6 +800,7 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
         if (p.ops.size() > 1) passes.push_back(std::move(p));  // ops[0] is the load layout
         remaining.swap(next);
     }
+    if (opt.fuse) hoist_global_phase(passes);
     if (stats) {
         stats->passes = int64_t(passes.size());
         stats->microops = 0;
