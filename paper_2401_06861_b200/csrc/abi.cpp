@@ -410,14 +410,21 @@ void sv_expect_raw(State& s, const uint64_t* flip, const uint64_t* signs, int nt
         for (int t = 0; t < nterms; ++t)
             eps[size_t(t)] = (flip[t] != 0 && (__builtin_popcountll(flip[t] & signs[t]) & 1)) ? 1 : 0;
         // 1) batches of terms whose flips fit one tile: one state read per batch
-        const int m = std::min(11, s.nloc);
-        const int lb = s.nloc <= 11 ? m : 4;
+        const int m = std::min(12, s.nloc);
+        const int lb = s.nloc <= 12 ? m : 4;
         const uint64_t lowm = (uint64_t(1) << lb) - 1;
         std::vector<ExpBatch> batches;
         std::vector<uint64_t> bhigh;
         std::vector<std::pair<int, int>> slot_of{static_cast<size_t>(nterms)};  // (batch or launch, index)
         std::vector<int> tiled(size_t(nterms), 0);
-        for (int t = 0; t < nterms; ++t) {
+        // X/Y-type terms pick the batches (their flips fix the tile bits);
+        // Z-type terms then fill free slots anywhere
+        std::vector<int> order;
+        for (int t = 0; t < nterms; ++t)
+            if (flip[t]) order.push_back(t);
+        for (int t = 0; t < nterms; ++t)
+            if (!flip[t]) order.push_back(t);
+        for (int t : order) {
             const uint64_t hi = flip[t] & ~lowm;
             if (__builtin_popcountll(hi) > m - lb) continue;
             size_t b = 0;
@@ -472,7 +479,8 @@ void sv_expect_raw(State& s, const uint64_t* flip, const uint64_t* signs, int nt
                 E.f0 = E.ftile ? __builtin_ctz(E.ftile) : 0;
                 E.eps_im = eps[size_t(t)];
             }
-            launch_expect_tiled(s.d, s.nloc, B, c.d_scratch, tiled_res + b * kMaxExpTerms, c.stream);
+            if (!jit_expect_launch(s.d, s.nloc, B, c.d_scratch, tiled_res + b * kMaxExpTerms, c.stream, s.dev))
+                launch_expect_tiled(s.d, s.nloc, B, c.d_scratch, tiled_res + b * kMaxExpTerms, c.stream);
         }
         // 2) terms with wide flips: one read per flip group
         double* results = tiled_res + res_tiled;

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 
 namespace nqe {
 
@@ -38,7 +39,8 @@ __global__ void __launch_bounds__(kThreads) k_expect_tile(const double2* __restr
     constexpr int SIZE = 1 << M;
     constexpr int T = SIZE < kThreads ? SIZE : kThreads;
     constexpr int EPT = SIZE / T;
-    __shared__ double2 tile[SIZE];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* tile = reinterpret_cast<double2*>(smem_raw);
     __shared__ uint64_t s_offj[EPT];
     __shared__ double red[kThreads / 32][kMaxExpTerms];
     const int tid = threadIdx.x;
@@ -117,7 +119,18 @@ __global__ void k_final_cols(const double* __restrict__ part, int nblk, int stri
 template <int M>
 void launch_m(const double2* a, const ExpBatch& b, int64_t ntiles, double* part, double* out, cudaStream_t s) {
     const int grid = int(std::min<int64_t>(ntiles, kGrid));
-    k_expect_tile<M><<<grid, kThreads, 0, s>>>(a, b, ntiles, part);
+    const size_t smem = size_t(16) << M;
+    if (smem > 48 * 1024) {
+        static std::atomic<uint64_t> done{0};  // devices that have the attribute set
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t bitd = uint64_t(1) << (dev & 63);
+        if (!(done.load() & bitd)) {
+            cudaFuncSetAttribute(k_expect_tile<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            done.fetch_or(bitd);
+        }
+    }
+    k_expect_tile<M><<<grid, kThreads, smem, s>>>(a, b, ntiles, part);
     k_final_cols<<<1, kThreads, 0, s>>>(part, grid, kMaxExpTerms, b.nt, out);
     g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
 }
@@ -139,8 +152,14 @@ void launch_expect_tiled(const double2* a, int nloc, const ExpBatch& b, double* 
     case 8: launch_m<8>(a, b, ntiles, part, out, s); break;
     case 9: launch_m<9>(a, b, ntiles, part, out, s); break;
     case 10: launch_m<10>(a, b, ntiles, part, out, s); break;
-    default: launch_m<11>(a, b, ntiles, part, out, s); break;
+    case 11: launch_m<11>(a, b, ntiles, part, out, s); break;
+    default: launch_m<12>(a, b, ntiles, part, out, s); break;
     }
+}
+
+void launch_expect_final(const double* part, int nblk, int nt, double* out, cudaStream_t s) {
+    k_final_cols<<<1, kThreads, 0, s>>>(part, nblk, kMaxExpTerms, nt, out);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 }  // namespace nqe

@@ -531,12 +531,11 @@ JitMode jit_mode() {
     return m;
 }
 
-bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,
-                uint64_t rankbase, cudaStream_t s, int device) {
-    const JitMode mode = jit_mode();
-    if (mode == JitMode::Off || h.m < 8 || h.m > 12) return false;
-    if (mode == JitMode::Auto && h.nloc < 18) return false;  // interpreter is fine for small states
-    std::string src = jit_source(h, ops, pool);
+namespace {
+
+// The compiled entry for `src` when it is ready; otherwise nullptr after
+// queueing its compilation (auto) or compiling it inline (sync).
+std::shared_ptr<Entry> acquire(const std::string& src, int device, JitMode mode) {
     Jit& J = jit();
     std::shared_ptr<Entry> e;
     {
@@ -564,7 +563,7 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
                 J.queue.emplace_back(src, e);
                 J.cv.notify_all();
                 ++J.stats.misses;
-                return false;
+                return nullptr;
             }
         } else {
             e = it->second;
@@ -572,24 +571,38 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
     }
     if (e->state.load() != 1) {
         ++J.stats.misses;
-        return false;
+        return nullptr;
     }
+    return e;
+}
+
+int occupancy(Entry& e, int device, int threads, size_t smem) {
+    Jit& J = jit();
+    std::lock_guard<std::mutex> lk(J.mu);
+    auto it = e.occ.find(device);
+    if (it != e.occ.end()) return it->second;
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(e.kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         220 * 1024);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(e.kern), threads, smem);
+    if (occ < 1) occ = 1;
+    e.occ[device] = occ;
+    return occ;
+}
+
+}  // namespace
+
+bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,
+                uint64_t rankbase, cudaStream_t s, int device) {
+    const JitMode mode = jit_mode();
+    if (mode == JitMode::Off || h.m < 8 || h.m > 12) return false;
+    if (mode == JitMode::Auto && h.nloc < 18) return false;  // interpreter is fine for small states
+    std::shared_ptr<Entry> e = acquire(jit_source(h, ops, pool), device, mode);
+    if (!e) return false;
+    Jit& J = jit();
     const int T = (1 << h.m) / (1 << ops[0].k);
     const size_t smem = (size_t(jit_knobs().prefetch ? 2 : 1) << h.m) * 16 + size_t(h.pool_n) * 16;
-    int occ = 0;
-    {
-        std::lock_guard<std::mutex> lk(J.mu);
-        auto it = e->occ.find(device);
-        if (it == e->occ.end()) {
-            cudaFuncSetAttribute(reinterpret_cast<const void*>(e->kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 220 * 1024);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(e->kern), T, smem);
-            if (occ < 1) occ = 1;
-            e->occ[device] = occ;
-        } else {
-            occ = it->second;
-        }
-    }
+    const int occ = occupancy(*e, device, T, smem);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const long long grid = std::min<long long>(h.ntiles, (long long)sms * occ);
@@ -604,6 +617,260 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
     }
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     ++J.stats.launches;
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// Expectation batches (K10, proj/src/statevector.cpp:241-277): one read of
+// the state evaluates up to 32 Pauli terms whose flip masks lie in the tile.
+//
+// Each thread owns 8 amplitudes of the staged tile at a time, in up to four
+// register layouts of 3 tile bits.  Terms are assigned to layouts so that
+// every flip (X/Y) bit of a term is a register bit: its pair products
+// conj(a[y^F]) a[y] are then formed in registers with compile-time signs, and
+// the thread-dependent part of the sign is one runtime bit per term.  Z-type
+// terms use layout 0: a 3-bit Walsh transform of |a|^2 gives every sign
+// pattern over the register bits at once.  Terms that do not fit (more than
+// 3 flip bits, or more than four layouts needed) loop over pairs in shared
+// memory.  The tile is double-buffered with cp.async; addresses use the
+// linear swizzle that makes the natural order and all layouts conflict free.
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kExpGrid = 296;  // fixed: the summation order never depends on the device
+
+struct ExpPlan {
+    std::vector<Layout> lays;
+    std::vector<int> lay_of;  // per term: layout or -1 (shared-memory pairs)
+};
+
+ExpPlan plan_expect(const ExpBatch& b) {
+    const int m = b.m;
+    ExpPlan P;
+    P.lay_of.assign(size_t(b.nt), -1);
+    std::vector<unsigned> bits;
+    std::vector<int> order;
+    for (int t = 0; t < b.nt; ++t) order.push_back(t);
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+        return __builtin_popcount(b.t[x].ftile) > __builtin_popcount(b.t[y].ftile);
+    });
+    for (int t : order) {
+        const unsigned f = b.t[t].ftile;
+        if (f == 0 || __builtin_popcount(f) > 3) continue;
+        size_t l = 0;
+        for (; l < bits.size(); ++l)
+            if (__builtin_popcount(bits[l] | f) <= 3) break;
+        if (l == bits.size()) {
+            if (bits.size() == 4) continue;
+            bits.push_back(0);
+        }
+        bits[l] |= f;
+        P.lay_of[size_t(t)] = int(l);
+    }
+    if (bits.empty()) bits.push_back(0);
+    for (int t = 0; t < b.nt; ++t)
+        if (b.t[t].ftile == 0) P.lay_of[size_t(t)] = 0;
+    for (auto& r : bits)
+        for (int p = m - 1; p >= 0 && __builtin_popcount(r) < 3; --p) r |= 1u << p;
+    for (unsigned r : bits) {
+        Layout L;
+        L.r = 3;
+        int k = 0;
+        for (int p = 0; p < m; ++p) {
+            if ((r >> p) & 1u) L.rp[k++] = p;
+            else L.nonr.push_back(p);
+        }
+        P.lays.push_back(L);
+    }
+    return P;
+}
+
+}  // namespace
+
+std::string expect_source(const ExpBatch& b) {
+    const int m = b.m;
+    const int SIZE = 1 << m;
+    const int T = SIZE / 8;
+    const int logT = m - 3;
+    const int NW = T / 32;
+    const int NT = b.nt;
+    const ExpPlan P = plan_expect(b);
+    const Swizzle sw = choose_swizzle(P.lays, m);
+    std::vector<int> q(b.q, b.q + m), rest(b.rest, b.rest + b.nrest);
+    auto reg_slots = [&](const Layout& L, unsigned mask) {
+        unsigned c = 0;
+        for (int j = 0; j < 3; ++j)
+            if ((mask >> L.rp[j]) & 1u) c |= 1u << j;
+        return c;
+    };
+    std::ostringstream s;
+    const int minb = std::max(1, 512 / T);
+    s << "#include \"pass_ops.cuh\"\n"
+      << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << minb << ")\n"
+      << "nqjit(const double2* __restrict__ st, double* __restrict__ part, long long ntiles) {\n"
+      << "  using namespace nq;\n"
+      << "  extern __shared__ __align__(16) unsigned char smem[];\n"
+      << "  double2* buf0 = reinterpret_cast<double2*>(smem);\n"
+      << "  double2* buf1 = buf0 + " << SIZE << ";\n"
+      << "  __shared__ double red[" << NW << "][" << NT << "];\n"
+      << "  const unsigned tid = threadIdx.x;\n";
+    {
+        std::vector<int> qlow(q.begin(), q.begin() + logT);
+        s << "  const unsigned long long goff = " << deposit_expr("(unsigned long long)tid", qlow, true) << ";\n";
+        s << "  const unsigned psw = " << swz_expr("tid", sw) << ";\n";
+    }
+    for (size_t k = 0; k < P.lays.size(); ++k) {
+        s << "  const unsigned e" << k << " = " << deposit_expr("tid", P.lays[k].nonr, false) << ";\n";
+        s << "  const unsigned s" << k << " = " << swz_expr("e" + std::to_string(k), sw) << ";\n";
+    }
+    bool any_glob = false;
+    s << "  unsigned ts = 0u;\n";
+    for (int t = 0; t < NT; ++t) {
+        const ExpTerm& E = b.t[t];
+        any_glob = any_glob || E.sglob != 0;
+        const int l = P.lay_of[size_t(t)];
+        if (l >= 0 && E.stile)
+            s << "  ts |= (unsigned(__popc(e" << l << " & " << E.stile << "u)) & 1u) << " << t << ";\n";
+    }
+    for (int t = 0; t < NT; ++t) s << "  double acc" << t << " = 0.0;\n";
+    // natural-order tile copy: element tid + j*T
+    auto issue = [&](const std::string& rexpr, const std::string& buf, const std::string& ind) {
+        s << ind << "{ const double2* src = st + (" << deposit_expr("(unsigned long long)(" + rexpr + ")", rest, true)
+          << ") + goff;\n";
+        for (int j = 0; j < 8; ++j) {
+            unsigned long long dep = 0;
+            const unsigned e = unsigned(j) << logT;
+            for (int i = 0; i < m; ++i)
+                if ((e >> i) & 1u) dep |= 1ull << q[size_t(i)];
+            s << ind << "  cp_async16(" << buf << " + (psw ^ " << (sw.apply(e) & ~0u) << "u), src + " << hex64(dep)
+              << ");\n";
+        }
+        s << ind << "}\n";
+    };
+    s << "  long long r = blockIdx.x;\n"
+      << "  if (r < ntiles) ";
+    issue("r", "buf0", "  ");
+    s << "  cp_async_commit();\n"
+      << "  for (int it = 0; r < ntiles; r += gridDim.x, ++it) {\n"
+      << "    double2* cur = (it & 1) ? buf1 : buf0;\n"
+      << "    double2* nxt = (it & 1) ? buf0 : buf1;\n"
+      << "    const long long rn = r + gridDim.x;\n"
+      << "    if (rn < ntiles) ";
+    issue("rn", "nxt", "    ");
+    s << "    cp_async_commit();\n"
+      << "    cp_async_wait<1>();\n"
+      << "    __syncthreads();\n";
+    if (any_glob) {
+        s << "    const unsigned long long base = " << deposit_expr("(unsigned long long)r", rest, true) << ";\n"
+          << "    unsigned gb = 0u;\n";
+        for (int t = 0; t < NT; ++t)
+            if (b.t[t].sglob)
+                s << "    gb |= (unsigned(__popcll(base & " << hex64(b.t[t].sglob) << ")) & 1u) << " << t << ";\n";
+    } else {
+        s << "    const unsigned gb = 0u;\n";
+    }
+    s << "    const unsigned gs = ts ^ gb;\n";
+    for (size_t k = 0; k < P.lays.size(); ++k) {
+        const Layout& L = P.lays[k];
+        bool used = false;
+        for (int t = 0; t < NT; ++t) used = used || P.lay_of[size_t(t)] == int(k);
+        if (!used) continue;
+        s << "    {\n";
+        for (int j = 0; j < 8; ++j)
+            s << "      const double2 v" << j << " = cur[s" << k << " ^ " << sw.apply(L.rconst(j)) << "u];\n";
+        bool anyz = false;
+        for (int t = 0; t < NT; ++t) anyz = anyz || (b.t[t].ftile == 0 && P.lay_of[size_t(t)] == int(k));
+        if (anyz) {
+            for (int j = 0; j < 8; ++j) s << "      double w" << j << " = fma(v" << j << ".x, v" << j << ".x, v" << j << ".y * v" << j << ".y);\n";
+            for (int bb = 0; bb < 3; ++bb)
+                for (int j = 0; j < 8; ++j) {
+                    if ((j >> bb) & 1) continue;
+                    const int h = j | (1 << bb);
+                    s << "      { const double x = w" << j << ", y = w" << h << "; w" << j << " = x + y; w" << h
+                      << " = x - y; }\n";
+                }
+        }
+        for (int t = 0; t < NT; ++t) {
+            if (P.lay_of[size_t(t)] != int(k)) continue;
+            const ExpTerm& E = b.t[t];
+            const unsigned cs = reg_slots(L, E.stile);
+            if (E.ftile == 0) {
+                s << "      acc" << t << " += ((gs >> " << t << ") & 1u) ? -w" << cs << " : w" << cs << ";\n";
+                continue;
+            }
+            const unsigned fr = reg_slots(L, E.ftile);
+            const int f0 = __builtin_ctz(fr);
+            s << "      { double x = 0.0;\n";
+            for (int j = 0; j < 8; ++j) {
+                if ((j >> f0) & 1) continue;
+                const int z = j ^ int(fr);
+                const bool neg = __builtin_popcount(unsigned(j) & cs) & 1;
+                std::ostringstream v;
+                if (E.eps_im)
+                    v << "fma(v" << z << ".x, v" << j << ".y, -(v" << z << ".y * v" << j << ".x))";
+                else
+                    v << "fma(v" << z << ".x, v" << j << ".x, v" << z << ".y * v" << j << ".y)";
+                s << "        x " << (neg ? "-= " : "+= ") << v.str() << ";\n";
+            }
+            s << "        acc" << t << " += ((gs >> " << t << ") & 1u) ? -x : x; }\n";
+        }
+        s << "    }\n";
+    }
+    for (int t = 0; t < NT; ++t) {
+        if (P.lay_of[size_t(t)] >= 0) continue;
+        const ExpTerm& E = b.t[t];
+        const int f0 = __builtin_ctz(E.ftile);
+        s << "    for (unsigned w = tid; w < " << SIZE / 2 << "u; w += " << T << "u) {\n"
+          << "      const unsigned y = ((w >> " << f0 << ") << " << f0 + 1 << ") | (w & " << ((1u << f0) - 1u)
+          << "u);\n"
+          << "      const unsigned z = y ^ " << E.ftile << "u;\n"
+          << "      const double2 ay = cur[" << swz_expr("y", sw) << "], az = cur[" << swz_expr("z", sw) << "];\n";
+        if (E.eps_im) s << "      const double x = fma(az.x, ay.y, -(az.y * ay.x));\n";
+        else s << "      const double x = fma(az.x, ay.x, az.y * ay.y);\n";
+        s << "      acc" << t << " += ((__popc(y & " << E.stile << "u) ^ (gb >> " << t << ")) & 1u) ? -x : x;\n"
+          << "    }\n";
+    }
+    s << "    __syncthreads();\n"
+      << "  }\n"
+      << "  cp_async_wait<0>();\n"
+      << "  const unsigned lane = tid & 31u, warp = tid >> 5;\n";
+    for (int t = 0; t < NT; ++t) {
+        s << "  { double v = acc" << t << ";\n"
+          << "    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);\n"
+          << "    if (lane == 0) red[warp][" << t << "] = v; }\n";
+    }
+    s << "  __syncthreads();\n"
+      << "  if (tid < " << NT << "u) {\n"
+      << "    double v = 0.0;\n"
+      << "    for (int w = 0; w < " << NW << "; ++w) v += red[w][tid];\n"
+      << "    part[size_t(blockIdx.x) * " << kMaxExpTerms << " + tid] = v;\n"
+      << "  }\n"
+      << "}\n";
+    return s.str();
+}
+
+bool jit_expect_launch(const double2* state, int nloc, const ExpBatch& b, double* part, double* out,
+                       cudaStream_t s, int device) {
+    const JitMode mode = jit_mode();
+    if (mode == JitMode::Off || b.m < 8 || b.m > 12 || b.nt < 1) return false;
+    if (mode == JitMode::Auto && nloc < 18) return false;
+    std::shared_ptr<Entry> e = acquire(expect_source(b), device, mode);
+    if (!e) return false;
+    const int T = (1 << b.m) / 8;
+    const size_t smem = (size_t(2) << b.m) * 16;
+    occupancy(*e, device, T, smem);
+    const long long ntiles = 1ll << (nloc - b.m);
+    const long long grid = std::min<long long>(ntiles, kExpGrid);
+    long long nt = ntiles;
+    void* args[] = {const_cast<double2**>(&state), &part, &nt};
+    if (cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(unsigned(grid)), dim3(unsigned(T)), args, smem,
+                         s) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+    ++jit().stats.launches;
+    launch_expect_final(part, int(grid), b.nt, out, s);
     return true;
 }
 

@@ -2,6 +2,7 @@
 #pragma once
 
 #include "engine.hpp"
+#include "kernels.hpp"
 
 #include <cuda_runtime.h>
 
@@ -39,6 +40,13 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool);
 // false when the caller must run the interpreter kernel instead.
 bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,
                 uint64_t rankbase, cudaStream_t s, int device);
+
+// Expectation batch kernel specialised to the batch's term structure: source,
+// and launch (plus the per-term final sums into out[0..nt)); false when the
+// caller must use the generic tiled kernel (not compiled yet, or mode off).
+std::string expect_source(const ExpBatch& b);
+bool jit_expect_launch(const double2* state, int nloc, const ExpBatch& b, double* part, double* out,
+                       cudaStream_t s, int device);
 
 // NVRTC compile without loading (CPU-testable); false + log on failure.
 bool jit_compile_only(const std::string& src, std::string* log);

@@ -45,6 +45,8 @@ struct ExpBatch {
 };
 size_t expect_tiled_scratch();
 void launch_expect_tiled(const double2* a, int nloc, const ExpBatch& b, double* part, double* out, cudaStream_t s);
+// out[t] = sum over nblk rows of part (row stride kMaxExpTerms), fixed order
+void launch_expect_final(const double* part, int nblk, int nt, double* out, cudaStream_t s);
 
 // half-shard pack/unpack for global<->local qubit swaps (comm_kernels.cu)
 void launch_half_pack(const double2* st, double2* buf, uint64_t k0, uint64_t len, int v, uint64_t val,

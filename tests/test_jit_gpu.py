@@ -42,6 +42,26 @@ SCRIPT = textwrap.dedent(
         noise = NoiseSpec(n, e1=0.01, e2=0.05)
         rho = naqs.run_density(circ, naqs.load_calibration(noise.calibration_json()))
         worst = max(worst, float(np.max(np.abs(rho - port.dm_run_noisy(n, c, noise)))))
+    # expectation batches: specialised register-layout kernels (tile 12)
+    from paper_2401_06861_b200 import workloads
+    rng = np.random.default_rng(7)
+    for n, seed in [(13, 11), (16, 12), (19, 13)]:
+        ops = port.random_circuit(seed, n, 120)
+        sv = abi.SV(n)
+        sv.apply(ops)
+        amps = sv.amplitudes()
+        terms = list(workloads.tfim_hamiltonian(n, periodic=True))
+        for _ in range(40):
+            w = int(rng.integers(1, 6))
+            L = ["I"] * n
+            for q in rng.choice(n, size=w, replace=False):
+                L[int(q)] = "XYZ"[int(rng.integers(0, 3))]
+            terms.append(("".join(L), float(rng.normal())))
+        got = sv.expectations(terms)
+        for (letters, coeff), g in zip(terms, got):
+            ref = port.expectation(amps, letters, coeff)
+            worst = max(worst, abs(g - ref))
+        assert np.array_equal(sv.expectations(terms), got)  # deterministic
     st = abi.jit_stats()
     assert st["launches"] > 0 and st["failed"] == 0, st
     print("WORST", worst, st)
