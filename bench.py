@@ -419,7 +419,8 @@ def main():
             "jit": jit,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_from_profiles(),
-                         "kernel": "pass_kernel<12>", "bytes_per_launch": bytes_per_launch,
+                         "kernel": ("nqjit (pass-specialised fused pass, NVRTC)" if jit.get("launches", 0) > 0
+                                    else "pass_kernel (fused pass interpreter)"), "bytes_per_launch": bytes_per_launch,
                          "avg_launch_ms": pass_avg_ms, "launches": prof["pass_launches"],
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
             "clocks": clk.summary(),

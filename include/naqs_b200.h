@@ -233,6 +233,10 @@ nq_status nq_profile_end(int device, nq_profile* out);
 /* Run-time specialised pass kernels (NVRTC, cached per pass structure;
  * policy NQ_JIT=off|auto|sync).  Wait for queued compilations / counters. */
 nq_status nq_jit_wait(void);
+/* Cancel queued compilations and wait for running ones; later flushes use the
+ * already compiled kernels or the generic ones.  Call before process exit
+ * when compilations may be in flight (the Python packages do this at exit). */
+nq_status nq_jit_shutdown(void);
 nq_status nq_jit_stats(int64_t* compiled, int64_t* failed, int64_t* misses, int64_t* launches);
 /* Generated source of pass `pass_index` of an SV plan, optionally compiled
  * with NVRTC (no device needed); *compiled_ok = 1/0, or -1 when not compiled. */

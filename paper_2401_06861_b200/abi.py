@@ -7,6 +7,7 @@ fails loudly when it is missing -- there is no fallback implementation.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
 from typing import Iterable, Sequence
@@ -145,6 +146,7 @@ SIGNATURES = {
     "nq_profile_begin": ([C.c_int, C.c_int], C.c_int),
     "nq_profile_end": ([C.c_int, C.POINTER(nq_profile)], C.c_int),
     "nq_jit_wait": ([], C.c_int),
+    "nq_jit_shutdown": ([], C.c_int),
     "nq_jit_stats": ([_i64p, _i64p, _i64p, _i64p], C.c_int),
     "nq_jit_debug": ([C.c_int, _p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int64, _i64p,
                       C.POINTER(C.c_int)], C.c_int),
@@ -155,6 +157,10 @@ for _name, (_args, _res) in SIGNATURES.items():
     _f = getattr(lib, _name)
     _f.argtypes = _args
     _f.restype = _res
+
+# Run-time kernel compilations still in flight at interpreter exit are
+# cancelled / awaited before native teardown starts.
+atexit.register(lib.nq_jit_shutdown)
 
 
 def check(status: int) -> None:

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -137,6 +138,40 @@ void state_free(State& s) {
     shard_free(s);
 }
 
+// NQ_PLAN_TRACE=1: one stderr line per planned pass (micro-op kinds, arity,
+// real/zero structure of the matrices) for plan inspection.
+bool plan_trace() {
+    static const bool on = [] {
+        const char* e = std::getenv("NQ_PLAN_TRACE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+void trace_passes(const std::vector<PlannedPass>& passes, bool dm) {
+    static const char* names[] = {"D", "G", "X", "S", "P", "L"};
+    for (size_t i = 0; i < passes.size(); ++i) {
+        const PlannedPass& p = passes[i];
+        std::string line;
+        for (const MOp& op : p.ops) {
+            line += ' ';
+            line += op.type < 6 ? names[op.type] : "?";
+            line += std::to_string(int(op.k));
+            if (op.type == MOP_DENSE) {
+                const size_t n = size_t(1) << (2 * op.k);
+                size_t nz = 0, re = 0;
+                for (size_t e = 0; e < n; ++e) {
+                    const cplx v = p.pool[op.mat + e];
+                    nz += v != cplx(0.0, 0.0);
+                    re += v.imag() == 0.0;
+                }
+                line += "[" + std::to_string(nz) + "/" + std::to_string(n) + (re == n ? "r" : "") + "]";
+            }
+        }
+        std::fprintf(stderr, "[plan%s] pass %zu m=%zu:%s\n", dm ? " dm" : "", i, p.q.size(), line.c_str());
+    }
+}
+
 void state_flush(State& s) {
     if (s.queue.empty()) return;
     if (s.world > 1) {
@@ -155,6 +190,7 @@ void state_flush(State& s) {
     s.last_source_ops = st.source_ops;
     s.last_launches = int64_t(passes.size());
     if (buf.empty()) return;
+    if (plan_trace()) trace_passes(passes, s.dm);
     c.stage(buf.data(), buf.size());
     for (size_t i = 0; i < passes.size(); ++i) {
         PassHdr h;
@@ -1017,6 +1053,10 @@ nq_status nq_profile_end(int device, nq_profile* out) {
 
 nq_status nq_jit_wait(void) {
     return guard([&] { jit_wait(); });
+}
+
+nq_status nq_jit_shutdown(void) {
+    return guard([&] { jit_shutdown(); });
 }
 
 nq_status nq_jit_stats(int64_t* compiled, int64_t* failed, int64_t* misses, int64_t* launches) {

@@ -35,6 +35,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <execinfo.h>
+#include <csignal>
+#include <unistd.h>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -67,6 +70,7 @@ struct Jit {
     std::deque<std::pair<std::string, std::shared_ptr<Entry>>> queue;
     int busy = 0;
     bool started = false;
+    bool exiting = false;
     int device = 0;
     JitStats stats;
 };
@@ -213,6 +217,60 @@ const JitKnobs& jit_knobs() {
     return k;
 }
 
+// Dense k <= 2 operator with structural zeros (Liouville superoperators of
+// damping / dephasing channels, diagonal-times-permutation products): only the
+// nonzero entries are multiplied, and entries with an exact zero imaginary
+// part use real-times-complex products.  Values stay in the shared pool, so the
+// kernel is reused for every matrix with the same zero / real pattern.
+std::string sparse_dense(const MOp& op, const cplx* u, int E, const std::string& P) {
+    const int d = 1 << op.k;
+    std::ostringstream s;
+    s << "    {\n";
+    for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c) {
+            const cplx v = u[r * d + c];
+            if (v == cplx(0.0, 0.0)) continue;
+            s << "      const " << (v.imag() == 0.0 ? "double" : "double2") << " u" << r << "_" << c << " = lds(" << P
+              << " + " << (r * d + c) << ")" << (v.imag() == 0.0 ? ".x" : "") << ";\n";
+        }
+    unsigned smask = 0;
+    for (int j = 0; j < op.k; ++j) smask |= 1u << op.pos[j];
+    for (int l = 0; l < E; ++l) {
+        if (unsigned(l) & smask) continue;
+        auto idx = [&](int i) {
+            int x = l;
+            for (int j = 0; j < op.k; ++j)
+                if ((i >> j) & 1) x |= 1 << op.pos[j];
+            return x;
+        };
+        s << "      {";
+        for (int c = 0; c < d; ++c) s << " const double2 x" << c << " = a[" << idx(c) << "];";
+        s << "\n";
+        for (int r = 0; r < d; ++r) {
+            const std::string dst = "a[" + std::to_string(idx(r)) + "]";
+            bool first = true;
+            for (int c = 0; c < d; ++c) {
+                const cplx v = u[r * d + c];
+                if (v == cplx(0.0, 0.0)) continue;
+                const std::string un = "u" + std::to_string(r) + "_" + std::to_string(c);
+                const std::string xn = "x" + std::to_string(c);
+                const bool re = v.imag() == 0.0;
+                s << "        ";
+                if (first && re) s << dst << " = make_double2(" << un << " * " << xn << ".x, " << un << " * " << xn << ".y);\n";
+                else if (first) s << dst << " = cmul(" << un << ", " << xn << ");\n";
+                else if (re) s << dst << ".x = fma(" << un << ", " << xn << ".x, " << dst << ".x); " << dst << ".y = fma("
+                               << un << ", " << xn << ".y, " << dst << ".y);\n";
+                else s << dst << " = cfma(" << un << ", " << xn << ", " << dst << ");\n";
+                first = false;
+            }
+            if (first) s << "        " << dst << " = make_double2(0.0, 0.0);\n";
+        }
+        s << "      }\n";
+    }
+    s << "    }\n";
+    return s.str();
+}
+
 std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     const int m = h.m;
     const int SIZE = 1 << m;
@@ -347,9 +405,16 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
         }
         case MOP_DENSE: {
             bool real = true;
-            for (size_t i = 0; i < (size_t(1) << (2 * op.k)) && real; ++i) real = pool[op.mat + i].imag() == 0.0;
+            size_t nnz = 0;
+            const size_t nent = size_t(1) << (2 * op.k);
+            for (size_t i = 0; i < nent; ++i) {
+                real = real && pool[op.mat + i].imag() == 0.0;
+                nnz += pool[op.mat + i] != cplx(0.0, 0.0);
+            }
             const char* R = real ? ", true" : "";
-            if (op.k == 1) {
+            if (op.k <= 2 && nnz < nent) {
+                s << sparse_dense(op, pool + op.mat, E, P);
+            } else if (op.k == 1) {
                 s << "    d1<" << E << ", " << int(op.pos[0]) << R << ">(a, " << P << ");\n";
             } else if (op.k == 2) {
                 s << "    d2<" << E << ", " << int(op.pos[0]) << ", " << int(op.pos[1]) << R << ">(a, " << P << ");\n";
@@ -464,6 +529,14 @@ namespace {
 const char* kNvrtcOpts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"};
 
 bool compile_entry(const std::string& src, Entry& e, int device) {
+    if (const char* dir = std::getenv("NQ_JIT_DUMP")) {  // debugging: keep every generated source
+        static std::atomic<int> seq{0};
+        const std::string path = std::string(dir) + "/nqjit_" + std::to_string(seq.fetch_add(1)) + ".cu";
+        if (FILE* f = std::fopen(path.c_str(), "w")) {
+            std::fwrite(src.data(), 1, src.size(), f);
+            std::fclose(f);
+        }
+    }
     nvrtcProgram prog;
     const char* hdrs[1] = {kPassOpsSrc};
     const char* names[1] = {"pass_ops.cuh"};
@@ -507,7 +580,7 @@ void worker_loop() {
         std::pair<std::string, std::shared_ptr<Entry>> job;
         {
             std::unique_lock<std::mutex> lk(J.mu);
-            J.cv.wait(lk, [&] { return !J.queue.empty(); });
+            J.cv.wait(lk, [&] { return !J.queue.empty() && !J.exiting; });
             job = std::move(J.queue.front());
             J.queue.pop_front();
             ++J.busy;
@@ -526,9 +599,56 @@ void worker_loop() {
 
 }  // namespace
 
+namespace {
+// NQ_SEGV_TRACE=1: print a native backtrace on SIGSEGV (debugging aid).
+void segv_handler(int sig) {
+    void* frames[64];
+    const int n = backtrace(frames, 64);
+    const char msg[] = "\n[naqs_b200] fatal signal, native backtrace:\n";
+    (void)!write(2, msg, sizeof msg - 1);
+    backtrace_symbols_fd(frames, n, 2);
+    std::signal(sig, SIG_DFL);
+    std::raise(sig);
+}
+const bool g_segv_trace = [] {
+    const char* e = std::getenv("NQ_SEGV_TRACE");
+    if (e && e[0] == '1') std::signal(SIGSEGV, segv_handler);
+    return true;
+}();
+}  // namespace
+
 JitMode jit_mode() {
     static const JitMode m = mode_from_env();
     return m;
+}
+
+namespace {
+
+// Process exit with compilations in flight: drop the queued ones and wait for
+// the running ones, so no worker touches NVRTC / the CUDA runtime while they
+// are being torn down.
+void drain_at_exit() { jit_shutdown(); }
+
+// NVRTC initialises internal state (with exit-time destructors) on its first
+// compile.  One tiny compile before the exit hook is registered puts that
+// teardown after the hook, so the hook always runs while NVRTC is intact.
+void nvrtc_warm() {
+    nvrtcProgram prog;
+    const char* src = "extern \"C\" __global__ void nqwarm() {}";
+    if (nvrtcCreateProgram(&prog, src, "warm.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return;
+    nvrtcCompileProgram(prog, 3, kNvrtcOpts);
+    nvrtcDestroyProgram(&prog);
+}
+
+}  // namespace
+
+void jit_shutdown() {
+    Jit& J = jit();
+    std::unique_lock<std::mutex> lk(J.mu);
+    J.exiting = true;
+    for (auto& job : J.queue) job.second->state.store(2);
+    J.queue.clear();
+    J.cv.wait(lk, [&] { return J.busy == 0; });
 }
 
 namespace {
@@ -552,13 +672,16 @@ std::shared_ptr<Entry> acquire(const std::string& src, int device, JitMode mode)
                 if (ok) ++J.stats.compiled;
                 else ++J.stats.failed;
             } else {
+                if (J.exiting) return nullptr;
                 J.device = device;
                 if (!J.started) {
+                    nvrtc_warm();
                     // NVRTC compiles are independent: a small pool of workers
                     const unsigned hw = std::thread::hardware_concurrency();
                     const unsigned nw = std::max(1u, std::min(8u, hw / 2));
                     for (unsigned w = 0; w < nw; ++w) std::thread(worker_loop).detach();
                     J.started = true;
+                    std::atexit(drain_at_exit);
                 }
                 J.queue.emplace_back(src, e);
                 J.cv.notify_all();

@@ -53,6 +53,9 @@ bool jit_compile_only(const std::string& src, std::string* log);
 
 // Block until every queued compilation has finished.
 void jit_wait();
+// Drop queued compilations, wait for running ones and accept no new ones
+// (process exit; also registered with atexit when the workers start).
+void jit_shutdown();
 JitStats jit_stats();
 
 }  // namespace nqe
