@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -109,6 +110,12 @@ void state_init(State& s, int n, bool dm, const nq_opts* opts) {
     // (best measured pass throughput on B200)
     s.popt.tile_bits = o.tile_qubits > 0 ? std::min(o.tile_qubits, kMaxTileBits) : 11;
     s.popt.low_bits = 4;
+    // A/B knobs (read per state): NQ_TILE_DM / NQ_LOW_BITS_DM for density matrices
+    if (dm) {
+        if (const char* e = std::getenv("NQ_TILE_DM"); e && o.tile_qubits <= 0)
+            s.popt.tile_bits = std::max(4, std::min(std::atoi(e), kMaxTileBits));
+        if (const char* e = std::getenv("NQ_LOW_BITS_DM")) s.popt.low_bits = std::max(0, std::min(std::atoi(e), 4));
+    }
     s.popt.fuse = o.fuse != 0;
     configure_caps(s.popt);
     DeviceCtx& c = ctx_for(dev);
