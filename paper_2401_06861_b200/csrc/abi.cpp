@@ -140,9 +140,16 @@ void state_free(State& s) {
     if (!s.d) return;
     DeviceCtx& c = ctx_for(s.dev);
     cudaSetDevice(s.dev);
-    cudaFreeAsync(s.d, c.stream);
+    if (s.plain_alloc) {
+        // peers may map this buffer: release the mappings (shard_free) first
+        cudaStreamSynchronize(c.stream);
+        shard_free(s);
+        cudaFree(s.d);
+    } else {
+        cudaFreeAsync(s.d, c.stream);
+        shard_free(s);
+    }
     s.d = nullptr;
-    shard_free(s);
 }
 
 // NQ_PLAN_TRACE=1: one stderr line per planned pass (micro-op kinds, arity,

@@ -53,6 +53,9 @@ void launch_half_pack(const double2* st, double2* buf, uint64_t k0, uint64_t len
                       cudaStream_t s);
 void launch_half_unpack(double2* st, const double2* buf, uint64_t k0, uint64_t len, int v, uint64_t val,
                         cudaStream_t s);
+// mine[ins(k, v, mval)] <-> peer[ins(k, v, pval)] for k in [k0, k1) (peer: IPC-mapped)
+void launch_swap_peer(double2* mine, double2* peer, int v, uint64_t mval, uint64_t pval, uint64_t k0, uint64_t k1,
+                      cudaStream_t s);
 
 void launch_probs(const double2* a, uint64_t n, double* p, cudaStream_t s);
 void launch_dm_probs(const double2* rho, uint64_t dim, double* p, double* scratch, cudaStream_t s);

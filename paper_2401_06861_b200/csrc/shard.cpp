@@ -108,6 +108,10 @@ NcclApi& nccl() {
 
 struct ShardComm {
     ncclComm_t comm = nullptr;
+    // peer-memory exchange: every rank's state mapped into this process (CUDA
+    // IPC over NVLink); empty when unavailable or NQ_EXCHANGE=nccl
+    std::vector<double2*> peer;
+    double* d_flag = nullptr;  // 1-element buffer for the stream barrier
     double2* sendbuf = nullptr;
     double2* recvbuf = nullptr;
     uint64_t chunk = 0;  // amplitudes per bounce buffer
@@ -281,12 +285,32 @@ void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops) {
     CUDA_TRY(cudaGetLastError());
 }
 
+// Device-side barrier: a one-element all-reduce completes only after every
+// rank's stream has reached it, so no rank touches a peer's state while that
+// peer's earlier kernels may still be running (and vice versa afterwards).
+void stream_barrier(ShardComm& sc, DeviceCtx& c) {
+    NCCL_TRY(ncclAllReduce(sc.d_flag, sc.d_flag, 1, ncclDouble, ncclSum, sc.comm, c.stream));
+}
+
 void run_exchange(State& s, DeviceCtx& c, int g, int v) {
     ShardComm& sc = *s.comm;
     const int j = g - s.nloc;
     const int partner = s.rank ^ (1 << j);
     const uint64_t mybit = uint64_t((s.rank >> j) & 1);
     const uint64_t half = s.count / 2;
+    if (!sc.peer.empty()) {
+        // One kernel per rank swaps its share of the element pairs directly in
+        // both states over NVLink: no bounce buffers, no pack / unpack passes.
+        // Pair k: my element with bit v = 1 - mybit <-> the partner's with bit v = mybit.
+        stream_barrier(sc, c);
+        const uint64_t k0 = mybit ? half / 2 : 0, k1 = mybit ? half : half / 2;
+        launch_swap_peer(s.d, sc.peer[size_t(partner)], v, 1 - mybit, mybit, k0, k1, c.stream);
+        stream_barrier(sc, c);
+        CUDA_TRY(cudaGetLastError());
+        sc.bytes += int64_t(half) * 16;
+        ++sc.exchanges;
+        return;
+    }
     for (uint64_t k0 = 0; k0 < half; k0 += sc.chunk) {
         const uint64_t len = std::min(sc.chunk, half - k0);
         launch_half_pack(s.d, sc.sendbuf, k0, len, v, 1 - mybit, c.stream);
@@ -325,6 +349,46 @@ std::vector<double> allgather_doubles(State& s, const std::vector<double>& mine)
     return all;
 }
 
+// Map every rank's state into this process (CUDA IPC); all ranks must agree,
+// so the outcome is all-reduced and any failure keeps the NCCL path everywhere.
+void setup_peer_exchange(State& s, ShardComm& sc, DeviceCtx& c) {
+    const char* mode = std::getenv("NQ_EXCHANGE");
+    const bool want = !(mode && std::string(mode) == "nccl");
+    cudaIpcMemHandle_t mine{};
+    bool ok = want && cudaIpcGetMemHandle(&mine, s.d) == cudaSuccess;
+    cudaGetLastError();
+    // all-gather the 64-byte handles as doubles (8 per handle) + an ok flag
+    constexpr size_t kW = sizeof(cudaIpcMemHandle_t) / sizeof(double) + 1;
+    std::vector<double> buf(kW, 0.0);
+    std::memcpy(buf.data(), &mine, sizeof(mine));
+    buf[kW - 1] = ok ? 1.0 : 0.0;
+    const std::vector<double> all = allgather_doubles(s, buf);
+    for (int r = 0; r < s.world; ++r) ok = ok && all[size_t(r) * kW + kW - 1] == 1.0;
+    std::vector<double2*> peer(size_t(s.world), nullptr);
+    for (int r = 0; ok && r < s.world; ++r) {
+        if (r == s.rank) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, all.data() + size_t(r) * kW, sizeof(h));
+        void* p = nullptr;
+        if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            ok = false;
+            break;
+        }
+        peer[size_t(r)] = static_cast<double2*>(p);
+    }
+    // agree: p2p only if every rank mapped every peer
+    const std::vector<double> oks = allgather_doubles(s, {ok ? 1.0 : 0.0});
+    for (double v : oks) ok = ok && v == 1.0;
+    if (ok) {
+        sc.peer = std::move(peer);
+    } else {
+        for (double2* p : peer)
+            if (p) cudaIpcCloseMemHandle(p);
+    }
+    (void)c;
+}
+
 void normalize_map(State& s) {
     ShardComm& sc = *s.comm;
     bool identity = true;
@@ -342,6 +406,9 @@ void shard_free(State& s) {
     cudaStreamSynchronize(c.stream);
     if (sc->sendbuf) cudaFree(sc->sendbuf);
     if (sc->recvbuf) cudaFree(sc->recvbuf);
+    if (sc->d_flag) cudaFree(sc->d_flag);
+    for (double2* p : sc->peer)
+        if (p) cudaIpcCloseMemHandle(p);
     if (sc->comm) ncclCommDestroy(sc->comm);
     delete sc;
     s.comm = nullptr;
@@ -358,11 +425,20 @@ void shard_flush(State& s) {
     ops.swap(s.queue);
     s.last_passes = s.last_microops = s.last_source_ops = s.last_launches = 0;
     std::vector<Action> acts = schedule(ops, sc.l2p, sc.p2l, s.nloc);
-    // Restore the identity qubit map at the end of the flush: every flush of
-    // the same circuit then runs the same physical program (so its
-    // pass-specialised kernels are reused), and readouts need no remap.
-    std::vector<Action> back = schedule_identity(sc.l2p, sc.p2l, s.nloc, s.n);
-    acts.insert(acts.end(), back.begin(), back.end());
+    // The qubit map is carried into the next flush (readouts normalise it
+    // first).  Re-running one circuit then converges to a map whose global
+    // qubits that circuit never needs as targets: after a step or two the
+    // flush needs few or no exchanges and runs the same physical program
+    // every time (its specialised kernels are reused).  NQ_SHARD_RESTORE=1
+    // restores the identity map at the end of every flush instead.
+    static const bool restore = [] {
+        const char* e = std::getenv("NQ_SHARD_RESTORE");
+        return e && e[0] == '1';
+    }();
+    if (restore) {
+        std::vector<Action> back = schedule_identity(sc.l2p, sc.p2l, s.nloc, s.n);
+        acts.insert(acts.end(), back.begin(), back.end());
+    }
     execute(s, acts);
 }
 
@@ -560,6 +636,15 @@ nq_status nq_sv_create_sharded(int n, int rank, int world, const unsigned char u
         nq_opts lo = o;
         lo.max_qubits = n;  // the local allocation is n - g qubits; state_init checks n
         state_init(s, n - g, false, &lo);
+        {
+            // IPC needs a plain (non-pool) allocation
+            DeviceCtx& c0 = ctx_for(s.dev);
+            CUDA_TRY(cudaFreeAsync(s.d, c0.stream));
+            CUDA_TRY(cudaStreamSynchronize(c0.stream));
+            s.d = nullptr;
+            CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&s.d), (size_t(1) << (n - g)) * sizeof(double2)));
+            s.plain_alloc = true;
+        }
         s.n = n;
         s.nbits = n;
         s.nloc = n - g;
@@ -581,7 +666,10 @@ nq_status nq_sv_create_sharded(int n, int rank, int world, const unsigned char u
         ncclUniqueId id;
         std::memcpy(&id, uid, 128);
         NCCL_TRY(ncclCommInitRank(&sc->comm, world, id, rank));
+        CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&sc->d_flag), sizeof(double)));
+        CUDA_TRY(cudaMemset(sc->d_flag, 0, sizeof(double)));
         s.comm = sc.release();
+        setup_peer_exchange(s, *s.comm, c);
         CUDA_TRY(cudaStreamSynchronize(c.stream));
         *out = h.release();
     });

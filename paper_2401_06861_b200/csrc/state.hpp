@@ -93,6 +93,7 @@ struct State {
     // sharded states (world > 1)
     int rank = 0, world = 1;
     ShardComm* comm = nullptr;
+    bool plain_alloc = false;  // cudaMalloc'd (IPC-exportable), freed with cudaFree
 };
 
 void sv_expect_raw(State& s, const uint64_t* flip, const uint64_t* signs, int nterms, std::vector<cplx>& totals);
