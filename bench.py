@@ -102,7 +102,16 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.proc = None
-        self.lines = []
+        self.lines = []  # (host time, csv line)
+        self.t_start = self.t_end = None
+
+    # nvidia-smi needs ~1 s to start streaming: the sampler is started before
+    # the warm-up and only samples stamped inside [mark_start, mark_end] count.
+    def mark_start(self):
+        self.t_start = time.time()
+
+    def mark_end(self):
+        self.t_end = time.time()
 
     def __enter__(self):
         try:
@@ -117,7 +126,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *exc):
         if self.proc:
@@ -130,7 +139,10 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lo = self.t_start if self.t_start is not None else -1e30
+        hi = (self.t_end if self.t_end is not None else 1e30) + 0.05
+        window = [ln for t, ln in self.lines if lo <= t <= hi]
+        for ln in window:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -350,6 +362,7 @@ def main():
         sv = abi.SV.sharded(n, rank, world, bytes(uid.cpu().numpy().tobytes()), device=dev,
                             tile_qubits=args.tile, max_qubits=n)
 
+    clk = ClockSampler(dev).__enter__()
     # warm-up: the first step plans the passes and queues their specialised
     # kernels for compilation (jit.cpp); wait for them, then warm the rest
     for _ in range(max(args.warmup, 3)):
@@ -362,11 +375,13 @@ def main():
     # ---- value: device time of K steps
     barrier(dist, local)
     sv.synchronize()
-    with ClockSampler(dev) as clk:
-        abi.profile_begin(dev, per_pass_events=True)
-        for _ in range(args.steps):
-            sv.apply(ops).flush()
-        prof = abi.profile_end(dev)
+    clk.mark_start()
+    abi.profile_begin(dev, per_pass_events=True)
+    for _ in range(args.steps):
+        sv.apply(ops).flush()
+    prof = abi.profile_end(dev)
+    clk.mark_end()
+    clk.__exit__(None, None, None)
     barrier(dist, local)
     ms = max_over_ranks(dist, local, prof["region_ms"])
     # one circuit on the whole (sharded) state; weak scaling: a gate on the
@@ -390,10 +405,15 @@ def main():
     sv.synchronize()
     abi.profile_begin(dev, per_pass_events=False)
     t0 = time.perf_counter()
+    lap = []
     for _ in range(args.steps):
         sv.apply(ops)  # host op array -> planner -> pinned staging -> H2D
         sv.expectations(e2e_term)  # D2H of the step's result
+        lap.append(time.perf_counter())
     t_e2e = time.perf_counter() - t0
+    if os.environ.get("NQ_BENCH_LAPS") == "1":
+        print(f"rank {rank} e2e step ms:", [round((b - a) * 1e3, 2) for a, b in zip([t0] + lap[:-1], lap)],
+              file=sys.stderr)
     prof_e2e = abi.profile_end(dev)
     t_e2e = max_over_ranks(dist, local, t_e2e)
     e2e = {"value": gates_total / t_e2e, "unit": "gates/s",

@@ -32,6 +32,8 @@ dist.barrier()
 
 
 def timed(label, fn, reps=3):
+    fn()
+    abi.jit_wait()
     dist.barrier()
     sv.synchronize()
     t0 = time.perf_counter()
@@ -41,9 +43,10 @@ def timed(label, fn, reps=3):
     dt = (time.perf_counter() - t0) / reps * 1e3
     c0 = sv.comm_stats()
     if rank == 0:
-        print(f"{label}: {dt:.2f} ms  comm={c0}", flush=True)
+        print(f"{label}: {dt:.2f} ms  comm={c0} jit={abi.jit_stats()}", flush=True)
 
 
+timed("flush", lambda: sv.apply(ops).flush())
 timed("flush", lambda: sv.apply(ops).flush())
 timed("expect", lambda: sv.expectations(term))
 timed("apply+expect", lambda: (sv.apply(ops), sv.expectations(term)))
