@@ -566,7 +566,9 @@ bool compile_entry(const std::string& src, Entry& e, int device) {
         cudaGetLastError();
         return false;
     }
-    if (cudaLibraryGetKernel(&e.kern, e.lib, "nqjit") != cudaSuccess) {
+    // pass kernels are `nqjit`, expectation batches `nqexp`
+    const char* name = src.find(" nqexp(") != std::string::npos ? "nqexp" : "nqjit";
+    if (cudaLibraryGetKernel(&e.kern, e.lib, name) != cudaSuccess) {
         e.log += " cudaLibraryGetKernel failed";
         cudaGetLastError();
         return false;
@@ -830,7 +832,7 @@ std::string expect_source(const ExpBatch& b) {
     const int minb = std::max(1, 512 / T);
     s << "#include \"pass_ops.cuh\"\n"
       << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << minb << ")\n"
-      << "nqjit(const double2* __restrict__ st, double* __restrict__ part, long long ntiles) {\n"
+      << " nqexp(const double2* __restrict__ st, double* __restrict__ part, long long ntiles) {\n"
       << "  using namespace nq;\n"
       << "  extern __shared__ __align__(16) unsigned char smem[];\n"
       << "  double2* buf0 = reinterpret_cast<double2*>(smem);\n"
