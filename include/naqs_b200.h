@@ -183,6 +183,23 @@ nq_status nq_dm_last_stats(const nq_dm* d, int64_t* passes, int64_t* microops,
                            int64_t* source_ops, int64_t* launches);
 nq_status nq_dm_synchronize(nq_dm* d);
 
+/* ---- batched Monte-Carlo trajectories ---------------- */
+/* ntraj independent run_trajectory() calls (statevector.cpp:339-401) of one
+ * schedule in one launch, each from |0...0>.  Every channel item consumes one
+ * uniform: trajectory t uses uniforms[t*C .. t*C+C) (C = channel items), which
+ * is exactly the sequential loop over trajectories sharing one Rng
+ * (acceptance_main.cpp:154-160).  Gates: MEASURE and BARRIER skipped as in
+ * run_trajectory.  Outputs per trajectory: the Pauli expectations (as
+ * nq_sv_expectation_batch) in out[t*nterms + j]; optionally the chosen Kraus
+ * branch per channel (branch_out, ntraj*C) and the final amplitudes
+ * (amps_out, ntraj * 2^n complex).  1 <= n <= 13.  A channel whose branch
+ * weights do not sum to 1 within 1e-8 fails with NQ_ERR_CONTRACT (the
+ * reference's trace-preservation check). */
+nq_status nq_traj_run(int num_qubits, const nq_sched_item* items, int64_t count, const double* kraus_pool,
+                      int64_t ntraj, const double* uniforms, const uint64_t* flip, const uint64_t* signs,
+                      const int32_t* ny, const double* coeff, int nterms, double* out, int32_t* branch_out,
+                      double* amps_out, int device);
+
 /* ---- readout (replaces readout_apply_dist, noise.cpp:177-203) --------- */
 /* Tensor-product confusion map on a 2^n distribution, on the device.
  * Validates length implicitly (n) and sum within 1e-9 (contract error). */

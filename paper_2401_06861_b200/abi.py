@@ -147,6 +147,8 @@ SIGNATURES = {
     "nq_profile_end": ([C.c_int, C.POINTER(nq_profile)], C.c_int),
     "nq_jit_wait": ([], C.c_int),
     "nq_jit_shutdown": ([], C.c_int),
+    "nq_traj_run": ([C.c_int, _p, C.c_int64, _dp, C.c_int64, _p, _p, _p, _p, _p, C.c_int, _p, _p, _dp, C.c_int],
+                    C.c_int),
     "nq_jit_stats": ([_i64p, _i64p, _i64p, _i64p], C.c_int),
     "nq_jit_debug": ([C.c_int, _p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int64, _i64p,
                       C.POINTER(C.c_int)], C.c_int),
@@ -398,24 +400,7 @@ class DM:
 
     def apply_schedule(self, items):
         """items: [("gate", (name, qubits, params)) | ("channel", qubits, kraus_list)]."""
-        arr = np.zeros(len(items), dtype=SCHED_DTYPE)
-        pool = []
-        off = 0
-        for i, it in enumerate(items):
-            if it[0] == "gate":
-                arr[i]["type"] = 0
-                arr[i]["op"] = make_ops([it[1]])[0]
-            else:
-                qubits, kraus = it[1], np.asarray(it[2], dtype=np.complex128)
-                arr[i]["type"] = 1
-                arr[i]["nkraus"] = len(kraus)
-                arr[i]["kraus_offset"] = off
-                arr[i]["op"]["nqubits"] = len(qubits)
-                for j, q in enumerate(qubits):
-                    arr[i]["op"]["qubits"][j] = q
-                pool.append(kraus.reshape(-1))
-                off += kraus.size
-        p = np.ascontiguousarray(np.concatenate(pool) if pool else np.zeros(1, dtype=np.complex128))
+        arr, p = make_schedule(items)
         check(lib.nq_dm_apply_schedule(self.h, arr.ctypes.data, len(arr), p.view(np.float64).ctypes.data_as(_dp)))
 
     def flush(self):
@@ -533,6 +518,53 @@ def jit_debug(n: int, ops, pass_index: int, tile_qubits: int = 0, compile: bool 
     check(lib.nq_jit_debug(n, arr.ctypes.data, len(arr), tile_qubits, pass_index, 1 if compile else 0, buf,
                            len(buf), C.byref(size), C.byref(ok)))
     return buf.raw[: size.value].decode(), ok.value
+
+
+def make_schedule(items):
+    """Encode [("gate", (name, qubits, params)) | ("channel", qubits, kraus_list)]
+    as (nq_sched_item array, complex Kraus pool)."""
+    arr = np.zeros(len(items), dtype=SCHED_DTYPE)
+    pool = []
+    off = 0
+    for i, it in enumerate(items):
+        if it[0] == "gate":
+            arr[i]["type"] = 0
+            arr[i]["op"] = make_ops([it[1]])[0]
+        else:
+            qubits, kraus = it[1], np.asarray(it[2], dtype=np.complex128)
+            arr[i]["type"] = 1
+            arr[i]["nkraus"] = len(kraus)
+            arr[i]["kraus_offset"] = off
+            arr[i]["op"]["nqubits"] = len(qubits)
+            for j, q in enumerate(qubits):
+                arr[i]["op"]["qubits"][j] = q
+            pool.append(kraus.reshape(-1))
+            off += kraus.size
+    p = np.ascontiguousarray(np.concatenate(pool) if pool else np.zeros(1, dtype=np.complex128))
+    return arr, p
+
+
+def traj_run(n: int, items, ntraj: int, uniforms, terms, branches: bool = False, amplitudes: bool = False,
+             device: int = -1):
+    """Batched run_trajectory (nq_traj_run): `uniforms` is (ntraj, channels)
+    in the order the sequential loop draws them.  Returns (expectations
+    [ntraj, nterms], branches [ntraj, C] or None, amplitudes [ntraj, 2^n] or None)."""
+    arr, p = make_schedule(items)
+    nch = int(np.sum(arr["type"] == 1))
+    u = np.ascontiguousarray(np.asarray(uniforms, dtype=np.float64).reshape(ntraj, nch))
+    flip = np.array([pauli_masks(t[0])[0] for t in terms], dtype=np.uint64)
+    signs = np.array([pauli_masks(t[0])[1] for t in terms], dtype=np.uint64)
+    ny = np.array([pauli_masks(t[0])[2] for t in terms], dtype=np.int32)
+    coeff = np.array([t[1] for t in terms], dtype=np.float64)
+    out = np.zeros((ntraj, len(terms)))
+    br = np.zeros((ntraj, nch), dtype=np.int32) if branches else None
+    am = np.zeros((ntraj, 1 << n), dtype=np.complex128) if amplitudes else None
+    check(lib.nq_traj_run(n, arr.ctypes.data, len(arr), p.view(np.float64).ctypes.data_as(_dp), ntraj,
+                          _ptr(u, C.c_double), _ptr(flip, C.c_uint64), _ptr(signs, C.c_uint64),
+                          _ptr(ny, C.c_int32), _ptr(coeff, C.c_double), len(terms), _ptr(out, C.c_double),
+                          br.ctypes.data_as(C.POINTER(C.c_int32)) if br is not None else None,
+                          am.view(np.float64).ctypes.data_as(_dp) if am is not None else None, device))
+    return out, br, am
 
 
 def device_count() -> int:

@@ -1143,6 +1143,122 @@ nq_status nq_plan_debug(int n, const nq_op* ops, int64_t count, int tile_qubits,
 
 }  // extern "C"
 
+extern "C" {
+
+// ---- batched trajectories -----------------------------------------------------
+nq_status nq_traj_run(int n, const nq_sched_item* items, int64_t count, const double* kraus_pool, int64_t ntraj,
+                      const double* uniforms, const uint64_t* flip, const uint64_t* signs, const int32_t* ny,
+                      const double* coeff, int nterms, double* out, int32_t* branch_out, double* amps_out,
+                      int device) {
+    return guard([&] {
+        if (n < 1 || n > kMaxTrajQubits)
+            throw NqError{NQ_ERR_CONTRACT, "trajectory batch qubit count must be in [1, " +
+                                               std::to_string(kMaxTrajQubits) + "], got " + std::to_string(n)};
+        if (ntraj < 0 || nterms < 0) throw NqError{NQ_ERR_CONTRACT, "negative trajectory or term count"};
+        std::vector<TrajItem> prog;
+        std::vector<cplx> pool;
+        int nch = 0;
+        for (int64_t i = 0; i < count; ++i) {
+            const nq_sched_item& it = items[i];
+            TrajItem t{};
+            if (it.type == 0) {
+                const nq_op& op = it.op;
+                if (op.kind == NQ_MEASURE || op.kind == NQ_BARRIER || op.kind == NQ_ID) continue;
+                check_op_shape(op);
+                check_range(op.qubits, op.nqubits, n);
+                t.type = 0;
+                t.k = op.nqubits;
+                for (int j = 0; j < t.k; ++j) t.q[j] = op.qubits[j];
+                t.nmat = 1;
+                t.mat = int64_t(pool.size());
+                const std::vector<cplx> m = full_gate_matrix(op);
+                pool.insert(pool.end(), m.begin(), m.end());
+            } else {
+                const int k = it.op.nqubits;
+                if (k < 1 || k > 3) throw NqError{NQ_ERR_CONTRACT, "channel arity must be 1..3"};
+                if (it.nkraus < 1 || it.nkraus > kMaxTrajKraus)
+                    throw NqError{NQ_ERR_CONTRACT, "channel Kraus count out of range"};
+                check_range(it.op.qubits, k, n);
+                t.type = 1;
+                t.k = k;
+                for (int j = 0; j < k; ++j) t.q[j] = it.op.qubits[j];
+                t.nmat = it.nkraus;
+                t.mat = int64_t(pool.size());
+                const size_t len = size_t(it.nkraus) << (2 * k);
+                const cplx* src = reinterpret_cast<const cplx*>(kraus_pool) + it.kraus_offset;
+                pool.insert(pool.end(), src, src + len);
+                ++nch;
+            }
+            prog.push_back(t);
+        }
+        if (ntraj == 0) return;
+        DeviceCtx& c = ctx_for(device < 0 ? 0 : device);
+        CUDA_TRY(cudaSetDevice(c.dev));
+        const size_t dim = size_t(1) << n;
+        const size_t nt = size_t(nterms), tr = size_t(ntraj), C = size_t(nch);
+        // one device block: items | pool | uniforms | flip | signs | re | im | branch | amps | err
+        auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+        const size_t o_items = 0, o_pool = al(o_items + prog.size() * sizeof(TrajItem));
+        const size_t o_u = al(o_pool + pool.size() * sizeof(cplx));
+        const size_t o_f = al(o_u + tr * C * sizeof(double));
+        const size_t o_s = al(o_f + nt * 8), o_re = al(o_s + nt * 8), o_im = al(o_re + tr * nt * 8);
+        const size_t o_br = al(o_im + tr * nt * 8), o_am = al(o_br + (branch_out ? tr * C * 4 : 0));
+        const size_t o_err = al(o_am + (amps_out ? tr * dim * 16 : 0)), total = o_err + 256;
+        unsigned char* d = nullptr;
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d), total, c.stream));
+        auto h2d = [&](size_t off, const void* src, size_t bytes) {
+            if (bytes) CUDA_TRY(cudaMemcpyAsync(d + off, src, bytes, cudaMemcpyHostToDevice, c.stream));
+            c.h2d_bytes += int64_t(bytes);
+        };
+        h2d(o_items, prog.data(), prog.size() * sizeof(TrajItem));
+        h2d(o_pool, pool.data(), pool.size() * sizeof(cplx));
+        h2d(o_u, uniforms, tr * C * sizeof(double));
+        h2d(o_f, flip, nt * 8);
+        h2d(o_s, signs, nt * 8);
+        CUDA_TRY(cudaMemsetAsync(d + o_err, 0, 4, c.stream));
+        TrajArgs p{};
+        p.n = n;
+        p.nitems = int(prog.size());
+        p.nchannels = nch;
+        p.nterms = nterms;
+        p.items = reinterpret_cast<const TrajItem*>(d + o_items);
+        p.pool = reinterpret_cast<const double2*>(d + o_pool);
+        p.uniforms = reinterpret_cast<const double*>(d + o_u);
+        p.flip = reinterpret_cast<const uint64_t*>(d + o_f);
+        p.signs = reinterpret_cast<const uint64_t*>(d + o_s);
+        p.out_re = reinterpret_cast<double*>(d + o_re);
+        p.out_im = reinterpret_cast<double*>(d + o_im);
+        p.branch_out = branch_out ? reinterpret_cast<int32_t*>(d + o_br) : nullptr;
+        p.amps_out = amps_out ? reinterpret_cast<double2*>(d + o_am) : nullptr;
+        p.err = reinterpret_cast<int*>(d + o_err);
+        launch_traj(p, ntraj, c.stream);
+        CUDA_TRY(cudaGetLastError());
+        std::vector<double> re(tr * nt), im(tr * nt);
+        int err = 0;
+        auto d2h = [&](void* dst, size_t off, size_t bytes) {
+            if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, d + off, bytes, cudaMemcpyDeviceToHost, c.stream));
+            c.d2h_bytes += int64_t(bytes);
+        };
+        d2h(re.data(), o_re, re.size() * 8);
+        d2h(im.data(), o_im, im.size() * 8);
+        if (branch_out) d2h(branch_out, o_br, tr * C * 4);
+        if (amps_out) d2h(amps_out, o_am, tr * dim * 16);
+        d2h(&err, o_err, 4);
+        CUDA_TRY(cudaFreeAsync(d, c.stream));
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        if (err)
+            throw NqError{NQ_ERR_CONTRACT,
+                          "Kraus branch probabilities do not sum to 1; channel is not trace preserving on this state"};
+        for (size_t b = 0; b < tr; ++b)
+            for (size_t j = 0; j < nt; ++j) {
+                const cplx tot(re[b * nt + j], im[b * nt + j]);
+                out[b * nt + j] = coeff[j] * (tot * kIPow[ny[j] & 3]).real();
+            }
+    });
+}
+
+}  // extern "C"
+
 extern "C" nq_status nq_sample_dist_sorted(const double* dist, uint64_t len, const double* sorted_u,
                                            uint64_t shots, uint64_t* idx_out, uint64_t* count_out,
                                            uint64_t* nout) {

@@ -48,6 +48,31 @@ void launch_expect_tiled(const double2* a, int nloc, const ExpBatch& b, double* 
 // out[t] = sum over nblk rows of part (row stride kMaxExpTerms), fixed order
 void launch_expect_final(const double* part, int nblk, int nt, double* out, cudaStream_t s);
 
+// batched trajectories (traj.cu)
+constexpr int kMaxTrajQubits = 13;  // state in shared memory
+constexpr int kMaxTrajKraus = 64;
+struct TrajItem {
+    int32_t type;  // 0 gate (one matrix), 1 channel (nmat Kraus matrices)
+    int32_t k;
+    int32_t q[3];
+    int32_t nmat;
+    int64_t mat;  // offset into the matrix pool (complex elements)
+};
+struct TrajArgs {
+    int n, nitems, nchannels, nterms;
+    const TrajItem* items;
+    const double2* pool;
+    const double* uniforms;  // ntraj x nchannels
+    const uint64_t* flip;
+    const uint64_t* signs;
+    double* out_re;  // ntraj x nterms
+    double* out_im;
+    int32_t* branch_out;  // ntraj x nchannels or null
+    double2* amps_out;    // ntraj x 2^n or null
+    int* err;             // set when a channel's branch weights do not sum to 1
+};
+void launch_traj(const TrajArgs& p, int64_t ntraj, cudaStream_t s);
+
 // half-shard pack/unpack for global<->local qubit swaps (comm_kernels.cu)
 void launch_half_pack(const double2* st, double2* buf, uint64_t k0, uint64_t len, int v, uint64_t val,
                       cudaStream_t s);

@@ -91,6 +91,35 @@ int kind_params(int kind) {
     }
 }
 
+// Full 2^k x 2^k matrix of any unitary kind, local bit j <-> qubits[j]
+// (proj/src/gates.cpp:26-47: CX control = bit 0, CCX controls = bits 0, 1).
+std::vector<cplx> full_gate_matrix(const nq_op& op) {
+    const int k = kind_arity(op.kind);
+    const int d = 1 << k;
+    std::vector<cplx> m(size_t(d) * d, cplx(0.0, 0.0));
+    auto at = [&](int r, int c) -> cplx& { return m[size_t(r) * d + c]; };
+    switch (op.kind) {
+    case NQ_CX:
+        for (int c = 0; c < 4; ++c) at((c & 1) ? c ^ 2 : c, c) = 1.0;
+        break;
+    case NQ_CZ:
+        for (int c = 0; c < 4; ++c) at(c, c) = c == 3 ? -1.0 : 1.0;
+        break;
+    case NQ_SWAP:
+        for (int c = 0; c < 4; ++c) at(((c & 1) << 1) | (c >> 1), c) = 1.0;
+        break;
+    case NQ_CCX:
+        for (int c = 0; c < 8; ++c) at((c & 3) == 3 ? c ^ 4 : c, c) = 1.0;
+        break;
+    default: {
+        cplx g[4];
+        gate_matrix_2x2(op.kind, op.params, g);
+        m.assign(g, g + 4);
+    }
+    }
+    return m;
+}
+
 // ---- state vector ------------------------------------------------------------
 void lower_sv_op(const nq_op& op, std::vector<EOp>& out) {
     EOp e;

@@ -11,6 +11,7 @@ int kind_arity(int kind);
 int kind_params(int kind);
 
 void lower_sv_op(const nq_op& op, std::vector<EOp>& out);
+std::vector<cplx> full_gate_matrix(const nq_op& op);
 EOp sv_matrix_op(const int* qubits, int k, const cplx* mat);
 
 void lower_dm_op(const nq_op& op, int n, std::vector<EOp>& out);
