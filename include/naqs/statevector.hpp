@@ -82,4 +82,12 @@ std::string index_to_bitstring(std::size_t index, int n);
 std::map<std::string, std::uint64_t> sample_distribution(const std::vector<double>& dist, int n,
                                                          std::uint64_t shots, std::uint64_t seed);
 
+/// Batched Monte-Carlo trajectories (beyond the reference API; SURVEY.md §8
+/// f1): `ntraj` runs of `schedule` from |0...0> in one device launch, drawing
+/// from `rng` exactly as the sequential loop
+/// `for (t) { StateVector s(n); s.run_trajectory(schedule, rng); }` does, so
+/// row t holds the `observables` of the same trajectory that loop would give.
+std::vector<std::vector<double>> run_trajectories(const NoisySchedule& schedule, std::uint64_t ntraj, Rng& rng,
+                                                  const std::vector<PauliString>& observables);
+
 } // namespace naqs

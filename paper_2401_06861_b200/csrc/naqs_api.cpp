@@ -946,6 +946,63 @@ void DensityMatrix::run(const Circuit& c) {
     mirror_ok_ = false;
 }
 
+std::vector<std::vector<double>> run_trajectories(const NoisySchedule& schedule, std::uint64_t ntraj, Rng& rng,
+                                                  const std::vector<PauliString>& observables) {
+    const int n = schedule.num_qubits;
+    std::vector<nq_sched_item> items;
+    std::vector<double> pool;
+    size_t nch = 0;
+    for (const auto& item : schedule.items) {
+        nq_sched_item it{};
+        if (const auto* op = std::get_if<GateOp>(&item)) {
+            if (op->kind == GateKind::MEASURE || op->kind == GateKind::BARRIER) continue;
+            it.type = 0;
+            it.op = to_abi(*op);
+        } else {
+            // every channel draws one uniform, identity channels included
+            // (apply_kraus_trajectory, statevector.cpp:339-386)
+            const auto& app = std::get<ChannelApplication>(item);
+            if (int(app.qubits.size()) != app.channel.arity)
+                throw ContractError("channel arity " + std::to_string(app.channel.arity) + " does not match " +
+                                    std::to_string(app.qubits.size()) + " qubits");
+            it.type = 1;
+            it.nkraus = int32_t(app.channel.kraus.size());
+            it.kraus_offset = int64_t(pool.size() / 2);
+            it.op.nqubits = int32_t(app.qubits.size());
+            for (size_t j = 0; j < app.qubits.size(); ++j) it.op.qubits[j] = app.qubits[j];
+            for (const auto& K : app.channel.kraus) {
+                auto f = flatten(K);
+                pool.insert(pool.end(), f.begin(), f.end());
+            }
+            ++nch;
+        }
+        items.push_back(it);
+    }
+    std::vector<double> u(size_t(ntraj) * nch);
+    for (auto& x : u) x = rng.next_double();
+    std::vector<uint64_t> flip, signs;
+    std::vector<int32_t> ny;
+    std::vector<double> coeff;
+    for (const auto& p : observables) {
+        if (p.n != n)
+            throw ContractError("Pauli string length " + std::to_string(p.n) + " does not match state qubit count " +
+                                std::to_string(n));
+        const PauliMasks m = masks_of(p);
+        flip.push_back(m.flip);
+        signs.push_back(m.signs);
+        ny.push_back(m.ny);
+        coeff.push_back(p.coefficient);
+    }
+    std::vector<double> flat(size_t(ntraj) * observables.size());
+    check(nq_traj_run(n, items.data(), int64_t(items.size()), pool.empty() ? nullptr : pool.data(), int64_t(ntraj),
+                      u.data(), flip.data(), signs.data(), ny.data(), coeff.data(), int(observables.size()),
+                      flat.data(), nullptr, nullptr, -1));
+    std::vector<std::vector<double>> out{static_cast<size_t>(ntraj)};
+    for (size_t t = 0; t < size_t(ntraj); ++t)
+        out[t].assign(flat.begin() + long(t * observables.size()), flat.begin() + long((t + 1) * observables.size()));
+    return out;
+}
+
 void DensityMatrix::run_schedule(const NoisySchedule& schedule) {
     if (schedule.num_qubits != n_) throw ContractError("schedule qubit count mismatch");
     std::vector<nq_sched_item> items;

@@ -98,3 +98,22 @@ def test_contract_errors():
     with pytest.raises(abi.ContractError):
         abi.traj_run(2, bad, 2, np.full((2, 1), 0.3), [("ZI", 1.0)])
     del port
+
+
+def test_python_api_acceptance5():
+    """naqs.trajectory_expectations: acceptance criterion 5 through the drop-in
+    Python surface (attach_noise + Rng(505) + 10^4 trajectories)."""
+    import json
+
+    n = 3
+    cal = {"name": "acc5", "qubits": [{"t1_us": 60.0, "t2_us": 40.0, "readout_p01": 0.0, "readout_p10": 0.0}] * n,
+           "default_1q": {"error": 0.02, "duration_ns": 100.0}, "default_2q": {"error": 0.02, "duration_ns": 100.0}}
+    model = naqs.load_calibration(json.dumps(cal))
+    c = naqs.Circuit(n)
+    for name, qs, ps in [("h", [0], []), ("cx", [0, 1], []), ("cx", [1, 2], []), ("rx", [0], [0.4]),
+                         ("rz", [1], [0.9]), ("cx", [0, 2], [])]:
+        c.add(name, qs, ps)
+    z = naqs.trajectory_expectations(c, ["ZII"], model, 10000, 505)[:, 0]
+    dm = naqs.density_expectation(c, "ZII", model)
+    se = np.sqrt(z.var() / len(z))
+    assert abs(z.mean() - dm) <= 3 * se
