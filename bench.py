@@ -329,7 +329,43 @@ def secondary_workloads(abi, workloads, device):
     out["vqe28"] = {"evals_per_s": 1.0 / dt, "ms_per_eval": dt * 1e3, "energy": e, "terms": len(terms),
                     "gates": len(vops)}
     sv.close()
+    # f1: batched Monte-Carlo trajectories (one launch) vs the reference's
+    # sequential loop (acceptance 5 shape, and a 10-qubit noisy TFIM)
+    out["trajectories"] = trajectory_workloads(workloads)
     return out
+
+
+def trajectory_workloads(workloads):
+    import numpy as np
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import NoiseSpec, Ref  # CPU baseline only
+    from paper_2401_06861_b200 import naqs
+
+    res = {}
+    cases = [("acc5_n3", 3, [("h", [0], []), ("cx", [0, 1], []), ("cx", [1, 2], []), ("rx", [0], [0.4]),
+                             ("rz", [1], [0.9]), ("cx", [0, 2], [])], 10000, 10000,
+              NoiseSpec(3, t1=60.0, t2=40.0, p01=0.0, p10=0.0, e1=0.02, d1=100.0, e2=0.02, d2=100.0)),
+             ("tfim_n10_5steps", 10, list(workloads.tfim_trotter(10, 0.5, steps=5)), 10000, 200,
+              NoiseSpec(10))]
+    for name, n, ops, ntraj, ncpu, spec in cases:
+        c = naqs.Circuit(n)
+        for g, qs, ps in ops:
+            c.add(g, qs, ps)
+        model = naqs.load_calibration(spec.calibration_json())
+        obs = ["Z" + "I" * (n - 1)]
+        naqs.trajectory_expectations(c, obs, model, 16, 1)  # warm
+        t0 = time.perf_counter()
+        z = naqs.trajectory_expectations(c, obs, model, ntraj, 505)[:, 0]
+        gpu_s = time.perf_counter() - t0
+        row = {"trajectories": ntraj, "gpu_wall_s": gpu_s, "gpu_traj_per_s": ntraj / gpu_s, "z0_mean": float(z.mean())}
+        if Ref.available():
+            ms, zref = Ref().traj_time(n, ops, spec, ncpu, 505)
+            row.update({"cpu_traj_per_s": ncpu / (ms / 1e3), "cpu_sample": f"first {ncpu} trajectories of the reference's "
+                        "sequential run_trajectory loop (shared Rng) on the host",
+                        "max_abs_diff_vs_cpu": float(np.max(np.abs(z[:ncpu] - zref)))})
+        res[name] = row
+    return res
 
 
 def main():

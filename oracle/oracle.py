@@ -395,6 +395,18 @@ class Ref:
         self._chk(self.lib.ref_sv_run_timed(h, arr.ctypes.data, len(arr), C.byref(ms)))
         return ms.value
 
+    def traj_time(self, n, ops, noise: NoiseSpec, ntraj, seed):
+        """Sequential reference trajectories (shared Rng): (wall ms, <Z0> per trajectory)."""
+        arr = ops if isinstance(ops, np.ndarray) else list_to_ops(ops)
+        ms = C.c_double()
+        z = np.zeros(ntraj)
+        t1, t2, p01, p10 = noise.arrays()
+        self._chk(self.lib.ref_traj_time(n, arr.ctypes.data, C.c_int64(len(arr)), t1, t2, p01, p10,
+                                         C.c_double(noise.e1), C.c_double(noise.d1), C.c_double(noise.e2),
+                                         C.c_double(noise.d2), C.c_int64(ntraj), C.c_uint64(seed), C.byref(ms),
+                                         _d(z)))
+        return ms.value, z
+
     def dm_time_noisy(self, n, ops, noise: NoiseSpec, reps):
         arr = ops if isinstance(ops, np.ndarray) else list_to_ops(ops)
         ms = np.zeros(reps)

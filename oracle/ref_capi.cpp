@@ -313,6 +313,30 @@ int ref_dm_time_noisy(int n, const RefOp* ops, int64_t nops, const double* t1, c
     });
 }
 
+// Sequential Monte-Carlo loop of acceptance criterion 5 (acceptance_main.cpp:
+// 154-160): ntraj trajectories sharing one Rng(seed); returns the wall time
+// and the per-trajectory <Z_0>.
+int ref_traj_time(int n, const RefOp* ops, int64_t nops, const double* t1, const double* t2, const double* p01,
+                  const double* p10, double e1, double d1, double e2, double d2, int64_t ntraj, uint64_t seed,
+                  double* ms, double* z0) {
+    return wrap([&] {
+        const DeviceNoiseModel m = model_from(n, t1, t2, p01, p10, e1, d1, e2, d2);
+        const NoisySchedule s = attach_noise(to_circuit(n, ops, nops), m);
+        std::string z(size_t(n), 'I');
+        z[0] = 'Z';
+        const PauliString pz(z);
+        Rng rng(seed);
+        const auto a = std::chrono::steady_clock::now();
+        for (int64_t t = 0; t < ntraj; ++t) {
+            StateVector sv(n);
+            sv.run_trajectory(s, rng);
+            z0[t] = sv.expectation(pz);
+        }
+        const auto b = std::chrono::steady_clock::now();
+        *ms = std::chrono::duration<double, std::milli>(b - a).count();
+    });
+}
+
 // Persistent state for CPU timing (bench.py cpu_baseline / --impl reference):
 // allocation and |0..0> fill happen once, outside the timed runs.
 void* ref_sv_new(int n) {

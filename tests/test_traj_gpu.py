@@ -117,3 +117,22 @@ def test_python_api_acceptance5():
     dm = naqs.density_expectation(c, "ZII", model)
     se = np.sqrt(z.var() / len(z))
     assert abs(z.mean() - dm) <= 3 * se
+
+
+@pytest.mark.skipif(not __import__("oracle").Ref.available(), reason="oracle/_ref not built")
+def test_per_trajectory_parity_with_reference_build():
+    """Row t equals trajectory t of the reference's own sequential loop
+    (run_trajectory with one shared Rng), within 1e-10."""
+    from oracle import Ref
+
+    n = 4
+    ops = [("h", [0], []), ("cx", [0, 1], []), ("ry", [2], [0.7]), ("cx", [1, 2], []), ("rz", [3], [0.2]),
+           ("cx", [2, 3], []), ("u3", [1], [0.4, 0.1, -0.3]), ("swap", [0, 3], [])]
+    spec = NoiseSpec(n, t1=50.0, t2=30.0, p01=0.0, p10=0.0, e1=0.03, d1=80.0, e2=0.05, d2=250.0)
+    _, zref = Ref().traj_time(n, ops, spec, 2000, 777)
+    c = naqs.Circuit(n)
+    for name, qs, ps in ops:
+        c.add(name, qs, ps)
+    z = naqs.trajectory_expectations(c, ["Z" + "I" * (n - 1)], naqs.load_calibration(spec.calibration_json()),
+                                     2000, 777)[:, 0]
+    assert np.max(np.abs(z - zref)) <= 1e-10
