@@ -395,6 +395,19 @@ class Ref:
         self._chk(self.lib.ref_sv_run_timed(h, arr.ctypes.data, len(arr), C.byref(ms)))
         return ms.value
 
+    def tfim_sweep(self, calib_json: str, n: int, t_max: float = 3.0, dt: float = 0.1, steps_per_unit: int = 100,
+                   max_rows: int = 1000):
+        """Reference magnetization sweep rows (no exact column): (t, ideal, noisy, wall ms)."""
+        t = np.zeros(max_rows)
+        ideal = np.zeros(max_rows)
+        noisy = np.zeros(max_rows)
+        nrows = C.c_int()
+        ms = C.c_double()
+        self._chk(self.lib.ref_tfim_sweep(calib_json.encode(), n, C.c_double(t_max), C.c_double(dt), steps_per_unit,
+                                          max_rows, _d(t), _d(ideal), _d(noisy), C.byref(nrows), C.byref(ms)))
+        k = nrows.value
+        return t[:k], ideal[:k], noisy[:k], ms.value
+
     def traj_time(self, n, ops, noise: NoiseSpec, ntraj, seed):
         """Sequential reference trajectories (shared Rng): (wall ms, <Z0> per trajectory)."""
         arr = ops if isinstance(ops, np.ndarray) else list_to_ops(ops)

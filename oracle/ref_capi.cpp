@@ -21,6 +21,7 @@
 #include "test_util.hpp"  // proj/tests/test_util.hpp: random_circuit()
 
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -332,6 +333,58 @@ int ref_traj_time(int n, const RefOp* ops, int64_t nops, const double* t1, const
             sv.run_trajectory(s, rng);
             z0[t] = sv.expectation(pz);
         }
+        const auto b = std::chrono::steady_clock::now();
+        *ms = std::chrono::duration<double, std::milli>(b - a).count();
+    });
+}
+
+// C1: the TFIM magnetization sweep of proj/src/tfim.cpp:139-184 without the
+// dense exact column (its eigensolver is outside the Eigen subset), shots = 0,
+// noise from calibration JSON.  build_trotter_circuit (tfim.cpp:36-62) is
+// restated here because tfim.cpp is not part of this build.
+int ref_tfim_sweep(const char* calib, int n, double t_max, double dt, int steps_per_unit, int max_rows,
+                   double* t_out, double* ideal_out, double* noisy_out, int* nrows, double* ms) {
+    return wrap([&] {
+        const DeviceNoiseModel m = load_calibration(std::string(calib));
+        const auto a = std::chrono::steady_clock::now();
+        int r = 0;
+        for (double t = 0.0; t <= t_max + 1e-12 && r < max_rows; t += dt, ++r) {
+            Circuit c(n);
+            if (t != 0.0) {
+                const int steps = static_cast<int>(std::ceil(t * steps_per_unit));
+                const double delta = t / steps;
+                for (int s = 0; s < steps; ++s) {
+                    for (int i = 0; i + 1 < n; ++i) {
+                        c.cx(i, i + 1);
+                        c.rz(i + 1, -2.0 * delta);
+                        c.cx(i, i + 1);
+                    }
+                    for (int i = 0; i < n; ++i) c.rx(i, -2.0 * delta);
+                }
+            }
+            StateVector sv(n);
+            sv.run(c);
+            double total = 0.0;
+            for (int q = 0; q < n; ++q) {
+                std::string z(size_t(n), 'I');
+                z[size_t(q)] = 'Z';
+                total += sv.expectation(PauliString(z));
+            }
+            const NoisySchedule sched = attach_noise(c, m);
+            DensityMatrix rho(n);
+            rho.run_schedule(sched);
+            const std::vector<double> dist = readout_apply_dist(rho.probabilities(), sched.readout);
+            double nz = 0.0;
+            for (int q = 0; q < n; ++q) {
+                double zq = 0.0;
+                for (size_t idx = 0; idx < dist.size(); ++idx) zq += ((idx >> q) & 1) ? -dist[idx] : dist[idx];
+                nz += zq;
+            }
+            t_out[r] = t;
+            ideal_out[r] = total / n;
+            noisy_out[r] = nz / n;
+        }
+        *nrows = r;
         const auto b = std::chrono::steady_clock::now();
         *ms = std::chrono::duration<double, std::milli>(b - a).count();
     });

@@ -171,3 +171,37 @@ def vqe_initial_params(n: int, layers: int, seed: int = 1):
     """proj/src/vqe.cpp:123-125: Rng(seed).uniform(-0.1, 0.1) per parameter."""
     rng = Rng(seed)
     return [rng.uniform(-0.1, 0.1) for _ in range(n * (layers + 1))]
+
+
+def tfim_sweep_times(t_max: float = 3.0, dt: float = 0.1):
+    """Row times of magnetization_sweep (proj/src/tfim.cpp:158): t += dt from 0
+    while t <= t_max + 1e-12 (accumulated, so 3.0 appears as 3.0000000000000013)."""
+    out = []
+    t = 0.0
+    while t <= t_max + 1e-12:
+        out.append(t)
+        t += dt
+    return out
+
+
+def tfim_sweep_rows(naqs, n: int, model, t_max: float = 3.0, dt: float = 0.1, steps_per_unit: int = 100):
+    """C1 driver over the drop-in API: (t, ideal <Z>, noisy <Z> after readout)
+    per row of magnetization_sweep (proj/src/tfim.cpp:139-184, shots = 0,
+    without the dense exact column)."""
+    zs = []
+    for q in range(n):
+        L = ["I"] * n
+        L[q] = "Z"
+        zs.append("".join(L))
+    rows = []
+    for t in tfim_sweep_times(t_max, dt):
+        c = naqs.Circuit(n)
+        for name, qs, ps in tfim_trotter(n, t, steps_per_unit):
+            c.add(name, qs, ps)
+        ideal = sum(naqs.expectations(c, zs)) / n
+        dist = naqs.noisy_distribution(c, model)
+        noisy = 0.0
+        for q in range(n):
+            noisy += sum(-p if (i >> q) & 1 else p for i, p in enumerate(dist))
+        rows.append((t, ideal, noisy / n))
+    return rows
