@@ -332,7 +332,38 @@ def secondary_workloads(abi, workloads, device):
     # f1: batched Monte-Carlo trajectories (one launch) vs the reference's
     # sequential loop (acceptance 5 shape, and a 10-qubit noisy TFIM)
     out["trajectories"] = trajectory_workloads(workloads)
+    out["tfim4_sweep"] = tfim4_sweep(workloads)
     return out
+
+
+def tfim4_sweep(workloads):
+    """C1: the n = 4 TFIM magnetization sweep (31 rows, ideal + noisy with
+    example_5q.json), end to end: all rows' state vectors in one launch and all
+    rows' noisy density matrices in another (naqs.batch_*), vs the reference's
+    own row loop on the host."""
+    import numpy as np
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Ref  # CPU baseline only
+    from paper_2401_06861_b200 import naqs
+
+    cal = open(os.path.join(ROOT, "tests", "golden", "example_5q.json")).read()
+    model = naqs.load_calibration(cal)
+    workloads.tfim_sweep_rows_batched(naqs, 4, model)  # warm
+    reps = 3
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        rows = np.array(workloads.tfim_sweep_rows_batched(naqs, 4, model))
+    gpu_s = (time.perf_counter() - t0) / reps
+    res = {"rows": len(rows), "gpu_wall_s": gpu_s, "gates": 60671, "note": "SV ideal + DM noisy columns, shots = 0"}
+    if Ref.available():
+        ref = Ref()
+        threads = ref.set_threads(cpu_threads())
+        _, ideal, noisy, ms = ref.tfim_sweep(cal, 4)
+        res.update({"cpu_wall_s": ms / 1e3, "cpu_threads": threads,
+                    "max_abs_diff_vs_cpu": float(max(np.max(np.abs(rows[:, 1] - ideal)),
+                                                     np.max(np.abs(rows[:, 2] - noisy))))})
+    return res
 
 
 def trajectory_workloads(workloads):

@@ -59,4 +59,10 @@ class DensityMatrix {
 
 DensityMatrix dm_run_noisy(const Circuit& c, const DeviceNoiseModel& m);
 
+/// Batches of small noisy circuits in one launch (the noisy
+/// column of magnetization_sweep): row b = readout_apply_dist(probabilities of
+/// dm_run_noisy(circuits[b], m), readout) (n <= 6).
+std::vector<std::vector<double>> batch_noisy_distributions(const std::vector<Circuit>& circuits,
+                                                           const DeviceNoiseModel& m);
+
 } // namespace naqs

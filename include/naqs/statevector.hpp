@@ -90,4 +90,10 @@ std::map<std::string, std::uint64_t> sample_distribution(const std::vector<doubl
 std::vector<std::vector<double>> run_trajectories(const NoisySchedule& schedule, std::uint64_t ntraj, Rng& rng,
                                                   const std::vector<PauliString>& observables);
 
+/// Batches of small independent circuits in one launch (
+/// TFIM sweep rows, VQE evaluations): row b = the observables of
+/// sv_run(circuits[b]) (all circuits on the same qubit count, n <= 12).
+std::vector<std::vector<double>> batch_expectations(const std::vector<Circuit>& circuits,
+                                                    const std::vector<PauliString>& observables);
+
 } // namespace naqs

@@ -200,6 +200,20 @@ nq_status nq_traj_run(int num_qubits, const nq_sched_item* items, int64_t count,
                       const int32_t* ny, const double* coeff, int nterms, double* out, int32_t* branch_out,
                       double* amps_out, int device);
 
+/* ---- batches of small independent circuits --------- */
+/* `batch` circuits, circuit b = items[item_off[b] .. item_off[b+1]), each run
+ * from |0...0> in one launch (one CTA per circuit, state in shared memory).
+ * dm = 0: ideal state vectors (gates only; n <= 12); out[b*nterms + j] as
+ * nq_sv_expectation_batch, probs[b*2^n + i] = |a_i|^2.
+ * dm = 1: density matrices with gates and channels as run_schedule
+ * (densitymatrix.cpp:154-167; n <= 6, channel arity <= 2); out as
+ * nq_dm_expectation_batch (out_im receives the imaginary residue, may be
+ * NULL), probs as DensityMatrix::probabilities (clip at 0, renormalise).
+ * MEASURE / BARRIER / ID items are skipped; probs may be NULL. */
+nq_status nq_batch_run(int num_qubits, int dm, int64_t batch, const int64_t* item_off, const nq_sched_item* items,
+                       const double* kraus_pool, const uint64_t* flip, const uint64_t* signs, const int32_t* ny,
+                       const double* coeff, int nterms, double* out, double* out_im, double* probs, int device);
+
 /* ---- readout (replaces readout_apply_dist, noise.cpp:177-203) --------- */
 /* Tensor-product confusion map on a 2^n distribution, on the device.
  * Validates length implicitly (n) and sum within 1e-9 (contract error). */

@@ -147,6 +147,8 @@ SIGNATURES = {
     "nq_profile_end": ([C.c_int, C.POINTER(nq_profile)], C.c_int),
     "nq_jit_wait": ([], C.c_int),
     "nq_jit_shutdown": ([], C.c_int),
+    "nq_batch_run": ([C.c_int, C.c_int, C.c_int64, _p, _p, _dp, _p, _p, _p, _p, C.c_int, _p, _p, _p, C.c_int],
+                     C.c_int),
     "nq_traj_run": ([C.c_int, _p, C.c_int64, _dp, C.c_int64, _p, _p, _p, _p, _p, C.c_int, _p, _p, _dp, C.c_int],
                     C.c_int),
     "nq_jit_stats": ([_i64p, _i64p, _i64p, _i64p], C.c_int),
@@ -565,6 +567,31 @@ def traj_run(n: int, items, ntraj: int, uniforms, terms, branches: bool = False,
                           br.ctypes.data_as(C.POINTER(C.c_int32)) if br is not None else None,
                           am.view(np.float64).ctypes.data_as(_dp) if am is not None else None, device))
     return out, br, am
+
+
+def batch_run(n: int, circuits_items, terms, dm: bool = False, probabilities: bool = False, device: int = -1):
+    """nq_batch_run: circuits_items = one schedule item list per circuit (see
+    make_schedule).  Returns (expectations [B, T], imaginary residue [B, T],
+    probabilities [B, 2^n] or None)."""
+    B = len(circuits_items)
+    flat, off = [], [0]
+    for items in circuits_items:
+        flat.extend(items)
+        off.append(len(flat))
+    arr, p = make_schedule(flat)
+    offs = np.array(off, dtype=np.int64)
+    flip = np.array([pauli_masks(t[0])[0] for t in terms], dtype=np.uint64)
+    signs = np.array([pauli_masks(t[0])[1] for t in terms], dtype=np.uint64)
+    ny = np.array([pauli_masks(t[0])[2] for t in terms], dtype=np.int32)
+    coeff = np.array([t[1] for t in terms], dtype=np.float64)
+    out = np.zeros((B, len(terms)))
+    oim = np.zeros((B, len(terms)))
+    pr = np.zeros((B, 1 << n)) if probabilities else None
+    check(lib.nq_batch_run(n, 1 if dm else 0, B, offs.ctypes.data, arr.ctypes.data,
+                           p.view(np.float64).ctypes.data_as(_dp), _ptr(flip, C.c_uint64), _ptr(signs, C.c_uint64),
+                           _ptr(ny, C.c_int32), _ptr(coeff, C.c_double), len(terms), _ptr(out, C.c_double),
+                           _ptr(oim, C.c_double), pr.ctypes.data if pr is not None else None, device))
+    return out, oim, pr
 
 
 def device_count() -> int:

@@ -14,6 +14,7 @@
 #include "state.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -23,6 +24,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <tuple>
 #include <vector>
 
 using namespace nqe;
@@ -1144,6 +1146,226 @@ nq_status nq_plan_debug(int n, const nq_op* ops, int64_t count, int tile_qubits,
 }  // extern "C"
 
 extern "C" {
+
+// ---- batches of small circuits ---------------------------------------------------
+nq_status nq_batch_run(int n, int dm, int64_t batch, const int64_t* item_off, const nq_sched_item* items,
+                       const double* kraus_pool, const uint64_t* flip, const uint64_t* signs, const int32_t* ny,
+                       const double* coeff, int nterms, double* out, double* out_im, double* probs, int device) {
+    return guard([&] {
+        const int maxq = dm ? kMaxBatchBits / 2 : kMaxBatchBits;
+        if (n < 1 || n > maxq)
+            throw NqError{NQ_ERR_CONTRACT, std::string(dm ? "density-matrix" : "state-vector") +
+                                               " batch qubit count must be in [1, " + std::to_string(maxq) +
+                                               "], got " + std::to_string(n)};
+        if (batch < 0 || nterms < 0) throw NqError{NQ_ERR_CONTRACT, "negative batch or term count"};
+        std::vector<TrajItem> prog;
+        std::vector<cplx> pool;
+        std::vector<int64_t> off(size_t(batch) + 1, 0);
+        // Liouville lowering with caches: a long noisy circuit repeats a few
+        // distinct superoperators, and products of consecutive ones on the same
+        // (or nested) bit sets are fused once and reused.
+        std::map<std::vector<double>, int64_t> content_at;  // matrix data -> pool offset
+        std::map<std::vector<double>, int64_t> gate_super_at;  // gate matrix U -> its superoperator
+        std::map<std::tuple<int64_t, int32_t, int>, int64_t> channel_at;  // (kraus_offset, nkraus, k) -> superop
+        std::map<std::tuple<int64_t, int64_t, unsigned>, int64_t> product_at;  // (new, last, positions) -> fused
+        auto intern = [&](const cplx* m, size_t len) {
+            std::vector<double> key(reinterpret_cast<const double*>(m), reinterpret_cast<const double*>(m) + 2 * len);
+            auto f = content_at.find(key);
+            if (f != content_at.end()) return f->second;
+            const int64_t at = int64_t(pool.size());
+            pool.insert(pool.end(), m, m + len);
+            content_at.emplace(std::move(key), at);
+            return at;
+        };
+        auto push_item = [&](int k, const int* q, int64_t mat, int64_t first_of_circuit) {
+            // fuse into the previous item of this circuit when our bits are a subset of its bits
+            if (dm && int64_t(prog.size()) > first_of_circuit) {
+                TrajItem& last = prog.back();
+                int pos[4];
+                bool subset = k <= last.k;
+                for (int j = 0; j < k && subset; ++j) {
+                    pos[j] = -1;
+                    for (int i = 0; i < last.k; ++i)
+                        if (last.q[i] == q[j]) pos[j] = i;
+                    subset = pos[j] >= 0;
+                }
+                if (subset) {
+                    unsigned code = unsigned(k);
+                    for (int j = 0; j < k; ++j) code |= unsigned(pos[j]) << (4 + 2 * j);
+                    const auto key = std::make_tuple(mat, last.mat, code);
+                    auto f = product_at.find(key);
+                    if (f == product_at.end()) {
+                        // fused = (A on positions pos) * M_last, column by column
+                        const int D = 1 << last.k, d = 1 << k;
+                        std::vector<cplx> M(pool.begin() + last.mat, pool.begin() + last.mat + size_t(D) * D);
+                        const cplx* A = pool.data() + mat;
+                        unsigned pm = 0;
+                        for (int j = 0; j < k; ++j) pm |= 1u << pos[j];
+                        std::vector<cplx> x(static_cast<size_t>(d)), y(static_cast<size_t>(d));
+                        for (int col = 0; col < D; ++col)
+                            for (int g = 0; g < D; ++g) {
+                                if (unsigned(g) & pm) continue;  // g: base with the sub bits clear
+                                for (int c = 0; c < d; ++c) {
+                                    int r = g;
+                                    for (int j = 0; j < k; ++j)
+                                        if ((c >> j) & 1) r |= 1 << pos[j];
+                                    x[size_t(c)] = M[size_t(r) * D + col];
+                                }
+                                for (int rr = 0; rr < d; ++rr) {
+                                    cplx acc(0.0, 0.0);
+                                    for (int c = 0; c < d; ++c) acc += A[size_t(rr) * d + c] * x[size_t(c)];
+                                    y[size_t(rr)] = acc;
+                                }
+                                for (int c = 0; c < d; ++c) {
+                                    int r = g;
+                                    for (int j = 0; j < k; ++j)
+                                        if ((c >> j) & 1) r |= 1 << pos[j];
+                                    M[size_t(r) * D + col] = y[size_t(c)];
+                                }
+                            }
+                        f = product_at.emplace(key, intern(M.data(), M.size())).first;
+                    }
+                    last.mat = f->second;
+                    return;
+                }
+            }
+            TrajItem t{};
+            t.type = 0;
+            t.k = k;
+            for (int j = 0; j < k; ++j) t.q[j] = q[j];
+            t.nmat = 1;
+            t.mat = mat;
+            prog.push_back(t);
+        };
+        for (int64_t b = 0; b < batch; ++b) {
+            const int64_t first = int64_t(prog.size());
+            off[size_t(b)] = first;
+            if (item_off[b + 1] < item_off[b]) throw NqError{NQ_ERR_CONTRACT, "item offsets must be non-decreasing"};
+            for (int64_t i = item_off[b]; i < item_off[b + 1]; ++i) {
+                const nq_sched_item& it = items[i];
+                if (it.type == 0) {
+                    const nq_op& op = it.op;
+                    if (op.kind == NQ_MEASURE || op.kind == NQ_BARRIER || op.kind == NQ_ID) continue;
+                    check_op_shape(op);
+                    check_range(op.qubits, op.nqubits, n);
+                    const std::vector<cplx> m = full_gate_matrix(op);
+                    const int k = op.nqubits;
+                    if (!dm) {
+                        push_item(k, op.qubits, intern(m.data(), m.size()), first);
+                        continue;
+                    }
+                    if (k <= 2) {
+                        // U (x) conj(U) on [qs, qs + n] (lower.cpp::superop with one Kraus operator),
+                        // cached by U
+                        std::vector<double> ukey(reinterpret_cast<const double*>(m.data()),
+                                                 reinterpret_cast<const double*>(m.data()) + 2 * m.size());
+                        auto g = gate_super_at.find(ukey);
+                        if (g == gate_super_at.end()) {
+                            const std::vector<cplx> S = superop(k, {m.data()});
+                            g = gate_super_at.emplace(std::move(ukey), intern(S.data(), S.size())).first;
+                        }
+                        int q2[4];
+                        for (int j = 0; j < k; ++j) {
+                            q2[j] = op.qubits[j];
+                            q2[j + k] = op.qubits[j] + n;
+                        }
+                        push_item(2 * k, q2, g->second, first);
+                    } else {
+                        // CCX: U on the row bits, conj(U) on the column bits
+                        int rq[3], cq[3];
+                        for (int j = 0; j < k; ++j) {
+                            rq[j] = op.qubits[j] + n;
+                            cq[j] = op.qubits[j];
+                        }
+                        std::vector<cplx> mc(m.size());
+                        for (size_t e = 0; e < m.size(); ++e) mc[e] = std::conj(m[e]);
+                        push_item(k, rq, intern(m.data(), m.size()), first);
+                        push_item(k, cq, intern(mc.data(), mc.size()), first);
+                    }
+                } else {
+                    if (!dm) throw NqError{NQ_ERR_CONTRACT, "channels need a density-matrix batch (or nq_traj_run)"};
+                    const int k = it.op.nqubits;
+                    if (k < 1 || k > 2) throw NqError{NQ_ERR_CONTRACT, "batch channel arity must be 1 or 2"};
+                    if (it.nkraus < 1) throw NqError{NQ_ERR_CONTRACT, "channel without Kraus operators"};
+                    check_range(it.op.qubits, k, n);
+                    const auto ckey = std::make_tuple(it.kraus_offset, it.nkraus, k);
+                    auto f = channel_at.find(ckey);
+                    if (f == channel_at.end()) {
+                        const cplx* src = reinterpret_cast<const cplx*>(kraus_pool) + it.kraus_offset;
+                        std::vector<const cplx*> ks;
+                        for (int kk = 0; kk < it.nkraus; ++kk) ks.push_back(src + (size_t(kk) << (2 * k)));
+                        const std::vector<cplx> S = superop(k, ks);
+                        f = channel_at.emplace(ckey, intern(S.data(), S.size())).first;
+                    }
+                    int q2[4];
+                    for (int j = 0; j < k; ++j) {
+                        q2[j] = it.op.qubits[j];
+                        q2[j + k] = it.op.qubits[j] + n;
+                    }
+                    push_item(2 * k, q2, f->second, first);
+                }
+            }
+        }
+        off[size_t(batch)] = int64_t(prog.size());
+        if (batch == 0) return;
+        const auto t_lowered = std::chrono::steady_clock::now();
+        DeviceCtx& c = ctx_for(device < 0 ? 0 : device);
+        CUDA_TRY(cudaSetDevice(c.dev));
+        const size_t dq = size_t(1) << n, nt = size_t(nterms), B = size_t(batch);
+        auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+        const size_t o_off = 0, o_items = al(o_off + off.size() * 8);
+        const size_t o_pool = al(o_items + prog.size() * sizeof(TrajItem));
+        const size_t o_f = al(o_pool + pool.size() * sizeof(cplx)), o_s = al(o_f + nt * 8);
+        const size_t o_re = al(o_s + nt * 8), o_im = al(o_re + B * nt * 8), o_p = al(o_im + B * nt * 8);
+        const size_t total = o_p + (probs ? B * dq * 8 : 0) + 256;
+        unsigned char* d = nullptr;
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d), total, c.stream));
+        auto h2d = [&](size_t o, const void* src, size_t bytes) {
+            if (bytes) CUDA_TRY(cudaMemcpyAsync(d + o, src, bytes, cudaMemcpyHostToDevice, c.stream));
+            c.h2d_bytes += int64_t(bytes);
+        };
+        h2d(o_off, off.data(), off.size() * 8);
+        h2d(o_items, prog.data(), prog.size() * sizeof(TrajItem));
+        h2d(o_pool, pool.data(), pool.size() * sizeof(cplx));
+        h2d(o_f, flip, nt * 8);
+        h2d(o_s, signs, nt * 8);
+        BatchArgs p{};
+        p.bits = dm ? 2 * n : n;
+        p.n = n;
+        p.dm = dm;
+        p.nterms = nterms;
+        p.prog_off = reinterpret_cast<const int64_t*>(d + o_off);
+        p.items = reinterpret_cast<const TrajItem*>(d + o_items);
+        p.pool = reinterpret_cast<const double2*>(d + o_pool);
+        p.flip = reinterpret_cast<const uint64_t*>(d + o_f);
+        p.signs = reinterpret_cast<const uint64_t*>(d + o_s);
+        p.out_re = reinterpret_cast<double*>(d + o_re);
+        p.out_im = reinterpret_cast<double*>(d + o_im);
+        p.probs = probs ? reinterpret_cast<double*>(d + o_p) : nullptr;
+        launch_batch(p, batch, c.stream);
+        CUDA_TRY(cudaGetLastError());
+        std::vector<double> re(B * nt), im(B * nt);
+        auto d2h = [&](void* dst, size_t o, size_t bytes) {
+            if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, d + o, bytes, cudaMemcpyDeviceToHost, c.stream));
+            c.d2h_bytes += int64_t(bytes);
+        };
+        d2h(re.data(), o_re, re.size() * 8);
+        d2h(im.data(), o_im, im.size() * 8);
+        if (probs) d2h(probs, o_p, B * dq * 8);
+        CUDA_TRY(cudaFreeAsync(d, c.stream));
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        if (std::getenv("NQ_BATCH_TIMING"))
+            std::fprintf(stderr, "[nq_batch_run] device+copies %.2f ms, %zu programs items, pool %zu\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_lowered).count(),
+                         prog.size(), pool.size());
+        for (size_t b = 0; b < B; ++b)
+            for (size_t j = 0; j < nt; ++j) {
+                const cplx tot = cplx(re[b * nt + j], im[b * nt + j]) * kIPow[ny[j] & 3];
+                out[b * nt + j] = coeff[j] * tot.real();
+                if (out_im) out_im[b * nt + j] = tot.imag();
+            }
+    });
+}
 
 // ---- batched trajectories -----------------------------------------------------
 nq_status nq_traj_run(int n, const nq_sched_item* items, int64_t count, const double* kraus_pool, int64_t ntraj,

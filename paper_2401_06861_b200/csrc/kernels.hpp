@@ -53,9 +53,10 @@ constexpr int kMaxTrajQubits = 13;  // state in shared memory
 constexpr int kMaxTrajKraus = 64;
 struct TrajItem {
     int32_t type;  // 0 gate (one matrix), 1 channel (nmat Kraus matrices)
-    int32_t k;
-    int32_t q[3];
+    int32_t k;     // <= 3 for trajectories, <= 4 in batches (2-qubit superoperators)
+    int32_t q[4];
     int32_t nmat;
+    int32_t pad;
     int64_t mat;  // offset into the matrix pool (complex elements)
 };
 struct TrajArgs {
@@ -72,6 +73,25 @@ struct TrajArgs {
     int* err;             // set when a channel's branch weights do not sum to 1
 };
 void launch_traj(const TrajArgs& p, int64_t ntraj, cudaStream_t s);
+
+// batches of independent small circuits (traj.cu): CTA b runs
+// items[prog_off[b] .. prog_off[b+1]) on its own state from |0..0>
+constexpr int kMaxBatchBits = 12;  // SV n <= 12, DM n <= 6
+struct BatchArgs {
+    int bits;  // state bits: SV n, DM 2n
+    int n;     // qubits
+    int dm;
+    int nterms;
+    const int64_t* prog_off;
+    const TrajItem* items;
+    const double2* pool;
+    const uint64_t* flip;
+    const uint64_t* signs;
+    double* out_re;  // batch x nterms
+    double* out_im;
+    double* probs;  // batch x 2^n or null
+};
+void launch_batch(const BatchArgs& p, int64_t batch, cudaStream_t s);
 
 // half-shard pack/unpack for global<->local qubit swaps (comm_kernels.cu)
 void launch_half_pack(const double2* st, double2* buf, uint64_t k0, uint64_t len, int v, uint64_t val,

@@ -17,6 +17,11 @@
 #include <json.hpp>
 
 #include <algorithm>
+#include <chrono>
+#include <map>
+#include <tuple>
+#include <cstdio>
+#include <cstdlib>
 #include <bit>
 #include <cmath>
 #include <cstdio>
@@ -608,6 +613,9 @@ NoisySchedule attach_noise(const Circuit& c, const DeviceNoiseModel& m) {
     s.num_qubits = c.num_qubits();
     const ReadoutModel full = m.readout();
     s.readout.qubits.assign(full.qubits.begin(), full.qubits.begin() + c.num_qubits());
+    // The channels of a gate depend only on (kind, qubits): build them once per
+    // distinct pair (a long Trotter circuit repeats a handful of them).
+    std::map<std::pair<int, std::vector<int>>, std::vector<ChannelApplication>> memo;
     for (const auto& op : c.ops()) {
         s.items.push_back(op);
         if (!gate_is_unitary(op.kind)) continue;
@@ -615,16 +623,23 @@ NoisySchedule attach_noise(const Circuit& c, const DeviceNoiseModel& m) {
         if (arity > 2)
             throw ContractError("no noise channel for " + std::string(gate_name(op.kind)) +
                                 ": gates on more than 2 qubits are not calibratable");
-        const auto gp = m.find_gate(gate_name(op.kind), op.qubits);
-        if (!gp)
-            throw ContractError("no calibration entry or default for gate '" + std::string(gate_name(op.kind)) +
-                                "' on qubits [" + std::to_string(op.qubits[0]) +
-                                (arity == 2 ? "," + std::to_string(op.qubits[1]) : "") + "]");
-        s.items.push_back(ChannelApplication{depolarizing(gp->error, arity), op.qubits});
-        for (int q : op.qubits) {
-            const auto& qp = m.qubits[size_t(q)];
-            s.items.push_back(ChannelApplication{thermal_relaxation(qp.t1_us, qp.t2_us, gp->duration_ns), {q}});
+        auto key = std::make_pair(int(op.kind), op.qubits);
+        auto it = memo.find(key);
+        if (it == memo.end()) {
+            const auto gp = m.find_gate(gate_name(op.kind), op.qubits);
+            if (!gp)
+                throw ContractError("no calibration entry or default for gate '" + std::string(gate_name(op.kind)) +
+                                    "' on qubits [" + std::to_string(op.qubits[0]) +
+                                    (arity == 2 ? "," + std::to_string(op.qubits[1]) : "") + "]");
+            std::vector<ChannelApplication> chans;
+            chans.push_back(ChannelApplication{depolarizing(gp->error, arity), op.qubits});
+            for (int q : op.qubits) {
+                const auto& qp = m.qubits[size_t(q)];
+                chans.push_back(ChannelApplication{thermal_relaxation(qp.t1_us, qp.t2_us, gp->duration_ns), {q}});
+            }
+            it = memo.emplace(std::move(key), std::move(chans)).first;
         }
+        for (const auto& ch : it->second) s.items.push_back(ch);
     }
     return s;
 }
@@ -1000,6 +1015,138 @@ std::vector<std::vector<double>> run_trajectories(const NoisySchedule& schedule,
     std::vector<std::vector<double>> out{static_cast<size_t>(ntraj)};
     for (size_t t = 0; t < size_t(ntraj); ++t)
         out[t].assign(flat.begin() + long(t * observables.size()), flat.begin() + long((t + 1) * observables.size()));
+    return out;
+}
+
+std::vector<std::vector<double>> batch_expectations(const std::vector<Circuit>& circuits,
+                                                    const std::vector<PauliString>& observables) {
+    if (circuits.empty()) return {};
+    const int n = circuits.front().num_qubits();
+    std::vector<nq_sched_item> items;
+    std::vector<int64_t> off{0};
+    for (const auto& c : circuits) {
+        if (c.num_qubits() != n) throw ContractError("batched circuits must have the same qubit count");
+        for (const auto& op : c.ops()) {
+            nq_sched_item it{};
+            it.type = 0;
+            it.op = to_abi(op);
+            items.push_back(it);
+        }
+        off.push_back(int64_t(items.size()));
+    }
+    std::vector<uint64_t> flip, signs;
+    std::vector<int32_t> ny;
+    std::vector<double> coeff;
+    for (const auto& p : observables) {
+        if (p.n != n)
+            throw ContractError("Pauli string length " + std::to_string(p.n) + " does not match state qubit count " +
+                                std::to_string(n));
+        const PauliMasks m = masks_of(p);
+        flip.push_back(m.flip);
+        signs.push_back(m.signs);
+        ny.push_back(m.ny);
+        coeff.push_back(p.coefficient);
+    }
+    const size_t B = circuits.size(), T = observables.size();
+    std::vector<double> flat(B * T);
+    check(nq_batch_run(n, 0, int64_t(B), off.data(), items.data(), nullptr, flip.data(), signs.data(), ny.data(),
+                       coeff.data(), int(T), flat.data(), nullptr, nullptr, -1));
+    std::vector<std::vector<double>> out{B};
+    for (size_t b = 0; b < B; ++b) out[b].assign(flat.begin() + long(b * T), flat.begin() + long((b + 1) * T));
+    return out;
+}
+
+std::vector<std::vector<double>> batch_noisy_distributions(const std::vector<Circuit>& circuits,
+                                                           const DeviceNoiseModel& m) {
+    if (circuits.empty()) return {};
+    const auto t_start = std::chrono::steady_clock::now();
+    const int n = circuits.front().num_qubits();
+    if (n > m.num_qubits())
+        throw ContractError("device model covers " + std::to_string(m.num_qubits()) + " qubits, circuit needs " +
+                            std::to_string(n));
+    std::vector<nq_sched_item> items;
+    std::vector<double> pool;
+    std::vector<int64_t> off{0};
+    // attach_noise (noise.cpp:383-426) without materialising the schedule: the
+    // channels of a gate depend only on (kind, qubits), so each distinct pair
+    // is built, validated and flattened once.
+    struct Chan {
+        int64_t at;  // pool offset (complex elements); -1: identity channel (skipped)
+        int32_t nkraus;
+        int q[2];
+        int k;
+    };
+    std::map<std::tuple<int, int, int>, std::vector<Chan>> memo;
+    auto add_channel = [&](const KrausChannel& ch, const std::vector<int>& qs, std::vector<Chan>& out) {
+        validate_channel(ch);
+        Chan c{-1, int32_t(ch.kraus.size()), {qs[0], qs.size() > 1 ? qs[1] : -1}, int(qs.size())};
+        if (!ch.is_identity()) {
+            c.at = int64_t(pool.size() / 2);
+            for (const auto& K : ch.kraus) {
+                auto f = flatten(K);
+                pool.insert(pool.end(), f.begin(), f.end());
+            }
+        }
+        out.push_back(c);
+    };
+    for (const auto& circ : circuits) {
+        if (circ.num_qubits() != n) throw ContractError("batched circuits must have the same qubit count");
+        for (const auto& op : circ.ops()) {
+            if (!gate_is_unitary(op.kind)) continue;  // unitaries_only()
+            nq_sched_item it{};
+            it.type = 0;
+            it.op = to_abi(op);
+            items.push_back(it);
+            const int arity = int(op.qubits.size());
+            if (arity > 2)
+                throw ContractError("no noise channel for " + std::string(gate_name(op.kind)) +
+                                    ": gates on more than 2 qubits are not calibratable");
+            const auto key = std::make_tuple(int(op.kind), op.qubits[0], arity == 2 ? op.qubits[1] : -1);
+            auto f = memo.find(key);
+            if (f == memo.end()) {
+                const auto gp = m.find_gate(gate_name(op.kind), op.qubits);
+                if (!gp)
+                    throw ContractError("no calibration entry or default for gate '" + std::string(gate_name(op.kind)) +
+                                        "' on qubits [" + std::to_string(op.qubits[0]) +
+                                        (arity == 2 ? "," + std::to_string(op.qubits[1]) : "") + "]");
+                std::vector<Chan> chans;
+                add_channel(depolarizing(gp->error, arity), op.qubits, chans);
+                for (int q : op.qubits) {
+                    const auto& qp = m.qubits[size_t(q)];
+                    add_channel(thermal_relaxation(qp.t1_us, qp.t2_us, gp->duration_ns), {q}, chans);
+                }
+                f = memo.emplace(key, std::move(chans)).first;
+            }
+            for (const Chan& c : f->second) {
+                if (c.at < 0) continue;
+                nq_sched_item ci{};
+                ci.type = 1;
+                ci.nkraus = c.nkraus;
+                ci.kraus_offset = c.at;
+                ci.op.nqubits = c.k;
+                for (int j = 0; j < c.k; ++j) ci.op.qubits[j] = c.q[j];
+                items.push_back(ci);
+            }
+        }
+        off.push_back(int64_t(items.size()));
+    }
+    ReadoutModel readout = m.readout();
+    readout.qubits.resize(size_t(n));
+    const size_t B = circuits.size(), dq = size_t(1) << n;
+    std::vector<double> probs(B * dq);
+    const auto t_host = std::chrono::steady_clock::now();
+    check(nq_batch_run(n, 1, int64_t(B), off.data(), items.data(), pool.empty() ? nullptr : pool.data(), nullptr,
+                       nullptr, nullptr, nullptr, 0, nullptr, nullptr, probs.data(), -1));
+    if (std::getenv("NQ_BATCH_TIMING"))
+        std::fprintf(stderr, "[batch dm] schedules %.2f ms, nq_batch_run %.2f ms, %zu items\n",
+                     std::chrono::duration<double, std::milli>(t_host - t_start).count(),
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host).count(),
+                     items.size());
+    std::vector<std::vector<double>> out;
+    out.reserve(B);
+    for (size_t b = 0; b < B; ++b)
+        out.push_back(readout_apply_dist(
+            std::vector<double>(probs.begin() + long(b * dq), probs.begin() + long((b + 1) * dq)), readout));
     return out;
 }
 

@@ -42,6 +42,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 
 // base index of group g: zeros inserted at the sorted target positions
 __device__ __forceinline__ uint32_t expand(uint32_t g, const int* sorted, int k) {
+#pragma unroll 4
     uint32_t x = g;
     for (int j = 0; j < k; ++j) {
         const int p = sorted[j];
@@ -50,67 +51,86 @@ __device__ __forceinline__ uint32_t expand(uint32_t g, const int* sorted, int k)
     return x;
 }
 
-// psi <- scale * M psi on qubits q[0..k) (local bit j <-> q[j])
-__device__ void apply_mat(double2* a, int n, const TrajItem& it, const double2* M, double scale) {
-    const int k = it.k, d = 1 << k;
-    int sorted[3] = {it.q[0], it.q[1], it.q[2]};
-    for (int i = 0; i < k; ++i)
-        for (int j = i + 1; j < k; ++j)
-            if (sorted[j] < sorted[i]) {
-                const int t = sorted[i];
-                sorted[i] = sorted[j];
-                sorted[j] = t;
+struct Targets {
+    int sorted[4];
+    uint32_t off[16];
+};
+
+template <int K>
+__device__ __forceinline__ void targets_of(const TrajItem& it, Targets& t) {
+    for (int j = 0; j < K; ++j) t.sorted[j] = it.q[j];
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+        for (int j = i + 1; j < K; ++j)
+            if (t.sorted[j] < t.sorted[i]) {
+                const int x = t.sorted[i];
+                t.sorted[i] = t.sorted[j];
+                t.sorted[j] = x;
             }
-    uint32_t off[8];
-    for (int c = 0; c < d; ++c) {
+#pragma unroll
+    for (int c = 0; c < (1 << K); ++c) {
         uint32_t o = 0;
-        for (int j = 0; j < k; ++j)
+#pragma unroll
+        for (int j = 0; j < K; ++j)
             if ((c >> j) & 1) o |= 1u << it.q[j];
-        off[c] = o;
+        t.off[c] = o;
     }
-    const uint32_t groups = 1u << (n - k);
+}
+
+// psi <- scale * M psi on qubits q[0..K) (local bit j <-> q[j])
+template <int K>
+__device__ void apply_mat_k(double2* a, int n, const TrajItem& it, const double2* M, double scale) {
+    constexpr int d = 1 << K;
+    Targets t;
+    targets_of<K>(it, t);
+    const uint32_t groups = 1u << (n - K);
     for (uint32_t g = threadIdx.x; g < groups; g += blockDim.x) {
-        const uint32_t base = expand(g, sorted, k);
-        double2 x[8], y[8];
-        for (int c = 0; c < d; ++c) x[c] = a[base + off[c]];
+        const uint32_t base = expand(g, t.sorted, K);
+        double2 x[d];
+#pragma unroll
+        for (int c = 0; c < d; ++c) x[c] = a[base + t.off[c]];
+#pragma unroll(K <= 2 ? d : 1)
         for (int r = 0; r < d; ++r) {
             double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
             for (int c = 0; c < d; ++c) {
                 const double2 p = cmul_(M[r * d + c], x[c]);
                 acc.x += p.x;
                 acc.y += p.y;
             }
-            y[r] = make_double2(acc.x * scale, acc.y * scale);
+            a[base + t.off[r]] = make_double2(acc.x * scale, acc.y * scale);
         }
-        for (int r = 0; r < d; ++r) a[base + off[r]] = y[r];
     }
 }
 
-__device__ double branch_weight(const double2* a, int n, const TrajItem& it, const double2* K) {
-    const int k = it.k, d = 1 << k;
-    int sorted[3] = {it.q[0], it.q[1], it.q[2]};
-    for (int i = 0; i < k; ++i)
-        for (int j = i + 1; j < k; ++j)
-            if (sorted[j] < sorted[i]) {
-                const int t = sorted[i];
-                sorted[i] = sorted[j];
-                sorted[j] = t;
-            }
-    uint32_t off[8];
-    for (int c = 0; c < d; ++c) {
-        uint32_t o = 0;
-        for (int j = 0; j < k; ++j)
-            if ((c >> j) & 1) o |= 1u << it.q[j];
-        off[c] = o;
+__device__ void apply_mat(double2* a, int n, const TrajItem& it, const double2* M, double scale) {
+    switch (it.k) {
+    case 1: apply_mat_k<1>(a, n, it, M, scale); break;
+    case 2: apply_mat_k<2>(a, n, it, M, scale); break;
+    case 3: apply_mat_k<3>(a, n, it, M, scale); break;
+    default: apply_mat_k<4>(a, n, it, M, scale); break;
     }
+}
+
+template <int K>
+__device__ double branch_weight_k(const double2* a, int n, const TrajItem& it, const double2* Km) {
+    constexpr int d = 1 << K;
+    Targets t;
+    targets_of<K>(it, t);
     double acc = 0.0;
-    const uint32_t groups = 1u << (n - k);
+    const uint32_t groups = 1u << (n - K);
     for (uint32_t g = threadIdx.x; g < groups; g += blockDim.x) {
-        const uint32_t base = expand(g, sorted, k);
+        const uint32_t base = expand(g, t.sorted, K);
+        double2 x[d];
+#pragma unroll
+        for (int c = 0; c < d; ++c) x[c] = a[base + t.off[c]];
+#pragma unroll(K <= 2 ? d : 1)
         for (int r = 0; r < d; ++r) {
             double2 w = make_double2(0.0, 0.0);
+#pragma unroll
             for (int c = 0; c < d; ++c) {
-                const double2 p = cmul_(K[r * d + c], a[base + off[c]]);
+                const double2 p = cmul_(Km[r * d + c], x[c]);
                 w.x += p.x;
                 w.y += p.y;
             }
@@ -118,6 +138,14 @@ __device__ double branch_weight(const double2* a, int n, const TrajItem& it, con
         }
     }
     return acc;
+}
+
+__device__ double branch_weight(const double2* a, int n, const TrajItem& it, const double2* Km) {
+    switch (it.k) {
+    case 1: return branch_weight_k<1>(a, n, it, Km);
+    case 2: return branch_weight_k<2>(a, n, it, Km);
+    default: return branch_weight_k<3>(a, n, it, Km);
+    }
 }
 
 __global__ void __launch_bounds__(kTrajThreads) k_traj(TrajArgs p) {
@@ -196,7 +224,76 @@ __global__ void __launch_bounds__(kTrajThreads) k_traj(TrajArgs p) {
     }
 }
 
+__global__ void __launch_bounds__(kTrajThreads) k_batch(BatchArgs p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double2* a = reinterpret_cast<double2*>(smem);
+    __shared__ double red[kTrajThreads / 32];
+    const int64_t b = blockIdx.x;
+    const uint32_t dim = 1u << p.bits;
+    for (uint32_t i = threadIdx.x; i < dim; i += blockDim.x) a[i] = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
+    __syncthreads();
+    for (int64_t i = p.prog_off[b]; i < p.prog_off[b + 1]; ++i) {
+        const TrajItem it = p.items[i];
+        apply_mat(a, p.bits, it, p.pool + it.mat, 1.0);
+        __syncthreads();
+    }
+    const uint32_t dq = 1u << p.n;
+    for (int t = 0; t < p.nterms; ++t) {
+        const uint64_t F = p.flip[t], S = p.signs[t];
+        double re = 0.0, im = 0.0;
+        for (uint32_t y = threadIdx.x; y < dq; y += blockDim.x) {
+            double xr, xi;
+            if (p.dm) {
+                // rho[y, y ^ F] (densitymatrix.cpp:196-218), row-major vec index
+                const double2 v = a[(y << p.n) | (y ^ uint32_t(F))];
+                xr = v.x;
+                xi = v.y;
+            } else {
+                const double2 ay = a[y], az = a[y ^ uint32_t(F)];
+                xr = az.x * ay.x + az.y * ay.y;
+                xi = az.x * ay.y - az.y * ay.x;
+            }
+            if (__popcll(uint64_t(y) & S) & 1) {
+                xr = -xr;
+                xi = -xi;
+            }
+            re += xr;
+            im += xi;
+        }
+        re = block_sum(re, red);
+        im = block_sum(im, red);
+        if (threadIdx.x == 0) {
+            p.out_re[b * p.nterms + t] = re;
+            p.out_im[b * p.nterms + t] = im;
+        }
+    }
+    if (p.probs) {
+        double* out = p.probs + size_t(b) * dq;
+        if (p.dm) {
+            // max(0, Re rho_ii) / sequential sum (densitymatrix.cpp:221-232)
+            if (threadIdx.x == 0) {
+                double sum = 0.0;
+                for (uint32_t i = 0; i < dq; ++i) {
+                    const double v = fmax(0.0, a[(i << p.n) | i].x);
+                    out[i] = v;
+                    sum += v;
+                }
+                for (uint32_t i = 0; i < dq; ++i) out[i] /= sum;
+            }
+        } else {
+            for (uint32_t i = threadIdx.x; i < dq; i += blockDim.x) out[i] = a[i].x * a[i].x + a[i].y * a[i].y;
+        }
+    }
+}
+
 }  // namespace
+
+void launch_batch(const BatchArgs& p, int64_t batch, cudaStream_t s) {
+    const size_t smem = (size_t(16) << p.bits);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k_batch<<<unsigned(batch), kTrajThreads, smem, s>>>(p);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+}
 
 void launch_traj(const TrajArgs& p, int64_t ntraj, cudaStream_t s) {
     const size_t smem = (size_t(16) << p.n);

@@ -205,3 +205,27 @@ def tfim_sweep_rows(naqs, n: int, model, t_max: float = 3.0, dt: float = 0.1, st
             noisy += sum(-p if (i >> q) & 1 else p for i, p in enumerate(dist))
         rows.append((t, ideal, noisy / n))
     return rows
+
+
+def tfim_sweep_rows_batched(naqs, n: int, model, t_max: float = 3.0, dt: float = 0.1, steps_per_unit: int = 100):
+    """tfim_sweep_rows with every row's ideal circuit in one launch and every
+    row's noisy density matrix in another (naqs.batch_* )."""
+    import numpy as np
+
+    zs = []
+    for q in range(n):
+        L = ["I"] * n
+        L[q] = "Z"
+        zs.append("".join(L))
+    times = tfim_sweep_times(t_max, dt)
+    circs = []
+    for t in times:
+        c = naqs.Circuit(n)
+        for name, qs, ps in tfim_trotter(n, t, steps_per_unit):
+            c.add(name, qs, ps)
+        circs.append(c)
+    ideal = naqs.batch_expectations(circs, zs).sum(axis=1) / n
+    dists = naqs.batch_noisy_distributions(circs, model)
+    sign = np.array([[-1.0 if (i >> q) & 1 else 1.0 for i in range(1 << n)] for q in range(n)])
+    noisy = (dists @ sign.T).sum(axis=1) / n
+    return [(t, float(a), float(b)) for t, a, b in zip(times, ideal, noisy)]
