@@ -138,7 +138,8 @@ nq_status nq_sv_kraus_weights(nq_sv* s, const int32_t* qubits, int k, int nkraus
 nq_status nq_sv_get_amplitudes(nq_sv* s, uint64_t offset, uint64_t count, double* host_out);
 /* Overwrite amplitudes [offset, offset+count) from host. */
 nq_status nq_sv_set_amplitudes(nq_sv* s, uint64_t offset, uint64_t count, const double* host_in);
-/* Device pointer to the (flushed) amplitude array, for zero-copy consumers. */
+/* Device pointer to the (flushed) amplitude array, for zero-copy consumers
+ * (sharded states: this rank's 2^(n-g) block, qubit map restored first). */
 nq_status nq_sv_device_ptr(nq_sv* s, void** out);
 /* Planner/executor statistics of the last flush: passes, fused micro-ops,
  * source ops, kernel launches. */

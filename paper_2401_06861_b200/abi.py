@@ -270,6 +270,20 @@ class SV:
         check(lib.nq_sv_get_amplitudes(self.h, offset, count, out.view(np.float64).ctypes.data_as(_dp)))
         return out
 
+    def device_view(self) -> "DeviceAmplitudes":
+        """Zero-copy view of the (flushed) amplitudes in HBM:
+        an object with ``__cuda_array_interface__`` (complex128, 2^n; for a
+        sharded state this rank's 2^nloc block), e.g. ``torch.as_tensor(view,
+        device="cuda")`` or CuPy.  Valid until the state is modified or closed;
+        the state's queued work is synchronised first."""
+        p = C.c_void_p()
+        check(lib.nq_sv_device_ptr(self.h, C.byref(p)))
+        check(lib.nq_sv_synchronize(self.h))
+        return DeviceAmplitudes(p.value, self.local_count())
+
+    def local_count(self) -> int:
+        return 1 << self.n if getattr(self, "world", 1) == 1 else 1 << (self.n - (self.world.bit_length() - 1))
+
     def set_amplitudes(self, amps, offset: int = 0):
         a = np.ascontiguousarray(np.asarray(amps, dtype=np.complex128))
         check(lib.nq_sv_set_amplitudes(self.h, offset, len(a), a.view(np.float64).ctypes.data_as(_dp)))
@@ -325,7 +339,9 @@ class SV:
         h = C.c_void_p()
         u = (C.c_ubyte * 128).from_buffer_copy(uid)
         check(lib.nq_sv_create_sharded(n, rank, world, u, C.byref(opts(**kw)), C.byref(h)))
-        return cls(n, handle=h)
+        sv = cls(n, handle=h)
+        sv.world = world
+        return sv
 
     def comm_stats(self):
         a, b = C.c_int64(), C.c_int64()
@@ -365,6 +381,18 @@ def shard_debug(n: int, world: int, ops):
             seg.append((types[t], k, [b0, b1, b2, b3][:k], ctrl & ((1 << 64) - 1), mat[:, 0] + 1j * mat[:, 1]))
         out.append(("segment", seg))
     return out
+
+
+class DeviceAmplitudes:
+    """``__cuda_array_interface__`` (v3) over a device amplitude array."""
+
+    def __init__(self, ptr: int, count: int):
+        self.ptr, self.count = ptr, count
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.count,), "typestr": "<c16", "data": (self.ptr, False), "version": 3,
+                "strides": None, "stream": None}
 
 
 class DM:

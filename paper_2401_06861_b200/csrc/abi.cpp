@@ -680,6 +680,7 @@ nq_status nq_sv_device_ptr(nq_sv* h, void** out) {
     return guard([&] {
         State& s = st(h);
         state_flush(s);
+        shard_normalize(s);  // sharded: this rank's block in logical order
         *out = s.d;
     });
 }

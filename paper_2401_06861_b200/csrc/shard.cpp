@@ -399,6 +399,10 @@ void normalize_map(State& s) {
 
 }  // namespace
 
+void shard_normalize(State& s) {
+    if (s.comm) normalize_map(s);
+}
+
 void shard_free(State& s) {
     if (!s.comm) return;
     ShardComm* sc = s.comm;

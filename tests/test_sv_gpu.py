@@ -179,3 +179,18 @@ def test_large_state_beyond_reference_guard(port):
     assert abs(sv.norm_sq() - 1) < 1e-12
     e = sv.expectations([("Z" * n, 1.0), ("X" * n, 1.0), ("Z" + "I" * (n - 1), 1.0)])
     np.testing.assert_allclose(e, [1.0, 1.0, 0.0], atol=1e-12)
+
+
+def test_device_view_zero_copy():
+    """f4: the amplitudes in HBM through __cuda_array_interface__ (torch),
+    no host copy, equal to nq_sv_get_amplitudes."""
+    import torch
+
+    n = 12
+    sv = abi.SV(n)
+    sv.apply(abi.make_ops([("h", [q], []) for q in range(n)] + [("rz", [3], [0.4]), ("cx", [3, 7], [])]))
+    view = sv.device_view()
+    t = torch.as_tensor(view, device="cuda")
+    assert t.dtype == torch.complex128 and t.numel() == 1 << n
+    assert t.data_ptr() == view.ptr
+    assert np.array_equal(t.cpu().numpy(), sv.amplitudes())
