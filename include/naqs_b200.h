@@ -278,7 +278,8 @@ nq_status nq_jit_debug(int num_qubits, const nq_op* ops, int64_t count, int tile
 /* ---- planner introspection (host logic, CPU-testable) ------------------ */
 /* Compile `ops` on an n-qubit state into the pass plan without executing it
  * and serialise it (see paper_2401_06861_b200/plan_format.py).  Writes
- * at most `cap` bytes; *size receives the full size. */
+ * at most `cap` bytes; *size receives the full size.  fuse: bit 0 = fusion,
+ * bit 1 = relabelling stores (as single-device state vectors run). */
 nq_status nq_plan_debug(int num_qubits, const nq_op* ops, int64_t count, int tile_qubits,
                         int fuse, unsigned char* buf, int64_t cap, int64_t* size);
 

@@ -508,13 +508,13 @@ def sample_dist_sorted(dist, sorted_u):
     return idx[: k.value].copy(), cnt[: k.value].copy()
 
 
-def plan_debug(n: int, ops, tile_qubits: int = 0, fuse: bool = True) -> bytes:
+def plan_debug(n: int, ops, tile_qubits: int = 0, fuse: bool = True, relabel: bool = False) -> bytes:
     arr = ops if isinstance(ops, np.ndarray) else make_ops(ops)
     size = C.c_int64()
-    check(lib.nq_plan_debug(n, arr.ctypes.data, len(arr), tile_qubits, 1 if fuse else 0, None, 0, C.byref(size)))
+    flags = (1 if fuse else 0) | (2 if relabel else 0)
+    check(lib.nq_plan_debug(n, arr.ctypes.data, len(arr), tile_qubits, flags, None, 0, C.byref(size)))
     buf = (C.c_ubyte * max(size.value, 1))()
-    check(lib.nq_plan_debug(n, arr.ctypes.data, len(arr), tile_qubits, 1 if fuse else 0, buf, size.value,
-                            C.byref(size)))
+    check(lib.nq_plan_debug(n, arr.ctypes.data, len(arr), tile_qubits, flags, buf, size.value, C.byref(size)))
     return bytes(buf)[: size.value]
 
 

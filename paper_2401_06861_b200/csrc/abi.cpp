@@ -112,7 +112,18 @@ void state_init(State& s, int n, bool dm, const nq_opts* opts) {
     // (best measured pass throughput on B200)
     s.popt.tile_bits = o.tile_qubits > 0 ? std::min(o.tile_qubits, kMaxTileBits) : 11;
     s.popt.low_bits = 4;
-    // A/B knobs (read per state): NQ_TILE_DM / NQ_LOW_BITS_DM for density matrices
+    // relabelling stores for state vectors (NQ_RELABEL=0 disables)
+    {
+        const char* e = std::getenv("NQ_RELABEL");
+        s.popt.relabel = !dm && !(e && e[0] == '0');
+    }
+    s.layout.resize(size_t(s.nbits));
+    for (int b = 0; b < s.nbits; ++b) s.layout[size_t(b)] = b;
+    // A/B knobs (read per state): NQ_LOW_BITS for state vectors, NQ_TILE_DM /
+    // NQ_LOW_BITS_DM for density matrices
+    if (!dm) {
+        if (const char* e = std::getenv("NQ_LOW_BITS")) s.popt.low_bits = std::max(0, std::min(std::atoi(e), 4));
+    }
     if (dm) {
         if (const char* e = std::getenv("NQ_TILE_DM"); e && o.tile_qubits <= 0)
             s.popt.tile_bits = std::max(4, std::min(std::atoi(e), kMaxTileBits));
@@ -188,23 +199,69 @@ void trace_passes(const std::vector<PlannedPass>& passes, bool dm) {
     }
 }
 
+void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStats& st, bool record = true);
+bool layout_is_identity(const State& s);
+
 void state_flush(State& s) {
     if (s.queue.empty()) return;
     if (s.world > 1) {
         shard_flush(s);
         return;
     }
+    PlanStats st;
+    const bool relabel = s.popt.relabel && int(s.layout.size()) == s.nbits;
+    std::vector<PlannedPass> passes = plan_passes(s.queue, s.popt, &st, relabel ? &s.layout : nullptr);
+    s.queue.clear();
+    run_passes(s, passes, st);
+}
+
+bool layout_is_identity(const State& s) {
+    for (size_t b = 0; b < s.layout.size(); ++b)
+        if (s.layout[b] != int(b)) return false;
+    return true;
+}
+
+void state_flush_normal(State& s) {
+    state_flush(s);
+    if (s.world > 1 || layout_is_identity(s)) return;
+    // transpositions of physical bits that bring logical qubit p back to bit p
+    std::vector<int> l2p = s.layout, p2l(l2p.size());
+    for (size_t b = 0; b < l2p.size(); ++b) p2l[size_t(l2p[b])] = int(b);
+    std::vector<EOp> swaps;
+    for (int p = 0; p < s.nbits; ++p) {
+        if (p2l[size_t(p)] == p) continue;
+        const int w = l2p[size_t(p)];  // physical bit holding logical p
+        EOp e;
+        e.type = E_SWAP;
+        e.k = 2;
+        e.bits[0] = std::min(p, w);
+        e.bits[1] = std::max(p, w);
+        swaps.push_back(e);
+        const int lp = p2l[size_t(p)];  // logical qubit at physical p moves to w
+        p2l[size_t(w)] = lp;
+        l2p[size_t(lp)] = w;
+        p2l[size_t(p)] = p;
+        l2p[size_t(p)] = p;
+    }
+    PlanOptions po = s.popt;
+    po.relabel = false;
+    PlanStats st;
+    std::vector<PlannedPass> passes = plan_passes(swaps, po, &st);
+    run_passes(s, passes, st, false);
+    for (size_t b = 0; b < s.layout.size(); ++b) s.layout[b] = int(b);
+}
+
+void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStats& st, bool record) {
     DeviceCtx& c = ctx_for(s.dev);
     CUDA_TRY(cudaSetDevice(s.dev));
-    PlanStats st;
-    std::vector<PlannedPass> passes = plan_passes(s.queue, s.popt, &st);
-    s.queue.clear();
     std::vector<size_t> offs;
     std::vector<unsigned char> buf = serialize_passes(passes, s.nloc, &offs);
-    s.last_passes = st.passes;
-    s.last_microops = st.microops;
-    s.last_source_ops = st.source_ops;
-    s.last_launches = int64_t(passes.size());
+    if (record) {
+        s.last_passes = st.passes;
+        s.last_microops = st.microops;
+        s.last_source_ops = st.source_ops;
+        s.last_launches = int64_t(passes.size());
+    }
     if (buf.empty()) return;
     if (plan_trace()) trace_passes(passes, s.dm);
     c.stage(buf.data(), buf.size());
@@ -333,7 +390,7 @@ nq_status nq_sv_clone(const nq_sv* h, nq_sv** out) {
     return guard([&] {
         State& src = const_cast<nq_sv*>(h)->s;
         if (src.world > 1) throw NqError{NQ_ERR_CONTRACT, "clone of a sharded state is not supported"};
-        state_flush(src);
+        state_flush_normal(src);
         auto c = std::make_unique<nq_sv>();
         c->s.dev = src.dev;
         c->s.n = src.n;
@@ -342,6 +399,7 @@ nq_status nq_sv_clone(const nq_sv* h, nq_sv** out) {
         c->s.nloc = src.nloc;
         c->s.count = src.count;
         c->s.popt = src.popt;
+        c->s.layout = src.layout;  // identity after state_flush_normal
         DeviceCtx& cx = ctx_for(src.dev);
         CUDA_TRY(cudaSetDevice(src.dev));
         CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&c->s.d), src.count * sizeof(double2), cx.stream));
@@ -360,6 +418,7 @@ nq_status nq_sv_reset(nq_sv* h) {
         const uint64_t one_at = (s.world > 1 && s.rank != 0) ? UINT64_MAX : 0;
         launch_init_basis(s.d, s.count, one_at, c.stream);
         shard_reset(s);
+        for (size_t b = 0; b < s.layout.size(); ++b) s.layout[b] = int(b);
         CUDA_TRY(cudaGetLastError());
     });
 }
@@ -443,8 +502,21 @@ nq_status nq_sv_expectation_batch(nq_sv* h, const uint64_t* flip, const uint64_t
             shard_expectation(s, flip, signs, ny, coeff, nterms, out);
             return;
         }
+        // masks in physical bits of the current layout (no normalising pass)
+        std::vector<uint64_t> pf(flip, flip + nterms), ps(signs, signs + nterms);
+        if (!layout_is_identity(s)) {
+            for (int t = 0; t < nterms; ++t) {
+                uint64_t f = 0, g = 0;
+                for (int q = 0; q < s.n; ++q) {
+                    if ((flip[t] >> q) & 1) f |= uint64_t(1) << s.layout[size_t(q)];
+                    if ((signs[t] >> q) & 1) g |= uint64_t(1) << s.layout[size_t(q)];
+                }
+                pf[size_t(t)] = f;
+                ps[size_t(t)] = g;
+            }
+        }
         std::vector<cplx> totals;
-        sv_expect_raw(s, flip, signs, nterms, totals);
+        sv_expect_raw(s, pf.data(), ps.data(), nterms, totals);
         for (int t = 0; t < nterms; ++t) out[t] = coeff[t] * (totals[size_t(t)] * kIPow[ny[t] & 3]).real();
     });
 }
@@ -584,7 +656,7 @@ extern "C" {
 nq_status nq_sv_probabilities(nq_sv* h, double* host_out) {
     return guard([&] {
         State& s = st(h);
-        state_flush(s);
+        state_flush_normal(s);
         if (s.world > 1) throw NqError{NQ_ERR_CONTRACT, "probabilities() of a sharded state: use sample"};
         DeviceCtx& c = ctx_for(s.dev);
         const uint64_t chunk = std::min<uint64_t>(s.count, uint64_t(1) << 26);
@@ -605,7 +677,7 @@ nq_status nq_sv_sample_sorted(nq_sv* h, const double* sorted_u, uint64_t shots, 
                               uint64_t* count_out, uint64_t* nout) {
     return guard([&] {
         State& s = st(h);
-        state_flush(s);
+        state_flush_normal(s);
         if (s.world > 1) {
             shard_sample(s, sorted_u, shots, idx_out, count_out, nout);
             return;
@@ -622,7 +694,7 @@ nq_status nq_sv_kraus_weights(nq_sv* h, const int32_t* qubits, int k, int nkraus
         if (k < 1 || k > 3) throw NqError{NQ_ERR_CONTRACT, "Kraus arity must be in [1, 3]"};
         if (nkraus < 1 || nkraus > 16) throw NqError{NQ_ERR_CONTRACT, "1..16 Kraus operators supported"};
         check_range(qubits, k, s.n);
-        state_flush(s);
+        state_flush_normal(s);
         if (s.world > 1) throw NqError{NQ_ERR_CONTRACT, "trajectories on a sharded state are not supported"};
         DeviceCtx& c = ctx_for(s.dev);
         const size_t D = size_t(1) << k;
@@ -645,7 +717,7 @@ nq_status nq_sv_kraus_weights(nq_sv* h, const int32_t* qubits, int k, int nkraus
 nq_status nq_sv_get_amplitudes(nq_sv* h, uint64_t offset, uint64_t count, double* host_out) {
     return guard([&] {
         State& s = st(h);
-        state_flush(s);
+        state_flush_normal(s);
         if (s.world > 1) {
             shard_get_amplitudes(s, offset, count, host_out);
             return;
@@ -664,7 +736,7 @@ nq_status nq_sv_get_amplitudes(nq_sv* h, uint64_t offset, uint64_t count, double
 nq_status nq_sv_set_amplitudes(nq_sv* h, uint64_t offset, uint64_t count, const double* host_in) {
     return guard([&] {
         State& s = st(h);
-        state_flush(s);
+        state_flush_normal(s);
         if (s.world > 1) throw NqError{NQ_ERR_CONTRACT, "set_amplitudes on a sharded state is not supported"};
         if (offset > s.count || count > s.count - offset)
             throw NqError{NQ_ERR_CONTRACT, "amplitude range out of bounds"};
@@ -679,7 +751,7 @@ nq_status nq_sv_set_amplitudes(nq_sv* h, uint64_t offset, uint64_t count, const 
 nq_status nq_sv_device_ptr(nq_sv* h, void** out) {
     return guard([&] {
         State& s = st(h);
-        state_flush(s);
+        state_flush_normal(s);
         shard_normalize(s);  // sharded: this rank's block in logical order
         *out = s.d;
     });
@@ -733,6 +805,7 @@ nq_status nq_dm_clone(const nq_dm* h, nq_dm** out) {
         c->s.nloc = src.nloc;
         c->s.count = src.count;
         c->s.popt = src.popt;
+        c->s.layout = src.layout;  // identity after state_flush_normal
         DeviceCtx& cx = ctx_for(src.dev);
         CUDA_TRY(cudaSetDevice(src.dev));
         CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&c->s.d), src.count * sizeof(double2), cx.stream));
@@ -1099,8 +1172,11 @@ nq_status nq_jit_debug(int n, const nq_op* ops, int64_t count, int tile_qubits, 
         p.nbits = n;
         p.nloc = n;
         p.tile_bits = tile_qubits > 0 ? std::min(tile_qubits, kMaxTileBits) : 12;
+        p.relabel = true;  // as single-device state vectors plan
         configure_caps(p);
-        auto passes = plan_passes(q, p, nullptr);
+        std::vector<int> layout(static_cast<size_t>(n));
+        for (int b = 0; b < n; ++b) layout[size_t(b)] = b;
+        auto passes = plan_passes(q, p, nullptr, &layout);
         if (pass_index < 0 || pass_index >= int(passes.size())) throw NqError{NQ_ERR_CONTRACT, "no such pass"};
         std::vector<size_t> offs;
         auto bytes = serialize_passes(passes, n, &offs);
@@ -1133,10 +1209,13 @@ nq_status nq_plan_debug(int n, const nq_op* ops, int64_t count, int tile_qubits,
         p.nbits = n;
         p.nloc = n;
         p.tile_bits = tile_qubits > 0 ? std::min(tile_qubits, kMaxTileBits) : 12;
-        p.fuse = fuse != 0;
+        p.fuse = (fuse & 1) != 0;
+        p.relabel = (fuse & 2) != 0;  // bit 1: relabelling stores (single-device state vectors)
         configure_caps(p);
         PlanStats stt;
-        auto passes = plan_passes(q, p, &stt);
+        std::vector<int> layout(static_cast<size_t>(n));
+        for (int b = 0; b < n; ++b) layout[size_t(b)] = b;
+        auto passes = plan_passes(q, p, &stt, &layout);
         std::vector<size_t> offs;
         auto bytes = serialize_passes(passes, n, &offs);
         *size = int64_t(bytes.size());

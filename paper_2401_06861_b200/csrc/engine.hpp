@@ -21,7 +21,8 @@ using cplx = std::complex<double>;
 constexpr int kMaxTileBits = 13;   // 2^13 * 16 B = 128 KiB of shared memory
 constexpr int kMaxStateBits = 48;
 constexpr int kMaxOpK = 4;         // dense micro-ops act on <= 4 tile bits
-constexpr int kMaxDiagK = 6;       // diagonal micro-ops act on <= 6 bits (64-entry table)
+constexpr int kMaxDiagK = 6;       // diagonal micro-ops act on <= 6 bits (64-entry table; 7-8 measured
+                                    // worse: bigger tables fill the pass pools sooner)
 
 // ---- device micro-ops ------------------------------------------------------
 enum MOpType : uint8_t {
@@ -58,8 +59,10 @@ struct PassHdr {
     uint32_t pool_off;  // byte offset of the complex pool from the pass header
     uint32_t pool_n;    // complex entries in the pool
     uint32_t bytes;     // total bytes of this pass record (header+ops+pool, 16B aligned)
-    int8_t q[16];       // tile bit i <-> state bit q[i] (ascending)
+    int8_t q[16];       // tile bit i is loaded from state bit q[i] (ascending)
     int8_t rest[56];    // non-tile state bits, ascending
+    int8_t qst[16];     // tile bit i is stored to state bit qst[i] (a permutation of q:
+                        // the pass relabels qubits among its tile bits for free)
 };
 static_assert(sizeof(PassHdr) % 16 == 0, "PassHdr alignment");
 
@@ -76,7 +79,7 @@ enum EOpType : uint8_t {
 struct EOp {
     EOpType type = E_NOP;
     int k = 0;
-    int bits[4] = {0, 0, 0, 0};
+    int bits[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // DIAG up to kMaxDiagK bits
     uint64_t ctrl = 0;
     std::vector<cplx> mat;  // DENSE: 4^k, DIAG: 2^k, DEPOL: 2
     int64_t src = 1;        // source (reference) ops this elementary op accounts for
@@ -91,10 +94,14 @@ struct PlanOptions {
     int reg_bits = 4;     // amplitudes per thread = 2^reg_bits (3 or 4)
     int max_ops_per_pass = 192;
     int max_pool_per_pass = 1536;  // complex entries
+    // Relabel qubits at pass stores (single-device state vectors): the qubits
+    // held by the low (contiguous) physical bits become a per-pass choice.
+    bool relabel = false;
 };
 
 struct PlannedPass {
-    std::vector<int> q;     // tile bits
+    std::vector<int> q;     // tile bits (physical, ascending) at load
+    std::vector<int> qst;   // physical store bit of tile bit i (empty: same as q)
     std::vector<MOp> ops;
     std::vector<cplx> pool;
 };
@@ -107,8 +114,12 @@ struct PlanStats {
 
 // Plan a sequence of elementary ops (all on local bits < nloc for the
 // non-diagonal targets; diagonal/control bits may be >= nloc).
+// ops are in logical bits; `map` (logical -> physical bit, size nbits) is the
+// layout of the state before the first pass and receives the layout after the
+// last one.  Without a map (or without opt.relabel) the layout is the identity
+// and stays so.
 std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops, const PlanOptions& opt,
-                                     PlanStats* stats);
+                                     PlanStats* stats, std::vector<int>* map = nullptr);
 
 // Serialise passes into one contiguous buffer of PassHdr records.
 std::vector<unsigned char> serialize_passes(const std::vector<PlannedPass>& passes, int nloc,

@@ -279,6 +279,8 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     int logT = 0;
     while ((1 << logT) < T) ++logT;
     std::vector<int> q(h.q, h.q + m), rest(h.rest, h.rest + h.nrest);
+    std::vector<int> qst(h.qst, h.qst + m);  // store positions (a permutation of q: relabelled pass)
+    const bool relabel = qst != q;
 
     std::vector<Layout> lays;
     std::vector<int> lay_of_op(size_t(h.nops), 0);
@@ -286,20 +288,35 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
         if (ops[i].type == MOP_LAYOUT) lays.push_back(layout_of(ops[i], m));
         lay_of_op[size_t(i)] = int(lays.size()) - 1;
     }
-    const Swizzle sw = choose_swizzle(lays, m);
-    auto reg_off = [&](const Layout& L, int l) {
+    // Relabelling pass: the tile bits a warp's lanes span must be the ones that
+    // store to the low (contiguous) physical bits, so the stores go through one
+    // more relayout into LS = the last layout with its thread bits ordered by
+    // store position.
+    // When the pass already relayouts, its last layout simply takes that
+    // thread-bit order (no extra shared-memory round trip).
+    auto by_store = [&](Layout L) {
+        std::stable_sort(L.nonr.begin(), L.nonr.end(), [&](int x, int y) { return qst[size_t(x)] < qst[size_t(y)]; });
+        return L;
+    };
+    if (relabel && lays.size() >= 2) lays.back() = by_store(lays.back());
+    const bool extra_relayout = relabel && lays.size() == 1;
+    const Layout LS = by_store(lays.back());
+    std::vector<Layout> sw_lays = lays;
+    if (extra_relayout) sw_lays.push_back(LS);
+    const Swizzle sw = choose_swizzle(sw_lays, m);
+    auto reg_off = [&](const Layout& L, int l, const std::vector<int>& pos) {
         unsigned long long c = 0;
         for (int j = 0; j < L.r; ++j)
-            if ((l >> j) & 1) c |= 1ull << q[size_t(L.rp[j])];
+            if ((l >> j) & 1) c |= 1ull << pos[size_t(L.rp[j])];
         return c;
     };
-    auto state_off = [&](const std::string& tbname, const std::vector<int>& bits) {
+    auto state_off = [&](const std::string& tbname, const std::vector<int>& bits, const std::vector<int>& pos) {
         std::ostringstream o;
         bool first = true;
         for (int b : bits) {
             if (!first) o << " | ";
             first = false;
-            o << "((unsigned long long)((" << tbname << " >> " << b << ") & 1u) << " << q[size_t(b)] << ")";
+            o << "((unsigned long long)((" << tbname << " >> " << b << ") & 1u) << " << pos[size_t(b)] << ")";
         }
         if (first) o << "0ull";
         return o.str();
@@ -326,7 +343,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     {
         std::vector<int> lowbits;
         for (int b = 0; b < logT; ++b) lowbits.push_back(b);
-        s << "  const unsigned long long poff = " << state_off("tid", lowbits) << ";\n";
+        s << "  const unsigned long long poff = " << state_off("tid", lowbits, q) << ";\n";
         s << "  const unsigned psw = " << swz_expr("tid", sw) << ";\n";
     }
     for (size_t k = 0; k < lays.size(); ++k) {
@@ -335,8 +352,14 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     }
     const Layout& L0 = lays.front();
     const Layout& LN = lays.back();
-    s << "  const unsigned long long toff_st = " << state_off("tb" + std::to_string(lays.size() - 1), LN.nonr)
-      << ";\n";
+    if (extra_relayout) {
+        s << "  const unsigned tbS = " << deposit_expr("tid", LS.nonr, false) << ";\n";
+        s << "  const unsigned swS = " << swz_expr("tbS", sw) << ";\n";
+        s << "  const unsigned long long toff_st = " << state_off("tbS", LS.nonr, qst) << ";\n";
+    } else {
+        s << "  const unsigned long long toff_st = "
+          << state_off("tb" + std::to_string(lays.size() - 1), LN.nonr, qst) << ";\n";
+    }
     // prefetch helper (inline lambda-free: a macro-like block emitted twice)
     auto prefetch = [&](const std::string& rexpr, const std::string& bufname, const std::string& indent) {
         s << indent << "{ const unsigned long long pb = " << deposit_expr("(unsigned long long)(" + rexpr + ")", rest, true)
@@ -374,7 +397,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
         for (int l = 0; l < E; ++l) s << "    a[" << l << "] = cur[sw0 ^ " << sw.apply(L0.rconst(l)) << "u];\n";
     } else {
         // direct streaming loads into the first register layout; one buffer
-        s << "  const unsigned long long toff_ld = " << state_off("tb0", L0.nonr) << ";\n"
+        s << "  const unsigned long long toff_ld = " << state_off("tb0", L0.nonr, q) << ";\n"
           << "  __syncthreads();\n"
           << "  for (long long r = blockIdx.x; r < ntiles; r += gridDim.x) {\n"
           << "    double2* cur = buf0;\n"
@@ -383,7 +406,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
           << "    (void)full;\n"
           << "    double2 a[" << E << "];\n"
           << "    { const double2* src = st + base + toff_ld;\n";
-        for (int l = 0; l < E; ++l) s << "      a[" << l << "] = ld_stream(src + " << hex64(reg_off(L0, l)) << ");\n";
+        for (int l = 0; l < E; ++l) s << "      a[" << l << "] = ld_stream(src + " << hex64(reg_off(L0, l, q)) << ");\n";
         s << "    }\n";
     }
     for (int i = 1; i < h.nops; ++i) {
@@ -514,8 +537,19 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
             break;
         }
     }
+    if (extra_relayout) {
+        // (the barrier also orders every load of the tile before any store:
+        // relabelled stores hit addresses other threads load)
+        const std::string swN = "sw" + std::to_string(lays.size() - 1);
+        s << "    __syncthreads();\n";
+        for (int l = 0; l < E; ++l)
+            s << "    cur[" << swN << " ^ " << sw.apply(LN.rconst(l)) << "u] = a[" << l << "];\n";
+        s << "    __syncthreads();\n";
+        for (int l = 0; l < E; ++l) s << "    a[" << l << "] = cur[swS ^ " << sw.apply(LS.rconst(l)) << "u];\n";
+    }
+    const Layout& LST = extra_relayout ? LS : LN;
     s << "    { double2* dst = st + base + toff_st;\n";
-    for (int l = 0; l < E; ++l) s << "      st_stream(dst + " << hex64(reg_off(LN, l)) << ", a[" << l << "]);\n";
+    for (int l = 0; l < E; ++l) s << "      st_stream(dst + " << hex64(reg_off(LST, l, qst)) << ", a[" << l << "]);\n";
     s << "    }\n"
       << "    __syncthreads();\n"
       << "  }\n";

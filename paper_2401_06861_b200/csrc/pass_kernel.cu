@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(Geo<M, RR>::T, (Geo<M, RR>::T >= 256 ? 512 / G
     constexpr int SIZE = Geo<M, RR>::SIZE, R = Geo<M, RR>::R, E = Geo<M, RR>::E, T = Geo<M, RR>::T;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int8_t s_q[16];
+    __shared__ int8_t s_qst[16];
     __shared__ int8_t s_rest[56];
 
     const PassHdr* h = reinterpret_cast<const PassHdr*>(rec);
@@ -263,7 +264,10 @@ __global__ void __launch_bounds__(Geo<M, RR>::T, (Geo<M, RR>::T >= 256 ? 512 / G
     const uint4* gops = reinterpret_cast<const uint4*>(rec + h->op_off);
     uint4* sops = reinterpret_cast<uint4*>(ops);
     for (int i = tid; i < nops * 2; i += T) sops[i] = gops[i];
-    for (int i = tid; i < 16; i += T) s_q[i] = h->q[i];
+    for (int i = tid; i < 16; i += T) {
+        s_q[i] = h->q[i];
+        s_qst[i] = h->qst[i];
+    }
     for (int i = tid; i < 56; i += T) s_rest[i] = h->rest[i];
     __syncthreads();
 
@@ -272,6 +276,8 @@ __global__ void __launch_bounds__(Geo<M, RR>::T, (Geo<M, RR>::T >= 256 ? 512 / G
     set_layout<M, RR>(L0, ops[0].pos, tid);
     const int nrest = h->nrest;
     const int64_t ntiles = h->ntiles;
+    bool relabel = false;  // stores go to a permutation of the loaded bits
+    for (int i = 0; i < M; ++i) relabel = relabel || h->q[i] != h->qst[i];
     const uint64_t off0 = tile_off<M, RR>(L0.tb, s_q);
     uint64_t roff0[4];
 #pragma unroll
@@ -320,10 +326,13 @@ __global__ void __launch_bounds__(Geo<M, RR>::T, (Geo<M, RR>::T >= 256 ? 512 / G
             }
         }
         {
-            const uint64_t offs = tile_off<M, RR>(L.tb, s_q);
+            // with a relabelling store another thread may still have to load
+            // the addresses this thread writes
+            if (relabel) __syncthreads();
+            const uint64_t offs = tile_off<M, RR>(L.tb, s_qst);
             uint64_t ro[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) ro[j] = j < R ? uint64_t(1) << s_q[L.rp[j]] : 0;
+            for (int j = 0; j < 4; ++j) ro[j] = j < R ? uint64_t(1) << s_qst[L.rp[j]] : 0;
             double2* dst = st + base + offs;
 #pragma unroll
             for (int l = 0; l < E; ++l) {

@@ -226,7 +226,10 @@ class PassBuilder {
 
     // Close the pass: map state bits to tile bits, split the micro-op program
     // into register-layout stages and encode register slots.
-    PlannedPass finish(const std::vector<int>& q) {
+    // l2p: logical -> physical bit for bits outside the tile (diagonal tables
+    // and controls read them from the full physical index); null = identity.
+    PlannedPass finish(const std::vector<int>& q, const std::vector<int>* l2p = nullptr) {
+        auto phys = [&](int b) { return l2p ? (*l2p)[size_t(b)] : b; };
         for (const auto& g : pend_) emit_group(g);
         pend_.clear();
         const int m = int(q.size());
@@ -327,11 +330,11 @@ class PassBuilder {
                 if (bb < kMaxStateBits && tpos[bb] >= 0)
                     op.cmask_tile |= uint32_t(1) << tpos[bb];
                 else
-                    op.cmask_glob |= bit(bb);
+                    op.cmask_glob |= bit(phys(bb));
             }
             if (b.type == MOP_DIAG) {
                 for (int j = 0; j < b.k; ++j)
-                    op.pos[j] = int8_t(tpos[b.bits[j]] >= 0 ? tpos[b.bits[j]] : -1 - b.bits[j]);
+                    op.pos[j] = int8_t(tpos[b.bits[j]] >= 0 ? tpos[b.bits[j]] : -1 - phys(b.bits[j]));
                 p.pool.insert(p.pool.end(), b.m.begin(), b.m.end());
             } else if (b.type == MOP_DENSE) {
                 // local bit i of the stored matrix = i-th smallest slot
@@ -669,7 +672,7 @@ void hoist_global_phase(std::vector<PlannedPass>& passes) {
 }  // namespace
 
 std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanOptions& opt,
-                                     PlanStats* stats) {
+                                     PlanStats* stats, std::vector<int>* map) {
     const std::vector<EOp> ops = opt.fuse ? cancel_perm_sandwiches(ops_in) : ops_in;
     const int nloc = opt.nloc;
     const int m = std::min(opt.tile_bits, nloc);
@@ -677,9 +680,22 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
     // Otherwise keep >= low_bits contiguous low bits for coalescing, but always
     // leave room for one 4-bit operator among the high tile bits.
     const int lb = (nloc <= opt.tile_bits) ? m : std::max(0, std::min(opt.low_bits, m - kMaxOpK));
-    const uint64_t low_mask = (lb >= 64) ? ~uint64_t(0) : (bit(lb) - 1);
     const uint64_t all_mask = (opt.nbits >= 64) ? ~uint64_t(0) : (bit(opt.nbits) - 1);
     const uint64_t loc_mask = (nloc >= 64) ? ~uint64_t(0) : (bit(nloc) - 1);
+    const bool relabel = opt.relabel && map && nloc > m && lb > 0 && int(map->size()) == opt.nbits;
+
+    // layout: logical <-> physical bit (identity unless relabelling)
+    std::vector<int> l2p(size_t(opt.nbits)), p2l(size_t(opt.nbits));
+    for (int b = 0; b < opt.nbits; ++b) l2p[size_t(b)] = b;
+    if (relabel) l2p = *map;
+    for (int b = 0; b < opt.nbits; ++b) p2l[size_t(l2p[size_t(b)])] = b;
+    // logical bits held by the lb low (contiguous) physical bits
+    auto low_of = [&] {
+        uint64_t lm = 0;
+        for (int p = 0; p < lb; ++p) lm |= bit(p2l[size_t(p)]);
+        return lm;
+    };
+    uint64_t low_mask = (lb >= 64) ? ~uint64_t(0) : low_of();
 
     std::vector<PlannedPass> passes;
     int64_t src_total = 0;
@@ -699,8 +715,8 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
         std::vector<const EOp*> next;
         explicit Trial(bool fuse) : pb(fuse) {}
     };
-    // One pass from `remaining`, with the high tile bits optionally pre-seeded.
-    auto build = [&](uint64_t seed) {
+    // One pass from `ops_list` with low bits `lowm`, the high tile bits optionally pre-seeded.
+    auto build = [&](const std::vector<const EOp*>& ops_list, uint64_t seed, uint64_t lowm) {
         Trial t(opt.fuse);
         t.pb.set_coalesce(coalesce_enabled());
         t.pb.set_reg_bits(reg_bits_env(opt.reg_bits));
@@ -708,8 +724,8 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
         uint64_t blocked = 0;
         std::vector<const EOp*> deferred;
         size_t i = 0;
-        for (; i < remaining.size(); ++i) {
-            const EOp* e = remaining[i];
+        for (; i < ops_list.size(); ++i) {
+            const EOp* e = ops_list[i];
             const uint64_t touched = bitmask_of(*e, true);
             if (touched & blocked) {
                 deferred.push_back(e);
@@ -720,7 +736,7 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
                 }
                 continue;
             }
-            const uint64_t nh = t.qhigh | (need_mask(*e) & ~low_mask);
+            const uint64_t nh = t.qhigh | (need_mask(*e) & ~lowm);
             const bool fits = popcount64(nh) <= m - lb;
             const bool caps = (t.pb.microops() + 1 <= size_t(opt.max_ops_per_pass)) &&
                               (t.pb.pool() + size_t(pool_cost(*e)) <= size_t(opt.max_pool_per_pass));
@@ -739,7 +755,7 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
             }
         }
         t.next = deferred;
-        t.next.insert(t.next.end(), remaining.begin() + long(i), remaining.end());
+        t.next.insert(t.next.end(), ops_list.begin() + long(i), ops_list.end());
         return t;
     };
     // Seeds: the plain in-order greedy, and the high bits most needed by the
@@ -768,13 +784,23 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
         return e && e[0] == '1';
     }();
     const bool multi_seed = seeds_env && opt.fuse && nloc > m;
+    // first position at which each logical bit is a non-diagonal target in `list`
+    auto next_use = [&](const std::vector<const EOp*>& list) {
+        std::vector<size_t> nu(size_t(opt.nbits), SIZE_MAX);
+        for (size_t i = list.size(); i-- > 0;) {
+            const uint64_t nm = need_mask(*list[i]);
+            for (int b = 0; b < opt.nbits; ++b)
+                if ((nm >> b) & 1) nu[size_t(b)] = i;
+        }
+        return nu;
+    };
     while (!remaining.empty()) {
-        Trial t = build(0);
+        Trial t = build(remaining, 0, low_mask);
         if (multi_seed) {
             for (size_t w : {size_t(24), size_t(48), size_t(96)}) {
                 const uint64_t seed = freq_seed(w);
                 if (!seed) continue;
-                Trial c = build(seed);
+                Trial c = build(remaining, seed, low_mask);
                 if (c.taken > t.taken) t = std::move(c);
             }
         }
@@ -789,15 +815,144 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
             pb.add(*next.front());
             next.erase(next.begin());
         }
-        // Tile bit set: low bits, required high bits, then fill upward.
+        // Tile bit set: low bits, required high bits, then fill.
         uint64_t qmask = low_mask | qhigh;
-        for (int b = 0; b < nloc && popcount64(qmask) < m; ++b) qmask |= bit(b);
-        std::vector<int> q;
-        for (int b = 0; b < nloc; ++b)
+        std::vector<size_t> nu;
+        // Last pass of a relabelling plan: when every displaced qubit fits in
+        // the tile, the pass stores them home and the plan ends on the
+        // identity layout (no normalising pass later; repeated circuits replan
+        // to the same passes).
+        bool restore = false;
+        if (relabel && next.empty()) {
+            uint64_t displaced = 0;
+            for (int b = 0; b < nloc; ++b)
+                if (l2p[size_t(b)] != b) displaced |= bit(b);
+            if (popcount64(qmask | displaced) <= m) {
+                qmask |= displaced;
+                restore = true;
+            }
+        }
+        if (relabel) {
+            // fill with the local bits the remaining ops need soonest
+            nu = next_use(next);
+            std::vector<int> cand;
+            for (int b = 0; b < nloc; ++b)
+                if (!((qmask >> b) & 1)) cand.push_back(b);
+            std::stable_sort(cand.begin(), cand.end(), [&](int x, int y) { return nu[size_t(x)] < nu[size_t(y)]; });
+            for (int b : cand) {
+                if (popcount64(qmask) >= m) break;
+                qmask |= bit(b);
+            }
+        } else {
+            for (int b = 0; b < nloc && popcount64(qmask) < m; ++b) qmask |= bit(b);
+        }
+        std::vector<int> q;  // logical tile bits in ascending physical order
+        for (int b = 0; b < opt.nbits; ++b)
             if ((qmask >> b) & 1) q.push_back(b);
+        std::sort(q.begin(), q.end(), [&](int x, int y) { return l2p[size_t(x)] < l2p[size_t(y)]; });
         if (int(q.size()) != m) throw std::logic_error("planner: tile size mismatch");
-        PlannedPass p = pb.finish(q);
-        if (p.ops.size() > 1) passes.push_back(std::move(p));  // ops[0] is the load layout
+        PlannedPass p = pb.finish(q, relabel ? &l2p : nullptr);
+        if (p.ops.size() > 1) {
+            for (size_t i = 0; i < q.size(); ++i) p.q[i] = l2p[size_t(q[i])];
+            if (restore) {
+                for (int x : q) {
+                    l2p[size_t(x)] = x;
+                    p2l[size_t(x)] = x;
+                }
+                low_mask = low_of();
+            } else if (relabel && !next.empty()) {
+                // Choose the tile qubits that the low physical bits hold after this
+                // pass: greedily, the set under which the next pass takes the most ops.
+                // A guest (a qubit whose home is a high bit, held by a low bit)
+                // only leaves the low bits to go home, so it stays when its home
+                // bit is not in this tile: at most 2 * lb qubits are ever displaced.
+                uint64_t chosen = 0;
+                {
+                    std::vector<int> tile_phys;
+                    for (int x : q) tile_phys.push_back(l2p[size_t(x)]);
+                    for (int pbit = 0; pbit < lb; ++pbit) {
+                        const int g = p2l[size_t(pbit)];
+                        if (g >= lb && std::find(tile_phys.begin(), tile_phys.end(), g) == tile_phys.end())
+                            chosen |= bit(g);
+                    }
+                }
+                for (int slot = popcount64(chosen); slot < lb; ++slot) {
+                    int best = -1;
+                    size_t best_taken = 0;
+                    std::vector<int> order(q);
+                    // current low qubits first (ties keep them: fewer moves)
+                    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+                        return ((low_mask >> x) & 1) > ((low_mask >> y) & 1);
+                    });
+                    for (int c : order) {
+                        if ((chosen >> c) & 1) continue;
+                        uint64_t trial = chosen | bit(c);
+                        // complete the trial set with the soonest-needed remaining tile qubits
+                        std::vector<int> rest;
+                        for (int x : q)
+                            if (!((trial >> x) & 1)) rest.push_back(x);
+                        std::stable_sort(rest.begin(), rest.end(),
+                                         [&](int x, int y) { return nu[size_t(x)] < nu[size_t(y)]; });
+                        for (int x : rest) {
+                            if (popcount64(trial) >= lb) break;
+                            trial |= bit(x);
+                        }
+                        const size_t tk = build(next, 0, trial).taken;
+                        if (best < 0 || tk > best_taken) {
+                            best = c;
+                            best_taken = tk;
+                        }
+                    }
+                    chosen |= bit(best);
+                }
+                // New layout, any permutation of this tile's physical bits: the
+                // chosen qubits take the low bits, and every qubit whose home bit
+                // is free goes home (fewer displaced qubits to restore later).
+                std::vector<int> phys_set;
+                for (int x : q) phys_set.push_back(l2p[size_t(x)]);
+                std::vector<int> newpos(size_t(opt.nbits), -1);
+                std::vector<char> used(size_t(opt.nbits), 0);
+                auto place = [&](int x, int pos) {
+                    newpos[size_t(x)] = pos;
+                    used[size_t(pos)] = 1;
+                };
+                // 1) chosen qubits: home if home is a low bit, then stay if already low
+                for (int x : q)
+                    if (((chosen >> x) & 1) && x < lb) place(x, x);
+                for (int x : q)
+                    if (((chosen >> x) & 1) && newpos[size_t(x)] < 0 && l2p[size_t(x)] < lb &&
+                        !used[size_t(l2p[size_t(x)])])
+                        place(x, l2p[size_t(x)]);
+                for (int x : q) {
+                    if (!((chosen >> x) & 1) || newpos[size_t(x)] >= 0) continue;
+                    for (int pbit = 0; pbit < lb; ++pbit)
+                        if (!used[size_t(pbit)]) {
+                            place(x, pbit);
+                            break;
+                        }
+                }
+                // 2) the others: home when it is a free high bit of this tile, else any free high bit
+                auto in_tile = [&](int pos) { return std::find(phys_set.begin(), phys_set.end(), pos) != phys_set.end(); };
+                for (int x : q)
+                    if (newpos[size_t(x)] < 0 && x >= lb && in_tile(x) && !used[size_t(x)]) place(x, x);
+                for (int x : q) {
+                    if (newpos[size_t(x)] >= 0) continue;
+                    for (int pos : phys_set)
+                        if (pos >= lb && !used[size_t(pos)]) {
+                            place(x, pos);
+                            break;
+                        }
+                }
+                for (int x : q) {
+                    l2p[size_t(x)] = newpos[size_t(x)];
+                    p2l[size_t(newpos[size_t(x)])] = x;
+                }
+                low_mask = low_of();
+            }
+            p.qst.resize(q.size());
+            for (size_t i = 0; i < q.size(); ++i) p.qst[i] = l2p[size_t(q[i])];
+            passes.push_back(std::move(p));
+        }
         remaining.swap(next);
     }
     if (opt.fuse) hoist_global_phase(passes);
@@ -807,6 +962,7 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
         for (const auto& p : passes) stats->microops += int64_t(p.ops.size());
         stats->source_ops = src_total;
     }
+    if (relabel) *map = l2p;
     return passes;
 }
 
@@ -821,7 +977,10 @@ std::vector<unsigned char> serialize_passes(const std::vector<PlannedPass>& pass
         h.nops = int32_t(p.ops.size());
         h.nloc = nloc;
         h.ntiles = int64_t(1) << (nloc - h.m);
-        for (size_t i = 0; i < p.q.size(); ++i) h.q[i] = int8_t(p.q[i]);
+        for (size_t i = 0; i < p.q.size(); ++i) {
+            h.q[i] = int8_t(p.q[i]);
+            h.qst[i] = int8_t(p.qst.empty() ? p.q[i] : p.qst[i]);
+        }
         int nr = 0;
         uint64_t qm = 0;
         for (int b : p.q) qm |= bit(b);

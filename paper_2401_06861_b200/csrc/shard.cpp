@@ -657,6 +657,8 @@ nq_status nq_sv_create_sharded(int n, int rank, int world, const unsigned char u
         s.world = world;
         s.popt.nbits = n;
         s.popt.nloc = s.nloc;
+        s.popt.relabel = false;  // the sharded layer keeps its own qubit map
+        s.layout.clear();
         configure_caps(s.popt);
         DeviceCtx& c = ctx_for(s.dev);
         launch_init_basis(s.d, s.count, rank == 0 ? 0 : UINT64_MAX, c.stream);

@@ -94,6 +94,9 @@ struct State {
     int rank = 0, world = 1;
     ShardComm* comm = nullptr;
     bool plain_alloc = false;  // cudaMalloc'd (IPC-exportable), freed with cudaFree
+    // single-device state vectors: logical qubit -> physical bit after the
+    // relabelling passes (identity otherwise); readouts normalise it
+    std::vector<int> layout;
 };
 
 void sv_expect_raw(State& s, const uint64_t* flip, const uint64_t* signs, int nterms, std::vector<cplx>& totals);
@@ -101,6 +104,8 @@ void sv_expect_raw(State& s, const uint64_t* flip, const uint64_t* signs, int nt
 void state_init(State& s, int n, bool dm, const nq_opts* opts);
 void state_free(State& s);
 void state_flush(State& s);
+// flush, then restore the identity layout (amplitude-order readouts)
+void state_flush_normal(State& s);
 void configure_caps(PlanOptions& p);
 double* result_slot(DeviceCtx& c, int i);
 void fetch(DeviceCtx& c, const double* dsrc, size_t count, double* host);

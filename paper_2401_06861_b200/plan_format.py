@@ -13,11 +13,11 @@ from typing import List
 import numpy as np
 
 MOP_NAMES = {0: "dense", 1: "diag", 2: "xperm", 3: "swap", 4: "depol", 5: "layout"}
-HDR_FMT = "<iiiiqIIII16b56b"
+HDR_FMT = "<iiiiqIIII16b56b16b"
 HDR_SIZE = struct.calcsize(HDR_FMT)
 MOP_FMT = "<BB8bHII4xQ"
 MOP_SIZE = struct.calcsize(MOP_FMT)
-assert HDR_SIZE == 112 and MOP_SIZE == 32
+assert HDR_SIZE == 128 and MOP_SIZE == 32
 
 
 @dataclass
@@ -38,6 +38,7 @@ class Pass:
     ntiles: int
     q: List[int]
     rest: List[int]
+    qst: List[int] = field(default_factory=list)  # store position of tile bit i (relabelling pass)
     ops: List[MicroOp] = field(default_factory=list)
     pool: np.ndarray = None
 
@@ -50,7 +51,8 @@ def decode(buf: bytes) -> List[Pass]:
         m, nops, nloc, nrest, ntiles, op_off, pool_off, pool_n, nbytes = f[:9]
         q = list(f[9:9 + 16])[:m]
         rest = list(f[25:25 + 56])[:nrest]
-        p = Pass(m=m, nloc=nloc, ntiles=ntiles, q=q, rest=rest)
+        qst = list(f[81:81 + 16])[:m]
+        p = Pass(m=m, nloc=nloc, ntiles=ntiles, q=q, rest=rest, qst=qst)
         for i in range(nops):
             f2 = struct.unpack_from(MOP_FMT, buf, at + op_off + i * MOP_SIZE)
             t, k = f2[0], f2[1]

@@ -25,11 +25,21 @@ def deposit(v, pos):
 
 
 def run_plan(n, passes, amps):
-    """Numpy emulator of the pass records (semantics of csrc/engine.hpp)."""
+    """Numpy emulator of the pass records (semantics of csrc/engine.hpp).
+    Relabelling passes store tile bit i at qst[i]; the result is returned in
+    logical qubit order (the final layout undone)."""
     a = amps.copy()
+    p2l = list(range(n))  # physical bit -> logical qubit
     for p in passes:
         size = 1 << p.m
         offs = np.array([deposit(e, p.q) for e in range(size)], dtype=np.int64)
+        qst = p.qst if p.qst else p.q
+        assert sorted(qst) == sorted(p.q)
+        offs_st = np.array([deposit(e, qst) for e in range(size)], dtype=np.int64)
+        new = list(p2l)
+        for i in range(p.m):
+            new[qst[i]] = p2l[p.q[i]]
+        p2l = new
         assert p.ops[0].type == "layout"
         for r in range(p.ntiles):
             base = deposit(r, p.rest)
@@ -41,7 +51,13 @@ def run_plan(n, passes, amps):
                     assert lay == sorted(lay)
                     continue
                 apply_mop(op, t, p.pool, base, p.m, lay)
-            a[base + offs] = t
+            a[base + offs_st] = t
+    if p2l != list(range(n)):
+        l2p = [0] * n
+        for ph, lq in enumerate(p2l):
+            l2p[lq] = ph
+        idx = np.array([deposit(x, l2p) for x in range(1 << n)], dtype=np.int64)
+        a = a[idx]
     return a
 
 
@@ -94,6 +110,26 @@ def test_plan_emulation_matches_oracle(port, n, tile, fuse):
         a0[0] = 1
         got = run_plan(n, passes, a0)
         np.testing.assert_allclose(got, port.sv_run(n, ops), atol=1e-10, rtol=0)
+
+
+@pytest.mark.parametrize("n,tile", [(12, 8), (14, 9), (16, 11), (13, 6)])
+def test_relabelling_plans_match_oracle(port, n, tile):
+    """Relabelling stores (low physical bits hold a per-pass choice of
+    qubits): emulated plan, final layout undone, equals the oracle; the
+    relabelled plan never needs more passes than the plain one."""
+    for seed in range(3):
+        ops = port.random_circuit(7100 + n + seed, n, 200)
+        plain = plan_format.decode(abi.plan_debug(n, ops, tile_qubits=tile))
+        passes = plan_format.decode(abi.plan_debug(n, ops, tile_qubits=tile, relabel=True))
+        assert any(p.qst != p.q for p in passes)
+        lb = max(0, min(4, tile - 4))
+        for p in passes:
+            assert p.q[:lb] == list(range(lb))  # the physical low bits stay in every tile
+        a0 = np.zeros(1 << n, dtype=complex)
+        a0[0] = 1
+        got = run_plan(n, passes, a0)
+        np.testing.assert_allclose(got, port.sv_run(n, ops), atol=1e-10, rtol=0)
+        assert len(passes) <= len(plain) + 1
 
 
 def test_tile_sets_respect_coalescing_and_capacity(port):
