@@ -122,7 +122,7 @@ void state_init(State& s, int n, bool dm, const nq_opts* opts) {
     // A/B knobs (read per state): NQ_LOW_BITS for state vectors, NQ_TILE_DM /
     // NQ_LOW_BITS_DM for density matrices
     if (!dm) {
-        if (const char* e = std::getenv("NQ_LOW_BITS")) s.popt.low_bits = std::max(0, std::min(std::atoi(e), 4));
+        if (const char* e = std::getenv("NQ_LOW_BITS")) s.popt.low_bits = std::max(0, std::min(std::atoi(e), 7));
     }
     if (dm) {
         if (const char* e = std::getenv("NQ_TILE_DM"); e && o.tile_qubits <= 0)
