@@ -262,32 +262,109 @@ class PassBuilder {
             for (int t = m - 1; t >= 0 && popcount64(r) < rsz; --t) r |= 1u << t;
             return r;
         };
-        std::vector<uint32_t> stage_of(live.size(), 0);
+        // Register stages.  The pass program may be reordered where ops commute
+        // (disjoint bits, or both diagonal): list scheduling over that
+        // dependency DAG runs every ready op the current register set allows
+        // before switching sets, and switches to the set under which the most
+        // ops become runnable.  Each switch is a shared-memory relayout of the
+        // whole tile, so fewer switches is less shared-memory traffic.
+        const size_t L = live.size();
+        std::vector<uint32_t> ndv(L);
+        std::vector<uint64_t> tch(L);
+        std::vector<char> isdiag(L);
+        for (size_t i = 0; i < L; ++i) {
+            ndv[i] = need(*live[i]);
+            tch[i] = live[i]->touch();
+            isdiag[i] = live[i]->type == MOP_DIAG;
+        }
+        std::vector<std::vector<int>> succ(L);
+        std::vector<int> npred(L, 0);
+        for (size_t i = 0; i < L; ++i)
+            for (size_t j = i + 1; j < L; ++j)
+                if ((tch[i] & tch[j]) && !(isdiag[i] && isdiag[j])) {
+                    succ[i].push_back(int(j));
+                    ++npred[j];
+                }
+        std::vector<int> order;
+        std::vector<uint32_t> stage_sched;
+        order.reserve(L);
+        std::vector<int> np = npred;
+        std::vector<char> done(L, 0);
         uint32_t cur = 0;
         bool have = false;
-        for (size_t i = 0; i < live.size(); ++i) {
-            const uint32_t nd = need(*live[i]);
-            if (nd == 0 || (have && (nd & ~cur) == 0)) {
-                stage_of[i] = cur;
-                continue;
+        // run every op runnable under register set R (need 0 or need within R),
+        // on copies of the state; returns how many ran
+        auto simulate = [&](uint32_t R, std::vector<int> p2, std::vector<char> d2) {
+            int ran = 0;
+            bool prog = true;
+            while (prog) {
+                prog = false;
+                for (size_t i = 0; i < L; ++i) {
+                    if (d2[i] || p2[i] != 0) continue;
+                    if (ndv[i] != 0 && (ndv[i] & ~R) != 0) continue;
+                    d2[i] = 1;
+                    ++ran;
+                    for (int j : succ[i]) --p2[size_t(j)];
+                    prog = true;
+                }
             }
-            uint32_t r = nd;
-            for (size_t j = i + 1; j < live.size(); ++j) {
-                const uint32_t nj = need(*live[j]);
-                if (popcount64(r | nj) > rsz) break;
-                r |= nj;
+            return ran;
+        };
+        while (order.size() < L) {
+            bool prog = false;
+            for (size_t i = 0; i < L; ++i) {
+                if (done[i] || np[i] != 0) continue;
+                if (ndv[i] != 0 && (!have || (ndv[i] & ~cur) != 0)) continue;
+                done[i] = 1;
+                order.push_back(int(i));
+                stage_sched.push_back(cur);
+                for (int j : succ[i]) --np[size_t(j)];
+                prog = true;
+                break;  // rescan from the lowest index: keeps program order where possible
             }
-            cur = fill(r);
-            if (!have) {  // ops before the first register-bound op share its layout
-                for (size_t j = 0; j < i; ++j) stage_of[j] = cur;
+            if (prog) continue;
+            // switch register sets: candidates seeded by each ready op's needs
+            uint32_t best = 0;
+            int best_ran = -1;
+            std::vector<uint32_t> tried;
+            // seed: a ready op's needs, then the needs of the following
+            // unscheduled ops in program order while they fit (lookahead)
+            for (size_t i = 0; i < L; ++i) {
+                if (done[i] || np[i] != 0 || ndv[i] == 0) continue;
+                for (int variant = 0; variant < 2; ++variant) {
+                    uint32_t r = ndv[i];
+                    for (size_t j = 0; j < L; ++j) {
+                        if (done[j] || ndv[j] == 0 || j == i) continue;
+                        if (popcount64(r | ndv[j]) <= rsz) r |= ndv[j];
+                        else if (variant == 0) break;
+                    }
+                    r = fill(r);
+                    if (std::find(tried.begin(), tried.end(), r) != tried.end()) continue;
+                    tried.push_back(r);
+                    const int ran = simulate(r, np, done);
+                    if (ran > best_ran) {
+                        best_ran = ran;
+                        best = r;
+                    }
+                }
             }
+            if (best_ran <= 0) throw std::logic_error("planner: stage scheduling made no progress");
+            if (!have) {  // ops scheduled before the first register-bound op share its layout
+                for (auto& st : stage_sched) st = best;
+            }
+            cur = best;
             have = true;
-            stage_of[i] = cur;
         }
         if (!have) {
             cur = fill(0);
-            for (auto& s : stage_of) s = cur;
+            for (auto& st : stage_sched) st = cur;
         }
+        {
+            std::vector<const BitOp*> reordered(L);
+            for (size_t k = 0; k < L; ++k) reordered[k] = live[size_t(order[k])];
+            live.swap(reordered);
+        }
+        std::vector<uint32_t> stage_of = stage_sched;
 
         PlannedPass p;
         p.q = q;
@@ -758,6 +835,29 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
         t.next.insert(t.next.end(), ops_list.begin() + long(i), ops_list.end());
         return t;
     };
+    // Ops the next pass would take under low bits `lowm` (the window logic of
+    // build() without building micro-ops: the relabel search's estimator).
+    auto count_taken = [&](const std::vector<const EOp*>& ops_list, uint64_t lowm) {
+        uint64_t qh = 0, blocked = 0;
+        size_t taken = 0;
+        for (const EOp* e : ops_list) {
+            const uint64_t touched = bitmask_of(*e, true);
+            if (touched & blocked) {
+                blocked |= touched;
+                if ((blocked & all_mask) == all_mask) break;
+                continue;
+            }
+            const uint64_t nh = qh | (need_mask(*e) & ~lowm);
+            if (popcount64(nh) <= m - lb) {
+                qh = nh;
+                ++taken;
+            } else {
+                blocked |= touched;
+                if ((blocked & all_mask) == all_mask) break;
+            }
+        }
+        return taken;
+    };
     // Seeds: the plain in-order greedy, and the high bits most needed by the
     // next W ops (W = 24, 48, 96); keep the trial that takes the most ops.
     auto freq_seed = [&](size_t w) {
@@ -866,6 +966,9 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
                 // A guest (a qubit whose home is a high bit, held by a low bit)
                 // only leaves the low bits to go home, so it stays when its home
                 // bit is not in this tile: at most 2 * lb qubits are ever displaced.
+                // the next pass is judged on a bounded window of the remaining ops
+                const std::vector<const EOp*> window(next.begin(),
+                                                     next.begin() + long(std::min<size_t>(next.size(), 128)));
                 uint64_t chosen = 0;
                 {
                     std::vector<int> tile_phys;
@@ -897,7 +1000,7 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
                             if (popcount64(trial) >= lb) break;
                             trial |= bit(x);
                         }
-                        const size_t tk = build(next, 0, trial).taken;
+                        const size_t tk = count_taken(window, trial);
                         if (best < 0 || tk > best_taken) {
                             best = c;
                             best_taken = tk;
