@@ -117,6 +117,7 @@ void state_init(State& s, int n, bool dm, const nq_opts* opts) {
         const char* e = std::getenv("NQ_RELABEL");
         s.popt.relabel = !dm && !(e && e[0] == '0');
     }
+    s.popt.stage_sched = !dm;
     s.layout.resize(size_t(s.nbits));
     for (int b = 0; b < s.nbits; ++b) s.layout[size_t(b)] = b;
     // A/B knobs (read per state): NQ_LOW_BITS for state vectors, NQ_TILE_DM /

@@ -97,6 +97,9 @@ struct PlanOptions {
     // Relabel qubits at pass stores (single-device state vectors): the qubits
     // held by the low (contiguous) physical bits become a per-pass choice.
     bool relabel = false;
+    // Reorder commuting micro-ops to reduce register-layout switches (state
+    // vectors; measured slower on the Liouville programs of density matrices).
+    bool stage_sched = true;
 };
 
 struct PlannedPass {

@@ -190,6 +190,9 @@ struct BitOp {
     }
 };
 
+bool stage_sched_enabled();
+uint32_t coalesce_mask();
+
 class PassBuilder {
   public:
     explicit PassBuilder(bool fuse) : fuse_(fuse) {}
@@ -365,6 +368,45 @@ class PassBuilder {
             live.swap(reordered);
         }
         std::vector<uint32_t> stage_of = stage_sched;
+        // Program order with lookahead packing (the previous scheme) is kept
+        // when it needs no more switches than the schedule.
+        auto switches = [](const std::vector<uint32_t>& st) {
+            int k = 0;
+            for (size_t i = 1; i < st.size(); ++i) k += st[i] != st[i - 1];
+            return k;
+        };
+        std::vector<const BitOp*> live_sched = live;
+        {
+            // A/B: program order, each switch packing the following ops' needs
+            live.clear();
+            for (const auto& b : ops_)
+                if (b.alive) live.push_back(&b);
+            for (size_t i = 0; i < L; ++i) ndv[i] = need(*live[i]);
+            stage_of.assign(L, 0);
+            uint32_t c2 = 0;
+            bool h2 = false;
+            for (size_t i = 0; i < L; ++i) {
+                if (ndv[i] == 0 || (h2 && (ndv[i] & ~c2) == 0)) {
+                    stage_of[i] = c2;
+                    continue;
+                }
+                uint32_t r = ndv[i];
+                for (size_t j = i + 1; j < L; ++j) {
+                    if (popcount64(r | ndv[j]) > rsz) break;
+                    r |= ndv[j];
+                }
+                c2 = fill(r);
+                if (!h2)
+                    for (size_t j = 0; j < i; ++j) stage_of[j] = c2;
+                h2 = true;
+                stage_of[i] = c2;
+            }
+            if (!h2) stage_of.assign(L, fill(0));
+        }
+        if (stage_sched_ && stage_sched_enabled() && switches(stage_sched) < switches(stage_of)) {
+            live = live_sched;
+            stage_of = stage_sched;
+        }
 
         PlannedPass p;
         p.q = q;
@@ -383,7 +425,7 @@ class PassBuilder {
         // lanes do not cover 32 consecutive amplitudes; then load (store) in
         // the layout of the 4 highest tile bits and relayout through shared
         // memory instead.
-        const uint32_t lane_bits = m >= 9 ? 0x1Fu : 0u;
+        const uint32_t lane_bits = m >= 9 ? coalesce_mask() : 0u;
         const uint32_t top = fill(0);
         if (coalesce_ && (lay & lane_bits)) p.ops.push_back(layout_op(top));
         p.ops.push_back(layout_op(lay));
@@ -443,6 +485,7 @@ class PassBuilder {
     }
 
     void set_coalesce(bool c) { coalesce_ = c; }
+    void set_stage_sched(bool v) { stage_sched_ = v; }
     void set_reg_bits(int r) { reg_bits_ = r; }
 
   private:
@@ -591,6 +634,7 @@ class PassBuilder {
 
     bool fuse_;
     bool coalesce_ = true;
+    bool stage_sched_ = true;
     int reg_bits_ = 4;
     std::vector<BitOp> ops_;
     std::vector<Group> pend_;
@@ -609,6 +653,25 @@ bool coalesce_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("NQ_COALESCE");
         return e && e[0] == '1';
+    }();
+    return on;
+}
+
+// Tile bits that must not be register bits of the load / store layouts
+// (NQ_COALESCE_MASK, default tile bits 0-4).
+uint32_t coalesce_mask() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("NQ_COALESCE_MASK");
+        return e ? uint32_t(std::strtoul(e, nullptr, 0)) : 0x1Fu;
+    }();
+    return v;
+}
+
+// NQ_STAGE_SCHED=0 keeps each pass program in source order (A/B).
+bool stage_sched_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("NQ_STAGE_SCHED");
+        return !(e && e[0] == '0');
     }();
     return on;
 }
@@ -797,6 +860,7 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
         Trial t(opt.fuse);
         t.pb.set_coalesce(coalesce_enabled());
         t.pb.set_reg_bits(reg_bits_env(opt.reg_bits));
+        t.pb.set_stage_sched(opt.stage_sched);
         t.qhigh = seed;
         uint64_t blocked = 0;
         std::vector<const EOp*> deferred;
