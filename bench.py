@@ -304,7 +304,9 @@ def secondary_workloads(abi, workloads, device):
     t0 = time.perf_counter()
     z = naqs.density_expectation(circ, "Z" + "I" * (nd - 1), model)
     dt = time.perf_counter() - t0
-    out["dm_noisy_tfim14"] = {"wall_s": dt, "items": len(circ) * 3 + sum(1 for o in circ.ops() if len(o[1]) == 2),
+    dm_cpu = dm_cpu_sample(workloads, nd)
+    out["dm_noisy_tfim14"] = {"wall_s": dt, "cpu": dm_cpu,
+                              "items": len(circ) * 3 + sum(1 for o in circ.ops() if len(o[1]) == 2),
                               "z0": z, "note": "end-to-end via naqs.density_expectation: attach_noise, superoperator "
                                                "compile, fused passes, expectation"}
     # C5: VQE n=28 energy evaluations (exact, 193 gates + 55 terms)
@@ -364,6 +366,26 @@ def tfim4_sweep(workloads):
                     "max_abs_diff_vs_cpu": float(max(np.max(np.abs(rows[:, 1] - ideal)),
                                                      np.max(np.abs(rows[:, 2] - noisy))))})
     return res
+
+
+def dm_cpu_sample(workloads, nd):
+    """The reference's noisy density-matrix run (dm_run_noisy, all host
+    threads) on a prefix of the same n = 14 TFIM circuit: seconds per source
+    gate, and that rate times the full circuit (an extrapolation, labelled)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import NoiseSpec, Ref  # CPU baseline only
+
+    if not Ref.available():
+        return None
+    ops = list(workloads.tfim_trotter(nd, 1.0, steps=10))
+    k = 3  # one ZZ bond (cx, rz, cx): each noisy 2-qubit gate costs the reference ~10 s at n = 14
+    spec = NoiseSpec(nd, t1=60.0, t2=40.0, p01=0.02, p10=0.02, e1=0.001, d1=50.0, e2=0.01, d2=300.0)
+    ref = Ref()
+    threads = ref.set_threads(cpu_threads())
+    ms = ref.dm_time_noisy(nd, ops[:k], spec, 1)
+    per_gate = float(ms[0]) / 1e3 / k
+    return {"sample": f"first {k} of {len(ops)} gates (with their noise channels), reference dm_run_noisy, "
+                      f"{threads} threads", "s_per_gate": per_gate, "extrapolated_wall_s": per_gate * len(ops)}
 
 
 def trajectory_workloads(workloads):
