@@ -88,6 +88,26 @@ void DeviceCtx::stage(const unsigned char* src, size_t bytes) {
 }
 
 // ---- state lifecycle ---------------------------------------------------------
+// Layout of a freshly initialised state (|0..0> looks the same in every
+// layout).  State vectors: identity.  Density matrices larger than one tile:
+// interleaved, column bit q -> physical 2q and row bit q -> physical 2q + 1,
+// so a tile's low contiguous bits are whole qubits (both bits of a qubit's
+// superoperators) instead of column bits alone.  Opt-in (NQ_DM_INTERLEAVE=1):
+// on noisy TFIM-14 it does not reduce the pass count (a chain sweeps the
+// qubits either way) and the readouts then need a normalising swap plan.
+void set_initial_layout(State& s) {
+    for (int b = 0; b < s.nbits; ++b) s.layout[size_t(b)] = b;
+    static const bool interleave = [] {
+        const char* e = std::getenv("NQ_DM_INTERLEAVE");
+        return e && e[0] == '1';
+    }();
+    if (!s.dm || !interleave || s.nloc <= s.popt.tile_bits) return;
+    for (int q = 0; q < s.n; ++q) {
+        s.layout[size_t(q)] = 2 * q;
+        s.layout[size_t(q + s.n)] = 2 * q + 1;
+    }
+}
+
 void state_init(State& s, int n, bool dm, const nq_opts* opts) {
     nq_opts o;
     nq_default_opts(&o);
@@ -119,7 +139,7 @@ void state_init(State& s, int n, bool dm, const nq_opts* opts) {
     }
     s.popt.stage_sched = !dm;
     s.layout.resize(size_t(s.nbits));
-    for (int b = 0; b < s.nbits; ++b) s.layout[size_t(b)] = b;
+    set_initial_layout(s);
     // A/B knobs (read per state): NQ_LOW_BITS for state vectors, NQ_TILE_DM /
     // NQ_LOW_BITS_DM for density matrices
     if (!dm) {
@@ -210,8 +230,8 @@ void state_flush(State& s) {
         return;
     }
     PlanStats st;
-    const bool relabel = s.popt.relabel && int(s.layout.size()) == s.nbits;
-    std::vector<PlannedPass> passes = plan_passes(s.queue, s.popt, &st, relabel ? &s.layout : nullptr);
+    const bool use_layout = int(s.layout.size()) == s.nbits && (s.popt.relabel || !layout_is_identity(s));
+    std::vector<PlannedPass> passes = plan_passes(s.queue, s.popt, &st, use_layout ? &s.layout : nullptr);
     s.queue.clear();
     run_passes(s, passes, st);
 }
@@ -797,7 +817,7 @@ nq_status nq_dm_destroy(nq_dm* h) {
 nq_status nq_dm_clone(const nq_dm* h, nq_dm** out) {
     return guard([&] {
         State& src = const_cast<nq_dm*>(h)->s;
-        state_flush(src);
+        state_flush_normal(src);
         auto c = std::make_unique<nq_dm>();
         c->s.dev = src.dev;
         c->s.n = src.n;
@@ -823,6 +843,7 @@ nq_status nq_dm_reset(nq_dm* h) {
         DeviceCtx& c = ctx_for(s.dev);
         CUDA_TRY(cudaSetDevice(s.dev));
         launch_init_basis(s.d, s.count, 0, c.stream);
+        set_initial_layout(s);
         CUDA_TRY(cudaGetLastError());
     });
 }
@@ -911,7 +932,7 @@ nq_status nq_dm_flush(nq_dm* h) {
 nq_status nq_dm_trace(nq_dm* h, double* out) {
     return guard([&] {
         State& s = st(h);
-        state_flush(s);
+        state_flush_normal(s);
         DeviceCtx& c = ctx_for(s.dev);
         const uint64_t dim = uint64_t(1) << s.n;
         c.ensure_scratch(scratch_doubles_needed(dim) + 64);
@@ -936,7 +957,7 @@ nq_status nq_dm_purity(nq_dm* h, double* out) {
 nq_status nq_dm_hermiticity_residual(nq_dm* h, double* out) {
     return guard([&] {
         State& s = st(h);
-        state_flush(s);
+        state_flush_normal(s);
         DeviceCtx& c = ctx_for(s.dev);
         c.ensure_scratch(2048 + 64);
         launch_herm(s.d, uint64_t(1) << s.n, c.d_scratch + 64, result_slot(c, 0), c.stream);
@@ -953,7 +974,7 @@ nq_status nq_dm_expectation_batch(nq_dm* h, const uint64_t* flip, const uint64_t
         for (int t = 0; t < nterms; ++t)
             if ((flip[t] & ~lim) || (signs[t] & ~lim))
                 throw NqError{NQ_ERR_CONTRACT, "Pauli mask exceeds the state's qubit count"};
-        state_flush(s);
+        state_flush_normal(s);
         DeviceCtx& c = ctx_for(s.dev);
         const uint64_t dim = uint64_t(1) << s.n;
         std::map<uint64_t, std::vector<int>> groups;
@@ -999,7 +1020,7 @@ nq_status nq_dm_expectation_batch(nq_dm* h, const uint64_t* flip, const uint64_t
 nq_status nq_dm_probabilities(nq_dm* h, double* host_out) {
     return guard([&] {
         State& s = st(h);
-        state_flush(s);
+        state_flush_normal(s);
         DeviceCtx& c = ctx_for(s.dev);
         const uint64_t dim = uint64_t(1) << s.n;
         c.ensure_scratch(scratch_doubles_needed(dim) + 64);
@@ -1016,7 +1037,7 @@ nq_status nq_dm_probabilities(nq_dm* h, double* host_out) {
 nq_status nq_dm_get_entries(nq_dm* h, uint64_t offset, uint64_t count, double* host_out) {
     return guard([&] {
         State& s = st(h);
-        state_flush(s);
+        state_flush_normal(s);
         if (offset > s.count || count > s.count - offset)
             throw NqError{NQ_ERR_CONTRACT, "entry range out of bounds"};
         if (count == 0) return;
@@ -1030,7 +1051,7 @@ nq_status nq_dm_get_entries(nq_dm* h, uint64_t offset, uint64_t count, double* h
 nq_status nq_dm_set_entries(nq_dm* h, uint64_t offset, uint64_t count, const double* host_in) {
     return guard([&] {
         State& s = st(h);
-        state_flush(s);
+        state_flush_normal(s);
         if (offset > s.count || count > s.count - offset)
             throw NqError{NQ_ERR_CONTRACT, "entry range out of bounds"};
         if (count == 0) return;

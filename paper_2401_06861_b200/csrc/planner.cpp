@@ -827,7 +827,9 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
     // layout: logical <-> physical bit (identity unless relabelling)
     std::vector<int> l2p(size_t(opt.nbits)), p2l(size_t(opt.nbits));
     for (int b = 0; b < opt.nbits; ++b) l2p[size_t(b)] = b;
-    if (relabel) l2p = *map;
+    // a given layout is used even when it stays fixed (density matrices keep
+    // an interleaved layout: qubit q's column and row bits side by side)
+    if (map && int(map->size()) == opt.nbits) l2p = *map;
     for (int b = 0; b < opt.nbits; ++b) p2l[size_t(l2p[size_t(b)])] = b;
     // logical bits held by the lb low (contiguous) physical bits
     auto low_of = [&] {
@@ -1015,7 +1017,7 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
             if ((qmask >> b) & 1) q.push_back(b);
         std::sort(q.begin(), q.end(), [&](int x, int y) { return l2p[size_t(x)] < l2p[size_t(y)]; });
         if (int(q.size()) != m) throw std::logic_error("planner: tile size mismatch");
-        PlannedPass p = pb.finish(q, relabel ? &l2p : nullptr);
+        PlannedPass p = pb.finish(q, &l2p);
         if (p.ops.size() > 1) {
             for (size_t i = 0; i < q.size(); ++i) p.q[i] = l2p[size_t(q[i])];
             if (restore) {
