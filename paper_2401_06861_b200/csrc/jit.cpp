@@ -222,16 +222,37 @@ const JitKnobs& jit_knobs() {
 // nonzero entries are multiplied, and entries with an exact zero imaginary
 // part use real-times-complex products.  Values stay in the shared pool, so the
 // kernel is reused for every matrix with the same zero / real pattern.
+// Dense k <= 2 operator generated entry by entry with compile-time entry
+// classes: zero (skipped), real, pure imaginary (2 FP64 per product, like
+// real: U (x) conj(U) of RX and its products with damping / dephasing
+// superoperators are of this kind), or complex.  Values stay in the shared
+// pool, so the kernel is reused for every matrix with the same pattern.
+// Few nonzeros are hoisted into registers; otherwise each use reloads its
+// entry from shared memory (as the d2 template does) to spare registers.
 std::string sparse_dense(const MOp& op, const cplx* u, int E, const std::string& P) {
     const int d = 1 << op.k;
+    enum Cls { Z, R, I, C };
+    auto cls = [&](int e) {
+        const cplx v = u[e];
+        if (v == cplx(0.0, 0.0)) return Z;
+        if (v.imag() == 0.0) return R;
+        if (v.real() == 0.0) return I;
+        return C;
+    };
+    int nnz = 0;
+    for (int e = 0; e < d * d; ++e) nnz += cls(e) != Z;
+    const bool hoist = nnz <= 8;
+    auto load = [&](int e) {
+        std::ostringstream o;
+        o << "lds(" << P << " + " << e << ")" << (cls(e) == R ? ".x" : cls(e) == I ? ".y" : "");
+        return o.str();
+    };
     std::ostringstream s;
     s << "    {\n";
-    for (int r = 0; r < d; ++r)
-        for (int c = 0; c < d; ++c) {
-            const cplx v = u[r * d + c];
-            if (v == cplx(0.0, 0.0)) continue;
-            s << "      const " << (v.imag() == 0.0 ? "double" : "double2") << " u" << r << "_" << c << " = lds(" << P
-              << " + " << (r * d + c) << ")" << (v.imag() == 0.0 ? ".x" : "") << ";\n";
+    if (hoist)
+        for (int e = 0; e < d * d; ++e) {
+            if (cls(e) == Z) continue;
+            s << "      const " << (cls(e) == C ? "double2" : "double") << " u" << e << " = " << load(e) << ";\n";
         }
     unsigned smask = 0;
     for (int j = 0; j < op.k; ++j) smask |= 1u << op.pos[j];
@@ -250,17 +271,25 @@ std::string sparse_dense(const MOp& op, const cplx* u, int E, const std::string&
             const std::string dst = "a[" + std::to_string(idx(r)) + "]";
             bool first = true;
             for (int c = 0; c < d; ++c) {
-                const cplx v = u[r * d + c];
-                if (v == cplx(0.0, 0.0)) continue;
-                const std::string un = "u" + std::to_string(r) + "_" + std::to_string(c);
+                const int e = r * d + c;
+                const Cls k = cls(e);
+                if (k == Z) continue;
+                const std::string un = hoist ? "u" + std::to_string(e) : "(" + load(e) + ")";
                 const std::string xn = "x" + std::to_string(c);
-                const bool re = v.imag() == 0.0;
                 s << "        ";
-                if (first && re) s << dst << " = make_double2(" << un << " * " << xn << ".x, " << un << " * " << xn << ".y);\n";
-                else if (first) s << dst << " = cmul(" << un << ", " << xn << ");\n";
-                else if (re) s << dst << ".x = fma(" << un << ", " << xn << ".x, " << dst << ".x); " << dst << ".y = fma("
-                               << un << ", " << xn << ".y, " << dst << ".y);\n";
-                else s << dst << " = cfma(" << un << ", " << xn << ", " << dst << ");\n";
+                if (k == R) {
+                    if (first) s << dst << " = make_double2(" << un << " * " << xn << ".x, " << un << " * " << xn << ".y);\n";
+                    else s << dst << ".x = fma(" << un << ", " << xn << ".x, " << dst << ".x); " << dst << ".y = fma(" << un
+                           << ", " << xn << ".y, " << dst << ".y);\n";
+                } else if (k == I) {
+                    // (i w) x = (-w x.y, w x.x)
+                    if (first) s << dst << " = make_double2(-(" << un << " * " << xn << ".y), " << un << " * " << xn << ".x);\n";
+                    else s << dst << ".x = fma(-" << un << ", " << xn << ".y, " << dst << ".x); " << dst << ".y = fma(" << un
+                           << ", " << xn << ".x, " << dst << ".y);\n";
+                } else {
+                    if (first) s << dst << " = cmul(" << un << ", " << xn << ");\n";
+                    else s << dst << " = cfma(" << un << ", " << xn << ", " << dst << ");\n";
+                }
                 first = false;
             }
             if (first) s << "        " << dst << " = make_double2(0.0, 0.0);\n";
@@ -428,14 +457,15 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
         }
         case MOP_DENSE: {
             bool real = true;
-            size_t nnz = 0;
+            size_t generic = 0;  // entries that are neither zero, real nor pure imaginary
             const size_t nent = size_t(1) << (2 * op.k);
             for (size_t i = 0; i < nent; ++i) {
-                real = real && pool[op.mat + i].imag() == 0.0;
-                nnz += pool[op.mat + i] != cplx(0.0, 0.0);
+                const cplx v = pool[op.mat + i];
+                real = real && v.imag() == 0.0;
+                generic += v.real() != 0.0 && v.imag() != 0.0;
             }
             const char* R = real ? ", true" : "";
-            if (op.k <= 2 && nnz < nent) {
+            if (op.k <= 2 && !real && generic < nent) {
                 s << sparse_dense(op, pool + op.mat, E, P);
             } else if (op.k == 1) {
                 s << "    d1<" << E << ", " << int(op.pos[0]) << R << ">(a, " << P << ");\n";

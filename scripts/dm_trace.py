@@ -17,3 +17,4 @@ for name, qs, ps in workloads.tfim_trotter(nd, 1.0, steps=steps):
 print(naqs.density_expectation(circ, "Z" + "I" * (nd - 1), model))
 abi.jit_wait()  # second run uses the specialised pass kernels
 print(naqs.density_expectation(circ, "Z" + "I" * (nd - 1), model))
+print("jit", abi.jit_stats())
