@@ -63,7 +63,14 @@ struct PassHdr {
     int8_t rest[56];    // non-tile state bits, ascending
     int8_t qst[16];     // tile bit i is stored to state bit qst[i] (a permutation of q:
                         // the pass relabels qubits among its tile bits for free)
+    int32_t flags;      // PASS_MIRROR: Hermitian pass (density matrix, interleaved layout)
+    int32_t pad_[3];
 };
+// The pass maps Hermitian matrices to Hermitian matrices and its tile and rest
+// bits pair up as physical bits (2q, 2q+1) = (column, row) of qubit q: only
+// tiles whose rest index r <= mirror(r) are read, and each is also stored,
+// conjugated and transposed, as its mirror tile.
+constexpr int32_t PASS_MIRROR = 1;
 static_assert(sizeof(PassHdr) % 16 == 0, "PassHdr alignment");
 
 // ---- elementary ops (planner input) ----------------------------------------
@@ -83,6 +90,7 @@ struct EOp {
     uint64_t ctrl = 0;
     std::vector<cplx> mat;  // DENSE: 4^k, DIAG: 2^k, DEPOL: 2
     int64_t src = 1;        // source (reference) ops this elementary op accounts for
+    bool pair_next = false; // DM: the row copy of a permutation; its column copy follows
 };
 
 struct PlanOptions {
@@ -100,11 +108,16 @@ struct PlanOptions {
     // Reorder commuting micro-ops to reduce register-layout switches (state
     // vectors; measured slower on the Liouville programs of density matrices).
     bool stage_sched = true;
+    // Density matrices in the interleaved layout: n qubits, logical column bit
+    // q pairs with row bit q + n; tiles are kept closed under that pairing and
+    // passes that apply whole superoperators are flagged PASS_MIRROR.
+    int dm_mirror_n = 0;
 };
 
 struct PlannedPass {
     std::vector<int> q;     // tile bits (physical, ascending) at load
     std::vector<int> qst;   // physical store bit of tile bit i (empty: same as q)
+    int32_t flags = 0;
     std::vector<MOp> ops;
     std::vector<cplx> pool;
 };

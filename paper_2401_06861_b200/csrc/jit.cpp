@@ -209,6 +209,12 @@ std::string swz_expr(const std::string& x, const Swizzle& sw) {
 
 }  // namespace
 
+// NQ_DIAG_SKIP=1: runtime test of each hoisted diagonal factor (A/B).
+bool diag_runtime_skip() {
+    static const bool on = env_int("NQ_DIAG_SKIP", 0) != 0;
+    return on;
+}
+
 const JitKnobs& jit_knobs() {
     // Measured on B200 (random circuit, n = 30): direct loads with a 128-register
     // cap (512 threads / SM) beat the cp.async double buffer, whose extra 32-64 KB
@@ -310,6 +316,27 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     std::vector<int> q(h.q, h.q + m), rest(h.rest, h.rest + h.nrest);
     std::vector<int> qst(h.qst, h.qst + m);  // store positions (a permutation of q: relabelled pass)
     const bool relabel = qst != q;
+    // Hermitian (mirror) pass: tile / rest bits pair as physical (2q, 2q+1)
+    const JitKnobs& kn0 = jit_knobs();
+    bool mirror = (h.flags & PASS_MIRROR) && !kn0.prefetch && !relabel;
+    std::vector<int> tpair(size_t(m), -1), rpair(rest.size(), -1);
+    for (int i = 0; i < m && mirror; ++i)
+        for (int j = 0; j < m; ++j)
+            if (q[size_t(j)] == (q[size_t(i)] ^ 1)) tpair[size_t(i)] = j;
+    for (size_t i = 0; i < rest.size() && mirror; ++i)
+        for (size_t j = 0; j < rest.size(); ++j)
+            if (rest[j] == (rest[i] ^ 1)) rpair[i] = int(j);
+    for (int x : tpair) mirror = mirror && x >= 0;
+    for (int x : rpair) mirror = mirror && x >= 0;
+    std::vector<int> qmir(static_cast<size_t>(m));
+    for (int i = 0; i < m && mirror; ++i) qmir[size_t(i)] = qst[size_t(tpair[size_t(i)])];
+    auto mirror_rest_expr = [&](const std::string& r) {
+        std::ostringstream o;
+        o << "0ull";
+        for (size_t j = 0; j < rest.size(); ++j)
+            o << " | (((" << r << " >> " << j << ") & 1ull) << " << rpair[j] << ")";
+        return o.str();
+    };
 
     std::vector<Layout> lays;
     std::vector<int> lay_of_op(size_t(h.nops), 0);
@@ -388,6 +415,9 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     } else {
         s << "  const unsigned long long toff_st = "
           << state_off("tb" + std::to_string(lays.size() - 1), LN.nonr, qst) << ";\n";
+        if (mirror)
+            s << "  const unsigned long long toff_mir = "
+              << state_off("tb" + std::to_string(lays.size() - 1), LN.nonr, qmir) << ";\n";
     }
     // prefetch helper (inline lambda-free: a macro-like block emitted twice)
     auto prefetch = [&](const std::string& rexpr, const std::string& bufname, const std::string& indent) {
@@ -428,8 +458,13 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
         // direct streaming loads into the first register layout; one buffer
         s << "  const unsigned long long toff_ld = " << state_off("tb0", L0.nonr, q) << ";\n"
           << "  __syncthreads();\n"
-          << "  for (long long r = blockIdx.x; r < ntiles; r += gridDim.x) {\n"
-          << "    double2* cur = buf0;\n"
+          << "  for (long long r = blockIdx.x; r < ntiles; r += gridDim.x) {\n";
+        if (mirror) {
+            // Hermitian pass: only canonical tiles (r <= mirror(r)) are read
+            s << "    const long long rstar = (long long)(" << mirror_rest_expr("(unsigned long long)r") << ");\n"
+              << "    if (rstar < r) continue;\n";
+        }
+        s << "    double2* cur = buf0;\n"
           << "    const unsigned long long base = " << deposit_expr("(unsigned long long)r", rest, true) << ";\n"
           << "    const unsigned long long full = rankbase | base;\n"
           << "    (void)full;\n"
@@ -540,6 +575,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
                 // complex multiply per amplitude (exact ones skipped at compile time)
                 std::map<unsigned, int> fidx;
                 std::ostringstream body;
+                std::vector<std::ostringstream> skip_body(16);
                 for (int l = 0; l < E; ++l) {
                     unsigned c = 0;
                     for (int t = 0; t < 4; ++t)
@@ -557,9 +593,18 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
                         s << "      const double2 f" << id << " = lds(D + " << c << "u);\n";
                         it = fidx.find(c);
                     }
+                    skip_body[size_t(it->second)] << "      a[" << l << "] = cmul(f" << it->second << ", a[" << l << "]);\n";
                     body << "      a[" << l << "] = cmul(f" << it->second << ", a[" << l << "]);\n";
                 }
-                s << body.str() << "    }\n";
+                if (diag_runtime_skip()) {
+                    // factors that depend on thread / tile bits are often exactly 1
+                    // for a whole warp: test once per distinct factor
+                    for (size_t f = 0; f < fidx.size(); ++f)
+                        s << "      if (!is_one(f" << f << ")) {\n" << skip_body[f].str() << "      }\n";
+                    s << "    }\n";
+                } else {
+                    s << body.str() << "    }\n";
+                }
             }
             break;
         }
@@ -580,7 +625,18 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     const Layout& LST = extra_relayout ? LS : LN;
     s << "    { double2* dst = st + base + toff_st;\n";
     for (int l = 0; l < E; ++l) s << "      st_stream(dst + " << hex64(reg_off(LST, l, qst)) << ", a[" << l << "]);\n";
-    s << "    }\n"
+    s << "    }\n";
+    if (mirror) {
+        // the mirror tile holds the conjugate transpose: element e of tile r is
+        // conj'd into element e* (column/row bits swapped) of tile mirror(r)
+        s << "    if (rstar != r) {\n"
+          << "      double2* dst = st + (" << deposit_expr("(unsigned long long)rstar", rest, true) << ") + toff_mir;\n";
+        for (int l = 0; l < E; ++l)
+            s << "      st_stream(dst + " << hex64(reg_off(LST, l, qmir)) << ", make_double2(a[" << l << "].x, -a[" << l
+              << "].y));\n";
+        s << "    }\n";
+    }
+    s << ""
       << "    __syncthreads();\n"
       << "  }\n";
     if (kn.prefetch) s << "  cp_async_wait<0>();\n";

@@ -22,11 +22,13 @@ size_t scratch_doubles_needed(uint64_t n);
 int terms_per_launch();
 
 void launch_sumsq(const double2* a, uint64_t n, double* scratch, double* out, cudaStream_t s);
-void launch_trace(const double2* rho, uint64_t dim, double* scratch, double* out, cudaStream_t s);
+// il = 1: the density matrix is in the interleaved layout (column bit q at
+// physical 2q, row bit q at 2q + 1)
+void launch_trace(const double2* rho, uint64_t dim, double* scratch, double* out, cudaStream_t s, int il = 0);
 void launch_expect_sv(const double2* a, int nbits, uint64_t flip, const uint64_t* signs,
                       const int* eps_im, int nt, double* scratch, double* out, cudaStream_t s);
 void launch_expect_dm(const double2* rho, int n, uint64_t flip, const uint64_t* signs, int nt,
-                      double* scratch, double* out, cudaStream_t s);
+                      double* scratch, double* out, cudaStream_t s, int il = 0);
 // Tiled multi-term expectations (expect.cu): every term's flip mask lies in
 // the tile bits q[0..m); sign masks are split into tile and full-index parts.
 constexpr int kMaxExpTerms = 32;
@@ -103,7 +105,7 @@ void launch_swap_peer(double2* mine, double2* peer, int v, uint64_t mval, uint64
                       cudaStream_t s);
 
 void launch_probs(const double2* a, uint64_t n, double* p, cudaStream_t s);
-void launch_dm_probs(const double2* rho, uint64_t dim, double* p, double* scratch, cudaStream_t s);
+void launch_dm_probs(const double2* rho, uint64_t dim, double* p, double* scratch, cudaStream_t s, int il = 0);
 void launch_sum_real(const double* x, uint64_t n, double* scratch, double* out, cudaStream_t s);
 void launch_herm(const double2* rho, uint64_t dim, double* scratch, double* out, cudaStream_t s);
 void launch_kraus_weights(const double2* a, int nbits, const int* qubits, int k, int nk,

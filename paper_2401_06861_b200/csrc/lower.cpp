@@ -228,6 +228,7 @@ void lower_dm_op(const nq_op& op, int n, std::vector<EOp>& out) {
             if ((e.ctrl >> b) & 1) rc |= uint64_t(1) << (b + n);
         row.ctrl = rc;
         e.src = 0;
+        row.pair_next = true;
         out.push_back(row);
         out.push_back(e);
     };

@@ -815,11 +815,22 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
                                      PlanStats* stats, std::vector<int>* map) {
     const std::vector<EOp> ops = opt.fuse ? cancel_perm_sandwiches(ops_in) : ops_in;
     const int nloc = opt.nloc;
-    const int m = std::min(opt.tile_bits, nloc);
+    const int dmn = opt.dm_mirror_n;
+    const bool mirror_mode = dmn > 0 && nloc > opt.tile_bits && map && int(map->size()) == opt.nbits;
+    int m = std::min(opt.tile_bits, nloc);
     // A state no larger than one tile is processed whole: every bit is "low".
     // Otherwise keep >= low_bits contiguous low bits for coalescing, but always
     // leave room for one 4-bit operator among the high tile bits.
     const int lb = (nloc <= opt.tile_bits) ? m : std::max(0, std::min(opt.low_bits, m - kMaxOpK));
+    if (mirror_mode && ((m - lb) & 1)) --m;  // high bits come in (column, row) pairs
+    // logical partner of a density-matrix bit: column q <-> row q + n
+    auto closure = [&](uint64_t mask) {
+        if (!mirror_mode) return mask;
+        uint64_t r = mask;
+        for (int b = 0; b < 2 * dmn; ++b)
+            if ((mask >> b) & 1) r |= bit(b < dmn ? b + dmn : b - dmn);
+        return r;
+    };
     const uint64_t all_mask = (opt.nbits >= 64) ? ~uint64_t(0) : (bit(opt.nbits) - 1);
     const uint64_t loc_mask = (nloc >= 64) ? ~uint64_t(0) : (bit(nloc) - 1);
     const bool relabel = opt.relabel && map && nloc > m && lb > 0 && int(map->size()) == opt.nbits;
@@ -855,6 +866,8 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
         uint64_t qhigh = 0;
         size_t taken = 0;
         std::vector<const EOp*> next;
+        bool open_pair = false;  // took a row permutation, its column copy not yet
+        bool broken_pair = false;
         explicit Trial(bool fuse) : pb(fuse) {}
     };
     // One pass from `ops_list` with low bits `lowm`, the high tile bits optionally pre-seeded.
@@ -879,16 +892,21 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
                 }
                 continue;
             }
-            const uint64_t nh = t.qhigh | (need_mask(*e) & ~lowm);
+            const uint64_t nh = t.qhigh | (closure(need_mask(*e)) & ~lowm);
             const bool fits = popcount64(nh) <= m - lb;
             const bool caps = (t.pb.microops() + 1 <= size_t(opt.max_ops_per_pass)) &&
                               (t.pb.pool() + size_t(pool_cost(*e)) <= size_t(opt.max_pool_per_pass));
-            if (!caps && t.taken > 0) break;  // close the pass; the rest goes to the next one
+            // close the pass; the rest goes to the next one (never between the
+            // row and column copies of a density-matrix permutation)
+            if (!caps && t.taken > 0 && !t.open_pair) break;
             if (fits) {
+                if (t.open_pair && e->pair_next) t.broken_pair = true;
+                t.open_pair = e->pair_next;
                 t.qhigh = nh;
                 t.pb.add(*e);
                 ++t.taken;
             } else {
+                if (t.open_pair) t.broken_pair = true;
                 deferred.push_back(e);
                 blocked |= touched;
                 if ((blocked & all_mask) == all_mask) {
@@ -974,12 +992,20 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
         uint64_t qhigh = t.qhigh;
         size_t taken = t.taken;
         std::vector<const EOp*> next = std::move(t.next);
+        bool pair_ok = !t.open_pair && !t.broken_pair;
         if (taken == 0 && !next.empty()) {
             // every op needs <= kMaxOpK <= m - lb high bits, so the first one always
-            // fits alone; take it to guarantee progress
-            qhigh = need_mask(*next.front()) & ~low_mask;
+            // fits alone; take it to guarantee progress (with its column copy)
+            qhigh = closure(need_mask(*next.front())) & ~low_mask;
+            const bool pair = next.front()->pair_next && next.size() > 1;
             pb.add(*next.front());
             next.erase(next.begin());
+            if (pair) {
+                qhigh |= closure(need_mask(*next.front())) & ~low_mask;
+                pb.add(*next.front());
+                next.erase(next.begin());
+            }
+            pair_ok = true;
         }
         // Tile bit set: low bits, required high bits, then fill.
         uint64_t qmask = low_mask | qhigh;
@@ -1009,6 +1035,8 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
                 if (popcount64(qmask) >= m) break;
                 qmask |= bit(b);
             }
+        } else if (mirror_mode) {
+            for (int b = 0; b < dmn && popcount64(qmask) + 2 <= m; ++b) qmask |= closure(bit(b));
         } else {
             for (int b = 0; b < nloc && popcount64(qmask) < m; ++b) qmask |= bit(b);
         }
@@ -1020,6 +1048,13 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
         PlannedPass p = pb.finish(q, &l2p);
         if (p.ops.size() > 1) {
             for (size_t i = 0; i < q.size(); ++i) p.q[i] = l2p[size_t(q[i])];
+            if (mirror_mode && pair_ok && closure(qmask) == qmask) {
+                // physical pairs (2q, 2q+1) in the tile: mirror-closed by construction
+                bool sym = true;
+                for (int x : q) sym = sym && ((qmask >> (x < dmn ? x + dmn : x - dmn)) & 1);
+                for (int x : q) sym = sym && (l2p[size_t(x < dmn ? x + dmn : x - dmn)] == (l2p[size_t(x)] ^ 1));
+                if (sym) p.flags |= PASS_MIRROR;
+            }
             if (restore) {
                 for (int x : q) {
                     l2p[size_t(x)] = x;
@@ -1150,6 +1185,7 @@ std::vector<unsigned char> serialize_passes(const std::vector<PlannedPass>& pass
             h.q[i] = int8_t(p.q[i]);
             h.qst[i] = int8_t(p.qst.empty() ? p.q[i] : p.qst[i]);
         }
+        h.flags = p.flags;
         int nr = 0;
         uint64_t qm = 0;
         for (int b : p.q) qm |= bit(b);

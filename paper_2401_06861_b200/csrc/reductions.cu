@@ -78,14 +78,29 @@ __global__ void __launch_bounds__(kThreads) k_sumsq(const double2* __restrict__ 
     block_reduce_store<1>(acc, part, 1);
 }
 
-// sum of Re(a[i * stride]) for i < n (DM trace)
-__global__ void __launch_bounds__(kThreads) k_strided_re(const double2* __restrict__ a, uint64_t n,
-                                                        uint64_t stride, uint64_t chunk,
-                                                        double* __restrict__ part) {
+// Index of rho[row, col] in HBM: row-major (vec bits: columns low, rows
+// high), or interleaved (column bit q at 2q, row bit q at 2q + 1; the layout
+// of the Hermitian pass kernels).
+__device__ __forceinline__ uint64_t spread_bits(uint64_t x) {
+    x &= 0xFFFFFFFFull;
+    x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+    x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+    x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    x = (x | (x << 2)) & 0x3333333333333333ull;
+    x = (x | (x << 1)) & 0x5555555555555555ull;
+    return x;
+}
+__device__ __forceinline__ uint64_t dm_index(uint64_t row, uint64_t col, uint64_t dim, int il) {
+    return il ? ((spread_bits(row) << 1) | spread_bits(col)) : row * dim + col;
+}
+
+// sum of Re(rho[i, i]) for i < n (DM trace)
+__global__ void __launch_bounds__(kThreads) k_strided_re(const double2* __restrict__ a, uint64_t n, int il,
+                                                        uint64_t chunk, double* __restrict__ part) {
     const uint64_t lo = uint64_t(blockIdx.x) * chunk;
     const uint64_t hi = min(n, lo + chunk);
     double acc[1] = {0.0};
-    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) acc[0] += a[i * stride].x;
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) acc[0] += a[dm_index(i, i, n, il)].x;
     block_reduce_store<1>(acc, part, 1);
 }
 
@@ -152,7 +167,7 @@ __global__ void __launch_bounds__(kThreads) k_expect(const double2* __restrict__
 }
 
 // DM Pauli expectations: sum_y s(y) rho[y, y^F] (complex), dim = 2^n.
-__global__ void __launch_bounds__(kThreads) k_dm_expect(const double2* __restrict__ rho, uint64_t dim,
+__global__ void __launch_bounds__(kThreads) k_dm_expect(const double2* __restrict__ rho, uint64_t dim, int il,
                                                        uint64_t flip, uint64_t chunk, TermBatch tb,
                                                        double* __restrict__ part) {
     double acc[2 * kTermsPerLaunch];
@@ -161,7 +176,7 @@ __global__ void __launch_bounds__(kThreads) k_dm_expect(const double2* __restric
     const uint64_t lo = uint64_t(blockIdx.x) * chunk;
     const uint64_t hi = min(dim, lo + chunk);
     for (uint64_t y = lo + threadIdx.x; y < hi; y += blockDim.x) {
-        const double2 v = rho[y * dim + (y ^ flip)];
+        const double2 v = rho[dm_index(y, y ^ flip, dim, il)];
 #pragma unroll
         for (int t = 0; t < kTermsPerLaunch; ++t) {
             if (t < tb.nt) {
@@ -183,10 +198,10 @@ __global__ void k_probs(const double2* __restrict__ a, uint64_t n, double* __res
 }
 
 // DM diagonal: max(0, Re rho_ii)
-__global__ void k_dm_diag(const double2* __restrict__ rho, uint64_t dim, double* __restrict__ p) {
+__global__ void k_dm_diag(const double2* __restrict__ rho, uint64_t dim, int il, double* __restrict__ p) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < dim;
          i += uint64_t(gridDim.x) * blockDim.x)
-        p[i] = fmax(0.0, rho[i * dim + i].x);
+        p[i] = fmax(0.0, rho[dm_index(i, i, dim, il)].x);
 }
 
 __global__ void k_sum_real(const double* __restrict__ x, uint64_t n, uint64_t chunk,
@@ -475,11 +490,11 @@ void launch_sumsq(const double2* a, uint64_t n, double* scratch, double* out, cu
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-void launch_trace(const double2* rho, uint64_t dim, double* scratch, double* out, cudaStream_t s) {
+void launch_trace(const double2* rho, uint64_t dim, double* scratch, double* out, cudaStream_t s, int il) {
     uint64_t chunk;
     int nblk;
     reduction_geometry(dim, &chunk, &nblk);
-    k_strided_re<<<nblk, kThreads, 0, s>>>(rho, dim, dim + 1, chunk, scratch);
+    k_strided_re<<<nblk, kThreads, 0, s>>>(rho, dim, il, chunk, scratch);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     k_final<<<1, kThreads, 0, s>>>(scratch, nblk, 1, out);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
@@ -515,7 +530,7 @@ void launch_expect_sv(const double2* a, int nbits, uint64_t flip, const uint64_t
 }
 
 void launch_expect_dm(const double2* rho, int n, uint64_t flip, const uint64_t* signs, int nt,
-                      double* scratch, double* out, cudaStream_t s) {
+                      double* scratch, double* out, cudaStream_t s, int il) {
     TermBatch tb{};
     tb.nt = nt;
     for (int t = 0; t < nt; ++t) tb.signs[t] = signs[t];
@@ -523,7 +538,7 @@ void launch_expect_dm(const double2* rho, int n, uint64_t flip, const uint64_t* 
     uint64_t chunk;
     int nblk;
     reduction_geometry(dim, &chunk, &nblk);
-    k_dm_expect<<<nblk, kThreads, 0, s>>>(rho, dim, flip, chunk, tb, scratch);
+    k_dm_expect<<<nblk, kThreads, 0, s>>>(rho, dim, il, flip, chunk, tb, scratch);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     k_final<<<1, kThreads, 0, s>>>(scratch, nblk, 2 * kTermsPerLaunch, out);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
@@ -534,8 +549,8 @@ void launch_probs(const double2* a, uint64_t n, double* p, cudaStream_t s) {
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-void launch_dm_probs(const double2* rho, uint64_t dim, double* p, double* scratch, cudaStream_t s) {
-    k_dm_diag<<<grid_for(dim), kThreads, 0, s>>>(rho, dim, p);
+void launch_dm_probs(const double2* rho, uint64_t dim, double* p, double* scratch, cudaStream_t s, int il) {
+    k_dm_diag<<<grid_for(dim), kThreads, 0, s>>>(rho, dim, il, p);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     uint64_t chunk;
     int nblk;

@@ -13,11 +13,11 @@ from typing import List
 import numpy as np
 
 MOP_NAMES = {0: "dense", 1: "diag", 2: "xperm", 3: "swap", 4: "depol", 5: "layout"}
-HDR_FMT = "<iiiiqIIII16b56b16b"
+HDR_FMT = "<iiiiqIIII16b56b16biiii"
 HDR_SIZE = struct.calcsize(HDR_FMT)
 MOP_FMT = "<BB8bHII4xQ"
 MOP_SIZE = struct.calcsize(MOP_FMT)
-assert HDR_SIZE == 128 and MOP_SIZE == 32
+assert HDR_SIZE == 144 and MOP_SIZE == 32
 
 
 @dataclass
