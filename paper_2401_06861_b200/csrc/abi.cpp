@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -235,16 +236,71 @@ void trace_passes(const std::vector<PlannedPass>& passes, bool dm) {
 void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStats& st, bool record = true);
 bool layout_is_identity(const State& s);
 
+// Fused-schedule cache: a flush whose queue (kinds, bits, controls,
+// matrices), starting layout and plan options equal a recent flush's reuses
+// its planned passes and final layout (repeated circuits: benchmark steps,
+// sampling loops, re-runs of a parsed circuit).  Keyed by content.
+struct PlanCacheEntry {
+    std::vector<unsigned char> key;
+    std::vector<PlannedPass> passes;
+    PlanStats st;
+    std::vector<int> layout_out;
+};
+
+std::vector<unsigned char> plan_key(const State& s, bool use_layout) {
+    std::vector<unsigned char> k;
+    auto put = [&](const void* p, size_t n) {
+        const unsigned char* b = static_cast<const unsigned char*>(p);
+        k.insert(k.end(), b, b + n);
+    };
+    const PlanOptions& o = s.popt;
+    const int32_t opts[] = {o.nbits, o.nloc, o.tile_bits, o.low_bits, o.fuse, o.reg_bits, o.max_ops_per_pass,
+                            o.max_pool_per_pass, o.relabel, o.stage_sched, o.dm_mirror_n, use_layout};
+    put(opts, sizeof opts);
+    if (use_layout) put(s.layout.data(), s.layout.size() * sizeof(int));
+    for (const EOp& e : s.queue) {
+        const int32_t head[] = {int32_t(e.type), e.k, e.pair_next, int32_t(e.mat.size())};
+        put(head, sizeof head);
+        put(e.bits, size_t(e.k) * sizeof(int));
+        put(&e.ctrl, sizeof e.ctrl);
+        put(&e.src, sizeof e.src);
+        if (!e.mat.empty()) put(e.mat.data(), e.mat.size() * sizeof(cplx));
+    }
+    return k;
+}
+
 void state_flush(State& s) {
     if (s.queue.empty()) return;
     if (s.world > 1) {
         shard_flush(s);
         return;
     }
+    static std::mutex mu;
+    static std::deque<PlanCacheEntry> cache;  // most recent first
+    constexpr size_t kCacheEntries = 8;
     PlanStats st;
     const bool use_layout = int(s.layout.size()) == s.nbits && (s.popt.relabel || !layout_is_identity(s));
+    std::vector<unsigned char> key = plan_key(s, use_layout);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto it = cache.begin(); it != cache.end(); ++it) {
+            if (it->key != key) continue;
+            PlanCacheEntry e = *it;
+            cache.erase(it);
+            cache.push_front(e);
+            if (use_layout) s.layout = e.layout_out;
+            s.queue.clear();
+            run_passes(s, e.passes, e.st);
+            return;
+        }
+    }
     std::vector<PlannedPass> passes = plan_passes(s.queue, s.popt, &st, use_layout ? &s.layout : nullptr);
     s.queue.clear();
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        cache.push_front(PlanCacheEntry{std::move(key), passes, st, s.layout});
+        if (cache.size() > kCacheEntries) cache.pop_back();
+    }
     run_passes(s, passes, st);
 }
 
