@@ -433,7 +433,10 @@ def main():
     args = parse_args()
     world, rank, local, dist = dist_setup(args)
     if args.impl == "reference":
-        return run_reference_arm(args, world, rank)
+        rc = run_reference_arm(args, world, rank)
+        if dist is not None:
+            dist.destroy_process_group()
+        return rc
 
     from paper_2401_06861_b200 import abi, workloads
 

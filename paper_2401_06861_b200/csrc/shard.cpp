@@ -331,6 +331,16 @@ void run_exchange(State& s, DeviceCtx& c, int g, int v) {
 // Relabelling passes permute local physical bits inside a segment; the later
 // actions (scheduled on the pre-relabel bits) are remapped through `perm`,
 // and the composed permutation is folded into the shard's qubit map.
+// NQ_SHARD_RELABEL_RESTORE=0: keep a segment's final relabelling (composed
+// into the qubit map) instead of restoring it inside the segment.
+bool shard_relabel_restore() {
+    static const bool on = [] {
+        const char* e = std::getenv("NQ_SHARD_RELABEL_RESTORE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 EOp remap(const EOp& e, const std::vector<int>& perm) {
     EOp r = e;
     for (int j = 0; j < e.k; ++j) r.bits[j] = perm[size_t(e.bits[j])];
@@ -359,6 +369,31 @@ void execute(State& s, const std::vector<Action>& acts, bool relabel = false) {
             std::vector<int> layout(size_t(s.n));
             for (int b = 0; b < s.n; ++b) layout[size_t(b)] = b;
             run_segment(s, c, ops, &layout);
+            bool ident = true;
+            for (int b = 0; b < s.n; ++b) ident = ident && layout[size_t(b)] == b;
+            if (!ident && shard_relabel_restore()) {
+                // the segment's last pass could not store every qubit home:
+                // restore here, so every flush runs on the scheduled bits
+                std::vector<int> p2l(size_t(s.n));
+                for (int b = 0; b < s.n; ++b) p2l[size_t(layout[size_t(b)])] = b;
+                std::vector<EOp> swaps;
+                for (int pb = 0; pb < s.nloc; ++pb) {
+                    if (p2l[size_t(pb)] == pb) continue;
+                    const int w = layout[size_t(pb)];
+                    EOp e;
+                    e.type = E_SWAP;
+                    e.k = 2;
+                    e.bits[0] = std::min(pb, w);
+                    e.bits[1] = std::max(pb, w);
+                    swaps.push_back(e);
+                    const int lp = p2l[size_t(pb)];
+                    p2l[size_t(w)] = lp;
+                    layout[size_t(lp)] = w;
+                    p2l[size_t(pb)] = pb;
+                    layout[size_t(pb)] = pb;
+                }
+                run_segment(s, c, swaps);
+            }
             for (int b = 0; b < s.n; ++b) {
                 perm[size_t(b)] = layout[size_t(perm[size_t(b)])];
                 moved = moved || perm[size_t(b)] != b;
