@@ -452,7 +452,9 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
           << "    const unsigned long long base = " << deposit_expr("(unsigned long long)r", rest, true) << ";\n"
           << "    const unsigned long long full = rankbase | base;\n"
           << "    (void)full;\n"
-          << "    double2 a[" << E << "];\n";
+          << "    double2 a[" << E << "];\n"
+          << "    double2 ug = make_double2(1.0, 0.0);\n"
+          << "    (void)ug;\n";
         for (int l = 0; l < E; ++l) s << "    a[" << l << "] = cur[sw0 ^ " << sw.apply(L0.rconst(l)) << "u];\n";
     } else {
         // direct streaming loads into the first register layout; one buffer
@@ -469,10 +471,20 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
           << "    const unsigned long long full = rankbase | base;\n"
           << "    (void)full;\n"
           << "    double2 a[" << E << "];\n"
+          << "    double2 ug = make_double2(1.0, 0.0);\n"
+          << "    (void)ug;\n"
           << "    { const double2* src = st + base + toff_ld;\n";
         for (int l = 0; l < E; ++l) s << "      a[" << l << "] = ld_stream(src + " << hex64(reg_off(L0, l, q)) << ");\n";
         s << "    }\n";
     }
+    bool ug_pending = false;
+    auto flush_ug = [&] {
+        if (!ug_pending) return;
+        s << "    if (!is_one(ug)) {\n";
+        for (int l = 0; l < E; ++l) s << "      a[" << l << "] = cmul(ug, a[" << l << "]);\n";
+        s << "    }\n";
+        ug_pending = false;
+    };
     for (int i = 1; i < h.nops; ++i) {
         const MOp& op = ops[i];
         const int li = lay_of_op[size_t(i)];
@@ -482,6 +494,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
         switch (op.type) {
         case MOP_LAYOUT: {
             const Layout& A = lays[size_t(li - 1)];
+            flush_ug();
             s << "    __syncthreads();\n";
             for (int l = 0; l < E; ++l)
                 s << "    cur[sw" << (li - 1) << " ^ " << sw.apply(A.rconst(l)) << "u] = a[" << l << "];\n";
@@ -566,9 +579,11 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
             const cplx* tab = pool + op.mat;
             s << "    { const unsigned g = " << g.str() << "; const double2* D = " << P << " + g;\n";
             if (!anyreg) {
-                s << "      const double2 f = lds(D); if (!is_one(f)) {\n";
-                for (int l = 0; l < E; ++l) s << "      a[" << l << "] = cmul(f, a[" << l << "]);\n";
-                s << "      } }\n";
+                // a factor uniform over the thread's amplitudes: accumulate it and
+                // apply the product once (scalars commute with every in-thread op)
+                if (ug_pending) s << "      ug = cmul(ug, lds(D)); }\n";
+                else s << "      ug = lds(D); }\n";
+                ug_pending = true;
             } else {
                 const unsigned regmask = slotc[0] | slotc[1] | slotc[2] | slotc[3];
                 // one shared-memory load per distinct table entry, then a plain
@@ -612,6 +627,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
             break;
         }
     }
+    flush_ug();
     if (extra_relayout) {
         // (the barrier also orders every load of the tile before any store:
         // relabelled stores hit addresses other threads load)
