@@ -465,9 +465,25 @@ def main():
     clk = ClockSampler(dev).__enter__()
     # warm-up: the first step plans the passes and queues their specialised
     # kernels for compilation (jit.cpp); wait for them, then warm the rest
-    for _ in range(max(args.warmup, 3)):
+    # Warm-up: at least W steps, continued (up to 16) while steps still meet
+    # pass structures that had to be compiled -- a sharded state carries its
+    # qubit map from step to step and settles into a short cycle of layouts.
+    # All ranks take the same decision (the flushes are collective).
+    warm = 0
+    while True:
+        before = abi.jit_stats()["compiled"]
         sv.apply(ops).flush()
-        abi.jit_wait()  # sharded: the carried qubit map settles within a few steps
+        abi.jit_wait()
+        warm += 1
+        fresh = abi.jit_stats()["compiled"] > before
+        if dist is not None:
+            import torch
+
+            flag = torch.tensor([1.0 if fresh else 0.0], device=f"cuda:{local}")
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            fresh = flag.item() > 0
+        if warm >= max(args.warmup, 3) and (not fresh or warm >= 16):
+            break
     sv.synchronize()
     jit = abi.jit_stats()
     stats = sv.stats()
@@ -541,6 +557,7 @@ def main():
                        "parallelism": "single" if world == 1 else
                        f"sharded x{world}: {g} global qubits, NCCL half-shard exchanges",
                        "local_qubits": n_local,
+                       "warmup_steps_run": warm,
                        "unit_note": (f"gates/s of {n_local}-qubit gate equivalents: each gate on the {n}-qubit "
                                      f"state counts {world} (2^{g}); whole-job aggregate over {world} GPU(s)"),
                        "comm": sv.comm_stats() if world > 1 else None,

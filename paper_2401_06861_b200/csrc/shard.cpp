@@ -108,6 +108,7 @@ NcclApi& nccl() {
 
 struct ShardComm {
     ncclComm_t comm = nullptr;
+    std::vector<EOp> prev_ops;  // the previous flush (logical), for repeat prediction
     // peer-memory exchange: every rank's state mapped into this process (CUDA
     // IPC over NVLink); empty when unavailable or NQ_EXCHANGE=nccl
     std::vector<double2*> peer;
@@ -193,9 +194,33 @@ int choose_victim(const std::vector<EOp>& ops, size_t from, const std::vector<in
 
 }  // namespace
 
+// NQ_SHARD_CYCLIC=1 enables the repeat prediction of schedule().  Off by
+// default: on the random-circuit benchmark it cut exchanges but made the
+// carried qubit map cycle through many layouts (uncompiled pass structures):
+// N = 4 with 33 local qubits 661 -> 1012, but with 30 local 9050 -> 4779.
+bool shard_cyclic_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("NQ_SHARD_CYCLIC");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 // Split a queue (logical bits) into segments of local work and exchanges,
 // updating the qubit map as the exchanges will.
-std::vector<Action> schedule(const std::vector<EOp>& ops, std::vector<int>& l2p, std::vector<int>& p2l, int nloc) {
+std::vector<Action> schedule(const std::vector<EOp>& ops, std::vector<int>& l2p, std::vector<int>& p2l, int nloc,
+                             bool repeat) {
+    // A flush that repeats the previous one (same op structure: iterative
+    // workloads, benchmark steps) is predicted to be followed by itself: the
+    // victims' next uses are looked up in this flush's remainder and then in
+    // the predicted next flush, so a qubit needed at the start of the next
+    // repetition is not evicted at the end of this one.
+    std::vector<EOp> ext;
+    if (repeat) {
+        ext = ops;
+        ext.insert(ext.end(), ops.begin(), ops.end());
+    }
+    const std::vector<EOp>& future = repeat ? ext : ops;
     std::vector<Action> acts;
     Action seg{Action::Segment, {}, 0, 0};
     const uint64_t loc_mask = (uint64_t(1) << nloc) - 1;
@@ -209,7 +234,7 @@ std::vector<Action> schedule(const std::vector<EOp>& ops, std::vector<int>& l2p,
             while (glob) {
                 const int g = __builtin_ctzll(glob);
                 glob &= glob - 1;
-                const int v = choose_victim(ops, i + 1, p2l, nloc, protect);
+                const int v = choose_victim(future, i + 1, p2l, nloc, protect);
                 acts.push_back(Action{Action::Exchange, {}, g, v});
                 swap_map(l2p, p2l, g, v);
             }
@@ -503,7 +528,14 @@ void shard_flush(State& s) {
     std::vector<EOp> ops;
     ops.swap(s.queue);
     s.last_passes = s.last_microops = s.last_source_ops = s.last_launches = 0;
-    std::vector<Action> acts = schedule(ops, sc.l2p, sc.p2l, s.nloc);
+    bool repeat = ops.size() == sc.prev_ops.size();
+    for (size_t i = 0; i < ops.size() && repeat; ++i) {
+        const EOp &a = ops[i], &b = sc.prev_ops[i];
+        repeat = a.type == b.type && a.k == b.k && a.ctrl == b.ctrl &&
+                 std::equal(a.bits, a.bits + a.k, b.bits);
+    }
+    std::vector<Action> acts = schedule(ops, sc.l2p, sc.p2l, s.nloc, repeat && shard_cyclic_enabled());
+    sc.prev_ops = ops;
     // The qubit map is carried into the next flush (readouts normalise it
     // first).  Re-running one circuit then converges to a map whose global
     // qubits that circuit never needs as targets: after a step or two the
@@ -787,7 +819,7 @@ nq_status nq_shard_debug(int n, int world, const nq_op* ops, int64_t count, int6
         const size_t nn = static_cast<size_t>(n);
         std::vector<int> l2p(nn), p2l(nn);
         for (int i = 0; i < n; ++i) l2p[size_t(i)] = p2l[size_t(i)] = i;
-        auto acts = schedule(q, l2p, p2l, n - g);
+        auto acts = schedule(q, l2p, p2l, n - g, false);
         auto fin = schedule_identity(l2p, p2l, n - g, n);
         acts.insert(acts.end(), fin.begin(), fin.end());
         std::vector<int64_t> out;
