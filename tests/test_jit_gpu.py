@@ -23,7 +23,7 @@ SCRIPT = textwrap.dedent(
     from paper_2401_06861_b200 import abi, naqs
     port = Port()
     worst = 0.0
-    for n, tile, seed in [(12, 8, 1), (14, 10, 2), (16, 12, 3), (18, 12, 4), (17, 9, 5), (20, 13, 6)]:
+    for n, tile, seed in [(12, 8, 1), (14, 10, 2), (16, 12, 3), (18, 12, 4), (17, 9, 5), (20, 13, 6), (22, 11, 7)]:
         ops = port.random_circuit(seed, n, 250)
         sv = abi.SV(n, tile_qubits=tile)
         sv.apply(ops)
@@ -33,8 +33,9 @@ SCRIPT = textwrap.dedent(
         sv.reset()
         sv.apply(ops)
         assert np.array_equal(sv.amplitudes(), got)
-    # density matrix with noise (Liouville superoperators, depolarizing maps)
-    for n in (5, 6):
+    # density matrix with noise (Liouville superoperators, depolarizing maps);
+    # n >= 6 runs the Hermitian (mirror) passes on the interleaved layout
+    for n in (5, 6, 8, 9):
         c = port.random_circuit(100 + n, n, 60, 2)
         circ = naqs.Circuit(n)
         for k, q, p in ops_to_list(c):
