@@ -219,7 +219,7 @@ const JitKnobs& jit_knobs() {
     // Measured on B200 (random circuit, n = 30): direct loads with a 128-register
     // cap (512 threads / SM) beat the cp.async double buffer, whose extra 32-64 KB
     // of shared memory halves the resident CTAs.  -1 = auto (512 / threads).
-    static const JitKnobs k{env_int("NQ_JIT_PREFETCH", 0) != 0, env_int("NQ_JIT_MINB", -1)};
+    static const JitKnobs k{env_int("NQ_JIT_PREFETCH", 0) != 0, env_int("NQ_JIT_MINB", -1), env_int("NQ_JIT_TMA", 0) != 0};
     return k;
 }
 
@@ -330,6 +330,9 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     for (int x : rpair) mirror = mirror && x >= 0;
     std::vector<int> qmir(static_cast<size_t>(m));
     for (int i = 0; i < m && mirror; ++i) qmir[size_t(i)] = qst[size_t(tpair[size_t(i)])];
+    // bulk-copy staging needs the 16 contiguous low amplitudes as tile bits 0-3
+    bool use_tma = kn0.tma && !kn0.prefetch && !mirror && m >= 8;
+    for (int b = 0; b < 4 && use_tma; ++b) use_tma = q[size_t(b)] == b;
     auto mirror_rest_expr = [&](const std::string& r) {
         std::ostringstream o;
         o << "0ull";
@@ -391,7 +394,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
       << "  using namespace nq;\n"
       << "  extern __shared__ __align__(16) unsigned char smem[];\n"
       << "  double2* buf0 = reinterpret_cast<double2*>(smem);\n"
-      << "  double2* buf1 = buf0 + " << (kn.prefetch ? SIZE : 0) << ";\n"
+      << "  double2* buf1 = buf0 + " << ((kn.prefetch || use_tma) ? SIZE : 0) << ";\n"
       << "  double2* pool = buf1 + " << SIZE << ";\n"
       << "  const unsigned tid = threadIdx.x;\n"
       << "  for (unsigned i = tid; i < " << h.pool_n << "u; i += " << T << "u) pool[i] = gpool[i];\n";
@@ -433,7 +436,47 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
         }
         s << indent << "}\n";
     };
-    if (kn.prefetch) {
+    if (use_tma) {
+        // warp 0 stages the next tile with bulk copies of 256-byte chunks (the
+        // 16 contiguous low amplitudes) onto an mbarrier while every warp
+        // computes the current one
+        const int nch = SIZE / 16;
+        std::vector<int> qhi(q.begin() + 4, q.end());
+        s << "  __shared__ __align__(8) unsigned long long mbar[2];\n"
+          << "  if (tid == 0) { mbar_init(&mbar[0], 1); mbar_init(&mbar[1], 1); mbar_fence_init(); }\n"
+          << "  __syncthreads();\n";
+        auto issue = [&](const std::string& rexpr, const std::string& bufname, const std::string& bar,
+                         const std::string& ind) {
+            s << ind << "if (tid < 32u) {\n"
+              << ind << "  const double2* src = st + (" << deposit_expr("(unsigned long long)(" + rexpr + ")", rest, true)
+              << ");\n"
+              << ind << "  if (tid == 0) mbar_expect_tx(" << bar << ", " << SIZE * 16 << "u);\n"
+              << ind << "  for (unsigned c = tid; c < " << nch << "u; c += 32u)\n"
+              << ind << "    bulk_g2s(" << bufname << " + c * 16u, src + (" << deposit_expr("(unsigned long long)c", qhi, true)
+              << "), 256u, " << bar << ");\n"
+              << ind << "}\n";
+        };
+        s << "  long long r = blockIdx.x;\n"
+          << "  if (r < ntiles) {\n";
+        issue("r", "buf0", "&mbar[0]", "    ");
+        s << "  }\n"
+          << "  for (int it = 0; r < ntiles; r += gridDim.x, ++it) {\n"
+          << "    double2* cur = (it & 1) ? buf1 : buf0;\n"
+          << "    double2* nxt = (it & 1) ? buf0 : buf1;\n"
+          << "    const long long rn = r + gridDim.x;\n"
+          << "    if (rn < ntiles) {\n"
+          << "      fence_proxy_async();\n";
+        issue("rn", "nxt", "&mbar[(it + 1) & 1]", "      ");
+        s << "    }\n"
+          << "    mbar_wait(&mbar[it & 1], (unsigned)(it >> 1) & 1u);\n"
+          << "    const unsigned long long base = " << deposit_expr("(unsigned long long)r", rest, true) << ";\n"
+          << "    const unsigned long long full = rankbase | base;\n"
+          << "    (void)full;\n"
+          << "    double2 a[" << E << "];\n"
+          << "    double2 ug = make_double2(1.0, 0.0);\n"
+          << "    (void)ug;\n";
+        for (int l = 0; l < E; ++l) s << "    a[" << l << "] = cur[tb0 | " << L0.rconst(l) << "u];\n";
+    } else if (kn.prefetch) {
         s << "  long long r = blockIdx.x;\n"
           << "  if (r < ntiles) {\n";
         prefetch("r", "buf0", "    ");
@@ -862,7 +905,7 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
     if (!e) return false;
     Jit& J = jit();
     const int T = (1 << h.m) / (1 << ops[0].k);
-    const size_t smem = (size_t(jit_knobs().prefetch ? 2 : 1) << h.m) * 16 + size_t(h.pool_n) * 16;
+    const size_t smem = (size_t((jit_knobs().prefetch || jit_knobs().tma) ? 2 : 1) << h.m) * 16 + size_t(h.pool_n) * 16;
     const int occ = occupancy(*e, device, T, smem);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);

@@ -29,6 +29,7 @@ JitMode jit_mode();
 struct JitKnobs {
     bool prefetch;
     int min_blocks;
+    bool tma;  // NQ_JIT_TMA=1: next tile staged by bulk (TMA) copies on an mbarrier
 };
 const JitKnobs& jit_knobs();
 
