@@ -304,6 +304,20 @@ def secondary_workloads(abi, workloads, device):
     t0 = time.perf_counter()
     z = naqs.density_expectation(circ, "Z" + "I" * (nd - 1), model)
     dt = time.perf_counter() - t0
+    # C4 upper end: n = 16 (4^16 entries = 69 GB; beyond the reference's
+    # 14-qubit guard, so GPU only)
+    nd16 = 16
+    cal16 = dict(cal, qubits=cal["qubits"][:1] * nd16)
+    model16 = naqs.load_calibration(json.dumps(cal16))
+    circ16 = naqs.Circuit(nd16)
+    for name, qs, ps in workloads.tfim_trotter(nd16, 1.0, steps=10):
+        circ16.add(name, qs, ps)
+    naqs.density_expectation(circ16, "Z" + "I" * (nd16 - 1), model16, max_qubits=16)
+    abi.jit_wait()
+    t0 = time.perf_counter()
+    z16 = naqs.density_expectation(circ16, "Z" + "I" * (nd16 - 1), model16, max_qubits=16)
+    out["dm_noisy_tfim16"] = {"wall_s": time.perf_counter() - t0, "z0": z16, "cpu": None,
+                              "note": "beyond the reference's 14-qubit guard: no CPU baseline"}
     dm_cpu = dm_cpu_sample(workloads, nd)
     out["dm_noisy_tfim14"] = {"wall_s": dt, "cpu": dm_cpu,
                               "items": len(circ) * 3 + sum(1 for o in circ.ops() if len(o[1]) == 2),
