@@ -27,6 +27,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -288,6 +289,8 @@ void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vecto
     po.relabel = layout != nullptr;
     PlanStats st;
     std::vector<PlannedPass> passes = plan_passes(ops, po, &st, layout);
+    if (s.rank == 0 && std::getenv("NQ_SHARD_TRACE"))
+        std::fprintf(stderr, "[shard] segment: %zu ops -> %lld passes\n", ops.size(), (long long)st.passes);
     std::vector<size_t> offs;
     std::vector<unsigned char> buf = serialize_passes(passes, s.nloc, &offs);
     s.last_passes += st.passes;
@@ -322,6 +325,7 @@ void stream_barrier(ShardComm& sc, DeviceCtx& c) {
 
 void run_exchange(State& s, DeviceCtx& c, int g, int v) {
     ShardComm& sc = *s.comm;
+    if (s.rank == 0 && std::getenv("NQ_SHARD_TRACE")) std::fprintf(stderr, "[shard] exchange g=%d v=%d\n", g, v);
     const int j = g - s.nloc;
     const int partner = s.rank ^ (1 << j);
     const uint64_t mybit = uint64_t((s.rank >> j) & 1);
