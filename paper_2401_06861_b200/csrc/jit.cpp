@@ -318,7 +318,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     const bool relabel = qst != q;
     // Hermitian (mirror) pass: tile / rest bits pair as physical (2q, 2q+1)
     const JitKnobs& kn0 = jit_knobs();
-    bool mirror = (h.flags & PASS_MIRROR) && !kn0.prefetch && !relabel;
+    bool mirror = (h.flags & PASS_MIRROR) && !kn0.prefetch;
     std::vector<int> tpair(size_t(m), -1), rpair(rest.size(), -1);
     for (int i = 0; i < m && mirror; ++i)
         for (int j = 0; j < m; ++j)
@@ -359,6 +359,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     };
     if (relabel && lays.size() >= 2) lays.back() = by_store(lays.back());
     const bool extra_relayout = relabel && lays.size() == 1;
+    if (extra_relayout) mirror = false;  // (full tiles then; the mirror store path expects the last layout)
     const Layout LS = by_store(lays.back());
     std::vector<Layout> sw_lays = lays;
     if (extra_relayout) sw_lays.push_back(LS);

@@ -25,6 +25,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <functional>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -931,7 +932,7 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
                 if ((blocked & all_mask) == all_mask) break;
                 continue;
             }
-            const uint64_t nh = qh | (need_mask(*e) & ~lowm);
+            const uint64_t nh = qh | (closure(need_mask(*e)) & ~lowm);
             if (popcount64(nh) <= m - lb) {
                 qh = nh;
                 ++taken;
@@ -978,6 +979,104 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
         }
         return nu;
     };
+    // home physical bit of a logical bit: identity for state vectors, the
+    // interleaved (column 2q, row 2q + 1) position for density matrices
+    auto home = [&](int b) { return mirror_mode ? (b < dmn ? 2 * b : 2 * (b - dmn) + 1) : b; };
+    // Relabelling for density matrices works on whole qubits: the low physical
+    // bit pairs hold a per-pass choice of qubits (column bit even, row bit
+    // odd, as the Hermitian passes need), chosen to maximise the next pass;
+    // guests leave the low pairs only to go home.
+    auto relabel_pairs = [&](const std::vector<int>& q, const std::vector<const EOp*>& next) {
+        const int lq = lb / 2;  // low qubit slots
+        const std::vector<const EOp*> window(next.begin(), next.begin() + long(std::min<size_t>(next.size(), 128)));
+        std::vector<int> units;  // tile qubits
+        for (int x : q)
+            if (x < dmn) units.push_back(x);
+        std::vector<int> tile_pairs;
+        for (int u : units) tile_pairs.push_back(l2p[size_t(u)] >> 1);
+        auto in_tile = [&](int pr) { return std::find(tile_pairs.begin(), tile_pairs.end(), pr) != tile_pairs.end(); };
+        std::vector<int> forced;
+        for (int pr = 0; pr < lq; ++pr) {
+            const int u = p2l[size_t(2 * pr)];
+            if (u >= lq && !in_tile(u)) forced.push_back(u);  // a guest whose home pair is not here
+        }
+        auto lowmask_of = [&](const std::vector<int>& qs) {
+            uint64_t mk = 0;
+            for (int u : qs) mk |= closure(bit(u));
+            return mk;
+        };
+        std::vector<int> best = forced;
+        size_t best_taken = 0;
+        bool have = false;
+        // exhaustive over the free low slots (at most a few tile qubits)
+        std::vector<int> free_units;
+        for (int u : units)
+            if (std::find(forced.begin(), forced.end(), u) == forced.end()) free_units.push_back(u);
+        // current low qubits first: ties keep them (fewer moves)
+        std::stable_sort(free_units.begin(), free_units.end(),
+                         [&](int a, int b) { return (l2p[size_t(a)] >> 1) < lq && (l2p[size_t(b)] >> 1) >= lq; });
+        const int need = lq - int(forced.size());
+        std::vector<int> pick;
+        std::function<void(size_t)> rec = [&](size_t from) {
+            if (int(pick.size()) == need) {
+                std::vector<int> trial = forced;
+                trial.insert(trial.end(), pick.begin(), pick.end());
+                const size_t tk = count_taken(window, lowmask_of(trial));
+                if (!have || tk > best_taken) {
+                    best = trial;
+                    best_taken = tk;
+                    have = true;
+                }
+                return;
+            }
+            for (size_t i = from; i < free_units.size(); ++i) {
+                pick.push_back(free_units[i]);
+                rec(i + 1);
+                pick.pop_back();
+            }
+        };
+        if (need > 0) rec(0);
+        // placement on physical pairs of this tile
+        std::vector<int> newpair(size_t(dmn), -1);
+        std::vector<char> used(size_t(nloc / 2 + 1), 0);
+        auto place = [&](int u, int pr) {
+            newpair[size_t(u)] = pr;
+            used[size_t(pr)] = 1;
+        };
+        auto chosen = [&](int u) { return std::find(best.begin(), best.end(), u) != best.end(); };
+        for (int u : units)
+            if (chosen(u) && u < lq) place(u, u);
+        for (int u : units) {
+            const int cur = l2p[size_t(u)] >> 1;
+            if (chosen(u) && newpair[size_t(u)] < 0 && cur < lq && !used[size_t(cur)]) place(u, cur);
+        }
+        for (int u : units) {
+            if (!chosen(u) || newpair[size_t(u)] >= 0) continue;
+            for (int pr = 0; pr < lq; ++pr)
+                if (!used[size_t(pr)]) {
+                    place(u, pr);
+                    break;
+                }
+        }
+        for (int u : units)
+            if (newpair[size_t(u)] < 0 && u >= lq && in_tile(u) && !used[size_t(u)]) place(u, u);
+        for (int u : units) {
+            if (newpair[size_t(u)] >= 0) continue;
+            for (int pr : tile_pairs)
+                if (pr >= lq && !used[size_t(pr)]) {
+                    place(u, pr);
+                    break;
+                }
+        }
+        for (int u : units) {
+            const int pr = newpair[size_t(u)];
+            l2p[size_t(u)] = 2 * pr;
+            l2p[size_t(u + dmn)] = 2 * pr + 1;
+            p2l[size_t(2 * pr)] = u;
+            p2l[size_t(2 * pr + 1)] = u + dmn;
+        }
+        low_mask = low_of();
+    };
     while (!remaining.empty()) {
         Trial t = build(remaining, 0, low_mask);
         if (multi_seed) {
@@ -1018,13 +1117,25 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
         if (relabel && next.empty()) {
             uint64_t displaced = 0;
             for (int b = 0; b < nloc; ++b)
-                if (l2p[size_t(b)] != b) displaced |= bit(b);
+                if (l2p[size_t(b)] != home(b)) displaced |= bit(b);
             if (popcount64(qmask | displaced) <= m) {
                 qmask |= displaced;
                 restore = true;
             }
         }
-        if (relabel) {
+        if (relabel && mirror_mode) {
+            // fill with the qubits (column + row bit pairs) needed soonest
+            nu = next_use(next);
+            std::vector<int> cand;
+            for (int u = 0; u < dmn; ++u)
+                if (!((qmask >> u) & 1)) cand.push_back(u);
+            auto unu = [&](int u) { return std::min(nu[size_t(u)], nu[size_t(u + dmn)]); };
+            std::stable_sort(cand.begin(), cand.end(), [&](int x, int y) { return unu(x) < unu(y); });
+            for (int u : cand) {
+                if (popcount64(qmask) + 2 > m) break;
+                qmask |= closure(bit(u));
+            }
+        } else if (relabel) {
             // fill with the local bits the remaining ops need soonest
             nu = next_use(next);
             std::vector<int> cand;
@@ -1057,10 +1168,12 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
             }
             if (restore) {
                 for (int x : q) {
-                    l2p[size_t(x)] = x;
-                    p2l[size_t(x)] = x;
+                    l2p[size_t(x)] = home(x);
+                    p2l[size_t(home(x))] = x;
                 }
                 low_mask = low_of();
+            } else if (relabel && mirror_mode && !next.empty()) {
+                relabel_pairs(q, next);
             } else if (relabel && !next.empty()) {
                 // Choose the tile qubits that the low physical bits hold after this
                 // pass: greedily, the set under which the next pass takes the most ops.
