@@ -256,14 +256,14 @@ def run_reference_arm(args, world, rank):
                        "unit_note": "30-qubit gate equivalents; the reference accepts n <= 30 only, so for "
                                     "N > 1 it is timed at n = 30 (the b200 arm runs 30 + log2 N qubits)"}}
     if res is None:
-        print(json.dumps({"impl": "reference", "unavailable": why}))
+        emit({"impl": "reference", "unavailable": why})
         return 0
     base.update({"value": res["value"], "ms_per_step": res["ms_per_run"], "dtype": "c128",
                  "data": "synthetic", "scaling": "weak",
                  "cpu_baseline": {k2: res[k2] for k2 in ("value", "unit", "cores", "kind", "sample")},
                  "e2e": {"value": res["value"], "unit": "gates/s", "h2d_bytes_per_step": 0,
                          "d2h_bytes_per_step": 0}})
-    print(json.dumps(base))
+    emit(base)
     return 0
 
 
@@ -443,7 +443,27 @@ def trajectory_workloads(workloads):
     return res
 
 
+_JSON_OUT = None
+
+
+def claim_stdout():
+    """Keep stdout for the one JSON line: anything else written to fd 1 (NCCL's
+    version banner, native or library prints) is sent to stderr instead."""
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(obj):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(obj) + "\n")
+    out.flush()
+
+
 def main():
+    claim_stdout()
     args = parse_args()
     world, rank, local, dist = dist_setup(args)
     if args.impl == "reference":
@@ -546,9 +566,12 @@ def main():
               file=sys.stderr)
     prof_e2e = abi.profile_end(dev)
     t_e2e = max_over_ranks(dist, local, t_e2e)
+    laps_ms = sorted((b - a) * 1e3 for a, b in zip([t0] + lap[:-1], lap))
     e2e = {"value": gates_total / t_e2e, "unit": "gates/s",
            "h2d_bytes_per_step": int(prof_e2e["h2d_bytes"] / args.steps),
-           "d2h_bytes_per_step": int(prof_e2e["d2h_bytes"] / args.steps)}
+           "d2h_bytes_per_step": int(prof_e2e["d2h_bytes"] / args.steps),
+           "step_ms_median_rank0": laps_ms[len(laps_ms) // 2], "step_ms_max_rank0": laps_ms[-1]}
+    jit_end = abi.jit_stats()
 
     out = None
     if rank == 0:
@@ -582,6 +605,7 @@ def main():
             "microops_per_step": stats["microops"],
             "gpu_launches": prof["kernel_launches"],
             "jit": jit,
+            "jit_end": jit_end,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_from_profiles(),
                          "kernel": ("nqjit (pass-specialised fused pass, NVRTC)" if jit.get("launches", 0) > 0
@@ -602,7 +626,7 @@ def main():
         out["cpu_baseline"] = (
             {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")} if res else {"unavailable": why})
     if rank == 0:
-        print(json.dumps(out))
+        emit(out)
     if dist is not None:
         dist.destroy_process_group()
     return 0

@@ -239,6 +239,10 @@ nq_status nq_sv_create_sharded(int num_qubits, int rank, int world, const unsign
                                const nq_opts* opts, nq_sv** out);
 /* Number of global-qubit exchanges performed so far and bytes sent. */
 nq_status nq_sv_comm_stats(const nq_sv* s, int64_t* exchanges, int64_t* bytes_sent);
+/* Of those exchanges, how many were fused into the preceding pass (the pass
+ * wrote its output out of place, the moved half straight into the partner's
+ * second buffer over NVLink), and whether this rank holds that second buffer. */
+nq_status nq_sv_comm_fused(const nq_sv* s, int64_t* fused, int* has_alt_buffer);
 /* Host-side schedule of a sharded flush (no device, no NCCL): the segments of
  * local work and the global<->local exchanges `ops` would produce on `world`
  * ranks, followed by the exchanges restoring the identity qubit map.
@@ -271,7 +275,9 @@ nq_status nq_jit_wait(void);
 nq_status nq_jit_shutdown(void);
 nq_status nq_jit_stats(int64_t* compiled, int64_t* failed, int64_t* misses, int64_t* launches);
 /* Generated source of pass `pass_index` of an SV plan, optionally compiled
- * with NVRTC (no device needed); *compiled_ok = 1/0, or -1 when not compiled. */
+ * with NVRTC (no device needed); *compiled_ok = 1/0, or -1 when not compiled.
+ * compile: bit 0 = compile, bit 1 = the exchange-store variant (the kernel a
+ * sharded flush fuses with a global-qubit exchange). */
 nq_status nq_jit_debug(int num_qubits, const nq_op* ops, int64_t count, int tile_qubits, int pass_index,
                        int compile, char* src_out, int64_t cap, int64_t* size, int* compiled_ok);
 

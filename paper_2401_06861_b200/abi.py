@@ -142,6 +142,7 @@ SIGNATURES = {
     "nq_comm_unique_id": ([_ucp], C.c_int),
     "nq_sv_create_sharded": ([C.c_int, C.c_int, C.c_int, _ucp, C.POINTER(nq_opts), _pp], C.c_int),
     "nq_sv_comm_stats": ([_p, _i64p, _i64p], C.c_int),
+    "nq_sv_comm_fused": ([_p, _i64p, C.POINTER(C.c_int)], C.c_int),
     "nq_shard_debug": ([C.c_int, C.c_int, _p, C.c_int64, _i64p, C.c_int64, _i64p], C.c_int),
     "nq_profile_begin": ([C.c_int, C.c_int], C.c_int),
     "nq_profile_end": ([C.c_int, C.POINTER(nq_profile)], C.c_int),
@@ -346,7 +347,9 @@ class SV:
     def comm_stats(self):
         a, b = C.c_int64(), C.c_int64()
         check(lib.nq_sv_comm_stats(self.h, C.byref(a), C.byref(b)))
-        return {"exchanges": a.value, "bytes_sent": b.value}
+        f, alt = C.c_int64(), C.c_int()
+        check(lib.nq_sv_comm_fused(self.h, C.byref(f), C.byref(alt)))
+        return {"exchanges": a.value, "bytes_sent": b.value, "fused": f.value, "alt_buffer": bool(alt.value)}
 
 
 def comm_unique_id() -> bytes:
@@ -538,14 +541,15 @@ def jit_stats() -> dict:
     return dict(zip(("compiled", "failed", "misses", "launches"), (x.value for x in v)))
 
 
-def jit_debug(n: int, ops, pass_index: int, tile_qubits: int = 0, compile: bool = True):
+def jit_debug(n: int, ops, pass_index: int, tile_qubits: int = 0, compile: bool = True, xstore: bool = False):
     arr = ops if isinstance(ops, np.ndarray) else make_ops(ops)
     size = C.c_int64()
     ok = C.c_int()
-    check(lib.nq_jit_debug(n, arr.ctypes.data, len(arr), tile_qubits, pass_index, 0, None, 0, C.byref(size),
+    xs = 2 if xstore else 0
+    check(lib.nq_jit_debug(n, arr.ctypes.data, len(arr), tile_qubits, pass_index, xs, None, 0, C.byref(size),
                            C.byref(ok)))
     buf = C.create_string_buffer(size.value + 1 << 16)
-    check(lib.nq_jit_debug(n, arr.ctypes.data, len(arr), tile_qubits, pass_index, 1 if compile else 0, buf,
+    check(lib.nq_jit_debug(n, arr.ctypes.data, len(arr), tile_qubits, pass_index, (1 if compile else 0) | xs, buf,
                            len(buf), C.byref(size), C.byref(ok)))
     return buf.raw[: size.value].decode(), ok.value
 

@@ -1299,9 +1299,9 @@ nq_status nq_jit_debug(int n, const nq_op* ops, int64_t count, int tile_qubits, 
         PassHdr h;
         std::memcpy(&h, rec, sizeof(h));
         std::string src = jit_source(h, reinterpret_cast<const MOp*>(rec + h.op_off),
-                                     reinterpret_cast<const cplx*>(rec + h.pool_off));
+                                     reinterpret_cast<const cplx*>(rec + h.pool_off), (compile & 2) != 0);
         std::string log;
-        if (compiled_ok) *compiled_ok = compile ? int(jit_compile_only(src, &log)) : -1;
+        if (compiled_ok) *compiled_ok = (compile & 1) ? int(jit_compile_only(src, &log)) : -1;
         if (!log.empty()) src += "\n/* NVRTC LOG\n" + log + "\n*/\n";
         *size = int64_t(src.size());
         if (src_out && cap > 0) std::memcpy(src_out, src.data(), size_t(std::min<int64_t>(cap, *size)));

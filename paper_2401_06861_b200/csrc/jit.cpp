@@ -306,7 +306,7 @@ std::string sparse_dense(const MOp& op, const cplx* u, int E, const std::string&
     return s.str();
 }
 
-std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
+std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool xstore) {
     const int m = h.m;
     const int SIZE = 1 << m;
     const int E = 1 << ops[0].k;  // ops[0] is the load layout: 3 or 4 register bits
@@ -318,7 +318,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     const bool relabel = qst != q;
     // Hermitian (mirror) pass: tile / rest bits pair as physical (2q, 2q+1)
     const JitKnobs& kn0 = jit_knobs();
-    bool mirror = (h.flags & PASS_MIRROR) && !kn0.prefetch;
+    bool mirror = (h.flags & PASS_MIRROR) && !kn0.prefetch && !xstore;
     std::vector<int> tpair(size_t(m), -1), rpair(rest.size(), -1);
     for (int i = 0; i < m && mirror; ++i)
         for (int j = 0; j < m; ++j)
@@ -331,7 +331,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     std::vector<int> qmir(static_cast<size_t>(m));
     for (int i = 0; i < m && mirror; ++i) qmir[size_t(i)] = qst[size_t(tpair[size_t(i)])];
     // bulk-copy staging needs the 16 contiguous low amplitudes as tile bits 0-3
-    bool use_tma = kn0.tma && !kn0.prefetch && !mirror && m >= 8;
+    bool use_tma = kn0.tma && !kn0.prefetch && !mirror && m >= 8 && !xstore;
     for (int b = 0; b < 4 && use_tma; ++b) use_tma = q[size_t(b)] == b;
     auto mirror_rest_expr = [&](const std::string& r) {
         std::ostringstream o;
@@ -391,7 +391,8 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     if (minb > 0) s << ", " << minb;
     s << ")\n"
       << "nqjit(double2* __restrict__ st, const double2* __restrict__ gpool, unsigned long long rankbase,"
-         " long long ntiles) {\n"
+         " long long ntiles, double2* xout_l, double2* xout_r, unsigned long long xmask, unsigned long long xval,"
+         " int xrot) {\n"
       << "  using namespace nq;\n"
       << "  extern __shared__ __align__(16) unsigned char smem[];\n"
       << "  double2* buf0 = reinterpret_cast<double2*>(smem);\n"
@@ -477,7 +478,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
           << "    double2 ug = make_double2(1.0, 0.0);\n"
           << "    (void)ug;\n";
         for (int l = 0; l < E; ++l) s << "    a[" << l << "] = cur[tb0 | " << L0.rconst(l) << "u];\n";
-    } else if (kn.prefetch) {
+    } else if (kn.prefetch && !xstore) {
         s << "  long long r = blockIdx.x;\n"
           << "  if (r < ntiles) {\n";
         prefetch("r", "buf0", "    ");
@@ -510,8 +511,16 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
             s << "    const long long rstar = (long long)(" << mirror_rest_expr("(unsigned long long)r") << ");\n"
               << "    if (rstar < r) continue;\n";
         }
+        // exchange passes: tile counter bit 0 moves to rest position xrot, so
+        // that consecutive CTAs alternate between tiles stored locally and
+        // tiles stored to the partner (NVLink and HBM stores overlap)
+        const std::string rexpr = xstore ? "rr" : "(unsigned long long)r";
+        if (xstore)
+            s << "    const unsigned long long r1 = (unsigned long long)r >> 1;\n"
+              << "    const unsigned long long rr = ((r1 >> xrot) << (xrot + 1)) | (((unsigned long long)r & 1ull) << xrot)"
+                 " | (r1 & ((1ull << xrot) - 1ull));\n";
         s << "    double2* cur = buf0;\n"
-          << "    const unsigned long long base = " << deposit_expr("(unsigned long long)r", rest, true) << ";\n"
+          << "    const unsigned long long base = " << deposit_expr(rexpr, rest, true) << ";\n"
           << "    const unsigned long long full = rankbase | base;\n"
           << "    (void)full;\n"
           << "    double2 a[" << E << "];\n"
@@ -683,9 +692,20 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
         for (int l = 0; l < E; ++l) s << "    a[" << l << "] = cur[swS ^ " << sw.apply(LS.rconst(l)) << "u];\n";
     }
     const Layout& LST = extra_relayout ? LS : LN;
-    s << "    { double2* dst = st + base + toff_st;\n";
-    for (int l = 0; l < E; ++l) s << "      st_stream(dst + " << hex64(reg_off(LST, l, qst)) << ", a[" << l << "]);\n";
-    s << "    }\n";
+    if (xstore) {
+        // exchange store (sharded states): element o whose bit v (xmask)
+        // differs from this rank's bit (xval) goes to the partner's buffer at
+        // o ^ xmask, the rest to the local output buffer (out of place)
+        s << "    { const unsigned long long ob = base + toff_st;\n";
+        for (int l = 0; l < E; ++l)
+            s << "      { const unsigned long long o = ob + " << hex64(reg_off(LST, l, qst))
+              << "; st_stream(((o ^ xval) & xmask) ? xout_r + (o ^ xmask) : xout_l + o, a[" << l << "]); }\n";
+        s << "    }\n";
+    } else {
+        s << "    { double2* dst = st + base + toff_st;\n";
+        for (int l = 0; l < E; ++l) s << "      st_stream(dst + " << hex64(reg_off(LST, l, qst)) << ", a[" << l << "]);\n";
+        s << "    }\n";
+    }
     if (mirror) {
         // the mirror tile holds the conjugate transpose: element e of tile r is
         // conj'd into element e* (column/row bits swapped) of tile mirror(r)
@@ -699,7 +719,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool) {
     s << ""
       << "    __syncthreads();\n"
       << "  }\n";
-    if (kn.prefetch) s << "  cp_async_wait<0>();\n";
+    if (kn.prefetch && !xstore) s << "  cp_async_wait<0>();\n";
     s << "}\n";
     return s.str();
 }
@@ -897,12 +917,26 @@ int occupancy(Entry& e, int device, int threads, size_t smem) {
 
 }  // namespace
 
+bool jit_xstore_ok(const PassHdr& h, const MOp* ops) {
+    if (jit_mode() == JitMode::Off || h.m < 8 || h.m > 12 || h.nops < 1) return false;
+    if (h.flags & PASS_MIRROR) return false;
+    (void)ops;
+    return true;
+}
+
 bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,
-                uint64_t rankbase, cudaStream_t s, int device) {
+                uint64_t rankbase, cudaStream_t s, int device, const JitXStore* xs) {
     const JitMode mode = jit_mode();
-    if (mode == JitMode::Off || h.m < 8 || h.m > 12) return false;
-    if (mode == JitMode::Auto && h.nloc < 18) return false;  // interpreter is fine for small states
-    std::shared_ptr<Entry> e = acquire(jit_source(h, ops, pool), device, mode);
+    std::shared_ptr<Entry> e;
+    if (xs) {
+        if (!jit_xstore_ok(h, ops)) throw NqError{NQ_ERR_INTERNAL, "exchange pass cannot be specialised"};
+        e = acquire(jit_source(h, ops, pool, true), device, JitMode::Sync);
+        if (!e) throw NqError{NQ_ERR_INTERNAL, "exchange pass kernel failed to compile"};
+    } else {
+        if (mode == JitMode::Off || h.m < 8 || h.m > 12) return false;
+        if (mode == JitMode::Auto && h.nloc < 18) return false;  // interpreter is fine for small states
+        e = acquire(jit_source(h, ops, pool), device, mode);
+    }
     if (!e) return false;
     Jit& J = jit();
     const int T = (1 << h.m) / (1 << ops[0].k);
@@ -914,10 +948,15 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
     const double2* gpool = reinterpret_cast<const double2*>(dev_rec + h.pool_off);
     unsigned long long rb = rankbase;
     long long nt = h.ntiles;
-    void* args[] = {&state, &gpool, &rb, &nt};
+    double2* xl = xs ? xs->out_local : nullptr;
+    double2* xr = xs ? xs->out_remote : nullptr;
+    unsigned long long xm = xs ? xs->xmask : 0ull, xv = xs ? xs->xval : 0ull;
+    int xrot = xs ? xs->xrot : 0;
+    void* args[] = {&state, &gpool, &rb, &nt, &xl, &xr, &xm, &xv, &xrot};
     if (cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(unsigned(grid)), dim3(unsigned(T)), args, smem,
                          s) != cudaSuccess) {
         cudaGetLastError();
+        if (xs) throw NqError{NQ_ERR_CUDA, "exchange pass kernel launch failed"};
         return false;
     }
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);

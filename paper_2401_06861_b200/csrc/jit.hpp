@@ -33,14 +33,31 @@ struct JitKnobs {
 };
 const JitKnobs& jit_knobs();
 
-// CUDA source of the kernel specialised to one pass record.
-std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool);
+// CUDA source of the kernel specialised to one pass record.  xstore: the
+// exchange-store variant (sharded states, see JitXStore).
+std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool xstore = false);
+
+// A pass fused with a global<->local qubit exchange (shard.cpp): the pass
+// reads the state in place and writes out of place; element o of its output
+// goes to out_local[o] when (o & xmask) == xval, else to the partner rank's
+// buffer out_remote[o ^ xmask] (peer memory over NVLink).  xrot: rest-bit
+// position of the tile counter's lowest bit (interleaves local and remote tiles).
+struct JitXStore {
+    double2* out_local = nullptr;
+    double2* out_remote = nullptr;
+    uint64_t xmask = 0, xval = 0;
+    int xrot = 0;
+};
+// Whether a pass can run as an exchange-store kernel (deterministic: every
+// rank decides alike from the same pass record).
+bool jit_xstore_ok(const PassHdr& h, const MOp* ops);
 
 // Launch the specialised kernel for this pass if it is compiled (queueing the
 // compilation otherwise, or compiling inline under NQ_JIT=sync).  Returns
 // false when the caller must run the interpreter kernel instead.
+// With xs: compiled synchronously if needed; throws when it cannot run.
 bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,
-                uint64_t rankbase, cudaStream_t s, int device);
+                uint64_t rankbase, cudaStream_t s, int device, const JitXStore* xs = nullptr);
 
 // Expectation batch kernel specialised to the batch's term structure: source,
 // and launch (plus the per-term final sums into out[0..nt)); false when the

@@ -113,6 +113,13 @@ struct ShardComm {
     // peer-memory exchange: every rank's state mapped into this process (CUDA
     // IPC over NVLink); empty when unavailable or NQ_EXCHANGE=nccl
     std::vector<double2*> peer;
+    // fused exchanges (NQ_FUSED_EXCHANGE, default on when a second copy of the
+    // shard fits): the pass before an exchange writes its output out of place,
+    // locally into `alt` and remotely into the partner's `alt` (peer_alt), and
+    // the two buffers swap roles on every rank.
+    double2* alt = nullptr;
+    std::vector<double2*> peer_alt;
+    int64_t fused = 0;
     double* d_flag = nullptr;  // 1-element buffer for the stream barrier
     double2* sendbuf = nullptr;
     double2* recvbuf = nullptr;
@@ -284,7 +291,23 @@ __attribute__((unused)) uint64_t ins_bit(uint64_t k, int v, uint64_t val) {
 
 // `layout` (physical -> physical, size n): identity on entry; with relabelling
 // passes it receives where each local physical bit's qubit ends up.
-void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vector<int>* layout = nullptr) {
+struct FuseX {
+    int v = 0;           // local physical bit exchanged with the global bit
+    uint64_t mybit = 0;  // this rank's value of that global bit
+    double2* out_local = nullptr;
+    double2* out_remote = nullptr;
+    bool done = false;   // set when the segment's last pass carried the exchange
+};
+
+// Rest position of physical bit v in a pass (0 when v is a tile bit).
+int rest_pos(const PassHdr& h, int v) {
+    for (int j = 0; j < h.nrest; ++j)
+        if (h.rest[j] == v) return j;
+    return 0;
+}
+
+void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vector<int>* layout = nullptr,
+                 FuseX* fx = nullptr) {
     PlanOptions po = s.popt;
     po.relabel = layout != nullptr;
     PlanStats st;
@@ -306,7 +329,18 @@ void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vecto
         std::pair<cudaEvent_t, cudaEvent_t>* ev = c.prof_pass ? prof_slot(c) : nullptr;
         if (ev) CUDA_TRY(cudaEventRecord(ev->first, c.stream));
         const unsigned char* rec = buf.data() + offs[i];
-        if (!jit_launch(s.d, c.d_ops + offs[i], h, reinterpret_cast<const MOp*>(rec + h.op_off),
+        const MOp* mops = reinterpret_cast<const MOp*>(rec + h.op_off);
+        if (fx && i + 1 == passes.size() && layout == nullptr && jit_xstore_ok(h, mops)) {
+            JitXStore xs;
+            xs.out_local = fx->out_local;
+            xs.out_remote = fx->out_remote;
+            xs.xmask = uint64_t(1) << fx->v;
+            xs.xval = fx->mybit << fx->v;
+            xs.xrot = rest_pos(h, fx->v);
+            jit_launch(s.d, c.d_ops + offs[i], h, mops, reinterpret_cast<const cplx*>(rec + h.pool_off), rankbase,
+                       c.stream, s.dev, &xs);
+            fx->done = true;
+        } else if (!jit_launch(s.d, c.d_ops + offs[i], h, mops,
                         reinterpret_cast<const cplx*>(rec + h.pool_off), rankbase, c.stream, s.dev))
             launch_pass(s.d, c.d_ops + offs[i], h, rankbase, c.stream,
                         reinterpret_cast<const MOp*>(rec + h.op_off)[0].k);
@@ -357,6 +391,24 @@ void run_exchange(State& s, DeviceCtx& c, int g, int v) {
     ++sc.exchanges;
 }
 
+// After a pass fused with the exchange (g, v): every rank wrote its output
+// into the `alt` buffers, so the buffers swap roles; the barrier keeps any
+// rank from reading its new state before its partner's stores have landed
+// (and, as no rank touches its old buffer again before the next exchange,
+// no barrier is needed before such a pass).
+void fused_exchange_done(State& s, DeviceCtx& c, int g, int v) {
+    ShardComm& sc = *s.comm;
+    if (s.rank == 0 && std::getenv("NQ_SHARD_TRACE"))
+        std::fprintf(stderr, "[shard] exchange g=%d v=%d (fused into the pass)\n", g, v);
+    std::swap(s.d, sc.alt);
+    std::swap(sc.peer, sc.peer_alt);
+    stream_barrier(sc, c);
+    CUDA_TRY(cudaGetLastError());
+    sc.bytes += int64_t(s.count / 2) * 16;
+    ++sc.exchanges;
+    ++sc.fused;
+}
+
 // Relabelling passes permute local physical bits inside a segment; the later
 // actions (scheduled on the pre-relabel bits) are remapped through `perm`,
 // and the composed permutation is folded into the shard's qubit map.
@@ -386,9 +438,29 @@ void execute(State& s, const std::vector<Action>& acts, bool relabel = false) {
     std::vector<int> perm(size_t(s.n));
     for (int b = 0; b < s.n; ++b) perm[size_t(b)] = b;
     bool moved = false;
-    for (const auto& a : acts) {
+    ShardComm& scx = *s.comm;
+    for (size_t ai = 0; ai < acts.size(); ++ai) {
+        const Action& a = acts[ai];
         if (a.kind == Action::Segment) {
             if (!relabel) {
+                const bool next_x = ai + 1 < acts.size() && acts[ai + 1].kind == Action::Exchange;
+                if (next_x && scx.alt) {
+                    // fuse the exchange into the segment's last pass
+                    const Action& x = acts[ai + 1];
+                    const int j = x.gbit - s.nloc;
+                    const int partner = s.rank ^ (1 << j);
+                    FuseX fx;
+                    fx.v = x.vbit;
+                    fx.mybit = uint64_t((s.rank >> j) & 1);
+                    fx.out_local = scx.alt;
+                    fx.out_remote = scx.peer_alt[size_t(partner)];
+                    run_segment(s, c, a.ops, nullptr, &fx);
+                    if (fx.done) {
+                        fused_exchange_done(s, c, x.gbit, x.vbit);
+                        ++ai;
+                    }
+                    continue;
+                }
                 run_segment(s, c, a.ops);
                 continue;
             }
@@ -453,13 +525,12 @@ std::vector<double> allgather_doubles(State& s, const std::vector<double>& mine)
     return all;
 }
 
-// Map every rank's state into this process (CUDA IPC); all ranks must agree,
-// so the outcome is all-reduced and any failure keeps the NCCL path everywhere.
-void setup_peer_exchange(State& s, ShardComm& sc, DeviceCtx& c) {
-    const char* mode = std::getenv("NQ_EXCHANGE");
-    const bool want = !(mode && std::string(mode) == "nccl");
+// Map every rank's buffer `mine` into this process (CUDA IPC); all ranks must
+// agree, so the outcome is all-gathered and any failure (or `want` false on
+// any rank) returns an empty vector everywhere.
+std::vector<double2*> map_peers(State& s, double2* mine_ptr, bool want) {
     cudaIpcMemHandle_t mine{};
-    bool ok = want && cudaIpcGetMemHandle(&mine, s.d) == cudaSuccess;
+    bool ok = want && mine_ptr && cudaIpcGetMemHandle(&mine, mine_ptr) == cudaSuccess;
     cudaGetLastError();
     // all-gather the 64-byte handles as doubles (8 per handle) + an ok flag
     constexpr size_t kW = sizeof(cudaIpcMemHandle_t) / sizeof(double) + 1;
@@ -484,11 +555,41 @@ void setup_peer_exchange(State& s, ShardComm& sc, DeviceCtx& c) {
     // agree: p2p only if every rank mapped every peer
     const std::vector<double> oks = allgather_doubles(s, {ok ? 1.0 : 0.0});
     for (double v : oks) ok = ok && v == 1.0;
-    if (ok) {
-        sc.peer = std::move(peer);
-    } else {
+    if (!ok) {
         for (double2* p : peer)
             if (p) cudaIpcCloseMemHandle(p);
+        peer.clear();
+    }
+    return peer;
+}
+
+bool fused_exchange_wanted() {
+    const char* e = std::getenv("NQ_FUSED_EXCHANGE");
+    return !(e && e[0] == '0');
+}
+
+void setup_peer_exchange(State& s, ShardComm& sc, DeviceCtx& c) {
+    const char* mode = std::getenv("NQ_EXCHANGE");
+    const bool want = !(mode && std::string(mode) == "nccl");
+    sc.peer = map_peers(s, s.d, want);
+    if (sc.peer.empty()) return;
+    // a second copy of the shard for fused exchanges, when it fits with room
+    // to spare (2^30 amplitudes per GPU: 2 x 16 GiB; 2^33 does not fit)
+    bool fx = fused_exchange_wanted();
+    if (fx) {
+        size_t free_b = 0, total_b = 0;
+        fx = cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
+             free_b > size_t(s.count) * sizeof(double2) + (size_t(4) << 30);
+        cudaGetLastError();
+    }
+    if (fx && cudaMalloc(reinterpret_cast<void**>(&sc.alt), size_t(s.count) * sizeof(double2)) != cudaSuccess) {
+        cudaGetLastError();
+        sc.alt = nullptr;
+    }
+    sc.peer_alt = map_peers(s, sc.alt, sc.alt != nullptr);
+    if (sc.peer_alt.empty() && sc.alt) {
+        cudaFree(sc.alt);
+        sc.alt = nullptr;
     }
     (void)c;
 }
@@ -517,6 +618,9 @@ void shard_free(State& s) {
     if (sc->d_flag) cudaFree(sc->d_flag);
     for (double2* p : sc->peer)
         if (p) cudaIpcCloseMemHandle(p);
+    for (double2* p : sc->peer_alt)
+        if (p) cudaIpcCloseMemHandle(p);
+    if (sc->alt) cudaFree(sc->alt);
     if (sc->comm) ncclCommDestroy(sc->comm);
     delete sc;
     s.comm = nullptr;
@@ -805,6 +909,14 @@ nq_status nq_sv_comm_stats(const nq_sv* h, int64_t* exchanges, int64_t* bytes_se
         const State& s = h->s;
         if (exchanges) *exchanges = s.comm ? s.comm->exchanges : 0;
         if (bytes_sent) *bytes_sent = s.comm ? s.comm->bytes : 0;
+    });
+}
+
+nq_status nq_sv_comm_fused(const nq_sv* h, int64_t* fused, int* has_alt_buffer) {
+    return guard([&] {
+        const State& s = h->s;
+        if (fused) *fused = s.comm ? s.comm->fused : 0;
+        if (has_alt_buffer) *has_alt_buffer = (s.comm && s.comm->alt) ? 1 : 0;
     });
 }
 

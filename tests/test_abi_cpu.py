@@ -84,3 +84,18 @@ def test_workload_shapes():
     # ceil(t * spu) steps; 13 ops per step at n = 4 (tests/test_tfim.cpp:57-59)
     assert len(workloads.tfim_trotter(4, 0.5)) == 50 * 13
     assert len(workloads.tfim_trotter(4, 0.0)) == 0
+
+
+def test_pass_kernels_compile_with_nvrtc_including_exchange_stores():
+    """Every pass of a random-circuit plan specialises to source NVRTC accepts
+    for sm_100a, in both the in-place form and the exchange-store form a
+    sharded flush fuses with a global-qubit swap (out-of-place stores, the
+    moved half to the partner's buffer)."""
+    ops = workloads.random_circuit(2024, 24, 120)
+    for idx in range(2):
+        src, ok = abi.jit_debug(24, ops, idx)
+        assert ok == 1, src[-2000:]
+        assert "xout_r" not in src.split("{", 1)[1]  # in-place pass: no exchange stores
+        xsrc, xok = abi.jit_debug(24, ops, idx, xstore=True)
+        assert xok == 1, xsrc[-2000:]
+        assert "xout_r + (o ^ xmask)" in xsrc and "rr = " in xsrc

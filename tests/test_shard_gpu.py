@@ -16,7 +16,8 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _rank_main(rank, world, uid, n, seed, outdir):
+def _rank_main(rank, world, uid, n, seed, outdir, fused=True):
+    os.environ["NQ_FUSED_EXCHANGE"] = "1" if fused else "0"
     sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
     from oracle import Port
     from paper_2401_06861_b200 import abi as A
@@ -28,29 +29,40 @@ def _rank_main(rank, world, uid, n, seed, outdir):
     norm = sv.norm_sq()
     rng = np.random.default_rng(seed)
     terms = [("".join(rng.choice(list("IXYZ"), size=n)), float(rng.uniform(-1, 1))) for _ in range(12)]
-    terms.append(("X" * (n - 1) + "Z", 0.5))
+    g = world.bit_length() - 1
+    terms.append(("X" * (n - g) + "Z" * g, 0.5))  # flips every local qubit's worth
     ex = sv.expectations(terms)
     u = np.sort(port.rng_double(99, 4000))
     idx, cnt = sv.sample_sorted(u)
     amps = sv.amplitudes()
     stats = sv.comm_stats()
     np.savez(os.path.join(outdir, f"r{rank}.npz"), norm=norm, ex=ex, idx=idx, cnt=cnt, amps=amps,
-             exchanges=stats["exchanges"], letters=np.array([t[0] for t in terms]),
+             exchanges=stats["exchanges"], fused=stats["fused"], alt=stats["alt_buffer"],
+             letters=np.array([t[0] for t in terms]),
              coeff=np.array([t[1] for t in terms]))
 
 
-@pytest.mark.parametrize("n", [14, 20])
-def test_sharded_two_gpus(port, tmp_path, n):
-    if abi.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
-    world, seed = 2, 808 + n
+@pytest.mark.parametrize("n,world,fused", [(14, 2, True), (20, 2, True), (20, 2, False), (22, 4, True),
+                                           (22, 4, False)])
+def test_sharded_gpus(port, tmp_path, n, world, fused):
+    """Sharded run == oracle (amplitudes, norm, expectations, sampling), with
+    exchanges fused into the preceding pass (out-of-place exchange stores into
+    the partner's second buffer) or as standalone peer-memory swaps."""
+    if abi.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    seed = 808 + n
     uid = abi.comm_unique_id()
-    mp.start_processes(_rank_main, args=(world, uid, n, seed, str(tmp_path)), nprocs=world, start_method="spawn")
+    mp.start_processes(_rank_main, args=(world, uid, n, seed, str(tmp_path), fused), nprocs=world,
+                       start_method="spawn")
     ops = port.random_circuit(seed, n, 300)
     want = port.sv_run(n, ops)
     for r in range(world):
         d = np.load(tmp_path / f"r{r}.npz")
         assert int(d["exchanges"]) > 0
+        if fused:
+            assert bool(d["alt"]) and int(d["fused"]) > 0
+        else:
+            assert int(d["fused"]) == 0
         np.testing.assert_allclose(d["amps"], want, atol=1e-10, rtol=0)
         assert abs(float(d["norm"]) - 1.0) < 1e-10
         ref = [port.expectation(want, str(L), float(c)) for L, c in zip(d["letters"], d["coeff"])]
