@@ -246,9 +246,10 @@ nq_status nq_sv_comm_fused(const nq_sv* s, int64_t* fused, int* has_alt_buffer);
 /* Host-side schedule of a sharded flush (no device, no NCCL): the segments of
  * local work and the global<->local exchanges `ops` would produce on `world`
  * ranks, followed by the exchanges restoring the identity qubit map.
+ * flags bit 0: rebalance the segments around each exchange, as flushes do.
  * Serialised as int64 records (see paper_2401_06861_b200/abi.py:shard_debug). */
-nq_status nq_shard_debug(int num_qubits, int world, const nq_op* ops, int64_t count, int64_t* buf, int64_t cap,
-                         int64_t* size);
+nq_status nq_shard_debug(int num_qubits, int world, const nq_op* ops, int64_t count, int flags, int64_t* buf,
+                         int64_t cap, int64_t* size);
 
 /* ---- measurement (bench.py) -------------------------------------------- */
 typedef struct nq_profile {

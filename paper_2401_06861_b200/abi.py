@@ -143,7 +143,7 @@ SIGNATURES = {
     "nq_sv_create_sharded": ([C.c_int, C.c_int, C.c_int, _ucp, C.POINTER(nq_opts), _pp], C.c_int),
     "nq_sv_comm_stats": ([_p, _i64p, _i64p], C.c_int),
     "nq_sv_comm_fused": ([_p, _i64p, C.POINTER(C.c_int)], C.c_int),
-    "nq_shard_debug": ([C.c_int, C.c_int, _p, C.c_int64, _i64p, C.c_int64, _i64p], C.c_int),
+    "nq_shard_debug": ([C.c_int, C.c_int, _p, C.c_int64, C.c_int, _i64p, C.c_int64, _i64p], C.c_int),
     "nq_profile_begin": ([C.c_int, C.c_int], C.c_int),
     "nq_profile_end": ([C.c_int, C.POINTER(nq_profile)], C.c_int),
     "nq_jit_wait": ([], C.c_int),
@@ -358,14 +358,15 @@ def comm_unique_id() -> bytes:
     return bytes(u)
 
 
-def shard_debug(n: int, world: int, ops):
+def shard_debug(n: int, world: int, ops, rebalance: bool = True):
     """Host schedule of a sharded flush: list of ("exchange", gbit, vbit) and
     ("segment", [(type, k, bits, ctrl, matrix), ...]) in physical bits."""
     arr = ops if isinstance(ops, np.ndarray) else make_ops(ops)
     size = C.c_int64()
-    check(lib.nq_shard_debug(n, world, arr.ctypes.data, len(arr), None, 0, C.byref(size)))
+    fl = 1 if rebalance else 0
+    check(lib.nq_shard_debug(n, world, arr.ctypes.data, len(arr), fl, None, 0, C.byref(size)))
     buf = np.zeros(max(size.value, 1), dtype=np.int64)
-    check(lib.nq_shard_debug(n, world, arr.ctypes.data, len(arr), buf.ctypes.data_as(_i64p), len(buf),
+    check(lib.nq_shard_debug(n, world, arr.ctypes.data, len(arr), fl, buf.ctypes.data_as(_i64p), len(buf),
                              C.byref(size)))
     out, i = [], 0
     types = {0: "dense", 1: "diag", 2: "xperm", 3: "swap", 4: "depol", 5: "nop"}

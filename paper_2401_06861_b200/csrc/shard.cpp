@@ -27,12 +27,14 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 namespace nqe {
@@ -120,12 +122,33 @@ struct ShardComm {
     double2* alt = nullptr;
     std::vector<double2*> peer_alt;
     int64_t fused = 0;
+    std::unordered_map<uint64_t, std::vector<int>> rebalance_cache;  // see rebalance()  // acts_key -> ops moved per exchange
     double* d_flag = nullptr;  // 1-element buffer for the stream barrier
+    double* gather = nullptr;  // allgather_doubles buffer
+    size_t gather_cap = 0;
     double2* sendbuf = nullptr;
     double2* recvbuf = nullptr;
     uint64_t chunk = 0;  // amplitudes per bounce buffer
     std::vector<int> l2p, p2l;
     int64_t exchanges = 0, bytes = 0;
+};
+
+// NQ_SHARD_TIMING=<ms>: report host phases of sharded calls slower than that.
+struct PhaseTimer {
+    const char* name;
+    int rank;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    PhaseTimer(const char* n, int r) : name(n), rank(r) {}
+    ~PhaseTimer() {
+        static const double thresh = [] {
+            const char* e = std::getenv("NQ_SHARD_TIMING");
+            return e ? std::atof(e) : -1.0;
+        }();
+        if (thresh < 0) return;
+        const double ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (ms >= thresh) std::fprintf(stderr, "[shard-timing] rank %d %s %.2f ms\n", rank, name, ms);
+    }
 };
 
 // ---- host scheduling ----------------------------------------------------------
@@ -321,7 +344,11 @@ void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vecto
     s.last_source_ops += st.source_ops;
     s.last_launches += int64_t(passes.size());
     if (buf.empty()) return;
-    c.stage(buf.data(), buf.size());
+    {
+        PhaseTimer ps("stage", s.rank);
+        c.stage(buf.data(), buf.size());
+    }
+    PhaseTimer pl("launches", s.rank);
     const uint64_t rankbase = uint64_t(s.rank) << s.nloc;
     for (size_t i = 0; i < passes.size(); ++i) {
         PassHdr h;
@@ -432,6 +459,143 @@ EOp remap(const EOp& e, const std::vector<int>& perm) {
     return r;
 }
 
+// ---- segment rebalancing around exchanges ---------------------------------------
+// An exchange (g, v) only relabels the qubits at physical bits g and v, so an
+// op of the segment before it that does not need bit v as a non-diagonal
+// target, and commutes with the ops of that segment it would pass, can run
+// after it instead (its bits translated g <-> v).  Where the split falls
+// decides the pass count of the two segments (each ends in a partly filled
+// pass; the one before an exchange also carries it as its exchange store), so
+// for every Segment-Exchange-Segment triple the number j of such ops moved
+// (the last j movable ones) is chosen to minimise the planned passes of the
+// pair.  Random circuit, 2^30 amplitudes per GPU, steady state: 32 qubits
+// (N = 4) 10 -> 9 passes per step, 33 qubits (N = 8) 11 -> 9.
+// NQ_SHARD_REBALANCE=0 disables it.
+bool shard_rebalance_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("NQ_SHARD_REBALANCE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+bool commutes(const EOp& a, const EOp& b) {
+    if ((emask(a, true) & emask(b, true)) == 0) return true;
+    return a.type == E_DIAG && b.type == E_DIAG;
+}
+
+int64_t planned_passes(const std::vector<EOp>& ops, const PlanOptions& po) {
+    if (ops.empty()) return 0;
+    PlanStats st;
+    plan_passes(ops, po, &st);
+    return st.passes;
+}
+
+uint64_t acts_key(const std::vector<Action>& acts) {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](uint64_t x) {
+        h ^= x + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+        h *= 1099511628211ull;
+    };
+    for (const auto& a : acts) {
+        mix(uint64_t(a.kind) | (uint64_t(a.gbit) << 8) | (uint64_t(a.vbit) << 16) | (uint64_t(a.ops.size()) << 24));
+        for (const auto& e : a.ops) {
+            mix(uint64_t(e.type) | (uint64_t(e.k) << 8));
+            for (int j = 0; j < e.k; ++j) mix(uint64_t(e.bits[j]));
+            mix(e.ctrl);
+        }
+    }
+    return h;
+}
+
+using RebalanceCache = std::unordered_map<uint64_t, std::vector<int>>;
+
+void rebalance(std::vector<Action>& acts, PlanOptions po, int n, RebalanceCache* cache) {
+    po.relabel = false;
+    const uint64_t key = acts_key(acts);
+    RebalanceCache local;
+    RebalanceCache& rc = cache ? *cache : local;
+    auto hit = rc.find(key);
+    const bool cached = hit != rc.end();
+    std::vector<int> chosen;
+    size_t xi = 0;  // index of the exchange among the rebalanced triples
+    for (size_t k = 0; k + 2 < acts.size(); ++k) {
+        if (acts[k].kind != Action::Segment || acts[k + 1].kind != Action::Exchange ||
+            acts[k + 2].kind != Action::Segment)
+            continue;
+        const int g = acts[k + 1].gbit, v = acts[k + 1].vbit;
+        std::vector<EOp>& seg = acts[k].ops;
+        std::vector<EOp>& next = acts[k + 2].ops;
+        // movable ops, scanning back from the exchange
+        std::vector<char> mov(seg.size(), 0);
+        std::vector<const EOp*> stay;
+        for (size_t i = seg.size(); i-- > 0;) {
+            const EOp& e = seg[i];
+            bool ok = !((need_bits(e) >> v) & 1);
+            for (size_t t = 0; ok && t < stay.size(); ++t) ok = commutes(e, *stay[t]);
+            if (ok) mov[i] = 1;
+            else stay.push_back(&e);
+        }
+        std::vector<size_t> idx;
+        for (size_t i = 0; i < seg.size(); ++i)
+            if (mov[i]) idx.push_back(i);
+        std::vector<int> perm(static_cast<size_t>(n));
+        for (int b = 0; b < n; ++b) perm[size_t(b)] = b;
+        perm[size_t(g)] = v;
+        perm[size_t(v)] = g;
+        auto split = [&](size_t j, std::vector<EOp>* st, std::vector<EOp>* mv) {
+            std::vector<char> take(seg.size(), 0);
+            for (size_t t = idx.size() - j; t < idx.size(); ++t) take[idx[t]] = 1;
+            for (size_t i = 0; i < seg.size(); ++i) {
+                if (take[i]) mv->push_back(remap(seg[i], perm));
+                else st->push_back(seg[i]);
+            }
+        };
+        size_t best_j = 0;
+        if (cached) {
+            best_j = xi < hit->second.size() ? size_t(hit->second[xi]) : 0;
+            if (best_j > idx.size()) best_j = 0;
+        } else if (!idx.empty()) {
+            auto score = [&](size_t j) {
+                std::vector<EOp> st, mv;
+                split(j, &st, &mv);
+                mv.insert(mv.end(), next.begin(), next.end());
+                const int64_t ps = planned_passes(st, po);
+                // an exchange with no pass before it runs standalone (a full
+                // extra read + write of the shard over NVLink)
+                return double(ps + planned_passes(mv, po)) + (ps == 0 ? 1.5 : 0.0);
+            };
+            const size_t m = idx.size();
+            const size_t step = std::max<size_t>(1, m / 16);
+            double best = score(0);
+            for (size_t j = step; j <= m; j += step) {
+                const double sj = score(j);
+                if (sj < best) best = sj, best_j = j;
+            }
+            if (step > 1) {
+                const size_t lo = best_j > step ? best_j - step + 1 : 1, hi = std::min(m, best_j + step - 1);
+                for (size_t j = lo; j <= hi; ++j) {
+                    if (j == best_j) continue;
+                    const double sj = score(j);
+                    if (sj < best) best = sj, best_j = j;
+                }
+            }
+        }
+        chosen.push_back(int(best_j));
+        ++xi;
+        if (best_j == 0) continue;
+        std::vector<EOp> st, mv;
+        split(best_j, &st, &mv);
+        mv.insert(mv.end(), next.begin(), next.end());
+        seg = std::move(st);
+        next = std::move(mv);
+    }
+    if (!cached) {
+        if (rc.size() >= 64) rc.clear();
+        rc.emplace(key, std::move(chosen));
+    }
+}
+
 void execute(State& s, const std::vector<Action>& acts, bool relabel = false) {
     DeviceCtx& c = ctx_for(s.dev);
     CUDA_TRY(cudaSetDevice(s.dev));
@@ -512,15 +676,26 @@ void execute(State& s, const std::vector<Action>& acts, bool relabel = false) {
 
 // rank-ordered sum of one double per rank (deterministic)
 std::vector<double> allgather_doubles(State& s, const std::vector<double>& mine) {
+    PhaseTimer pt("allgather", s.rank);
     DeviceCtx& c = ctx_for(s.dev);
     const size_t k = mine.size();
-    double* d = nullptr;
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d), (size_t(s.world) + 1) * k * sizeof(double), c.stream));
+    // one persistent buffer: NCCL registers the buffers it sees, and a fresh
+    // pool address per call measured 40-1400 ms stalls every few calls
+    ShardComm& sc = *s.comm;
+    const size_t need = (size_t(s.world) + 1) * k;
+    if (need > sc.gather_cap) {
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        if (sc.gather) CUDA_TRY(cudaFree(sc.gather));
+        sc.gather = nullptr;
+        const size_t cap = std::max<size_t>(need, 1 << 16);
+        CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&sc.gather), cap * sizeof(double)));
+        sc.gather_cap = cap;
+    }
+    double* d = sc.gather;
     CUDA_TRY(cudaMemcpyAsync(d, mine.data(), k * sizeof(double), cudaMemcpyHostToDevice, c.stream));
-    NCCL_TRY(ncclAllGather(d, d + k, k, ncclDouble, s.comm->comm, c.stream));
+    NCCL_TRY(ncclAllGather(d, d + k, k, ncclDouble, sc.comm, c.stream));
     std::vector<double> all(size_t(s.world) * k);
     CUDA_TRY(cudaMemcpyAsync(all.data(), d + k, all.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-    CUDA_TRY(cudaFreeAsync(d, c.stream));
     CUDA_TRY(cudaStreamSynchronize(c.stream));
     return all;
 }
@@ -616,6 +791,7 @@ void shard_free(State& s) {
     if (sc->sendbuf) cudaFree(sc->sendbuf);
     if (sc->recvbuf) cudaFree(sc->recvbuf);
     if (sc->d_flag) cudaFree(sc->d_flag);
+    if (sc->gather) cudaFree(sc->gather);
     for (double2* p : sc->peer)
         if (p) cudaIpcCloseMemHandle(p);
     for (double2* p : sc->peer_alt)
@@ -632,6 +808,7 @@ void shard_reset(State& s) {
 }
 
 void shard_flush(State& s) {
+    PhaseTimer pt("flush", s.rank);
     ShardComm& sc = *s.comm;
     std::vector<EOp> ops;
     ops.swap(s.queue);
@@ -666,6 +843,10 @@ void shard_flush(State& s) {
         const char* e = std::getenv("NQ_SHARD_RELABEL");
         return e && e[0] == '1';
     }();
+    if (shard_rebalance_enabled() && !(relabel && !restore)) {
+        PhaseTimer pr("rebalance", s.rank);
+        rebalance(acts, s.popt, s.n, &sc.rebalance_cache);
+    }
     execute(s, acts, relabel && !restore);
 }
 
@@ -684,6 +865,7 @@ double shard_norm_sq(State& s) {
 
 void shard_expectation(State& s, const uint64_t* flip, const uint64_t* signs, const int32_t* ny, const double* coeff,
                        int nterms, double* out) {
+    PhaseTimer pt("expectation", s.rank);
     ShardComm& sc = *s.comm;
     const uint64_t loc_mask = (uint64_t(1) << s.nloc) - 1;
     for (int t = 0; t < nterms; ++t)
@@ -713,6 +895,7 @@ void shard_expectation(State& s, const uint64_t* flip, const uint64_t* signs, co
             sgn.push_back((__builtin_popcountll((g >> s.nloc) & uint64_t(s.rank)) & 1) ? -1.0 : 1.0);
         }
         std::vector<cplx> totals;
+        PhaseTimer pe("expect_raw", s.rank);
         sv_expect_raw(s, pf.data(), ps.data(), int(batch.size()), totals);
         for (size_t i = 0; i < batch.size(); ++i) {
             mine[2 * size_t(batch[i])] = sgn[i] * totals[i].real();
@@ -924,7 +1107,7 @@ nq_status nq_sv_comm_fused(const nq_sv* h, int64_t* fused, int* has_alt_buffer) 
 // would take from the identity map, serialised as int64 records:
 // [kind(0 seg,1 exch), a, b, nops_or_0] followed by nops * nq_op for segments
 // (ops in physical bits, as kinds/targets of the lowered elementary ops).
-nq_status nq_shard_debug(int n, int world, const nq_op* ops, int64_t count, int64_t* buf, int64_t cap,
+nq_status nq_shard_debug(int n, int world, const nq_op* ops, int64_t count, int flags, int64_t* buf, int64_t cap,
                          int64_t* size) {
     return guard([&] {
         int g = 0;
@@ -936,6 +1119,13 @@ nq_status nq_shard_debug(int n, int world, const nq_op* ops, int64_t count, int6
         std::vector<int> l2p(nn), p2l(nn);
         for (int i = 0; i < n; ++i) l2p[size_t(i)] = p2l[size_t(i)] = i;
         auto acts = schedule(q, l2p, p2l, n - g, false);
+        if (flags & 1) {
+            PlanOptions po;
+            po.nbits = n;
+            po.nloc = n - g;
+            configure_caps(po);
+            rebalance(acts, po, n, nullptr);
+        }
         auto fin = schedule_identity(l2p, p2l, n - g, n);
         acts.insert(acts.end(), fin.begin(), fin.end());
         std::vector<int64_t> out;

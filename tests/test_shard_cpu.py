@@ -91,7 +91,7 @@ def run_schedule_single(n, world, acts):
     return np.concatenate(shards), exchanges
 
 
-@pytest.mark.parametrize("n,world", [(6, 2), (8, 2), (8, 4), (10, 8), (12, 4)])
+@pytest.mark.parametrize("n,world", [(6, 2), (8, 2), (8, 4), (10, 8), (12, 4), (16, 4)])
 def test_sharded_schedule_matches_oracle(port, n, world):
     for seed in range(3):
         ops = port.random_circuit(70 + 13 * n + seed, n, 120)
@@ -99,6 +99,22 @@ def test_sharded_schedule_matches_oracle(port, n, world):
         state, ex = run_schedule_single(n, world, acts)
         np.testing.assert_allclose(state, port.sv_run(n, ops), atol=1e-10, rtol=0)
         assert ex > 0  # the random circuits do touch global qubits
+
+
+@pytest.mark.parametrize("n,world,seed", [(16, 4, 0), (16, 4, 2), (20, 4, 2)])
+def test_rebalanced_segments_match_oracle(port, n, world, seed):
+    """Ops moved across an exchange (csrc/shard.cpp rebalance: bits translated
+    g <-> v, order kept) give the same state; these cases do move ops."""
+    ops = port.random_circuit(70 + 13 * n + seed, n, 120)
+    plain = abi.shard_debug(n, world, ops, rebalance=False)
+    moved = abi.shard_debug(n, world, ops, rebalance=True)
+    sizes = lambda acts: [len(a[1]) if a[0] == "segment" else "X" for a in acts]  # noqa: E731
+    assert sizes(plain) != sizes(moved)
+    assert sum(len(a[1]) for a in plain if a[0] == "segment") == sum(len(a[1]) for a in moved if a[0] == "segment")
+    want = port.sv_run(n, ops)
+    for acts in (plain, moved):
+        state, _ = run_schedule_single(n, world, acts)
+        np.testing.assert_allclose(state, want, atol=1e-10, rtol=0)
 
 
 def test_diagonal_and_control_on_global_bits_need_no_exchange(port):
