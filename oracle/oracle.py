@@ -295,6 +295,21 @@ class Ref:
     def set_threads(self, t: int) -> int:
         return self.lib.ref_set_threads(t)
 
+    _OBJ = C.CFUNCTYPE(C.c_double, C.POINTER(C.c_double), C.c_int, C.c_void_p)
+
+    def minimize(self, f, x0, max_evals=500, x_tol=1e-8, f_tol=1e-10, initial_step=1.0):
+        """proj/src/neldermead.cpp on a Python objective: (trace, best_x, best_f, converged)."""
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        n = len(x0)
+        cb = self._OBJ(lambda p, k, _ctx: float(f([p[i] for i in range(k)])))
+        trace = np.zeros(max_evals)
+        best = np.zeros(n)
+        evals, conv, bf = C.c_int(), C.c_int(), C.c_double()
+        self._chk(self.lib.ref_minimize(cb, None, x0.ctypes.data_as(_dp), n, max_evals, C.c_double(x_tol),
+                                        C.c_double(f_tol), C.c_double(initial_step), trace.ctypes.data_as(_dp),
+                                        C.byref(evals), best.ctypes.data_as(_dp), C.byref(bf), C.byref(conv)))
+        return trace[: evals.value].copy(), best, bf.value, bool(conv.value)
+
     def rng_u64(self, seed, count):
         out = np.zeros(count, dtype=np.uint64)
         self.lib.ref_rng_u64(C.c_uint64(seed), count, out.ctypes.data_as(_u64p))

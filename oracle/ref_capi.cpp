@@ -14,6 +14,7 @@
 #include "naqs/circuit.hpp"
 #include "naqs/densitymatrix.hpp"
 #include "naqs/gates.hpp"
+#include "naqs/neldermead.hpp"
 #include "naqs/noise.hpp"
 #include "naqs/pauli.hpp"
 #include "naqs/rng.hpp"
@@ -411,6 +412,28 @@ int ref_sv_run_timed(void* h, const RefOp* ops, int64_t nops, double* ms) {
         s->run(c);
         const auto t1 = std::chrono::steady_clock::now();
         *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    });
+}
+
+// The reference's Nelder-Mead (proj/src/neldermead.cpp) on a C callback:
+// trace_out (capacity max_evals) receives every objective value, best_out
+// the best point; returns 0 / 1 / 2 like the other entry points.
+int ref_minimize(double (*f)(const double*, int, void*), void* ctx, const double* x0, int n, int max_evals,
+                 double x_tol, double f_tol, double initial_step, double* trace_out, int* evals, double* best_out,
+                 double* best_f, int* converged) {
+    return wrap([&] {
+        naqs::MinimizeOptions o;
+        o.max_evals = max_evals;
+        o.x_tol = x_tol;
+        o.f_tol = f_tol;
+        o.initial_step = initial_step;
+        const naqs::Objective obj = [&](const std::vector<double>& x) { return f(x.data(), int(x.size()), ctx); };
+        const naqs::MinimizeResult r = naqs::minimize(obj, std::vector<double>(x0, x0 + n), o);
+        for (size_t i = 0; i < r.trace.size(); ++i) trace_out[i] = r.trace[i];
+        *evals = r.iterations;
+        for (size_t i = 0; i < r.best_params.size(); ++i) best_out[i] = r.best_params[i];
+        *best_f = r.best_energy;
+        *converged = r.converged ? 1 : 0;
     });
 }
 

@@ -219,7 +219,8 @@ const JitKnobs& jit_knobs() {
     // Measured on B200 (random circuit, n = 30): direct loads with a 128-register
     // cap (512 threads / SM) beat the cp.async double buffer, whose extra 32-64 KB
     // of shared memory halves the resident CTAs.  -1 = auto (512 / threads).
-    static const JitKnobs k{env_int("NQ_JIT_PREFETCH", 0) != 0, env_int("NQ_JIT_MINB", -1), env_int("NQ_JIT_TMA", 0) != 0};
+    static const JitKnobs k{env_int("NQ_JIT_PREFETCH", 0) != 0, env_int("NQ_JIT_MINB", -1), env_int("NQ_JIT_TMA", 0) != 0,
+                            env_int("NQ_JIT_L2PF", 0)};
     return k;
 }
 
@@ -529,6 +530,19 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
           << "    { const double2* src = st + base + toff_ld;\n";
         for (int l = 0; l < E; ++l) s << "      a[" << l << "] = ld_stream(src + " << hex64(reg_off(L0, l, q)) << ");\n";
         s << "    }\n";
+        // L2 prefetch of a later tile (bulk, 256-byte chunks of the 16
+        // contiguous low amplitudes): its loads then hit L2 while this one computes
+        bool l2pf = kn.l2pf > 0 && !mirror && !xstore && m >= 8;
+        for (int b = 0; b < 4 && l2pf; ++b) l2pf = q[size_t(b)] == b;
+        if (l2pf) {
+            const int nch = SIZE / 16;
+            std::vector<int> qhi(q.begin() + 4, q.end());
+            s << "    { const long long rn = r + " << kn.l2pf << "ll * gridDim.x;\n"
+              << "      if (rn < ntiles" << (nch < T ? " && tid < " + std::to_string(nch) + "u" : "") << ")\n"
+              << "        prefetch_l2_bulk(st + (" << deposit_expr("(unsigned long long)rn", rest, true) << ") + ("
+              << deposit_expr("(unsigned long long)tid", qhi, true) << "), 256u);\n"
+              << "    }\n";
+        }
     }
     bool ug_pending = false;
     auto flush_ug = [&] {

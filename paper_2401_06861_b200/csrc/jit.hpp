@@ -30,6 +30,7 @@ struct JitKnobs {
     bool prefetch;
     int min_blocks;
     bool tma;  // NQ_JIT_TMA=1: next tile staged by bulk (TMA) copies on an mbarrier
+    int l2pf;  // NQ_JIT_L2PF=k: bulk L2 prefetch of the tile k iterations ahead (0 = off)
 };
 const JitKnobs& jit_knobs();
 

@@ -1,5 +1,6 @@
 """The reference's own doctest suites (proj/tests/test_gates_pauli.cpp,
-test_statevector.cpp, test_densitymatrix.cpp, test_noise.cpp, test_qasm.cpp)
+test_statevector.cpp, test_densitymatrix.cpp, test_noise.cpp, test_qasm.cpp,
+test_bench.cpp, test_tfim.cpp, test_vqe.cpp, test_neldermead.cpp)
 compiled unmodified against our headers and linked with our library
 (paper_2401_06861_b200/csrc/Makefile target `droptests`): the drop-in proof
 for the C++ boundary, run on the B200."""
