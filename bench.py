@@ -24,7 +24,8 @@ gates per second (whole job), plus achieved HBM GB/s.
             same circuit.
 For N > 1 (torchrun) the state is ONE sharded state of 30 + log2(N) qubits
 (2^30 amplitudes per GPU: weak scaling); non-diagonal gates on the log2(N)
-global qubits trigger NCCL half-shard exchanges.
+global qubits trigger half-shard exchanges over NVLink peer memory, fused into
+the preceding pass when a second copy of the shard fits.
 """
 from __future__ import annotations
 
@@ -592,7 +593,7 @@ def main():
                                    f"(proj/tests/test_util.hpp generator)",
                        "qubits": n, "depth": depth, "state_bytes": 16 << n,
                        "parallelism": "single" if world == 1 else
-                       f"sharded x{world}: {g} global qubits, NCCL half-shard exchanges",
+                       f"sharded x{world}: {g} global qubits; half-shard exchanges over NVLink peer memory, fused into the preceding pass",
                        "local_qubits": n_local,
                        "warmup_steps_run": warm,
                        "unit_note": (f"gates/s of {n_local}-qubit gate equivalents: each gate on the {n}-qubit "
