@@ -193,6 +193,11 @@ void configure_caps(PlanOptions& p) {
         p.max_ops_per_pass = 192;
         p.max_pool_per_pass = 1536;
     }
+    static const int cap = [] {
+        const char* e = std::getenv("NQ_MAX_OPS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (cap > 0) p.max_ops_per_pass = cap;  // A/B measurements
 }
 
 void state_free(State& s) {

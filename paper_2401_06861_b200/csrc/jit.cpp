@@ -210,6 +210,20 @@ std::string swz_expr(const std::string& x, const Swizzle& sw) {
 }  // namespace
 
 // NQ_DIAG_SKIP=1: runtime test of each hoisted diagonal factor (A/B).
+// Pending register permutation (NQ_JIT_PX=0 disables): an X whose controls
+// lie outside the register slots (thread / tile / global bits) is not applied
+// to the registers but XOR-ed into a per-thread mask px (the true amplitude
+// of register index l is a[l ^ px]); later operators read their matrices
+// conjugated by it, diagonals index their tables through it, and relayouts
+// and stores XOR it into their addresses, where it disappears.  Ops that need
+// the registers in true order (register-controlled X, k >= 3 operators,
+// sparse k <= 2 operators, depolarizing maps) first apply the pending bits
+// they touch.
+bool px_enabled() {
+    static const bool on = env_int("NQ_JIT_PX", 1) != 0;
+    return on;
+}
+
 bool diag_runtime_skip() {
     static const bool on = env_int("NQ_DIAG_SKIP", 0) != 0;
     return on;
@@ -544,6 +558,37 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
               << "    }\n";
         }
     }
+    // pending-permutation state (see px_enabled): dirty = register slots
+    // whose px bit may be set at this point of the program
+    const bool use_px = px_enabled() && !mirror;
+    unsigned dirty = 0;
+    if (use_px) s << "    unsigned px = 0u;\n";
+    auto px_bit = [](int b) { return "((px >> " + std::to_string(b) + ") & 1u)"; };
+    auto commit = [&](unsigned mask) {
+        const unsigned m = dirty & mask;
+        for (int b = 0; b < 4; ++b)
+            if ((m >> b) & 1u) s << "    if (px & " << (1u << b) << "u) xperm<" << E << ", " << b << ">(a, 0u);\n";
+        if (m) s << "    px &= ~" << m << "u;\n";
+        dirty &= ~m;
+    };
+    // swizzled shared-memory offset of the pending permutation in layout A
+    auto px_smem_xor = [&](const Layout& A) {
+        std::ostringstream rc;
+        rc << "0u";
+        for (int b = 0; b < A.r; ++b)
+            if ((dirty >> b) & 1u) rc << " | (" << px_bit(b) << " << " << A.rp[b] << ")";
+        s << "    const unsigned rcx" << " = " << rc.str() << ";\n"
+          << "    const unsigned kx = " << swz_expr("rcx", sw) << ";\n";
+    };
+    // state offset of the pending permutation at the store (layout A, positions pos)
+    auto px_state_xor = [&](const Layout& A, const std::vector<int>& pos) {
+        std::ostringstream o;
+        o << "0ull";
+        for (int b = 0; b < A.r; ++b)
+            if ((dirty >> b) & 1u)
+                o << " | ((unsigned long long)" << px_bit(b) << " << " << pos[size_t(A.rp[b])] << ")";
+        return o.str();
+    };
     bool ug_pending = false;
     auto flush_ug = [&] {
         if (!ug_pending) return;
@@ -563,8 +608,17 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
             const Layout& A = lays[size_t(li - 1)];
             flush_ug();
             s << "    __syncthreads();\n";
-            for (int l = 0; l < E; ++l)
-                s << "    cur[sw" << (li - 1) << " ^ " << sw.apply(A.rconst(l)) << "u] = a[" << l << "];\n";
+            if (use_px && dirty) {
+                s << "    {\n";
+                px_smem_xor(A);
+                for (int l = 0; l < E; ++l)
+                    s << "    cur[sw" << (li - 1) << " ^ " << sw.apply(A.rconst(l)) << "u ^ kx] = a[" << l << "];\n";
+                s << "    }\n    px = 0u;\n";
+                dirty = 0;
+            } else {
+                for (int l = 0; l < E; ++l)
+                    s << "    cur[sw" << (li - 1) << " ^ " << sw.apply(A.rconst(l)) << "u] = a[" << l << "];\n";
+            }
             s << "    __syncthreads();\n";
             for (int l = 0; l < E; ++l)
                 s << "    a[" << l << "] = cur[sw" << li << " ^ " << sw.apply(L.rconst(l)) << "u];\n";
@@ -580,7 +634,23 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
                 generic += v.real() != 0.0 && v.imag() != 0.0;
             }
             const char* R = real ? ", true" : "";
-            if (op.k <= 2 && !real && generic < nent) {
+            unsigned slots = 0;
+            for (int j = 0; j < op.k; ++j) slots |= 1u << op.pos[j];
+            const bool sparse = op.k <= 2 && !real && generic < nent;
+            if (use_px && (dirty & slots)) {
+                if (op.k == 1 && !sparse) {
+                    s << "    d1f<" << E << ", " << int(op.pos[0]) << R << ">(a, " << P << ", " << px_bit(op.pos[0])
+                      << " * 3u);\n";
+                    break;
+                }
+                if (op.k == 2 && !sparse) {
+                    s << "    d2f<" << E << ", " << int(op.pos[0]) << ", " << int(op.pos[1]) << R << ">(a, " << P << ", ("
+                      << px_bit(op.pos[0]) << " | (" << px_bit(op.pos[1]) << " << 1)) * 5u);\n";
+                    break;
+                }
+                commit(slots);
+            }
+            if (sparse) {
                 s << sparse_dense(op, pool + op.mat, E, P);
             } else if (op.k == 1) {
                 s << "    d1<" << E << ", " << int(op.pos[0]) << R << ">(a, " << P << ");\n";
@@ -593,10 +663,20 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
             }
             break;
         }
-        case MOP_SWAP:
-            s << "    swp<" << E << ", " << int(op.pos[0]) << ", " << int(op.pos[1]) << ">(a);\n";
+        case MOP_SWAP: {
+            const int j0 = op.pos[0], j1 = op.pos[1];
+            if (use_px && (dirty & ((1u << j0) | (1u << j1)))) {
+                // SWAP(j0, j1) . X^px = X^swap(px) . SWAP(j0, j1)
+                s << "    px = (px & ~" << ((1u << j0) | (1u << j1)) << "u) | (" << px_bit(j0) << " << " << j1 << ") | ("
+                  << px_bit(j1) << " << " << j0 << ");\n";
+                const unsigned d0 = (dirty >> j0) & 1u, d1 = (dirty >> j1) & 1u;
+                dirty = (dirty & ~((1u << j0) | (1u << j1))) | (d0 << j1) | (d1 << j0);
+            }
+            s << "    swp<" << E << ", " << j0 << ", " << j1 << ">(a);\n";
             break;
+        }
         case MOP_DEPOL:
+            if (use_px) commit(0xFu);
             if (op.k == 2) {
                 const int a0 = std::min(op.pos[0], op.pos[1]), a1 = std::max(op.pos[0], op.pos[1]);
                 s << "    dep2<" << E << ", " << a0 << ", " << a1 << ">(a, lds(" << P << ").x, lds(" << P << " + 1).x);\n";
@@ -618,8 +698,27 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
                 if (slot >= 0) cmL |= 1u << slot;
                 else cmT |= 1u << p;
             }
-            s << "    if (((full & " << hex64(op.cmask_glob) << ") == " << hex64(op.cmask_glob) << ") && ((" << tbn
-              << " & " << cmT << "u) == " << cmT << "u)) xperm<" << E << ", " << int(op.pos[0]) << ">(a, " << cmL << "u);\n";
+            const std::string cond = "((full & " + hex64(op.cmask_glob) + ") == " + hex64(op.cmask_glob) + ") && ((" +
+                                     tbn + " & " + std::to_string(cmT) + "u) == " + std::to_string(cmT) + "u)";
+            if (use_px && cmL == 0 && (op.cmask_glob != 0 || cmT != 0)) {
+                // controls outside the registers: record the X, move nothing
+                s << "    px ^= (" << cond << " ? 1u : 0u) << " << int(op.pos[0]) << ";\n";
+                dirty |= 1u << op.pos[0];
+                break;
+            }
+            const bool trivial = op.cmask_glob == 0 && cmT == 0;
+            if (use_px && trivial && __builtin_popcount(cmL) == 1 && (dirty & cmL)) {
+                // CX with its register control c pending: on the registers it is
+                // the plain CX when px_c = 0, and the CX followed by an X on the
+                // target when px_c = 1 -- which is recorded, not moved
+                const int c = __builtin_ctz(cmL);
+                s << "    xperm<" << E << ", " << int(op.pos[0]) << ">(a, " << cmL << "u);\n"
+                  << "    px ^= " << px_bit(c) << " << " << int(op.pos[0]) << ";\n";
+                dirty |= 1u << op.pos[0];
+                break;
+            }
+            if (use_px) commit(cmL);
+            s << "    if (" << cond << ") xperm<" << E << ", " << int(op.pos[0]) << ">(a, " << cmL << "u);\n";
             break;
         }
         case MOP_DIAG: {
@@ -645,6 +744,34 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
             }
             const cplx* tab = pool + op.mat;
             s << "    { const unsigned g = " << g.str() << "; const double2* D = " << P << " + g;\n";
+            unsigned dslots = 0;
+            for (int t = 0; t < 4; ++t)
+                if (slotc[t]) dslots |= 1u << t;
+            if (anyreg && use_px && (dirty & dslots)) {
+                // table entries selected through the pending permutation
+                std::ostringstream gx;
+                gx << "0u";
+                for (int t = 0; t < 4; ++t)
+                    if (((dirty & dslots) >> t) & 1u) gx << " | (" << px_bit(t) << " * " << slotc[t] << "u)";
+                s << "      const unsigned gx = " << gx.str() << ";\n";
+                std::map<unsigned, int> fidx;
+                std::ostringstream body;
+                for (int l = 0; l < E; ++l) {
+                    unsigned c = 0;
+                    for (int t = 0; t < 4; ++t)
+                        if ((l >> t) & 1) c |= slotc[t];
+                    auto it = fidx.find(c);
+                    if (it == fidx.end()) {
+                        const int id = int(fidx.size());
+                        fidx[c] = id;
+                        s << "      const double2 f" << id << " = lds(D + (" << c << "u ^ gx));\n";
+                        it = fidx.find(c);
+                    }
+                    body << "      a[" << l << "] = cmul(f" << it->second << ", a[" << l << "]);\n";
+                }
+                s << body.str() << "    }\n";
+                break;
+            }
             if (!anyreg) {
                 // a factor uniform over the thread's amplitudes: accumulate it and
                 // apply the product once (scalars commute with every in-thread op)
@@ -700,24 +827,37 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
         // relabelled stores hit addresses other threads load)
         const std::string swN = "sw" + std::to_string(lays.size() - 1);
         s << "    __syncthreads();\n";
-        for (int l = 0; l < E; ++l)
-            s << "    cur[" << swN << " ^ " << sw.apply(LN.rconst(l)) << "u] = a[" << l << "];\n";
+        if (use_px && dirty) {
+            s << "    {\n";
+            px_smem_xor(LN);
+            for (int l = 0; l < E; ++l)
+                s << "    cur[" << swN << " ^ " << sw.apply(LN.rconst(l)) << "u ^ kx] = a[" << l << "];\n";
+            s << "    }\n    px = 0u;\n";
+            dirty = 0;
+        } else {
+            for (int l = 0; l < E; ++l)
+                s << "    cur[" << swN << " ^ " << sw.apply(LN.rconst(l)) << "u] = a[" << l << "];\n";
+        }
         s << "    __syncthreads();\n";
         for (int l = 0; l < E; ++l) s << "    a[" << l << "] = cur[swS ^ " << sw.apply(LS.rconst(l)) << "u];\n";
     }
     const Layout& LST = extra_relayout ? LS : LN;
+    // pending permutation: register l holds the amplitude of index l ^ px
+    const std::string pxo = (use_px && dirty) ? " ^ pxo" : "";
+    if (use_px && dirty) s << "    const unsigned long long pxo = " << px_state_xor(LST, qst) << ";\n";
     if (xstore) {
         // exchange store (sharded states): element o whose bit v (xmask)
         // differs from this rank's bit (xval) goes to the partner's buffer at
         // o ^ xmask, the rest to the local output buffer (out of place)
         s << "    { const unsigned long long ob = base + toff_st;\n";
         for (int l = 0; l < E; ++l)
-            s << "      { const unsigned long long o = ob + " << hex64(reg_off(LST, l, qst))
+            s << "      { const unsigned long long o = ob + (" << hex64(reg_off(LST, l, qst)) << pxo << ")"
               << "; st_stream(((o ^ xval) & xmask) ? xout_r + (o ^ xmask) : xout_l + o, a[" << l << "]); }\n";
         s << "    }\n";
     } else {
         s << "    { double2* dst = st + base + toff_st;\n";
-        for (int l = 0; l < E; ++l) s << "      st_stream(dst + " << hex64(reg_off(LST, l, qst)) << ", a[" << l << "]);\n";
+        for (int l = 0; l < E; ++l)
+            s << "      st_stream(dst + (" << hex64(reg_off(LST, l, qst)) << pxo << "), a[" << l << "]);\n";
         s << "    }\n";
     }
     if (mirror) {

@@ -106,6 +106,42 @@ __device__ __forceinline__ void d1(double2 (&a)[E], const double2* u) {
     }
 }
 
+// d1 / d2 on registers that hold a pending X permutation (jit.cpp: the
+// true amplitude of register l is a[l ^ px]): the operator conjugated by
+// that X, i.e. entry e read at e ^ f (f = 3 p for k = 1, 5 p for k = 2 with p
+// the pending bits of the operator's slots).
+template <int E, int J, bool R = false>
+__device__ __forceinline__ void d1f(double2 (&a)[E], const double2* u, unsigned f) {
+    const double2 u00 = lds(u + f), u01 = lds(u + (1u ^ f)), u10 = lds(u + (2u ^ f)), u11 = lds(u + (3u ^ f));
+#pragma unroll
+    for (int l = 0; l < E; ++l) {
+        if ((l >> J) & 1) continue;
+        const int h = l | (1 << J);
+        const double2 x0 = a[l], x1 = a[h];
+        a[l] = mfma<R>(u00, x0, mmul<R>(u01, x1));
+        a[h] = mfma<R>(u10, x0, mmul<R>(u11, x1));
+    }
+}
+
+template <int E, int J0, int J1, bool R = false>
+__device__ __forceinline__ void d2f(double2 (&a)[E], const double2* u, unsigned f) {
+#pragma unroll
+    for (int l = 0; l < E; ++l) {
+        if (((l >> J0) & 1) || ((l >> J1) & 1)) continue;
+        const int i0 = l, i1 = l | (1 << J0), i2 = l | (1 << J1), i3 = l | (1 << J0) | (1 << J1);
+        const double2 x0 = a[i0], x1 = a[i1], x2 = a[i2], x3 = a[i3];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const unsigned e = 4u * unsigned(r);
+            double2 acc = mmul<R>(lds(u + (e ^ f)), x0);
+            acc = mfma<R>(lds(u + ((e + 1u) ^ f)), x1, acc);
+            acc = mfma<R>(lds(u + ((e + 2u) ^ f)), x2, acc);
+            acc = mfma<R>(lds(u + ((e + 3u) ^ f)), x3, acc);
+            a[r == 0 ? i0 : r == 1 ? i1 : r == 2 ? i2 : i3] = acc;
+        }
+    }
+}
+
 template <int E, int J0, int J1, bool R = false>
 __device__ __forceinline__ void d2(double2 (&a)[E], const double2* u) {
 #pragma unroll

@@ -33,6 +33,23 @@ SCRIPT = textwrap.dedent(
         sv.reset()
         sv.apply(ops)
         assert np.array_equal(sv.amplitudes(), got)
+    # permutation-heavy circuits: X-type gates whose controls sit on thread,
+    # tile or global bits are recorded in the pending register permutation
+    # (jit.cpp px) and must come out right through every later op kind
+    prng = np.random.default_rng(99)
+    kinds = [("cx", 2, 0), ("cx", 2, 0), ("ccx", 3, 0), ("swap", 2, 0), ("x", 1, 0), ("y", 1, 0), ("ry", 1, 1),
+             ("u3", 1, 3), ("h", 1, 0), ("t", 1, 0), ("rz", 1, 1), ("cz", 2, 0), ("s", 1, 0)]
+    for n, tile, seed in [(12, 8, 11), (15, 10, 12), (18, 11, 13), (21, 12, 14)]:
+        circ = []
+        for _ in range(300):
+            k, ar, npar = kinds[int(prng.integers(len(kinds)))]
+            qs = [int(q) for q in prng.choice(n, size=ar, replace=False)]
+            circ.append((k, qs, [float(v) for v in prng.uniform(-3, 3, size=npar)]))
+        for layers in range(2):  # a CX ladder (VQE ansatz shape)
+            circ += [("cx", [i, i + 1], []) for i in range(n - 1)] + [("ry", [q], [0.1 * q + 0.3]) for q in range(n)]
+        sv = abi.SV(n, tile_qubits=tile)
+        sv.apply(abi.make_ops(circ))
+        worst = max(worst, float(np.max(np.abs(sv.amplitudes() - port.sv_run(n, circ)))))
     # density matrix with noise (Liouville superoperators, depolarizing maps);
     # n >= 6 runs the Hermitian (mirror) passes on the interleaved layout
     for n in (5, 6, 8, 9):
@@ -71,8 +88,9 @@ SCRIPT = textwrap.dedent(
 )
 
 
-def test_specialised_kernels_match_oracle():
-    env = dict(os.environ, NQ_JIT="sync")
+@pytest.mark.parametrize("px", ["1", "0"])
+def test_specialised_kernels_match_oracle(px):
+    env = dict(os.environ, NQ_JIT="sync", NQ_JIT_PX=px)
     code = SCRIPT.format(root=ROOT, oracle=os.path.join(ROOT, "oracle"))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
