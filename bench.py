@@ -305,6 +305,19 @@ def secondary_workloads(abi, workloads, device):
     t0 = time.perf_counter()
     z = naqs.density_expectation(circ, "Z" + "I" * (nd - 1), model)
     dt = time.perf_counter() - t0
+    # C4: noisy QAOA-MaxCut ring (p = 2), same calibration, <Z0 Z1>
+    qc = naqs.Circuit(nd)
+    for name, qs, ps in workloads.qaoa_ring(nd, 2):
+        qc.add(name, qs, ps)
+    zz = "ZZ" + "I" * (nd - 2)
+    naqs.density_expectation(qc, zz, model)
+    abi.jit_wait()
+    naqs.density_expectation(qc, zz, model)
+    t0 = time.perf_counter()
+    zzq = naqs.density_expectation(qc, zz, model)
+    out["dm_noisy_qaoa14"] = {"wall_s": time.perf_counter() - t0, "z0z1": zzq, "gates": len(qc),
+                              "note": "QAOA-MaxCut ring p=2 (h; cx.rz.cx per edge; rx), end to end via "
+                                      "naqs.density_expectation"}
     # C4 upper end: n = 16 (4^16 entries = 69 GB; beyond the reference's
     # 14-qubit guard, so GPU only)
     nd16 = 16

@@ -113,3 +113,21 @@ def test_dm_guard_and_errors():
         d.apply([("measure", [0])])
     d.apply([("id", [0]), ("barrier", [0])])
     assert d.rho()[0, 0] == 1.0
+
+
+@pytest.mark.parametrize("n,kind", [(6, "qaoa"), (8, "qaoa"), (7, "tfim"), (9, "tfim")])
+def test_config_c4_circuits_noisy(port, n, kind):
+    """BASELINE config C4 shapes (noisy TFIM Trotter / QAOA-MaxCut ring, device
+    noise from a synthetic calibration) through the drop-in API, n >= 6 on the
+    Hermitian (mirror) passes, against the oracle's blockwise Kraus sums."""
+    from paper_2401_06861_b200 import naqs, workloads
+    from oracle import list_to_ops
+
+    ops = workloads.qaoa_ring(n, 2) if kind == "qaoa" else workloads.tfim_trotter(n, 0.3, steps=4)
+    noise = NoiseSpec(n)
+    circ = naqs.Circuit(n)
+    for name, qs, ps in ops:
+        circ.add(name, qs, ps)
+    rho = naqs.run_density(circ, naqs.load_calibration(noise.calibration_json()))
+    want = port.dm_run_noisy(n, list_to_ops(ops), noise)
+    np.testing.assert_allclose(rho, want, atol=TOL, rtol=0)
