@@ -169,6 +169,8 @@ void state_init(State& s, int n, bool dm, const nq_opts* opts) {
     // NQ_LOW_BITS_DM for density matrices
     if (!dm) {
         if (const char* e = std::getenv("NQ_LOW_BITS")) s.popt.low_bits = std::max(0, std::min(std::atoi(e), 7));
+        if (const char* e = std::getenv("NQ_TILE_SV"); e && o.tile_qubits <= 0)
+            s.popt.tile_bits = std::max(4, std::min(std::atoi(e), kMaxTileBits));
     }
     if (dm) {
         if (const char* e = std::getenv("NQ_TILE_DM"); e && o.tile_qubits <= 0)
