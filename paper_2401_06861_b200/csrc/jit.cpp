@@ -224,6 +224,20 @@ bool px_enabled() {
     return on;
 }
 
+// Warp-local relayouts (opt-in, NQ_JIT_WARPLOCAL=1): when a pass leaves at
+// least as many tile bits out of every register set as there are warp bits,
+// those bits become the warp index in every layout, so each warp only ever
+// exchanges amplitudes with itself through shared memory and the relayout
+// barriers are __syncwarp instead of __syncthreads (warps drift apart and
+// overlap their load, compute and store phases).  Measured slower on B200
+// (random-30 4044 -> 3750 gates/s, VQE-28 18.1 -> 24 ms, QFT-30 96 -> 105-110
+// ms): the warp bits must be tiles bits no register set uses, which pushes
+// the lanes onto higher tile bits (less coalesced per instruction).
+bool warplocal_enabled() {
+    static const bool on = env_int("NQ_JIT_WARPLOCAL", 0) != 0;
+    return on;
+}
+
 bool diag_runtime_skip() {
     static const bool on = env_int("NQ_DIAG_SKIP", 0) != 0;
     return on;
@@ -375,7 +389,41 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
     if (relabel && lays.size() >= 2) lays.back() = by_store(lays.back());
     const bool extra_relayout = relabel && lays.size() == 1;
     if (extra_relayout) mirror = false;  // (full tiles then; the mirror store path expects the last layout)
-    const Layout LS = by_store(lays.back());
+    Layout LS = by_store(lays.back());
+    // warp-local relayouts (see warplocal_enabled)
+    bool warp_local = false;
+    {
+        const int nwb = logT - 5;  // warp-index bits of the thread id
+        bool ok = warplocal_enabled() && !mirror && !kn0.prefetch && !use_tma && nwb >= 1 && lays.size() >= 2;
+        for (int i = 1; i < h.nops && ok; ++i) ok = !(ops[i].type == MOP_DENSE && ops[i].k >= 4);
+        unsigned used = 0;
+        for (const auto& L : lays)
+            for (int j = 0; j < L.r; ++j) used |= 1u << L.rp[j];
+        std::vector<int> fr;
+        for (int b = m - 1; b >= 0 && int(fr.size()) < nwb; --b)
+            if (!((used >> b) & 1u)) fr.push_back(b);
+        ok = ok && int(fr.size()) == nwb;
+        if (ok) {
+            std::reverse(fr.begin(), fr.end());
+            auto force = [&](Layout L) {
+                std::vector<int> rest_bits;
+                for (int b : L.nonr)
+                    if (std::find(fr.begin(), fr.end(), b) == fr.end()) rest_bits.push_back(b);
+                L.nonr = rest_bits;
+                L.nonr.insert(L.nonr.end(), fr.begin(), fr.end());
+                return L;
+            };
+            std::vector<Layout> wl;
+            for (const auto& L : lays) wl.push_back(force(L));
+            // (the lanes may move to higher tile bits: every thread's registers
+            // still cover whole 256-byte runs, and L2 merges the sectors)
+            if (ok) {
+                lays = wl;
+                LS = force(LS);
+                warp_local = true;
+            }
+        }
+    }
     std::vector<Layout> sw_lays = lays;
     if (extra_relayout) sw_lays.push_back(LS);
     const Swizzle sw = choose_swizzle(sw_lays, m);
@@ -589,6 +637,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
                 o << " | ((unsigned long long)" << px_bit(b) << " << " << pos[size_t(A.rp[b])] << ")";
         return o.str();
     };
+    bool full_barrier_done = false;
     bool ug_pending = false;
     auto flush_ug = [&] {
         if (!ug_pending) return;
@@ -607,7 +656,13 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
         case MOP_LAYOUT: {
             const Layout& A = lays[size_t(li - 1)];
             flush_ug();
-            s << "    __syncthreads();\n";
+            // warp-local: intra-warp exchange; a relabelled pass still needs one
+            // full barrier after every warp has consumed its loads (its stores
+            // hit addresses other warps load), taken at the first relayout
+            const char* bar1 = warp_local ? "__syncwarp()" : "__syncthreads()";
+            const char* bar2 = (warp_local && !(relabel && !full_barrier_done)) ? "__syncwarp()" : "__syncthreads()";
+            full_barrier_done = true;
+            s << "    " << bar1 << ";\n";
             if (use_px && dirty) {
                 s << "    {\n";
                 px_smem_xor(A);
@@ -619,7 +674,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
                 for (int l = 0; l < E; ++l)
                     s << "    cur[sw" << (li - 1) << " ^ " << sw.apply(A.rconst(l)) << "u] = a[" << l << "];\n";
             }
-            s << "    __syncthreads();\n";
+            s << "    " << bar2 << ";\n";
             for (int l = 0; l < E; ++l)
                 s << "    a[" << l << "] = cur[sw" << li << " ^ " << sw.apply(L.rconst(l)) << "u];\n";
             break;
@@ -871,7 +926,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
         s << "    }\n";
     }
     s << ""
-      << "    __syncthreads();\n"
+      << (warp_local ? "    __syncwarp();\n" : "    __syncthreads();\n")
       << "  }\n";
     if (kn.prefetch && !xstore) s << "  cp_async_wait<0>();\n";
     s << "}\n";
