@@ -778,7 +778,10 @@ nq_status nq_sv_probabilities(nq_sv* h, double* host_out) {
     return guard([&] {
         State& s = st(h);
         state_flush_normal(s);
-        if (s.world > 1) throw NqError{NQ_ERR_CONTRACT, "probabilities() of a sharded state: use sample"};
+        if (s.world > 1) {
+            shard_probabilities(s, host_out);
+            return;
+        }
         DeviceCtx& c = ctx_for(s.dev);
         const uint64_t chunk = std::min<uint64_t>(s.count, uint64_t(1) << 26);
         double* tmp = nullptr;
@@ -858,7 +861,10 @@ nq_status nq_sv_set_amplitudes(nq_sv* h, uint64_t offset, uint64_t count, const 
     return guard([&] {
         State& s = st(h);
         state_flush_normal(s);
-        if (s.world > 1) throw NqError{NQ_ERR_CONTRACT, "set_amplitudes on a sharded state is not supported"};
+        if (s.world > 1) {
+            shard_set_amplitudes(s, offset, count, host_in);
+            return;
+        }
         if (offset > s.count || count > s.count - offset)
             throw NqError{NQ_ERR_CONTRACT, "amplitude range out of bounds"};
         DeviceCtx& c = ctx_for(s.dev);

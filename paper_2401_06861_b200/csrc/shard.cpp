@@ -55,6 +55,7 @@ struct NcclApi {
     decltype(&::ncclRecv) Recv = nullptr;
     decltype(&::ncclAllGather) AllGather = nullptr;
     decltype(&::ncclAllReduce) AllReduce = nullptr;
+    decltype(&::ncclBroadcast) Broadcast = nullptr;
     decltype(&::ncclGetErrorString) GetErrorString = nullptr;
 };
 
@@ -83,6 +84,7 @@ NcclApi& nccl() {
         NQ_SYM(Recv, "ncclRecv");
         NQ_SYM(AllGather, "ncclAllGather");
         NQ_SYM(AllReduce, "ncclAllReduce");
+        NQ_SYM(Broadcast, "ncclBroadcast");
         NQ_SYM(GetErrorString, "ncclGetErrorString");
 #undef NQ_SYM
     });
@@ -100,6 +102,7 @@ NcclApi& nccl() {
 #define ncclRecv nccl().Recv
 #define ncclAllGather nccl().AllGather
 #define ncclAllReduce nccl().AllReduce
+#define ncclBroadcast nccl().Broadcast
 #define ncclGetErrorString nccl().GetErrorString
 
 #define NCCL_TRY(expr)                                                                                 \
@@ -126,6 +129,8 @@ struct ShardComm {
     double* d_flag = nullptr;  // 1-element buffer for the stream barrier
     double* gather = nullptr;  // allgather_doubles buffer
     size_t gather_cap = 0;
+    double* bcast = nullptr;   // shard_probabilities chunk buffer
+    size_t bcast_cap = 0;
     double2* sendbuf = nullptr;
     double2* recvbuf = nullptr;
     uint64_t chunk = 0;  // amplitudes per bounce buffer
@@ -792,6 +797,7 @@ void shard_free(State& s) {
     if (sc->recvbuf) cudaFree(sc->recvbuf);
     if (sc->d_flag) cudaFree(sc->d_flag);
     if (sc->gather) cudaFree(sc->gather);
+    if (sc->bcast) cudaFree(sc->bcast);
     for (double2* p : sc->peer)
         if (p) cudaIpcCloseMemHandle(p);
     for (double2* p : sc->peer_alt)
@@ -987,6 +993,48 @@ void shard_sample(State& s, const double* sorted_u, uint64_t shots, uint64_t* id
             ++o;
         }
     *nout = o;
+}
+
+// probabilities() of a sharded state: every rank receives the full 2^n
+// vector (the reference API's contract), rank by rank in 512 MiB chunks
+// broadcast from the owning rank through one persistent device buffer.
+void shard_probabilities(State& s, double* host_out) {
+    normalize_map(s);
+    ShardComm& sc = *s.comm;
+    DeviceCtx& c = ctx_for(s.dev);
+    const uint64_t chunk = std::min<uint64_t>(s.count, uint64_t(1) << 26);
+    if (sc.bcast_cap < chunk) {
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        if (sc.bcast) CUDA_TRY(cudaFree(sc.bcast));
+        sc.bcast = nullptr;
+        CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&sc.bcast), chunk * sizeof(double)));
+        sc.bcast_cap = chunk;
+    }
+    for (int r = 0; r < s.world; ++r) {
+        for (uint64_t off = 0; off < s.count; off += chunk) {
+            const uint64_t len = std::min(chunk, s.count - off);
+            if (r == s.rank) launch_probs(s.d + off, len, sc.bcast, c.stream);
+            NCCL_TRY(ncclBroadcast(sc.bcast, sc.bcast, size_t(len), ncclDouble, r, sc.comm, c.stream));
+            CUDA_TRY(cudaMemcpyAsync(host_out + (uint64_t(r) << s.nloc) + off, sc.bcast, len * sizeof(double),
+                                     cudaMemcpyDeviceToHost, c.stream));
+        }
+    }
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
+}
+
+// set_amplitudes on a sharded state: every rank passes the same host range
+// and copies the part it owns (logical order).
+void shard_set_amplitudes(State& s, uint64_t offset, uint64_t count, const double* host_in) {
+    if (offset > (uint64_t(1) << s.n) || count > (uint64_t(1) << s.n) - offset)
+        throw NqError{NQ_ERR_CONTRACT, "amplitude range out of bounds"};
+    normalize_map(s);
+    DeviceCtx& c = ctx_for(s.dev);
+    const uint64_t lo = uint64_t(s.rank) << s.nloc, hi = lo + s.count;
+    const uint64_t a = std::max(offset, lo), b = std::min(offset + count, hi);
+    if (a < b)
+        CUDA_TRY(cudaMemcpyAsync(s.d + (a - lo), host_in + 2 * (a - offset), (b - a) * sizeof(double2),
+                                 cudaMemcpyHostToDevice, c.stream));
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
 }
 
 void shard_get_amplitudes(State& s, uint64_t offset, uint64_t count, double* host_out) {

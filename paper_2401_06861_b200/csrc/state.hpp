@@ -127,6 +127,8 @@ void shard_expectation(State& s, const uint64_t* flip, const uint64_t* signs, co
 void shard_sample(State& s, const double* sorted_u, uint64_t shots, uint64_t* idx_out, uint64_t* count_out,
                   uint64_t* nout);
 void shard_get_amplitudes(State& s, uint64_t offset, uint64_t count, double* host_out);
+void shard_probabilities(State& s, double* host_out);
+void shard_set_amplitudes(State& s, uint64_t offset, uint64_t count, const double* host_in);
 // restore the identity qubit map (physical order == logical order)
 void shard_normalize(State& s);
 

@@ -35,8 +35,18 @@ def _rank_main(rank, world, uid, n, seed, outdir, fused=True):
     u = np.sort(port.rng_double(99, 4000))
     idx, cnt = sv.sample_sorted(u)
     amps = sv.amplitudes()
+    probs = sv.probabilities()
+    # set_amplitudes: every rank passes the whole vector, then more gates
+    srng = np.random.default_rng(seed + 1)
+    psi = srng.normal(size=1 << n) + 1j * srng.normal(size=1 << n)
+    psi /= np.linalg.norm(psi)
+    sv.set_amplitudes(psi)
+    more = port.random_circuit(seed + 2, n, 120)
+    sv.apply(more)
+    after = sv.amplitudes()
     stats = sv.comm_stats()
-    np.savez(os.path.join(outdir, f"r{rank}.npz"), norm=norm, ex=ex, idx=idx, cnt=cnt, amps=amps,
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), norm=norm, ex=ex, idx=idx, cnt=cnt, amps=amps, probs=probs,
+             psi=psi, after=after,
              exchanges=stats["exchanges"], fused=stats["fused"], alt=stats["alt_buffer"],
              letters=np.array([t[0] for t in terms]),
              coeff=np.array([t[1] for t in terms]))
@@ -64,6 +74,9 @@ def test_sharded_gpus(port, tmp_path, n, world, fused):
         else:
             assert int(d["fused"]) == 0
         np.testing.assert_allclose(d["amps"], want, atol=1e-10, rtol=0)
+        np.testing.assert_allclose(d["probs"], np.abs(want) ** 2, atol=1e-12, rtol=0)
+        more = port.random_circuit(seed + 2, n, 120)
+        np.testing.assert_allclose(d["after"], port.sv_apply(d["psi"].copy(), more), atol=1e-10, rtol=0)
         assert abs(float(d["norm"]) - 1.0) < 1e-10
         ref = [port.expectation(want, str(L), float(c)) for L, c in zip(d["letters"], d["coeff"])]
         np.testing.assert_allclose(d["ex"], ref, atol=1e-10, rtol=0)
