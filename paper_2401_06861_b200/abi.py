@@ -549,7 +549,7 @@ def jit_debug(n: int, ops, pass_index: int, tile_qubits: int = 0, compile: bool 
     xs = 2 if xstore else 0
     check(lib.nq_jit_debug(n, arr.ctypes.data, len(arr), tile_qubits, pass_index, xs, None, 0, C.byref(size),
                            C.byref(ok)))
-    buf = C.create_string_buffer(size.value + 1 << 16)
+    buf = C.create_string_buffer(size.value + (1 << 16))
     check(lib.nq_jit_debug(n, arr.ctypes.data, len(arr), tile_qubits, pass_index, (1 if compile else 0) | xs, buf,
                            len(buf), C.byref(size), C.byref(ok)))
     return buf.raw[: size.value].decode(), ok.value

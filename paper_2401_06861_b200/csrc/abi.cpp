@@ -252,7 +252,8 @@ void trace_passes(const std::vector<PlannedPass>& passes, bool dm) {
     }
 }
 
-void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStats& st, bool record = true);
+void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStats& st, bool record = true,
+                std::atomic<void*>* memo = nullptr);
 bool layout_is_identity(const State& s);
 
 // Fused-schedule cache: a flush whose queue (kinds, bits, controls,
@@ -264,6 +265,9 @@ struct PlanCacheEntry {
     std::vector<PlannedPass> passes;
     PlanStats st;
     std::vector<int> layout_out;
+    // compiled kernel of each pass, remembered after its first specialised
+    // launch (shared by copies of the entry; see jit_launch's memo)
+    std::shared_ptr<std::vector<std::atomic<void*>>> kern;
 };
 
 std::vector<unsigned char> plan_key(const State& s, bool use_layout) {
@@ -309,18 +313,20 @@ void state_flush(State& s) {
             cache.push_front(e);
             if (use_layout) s.layout = e.layout_out;
             s.queue.clear();
-            run_passes(s, e.passes, e.st);
+            run_passes(s, e.passes, e.st, true, e.kern ? e.kern->data() : nullptr);
             return;
         }
     }
     std::vector<PlannedPass> passes = plan_passes(s.queue, s.popt, &st, use_layout ? &s.layout : nullptr);
     s.queue.clear();
+    auto kern = std::make_shared<std::vector<std::atomic<void*>>>(passes.size());
+    for (auto& k : *kern) k.store(nullptr);
     {
         std::lock_guard<std::mutex> lk(mu);
-        cache.push_front(PlanCacheEntry{std::move(key), passes, st, s.layout});
+        cache.push_front(PlanCacheEntry{std::move(key), passes, st, s.layout, kern});
         if (cache.size() > kCacheEntries) cache.pop_back();
     }
-    run_passes(s, passes, st);
+    run_passes(s, passes, st, true, kern->data());
 }
 
 bool layout_is_identity(const State& s) {
@@ -372,7 +378,8 @@ void state_flush_normal(State& s) {
     for (size_t b = 0; b < s.layout.size(); ++b) s.layout[b] = int(b);
 }
 
-void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStats& st, bool record) {
+void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStats& st, bool record,
+                std::atomic<void*>* memo) {
     DeviceCtx& c = ctx_for(s.dev);
     CUDA_TRY(cudaSetDevice(s.dev));
     std::vector<size_t> offs;
@@ -393,7 +400,8 @@ void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStat
         if (ev) CUDA_TRY(cudaEventRecord(ev->first, c.stream));
         const unsigned char* rec = buf.data() + offs[i];
         if (!jit_launch(s.d, c.d_ops + offs[i], h, reinterpret_cast<const MOp*>(rec + h.op_off),
-                        reinterpret_cast<const cplx*>(rec + h.pool_off), 0, c.stream, s.dev))
+                        reinterpret_cast<const cplx*>(rec + h.pool_off), 0, c.stream, s.dev, nullptr,
+                        memo ? memo + i : nullptr))
             launch_pass(s.d, c.d_ops + offs[i], h, 0, c.stream,
                         reinterpret_cast<const MOp*>(rec + h.op_off)[0].k);
         if (ev) CUDA_TRY(cudaEventRecord(ev->second, c.stream));

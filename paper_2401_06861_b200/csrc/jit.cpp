@@ -1134,10 +1134,14 @@ bool jit_xstore_ok(const PassHdr& h, const MOp* ops) {
 }
 
 bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,
-                uint64_t rankbase, cudaStream_t s, int device, const JitXStore* xs) {
+                uint64_t rankbase, cudaStream_t s, int device, const JitXStore* xs, std::atomic<void*>* memo) {
     const JitMode mode = jit_mode();
     std::shared_ptr<Entry> e;
-    if (xs) {
+    Entry* known = (memo && !xs) ? static_cast<Entry*>(memo->load(std::memory_order_acquire)) : nullptr;
+    if (known) {
+        // the JIT cache never drops entries: the remembered one stays valid
+        e = std::shared_ptr<Entry>(std::shared_ptr<Entry>{}, known);
+    } else if (xs) {
         if (!jit_xstore_ok(h, ops)) throw NqError{NQ_ERR_INTERNAL, "exchange pass cannot be specialised"};
         e = acquire(jit_source(h, ops, pool, true), device, JitMode::Sync);
         if (!e) throw NqError{NQ_ERR_INTERNAL, "exchange pass kernel failed to compile"};
@@ -1145,6 +1149,7 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
         if (mode == JitMode::Off || h.m < 8 || h.m > 12) return false;
         if (mode == JitMode::Auto && h.nloc < 18) return false;  // interpreter is fine for small states
         e = acquire(jit_source(h, ops, pool), device, mode);
+        if (e && memo) memo->store(e.get(), std::memory_order_release);
     }
     if (!e) return false;
     Jit& J = jit();

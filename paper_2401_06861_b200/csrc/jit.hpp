@@ -57,8 +57,12 @@ bool jit_xstore_ok(const PassHdr& h, const MOp* ops);
 // compilation otherwise, or compiling inline under NQ_JIT=sync).  Returns
 // false when the caller must run the interpreter kernel instead.
 // With xs: compiled synchronously if needed; throws when it cannot run.
+// memo (optional, in-place passes only): an opaque handle of the compiled
+// kernel remembered by the caller for this exact pass record (plan cache):
+// when set, the source is not regenerated and looked up again.
 bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,
-                uint64_t rankbase, cudaStream_t s, int device, const JitXStore* xs = nullptr);
+                uint64_t rankbase, cudaStream_t s, int device, const JitXStore* xs = nullptr,
+                std::atomic<void*>* memo = nullptr);
 
 // Expectation batch kernel specialised to the batch's term structure: source,
 // and launch (plus the per-term final sums into out[0..nt)); false when the

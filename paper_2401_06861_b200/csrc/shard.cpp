@@ -27,7 +27,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <deque>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -125,7 +127,15 @@ struct ShardComm {
     double2* alt = nullptr;
     std::vector<double2*> peer_alt;
     int64_t fused = 0;
-    std::unordered_map<uint64_t, std::vector<int>> rebalance_cache;  // see rebalance()  // acts_key -> ops moved per exchange
+    std::unordered_map<uint64_t, std::vector<int>> rebalance_cache;  // see rebalance()
+    // planned segments of recent flushes (repeated circuits replan nothing and
+    // reuse their kernels): key = segment ops incl. matrices + plan options
+    struct SegPlan {
+        std::vector<PlannedPass> passes;
+        PlanStats st;
+        std::shared_ptr<std::vector<std::atomic<void*>>> kern;
+    };
+    std::deque<std::pair<std::vector<unsigned char>, std::shared_ptr<SegPlan>>> seg_cache;  // acts_key -> ops moved per exchange
     double* d_flag = nullptr;  // 1-element buffer for the stream barrier
     double* gather = nullptr;  // allgather_doubles buffer
     size_t gather_cap = 0;
@@ -334,12 +344,57 @@ int rest_pos(const PassHdr& h, int v) {
     return 0;
 }
 
+std::vector<unsigned char> segment_key(const PlanOptions& o, const std::vector<EOp>& ops) {
+    std::vector<unsigned char> k;
+    auto put = [&](const void* p, size_t n) {
+        const unsigned char* b = static_cast<const unsigned char*>(p);
+        k.insert(k.end(), b, b + n);
+    };
+    const int32_t opts[] = {o.nbits, o.nloc, o.tile_bits, o.low_bits, o.fuse, o.reg_bits, o.max_ops_per_pass,
+                            o.max_pool_per_pass, o.stage_sched};
+    put(opts, sizeof opts);
+    for (const EOp& e : ops) {
+        const int32_t head[] = {int32_t(e.type), e.k, e.pair_next, int32_t(e.mat.size())};
+        put(head, sizeof head);
+        put(e.bits, size_t(e.k) * sizeof(int));
+        put(&e.ctrl, sizeof e.ctrl);
+        put(&e.src, sizeof e.src);
+        if (!e.mat.empty()) put(e.mat.data(), e.mat.size() * sizeof(cplx));
+    }
+    return k;
+}
+
 void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vector<int>* layout = nullptr,
                  FuseX* fx = nullptr) {
     PlanOptions po = s.popt;
     po.relabel = layout != nullptr;
     PlanStats st;
-    std::vector<PlannedPass> passes = plan_passes(ops, po, &st, layout);
+    std::vector<PlannedPass> passes;
+    std::shared_ptr<std::vector<std::atomic<void*>>> kern;
+    if (layout == nullptr) {
+        ShardComm& sc = *s.comm;
+        std::vector<unsigned char> key = segment_key(po, ops);
+        for (auto it = sc.seg_cache.begin(); it != sc.seg_cache.end(); ++it) {
+            if (it->first != key) continue;
+            passes = it->second->passes;
+            st = it->second->st;
+            kern = it->second->kern;
+            break;
+        }
+        if (!kern) {
+            passes = plan_passes(ops, po, &st, nullptr);
+            auto sp = std::make_shared<ShardComm::SegPlan>();
+            sp->passes = passes;
+            sp->st = st;
+            sp->kern = std::make_shared<std::vector<std::atomic<void*>>>(passes.size());
+            for (auto& k : *sp->kern) k.store(nullptr);
+            kern = sp->kern;
+            sc.seg_cache.emplace_front(std::move(key), std::move(sp));
+            if (sc.seg_cache.size() > 16) sc.seg_cache.pop_back();
+        }
+    } else {
+        passes = plan_passes(ops, po, &st, layout);
+    }
     if (s.rank == 0 && std::getenv("NQ_SHARD_TRACE"))
         std::fprintf(stderr, "[shard] segment: %zu ops -> %lld passes\n", ops.size(), (long long)st.passes);
     std::vector<size_t> offs;
@@ -373,7 +428,8 @@ void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vecto
                        c.stream, s.dev, &xs);
             fx->done = true;
         } else if (!jit_launch(s.d, c.d_ops + offs[i], h, mops,
-                        reinterpret_cast<const cplx*>(rec + h.pool_off), rankbase, c.stream, s.dev))
+                        reinterpret_cast<const cplx*>(rec + h.pool_off), rankbase, c.stream, s.dev, nullptr,
+                        kern ? kern->data() + i : nullptr))
             launch_pass(s.d, c.d_ops + offs[i], h, rankbase, c.stream,
                         reinterpret_cast<const MOp*>(rec + h.op_off)[0].k);
         if (ev) CUDA_TRY(cudaEventRecord(ev->second, c.stream));
