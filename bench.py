@@ -1,38 +1,48 @@
 #!/usr/bin/env python
 """Benchmark of the B200 SV/DM simulation core (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c2|c3]
 
 Headline workload: the reference's seeded random circuit
 (proj/tests/test_util.hpp generator, Rng(2024)), 30 qubits, depth 200, on one
 B200.  One step = the whole circuit applied to the HBM-resident 2^30-amplitude
 state through the C ABI (fusion planning + fused passes).  Metric: source
-gates per second (whole job), plus achieved HBM GB/s.
+gates per second (whole job), plus achieved HBM GB/s.  `--config c3` is
+SURVEY.md §8d C3: 33 local qubits per GPU, random_circuit(Rng(4040 + n)).
 
 * value     device time of K steps (CUDA events on the library's stream),
             barrier + synchronize on both sides, max over ranks.
 * e2e       the same steps through the reference-facing C ABI with host
             buffers: each step copies its op list host->device (pinned
             staging) and reads a <Z_0> expectation back device->host; timed
-            on the host clock around synchronised steps, max over ranks.
+            on the host clock around synchronised steps, max over ranks.  The
+            same circuit every step, so plans and kernels are cached
+            (`e2e.plan` says so); `e2e_fresh` runs a NEW random circuit per
+            step (planner + kernel specialisation paid inside the step).
 * roofline  the fused-pass kernel: algorithmic bytes per launch (32 * 2^n:
             every amplitude read and written once) / its average CUDA-event
             duration inside the timed region, against MEASURED_PEAKS.json.
-* cpu_baseline  the reference engine compiled from its own sources
-            (oracle/_ref, kind "reference"; the C restatement "port" if that
-            build is absent), on the host cores, on a bounded prefix of the
-            same circuit.
-For N > 1 (torchrun) the state is ONE sharded state of 30 + log2(N) qubits
-(2^30 amplitudes per GPU: weak scaling); non-diagonal gates on the log2(N)
-global qubits trigger half-shard exchanges over NVLink peer memory, fused into
-the preceding pass when a second copy of the shard fits.
+* parity    (N = 1, C2) the timed circuit re-run once from |0..0> and
+            compared with the reference engine's own state (oracle/_ref, the
+            reference's sources) on the same circuit: norm, <Z_q> for 8
+            qubits, 4096 amplitudes; 1e-10 absolute.
+* cpu_baseline  that same reference run (all host threads, the whole
+            200-op circuit) and a single-thread sample (the reference's bench
+            convention, proj/src/bench.cpp:19-28).
+For N > 1 the state is ONE sharded state of n_local + log2(N) qubits
+(2^n_local amplitudes per GPU: weak scaling); non-diagonal gates on the
+log2(N) global qubits trigger half-shard exchanges over NVLink peer memory
+(DESIGN.md §6).  `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks.
 """
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -42,6 +52,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+PARITY_TOL = 1e-10  # north_star: reference-matching within 1e-10 absolute (FP64)
+
 
 def parse_args():
     ap = argparse.ArgumentParser()
@@ -49,18 +61,84 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--qubits", type=int, default=30)
+    ap.add_argument("--config", choices=["c2", "c3"], default="c2",
+                    help="c2: random circuit, 30 local qubits, Rng(2024); c3: 33 local qubits, Rng(4040+n)")
+    ap.add_argument("--qubits", type=int, default=0, help="override the local qubits per GPU")
     ap.add_argument("--depth", type=int, default=200)
-    ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--seed", type=int, default=-1, help="override the generator seed")
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
-    ap.add_argument("--cpu-ops", type=int, default=12, help="ops of the circuit prefix timed on the CPU")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-fresh", action="store_true", help="skip the e2e_fresh leg")
+    ap.add_argument("--ref-chunk", type=int, default=12,
+                    help="reference arm: ops per step (steps walk the circuit in chunks of this many ops)")
+    ap.add_argument("--single-thread-ops", type=int, default=8,
+                    help="ops of the single-thread reference sample (proj/src/bench.cpp convention)")
     return ap.parse_args()
 
 
 # ---------------------------------------------------------------------------
-def dist_setup(args):
+def workload(args, world: int):
+    """(n, n_local, g, seed, depth) of the configuration on `world` GPUs."""
+    g = world.bit_length() - 1
+    if (1 << g) != world:
+        raise SystemExit("bench.py: the sharded state needs a power-of-two number of GPUs")
+    n_local = args.qubits or (33 if args.config == "c3" else 30)
+    n = n_local + g
+    if args.seed >= 0:
+        seed = args.seed
+    else:
+        seed = 4040 + n if args.config == "c3" else 2024
+    return n, n_local, g, seed, args.depth
+
+
+def workload_config(args, world: int) -> dict:
+    """The `config` object, identical in both arms (same keys, same values)."""
+    n, n_local, g, seed, depth = workload(args, world)
+    return {"workload": f"random_circuit(Rng({seed})) n={n} depth={depth} (proj/tests/test_util.hpp generator)",
+            "config": args.config, "qubits": n, "depth": depth, "seed": seed, "state_bytes": 16 << n,
+            "local_qubits": n_local,
+            "parallelism": "single" if world == 1 else
+            f"sharded x{world}: {g} global qubits; half-shard exchanges over NVLink peer memory",
+            "unit_note": (f"gates/s of {n_local}-qubit gate equivalents: each gate on the {n}-qubit state counts "
+                          f"{world} (2^{g}); whole-job aggregate over {world} GPU(s)"),
+            "l2": f"state ({(16 << n_local) / 2**30:g} GiB per GPU) >> L2 (126 MB): every pass streams from HBM"}
+
+
+def load_workloads():
+    """workloads.py by path: input generation only, and it keeps the package
+    (and its libnaqs_b200.so) out of the reference arm's process."""
+    path = os.path.join(ROOT, "paper_2401_06861_b200", "workloads.py")
+    spec = importlib.util.spec_from_file_location("nq_workloads", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def maybe_self_launch(args) -> None:
+    """`--gpus N` (N > 1) outside torchrun: re-run this command as N ranks."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None:
+        if args.gpus > 1:
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+            sys.stdout.flush()
+            sys.exit(subprocess.call(cmd))
+        return
+    if int(world_env) != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world_env} but --gpus {args.gpus}: launch one rank per GPU")
+
+
+def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -196,119 +274,328 @@ def host_mem_gib() -> float:
     return 0.0
 
 
-def cpu_reference_rate(n: int, ops, n_ops: int, reps: int):
-    """Gates/s of the reference engine on the host: `reps` timed runs of the
-    first `n_ops` ops on one persistent n-qubit state (all host threads)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import numpy as np
-    from oracle import Port, Ref, list_to_ops  # checker / baseline only
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
+
+def oracle_mod():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle  # checker / CPU baseline only
+
+    return oracle
+
+
+def ref_state_fits(n: int):
     need = (16 << n) / (1 << 30) * 1.3 + 2
     if host_mem_gib() < need:
-        return None, f"host RAM {host_mem_gib():.0f} GiB < {need:.0f} GiB needed for n={n}"
-    arr = list_to_ops(ops[:n_ops])
-    cores = cpu_threads()
-    if Ref.available():
-        ref = Ref()
-        ref.set_threads(cores)
-        h = ref.sv_new(n)
-        try:
-            times = [ref.sv_run_timed(h, arr) for _ in range(reps)]
-        finally:
-            ref.sv_free(h)
-        kind = "reference"
-    else:
-        port = Port()
-        amps = np.zeros(1 << n, dtype=np.complex128)
-        amps[0] = 1
-        times = []
-        for _ in range(reps):
-            t0 = time.perf_counter()
-            port.sv_apply(amps, arr)
-            times.append((time.perf_counter() - t0) * 1e3)
-        kind, cores = "port", 1
-    ms = statistics.median(times)
-    return {"value": n_ops / (ms / 1e3), "unit": "gates/s", "cores": cores, "kind": kind,
-            "sample": f"first {n_ops} ops of random_circuit(Rng(2024), n={n}, depth=200) on one persistent "
-                      f"2^{n} state, median of {reps} runs, OMP threads={cores}",
-            "ms_per_run": ms}, None
+        return f"host RAM {host_mem_gib():.0f} GiB < {need:.0f} GiB needed for an n={n} reference state"
+    return None
 
 
+# ---------------------------------------------------------------------------
 def run_reference_arm(args, world, rank):
+    """The reference engine (oracle/_ref: proj/src compiled unmodified) on the
+    host cores, same metric/unit/config as the b200 arm.  Each step is a
+    bounded sample: `--ref-chunk` consecutive ops of the circuit, the steps
+    walking through it (so K steps cover K * chunk ops, wrapping)."""
     if rank != 0:
         return 0
-    from paper_2401_06861_b200 import workloads
-
-    # The b200 arm runs 30 + log2(N) qubits on N GPUs and reports 30-qubit
-    # gate equivalents (a gate on 2^(30+g) amplitudes counts 2^g).  The
-    # reference rejects n > 30 (proj/include/naqs/statevector.hpp:22), so it is
-    # timed at n = 30, where its rate is already in that unit.
-    n = args.qubits
-    ops = workloads.random_circuit(args.seed, n, args.depth)
-    # bounded sample: fewer ops per step as the state doubles (a few s per step)
-    k = max(1, min(args.cpu_ops >> max(0, n - 30), len(ops)))
-    total_steps = args.warmup + args.steps
-    res, why = cpu_reference_rate(n, ops, k, total_steps)
+    orc = oracle_mod()
+    wl = load_workloads()
+    n, n_local, g, seed, depth = workload(args, world)
     base = {"metric": "SV gates/s (random circuit, depth 200)", "unit": "gates/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "config": {"workload": f"random_circuit(Rng({args.seed})) n={args.qubits} depth={args.depth} "
-                                   f"(proj/tests/test_util.hpp generator)",
-                       "qubits": args.qubits,
-                       "unit_note": "30-qubit gate equivalents; the reference accepts n <= 30 only, so for "
-                                    "N > 1 it is timed at n = 30 (the b200 arm runs 30 + log2 N qubits)"}}
-    if res is None:
-        emit({"impl": "reference", "unavailable": why})
+            "config": workload_config(args, world)}
+    if not orc.Ref.available():
+        emit(dict(base, unavailable="oracle/_ref/libnaqs_ref.so not built"))
         return 0
-    base.update({"value": res["value"], "ms_per_step": res["ms_per_run"], "dtype": "c128",
-                 "data": "synthetic", "scaling": "weak",
-                 "cpu_baseline": {k2: res[k2] for k2 in ("value", "unit", "cores", "kind", "sample")},
-                 "e2e": {"value": res["value"], "unit": "gates/s", "h2d_bytes_per_step": 0,
-                         "d2h_bytes_per_step": 0}})
+    # The reference rejects n > 30 (proj/include/naqs/statevector.hpp:22): it is
+    # timed on the same generator at min(n, 30) qubits and its rate converted to
+    # n_local-qubit gate equivalents (its kernels are O(2^n) sweeps).
+    n_ref = min(n, 30)
+    scale = 2.0 ** (n_ref - n_local)
+    why = ref_state_fits(n_ref)
+    if why:
+        emit(dict(base, unavailable=why))
+        return 0
+    ops = orc.list_to_ops(wl.random_circuit(seed if n_ref == n else (4040 + n_ref if args.config == "c3" else seed),
+                                            n_ref, depth))
+    ref = orc.Ref()
+    cores = ref.set_threads(cpu_threads())
+    h = ref.sv_new(n_ref)
+    k = max(1, min(args.ref_chunk, depth))
+    pos = 0
+
+    def chunk():
+        nonlocal pos
+        idx = [(pos + j) % depth for j in range(k)]
+        pos = (pos + k) % depth
+        return ops[idx]
+
+    try:
+        for _ in range(args.warmup):
+            ref.sv_run_timed(h, chunk())
+        times = [ref.sv_run_timed(h, chunk()) for _ in range(args.steps)]
+        total_ms = sum(times)
+        value = args.steps * k / (total_ms / 1e3) * scale
+        # the reference's own bench convention: one OpenMP thread
+        ref.set_threads(1)
+        st_ops = max(1, min(args.single_thread_ops, depth))
+        st_ms = ref.sv_run_timed(h, ops[:st_ops])
+        ref.set_threads(cores)
+    finally:
+        ref.sv_free(h)
+    sample = (f"steps walk random_circuit(n={n_ref}, depth={depth}) in chunks of {k} consecutive ops on one "
+              f"persistent 2^{n_ref} state ({args.steps} timed steps = {args.steps * k} ops), OMP threads={cores}")
+    if scale != 1.0:
+        sample += f"; rate x {scale:g} to {n_local}-qubit gate equivalents (reference guard n <= 30)"
+    base.update({"value": value, "ms_per_step": total_ms / args.steps, "dtype": "c128", "data": "synthetic",
+                 "scaling": "weak", "vs_baseline": None, "reference_qubits": n_ref,
+                 "cpu_baseline": {"value": value, "unit": "gates/s", "cores": cores, "kind": "reference",
+                                  "sample": sample, "cpu_model": cpu_model(),
+                                  "single_thread": {"value": st_ops / (st_ms / 1e3) * scale, "unit": "gates/s",
+                                                    "cores": 1, "sample": f"first {st_ops} ops, OMP threads=1"}},
+                 "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
     emit(base)
     return 0
 
 
 # ---------------------------------------------------------------------------
-def secondary_workloads(abi, workloads, device):
-    """Quick numbers for the other BASELINE.json configurations (device time)."""
+def spot_indices(n: int, windows: int = 64, width: int = 64, seed: int = 0):
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    starts = rng.integers(0, (1 << n) - width, size=windows)
+    starts[0] = 0  # include |0..0> and its neighbours
+    return [(int(s), width) for s in starts]
+
+
+def z_terms(n: int, qubits):
+    out = []
+    for q in qubits:
+        L = ["I"] * n
+        L[q] = "Z"
+        out.append(("".join(L), 1.0))
+    return out
+
+
+def headline_parity_and_baseline(abi, sv, n, ops_arr, ops_list, args):
+    """Re-run the timed circuit once from |0..0> and compare with the
+    reference engine's own state; the reference run doubles as the all-cores
+    CPU baseline over the whole circuit."""
+    import numpy as np
+
+    orc = oracle_mod()
+    if not orc.Ref.available():
+        return {"unavailable": "oracle/_ref not built"}, {"unavailable": "oracle/_ref not built"}
+    why = ref_state_fits(n)
+    if why:
+        return {"unavailable": why}, {"unavailable": why}
+    sv.reset()
+    sv.apply(ops_arr).flush()
+    sv.synchronize()
+    ref = orc.Ref()
+    cores = ref.set_threads(cpu_threads())
+    h = ref.sv_new(n)
+    try:
+        arr = orc.list_to_ops(ops_list)
+        ms = ref.sv_run_timed(h, arr)
+        qs = sorted({0, 1, n // 4, n // 2, n - 5, n - 3, n - 2, n - 1})[:8]
+        terms = z_terms(n, qs) + [("X" * 2 + "I" * (n - 4) + "Y" + "Z", 0.5)]
+        e_ref = ref.sv_expectations_h(h, n, terms)
+        norm_ref = ref.sv_norm_sq_h(h)
+        amp_err, amp_n = 0.0, 0
+        for off, w in spot_indices(n):
+            a = sv.amplitudes(off, w)
+            b = ref.sv_gather(h, np.arange(off, off + w))
+            amp_err = max(amp_err, float(np.max(np.abs(a - b))))
+            amp_n += w
+        e_gpu = sv.expectations(terms)
+        norm_gpu = sv.norm_sq()
+        st_ops = max(1, min(args.single_thread_ops, len(arr)))
+        ref.set_threads(1)
+        st_ms = ref.sv_run_timed(h, arr[:st_ops])
+        ref.set_threads(cores)
+    finally:
+        ref.sv_free(h)
+    exp_err = float(np.max(np.abs(e_gpu - e_ref)))
+    parity = {"against": "oracle/_ref (reference sources, all host threads), same circuit from |0..0>",
+              "amplitudes_checked": amp_n, "max_abs_amplitude_diff": amp_err,
+              "norm_sq_diff": abs(norm_gpu - norm_ref), "expectations": [t[0] for t in terms],
+              "max_abs_expectation_diff": exp_err, "tolerance": PARITY_TOL,
+              "pass": max(amp_err, exp_err, abs(norm_gpu - norm_ref)) <= PARITY_TOL}
+    base = {"value": len(arr) / (ms / 1e3), "unit": "gates/s", "cores": cores, "kind": "reference",
+            "sample": f"the whole {len(arr)}-op circuit once on a fresh 2^{n} state, OMP threads={cores}",
+            "cpu_model": cpu_model(),
+            "single_thread": {"value": st_ops / (st_ms / 1e3), "unit": "gates/s", "cores": 1,
+                              "sample": f"first {st_ops} ops, OMP threads=1 (proj/src/bench.cpp:19-28 convention)"}}
+    return parity, base
+
+
+def secondary_workloads(abi, workloads, device, args):
+    """The other BASELINE.json configurations, each with its parity check."""
+    import numpy as np
+
     out = {}
-    # C2b: QFT-30
+    orc = oracle_mod()
+    have_ref = orc.Ref.available()
+    # ---- C2b: QFT-30 (device time) + closed-form parity
     n = 30
-    ops = abi.make_ops(workloads.qft(n))
+    qops = workloads.qft(n)
+    ops = abi.make_ops(qops)
     sv = abi.SV(n, device=device)
     sv.apply(ops).flush()
     abi.jit_wait()
     sv.apply(ops).flush()
     sv.synchronize()
-    abi.profile_begin(device, per_pass_events=False)
+    abi.profile_begin(device, per_pass_events=True)
     reps = 2
     for _ in range(reps):
         sv.apply(ops).flush()
     p = abi.profile_end(device)
     st = sv.stats()
-    out["qft30"] = {"gates_per_s": reps * len(ops) / (p["region_ms"] / 1e3), "ms_per_circuit": p["region_ms"] / reps,
-                    "gates": len(ops), "passes_per_circuit": st["passes"]}
+    pass_ms = p["pass_ms"] / max(p["pass_launches"], 1)
+    peak, _ = measured_peaks()
+    row = {"gates_per_s": reps * len(ops) / (p["region_ms"] / 1e3), "ms_per_circuit": p["region_ms"] / reps,
+           "gates": len(ops), "passes_per_circuit": st["passes"],
+           "roofline": {"bound": "hbm", "avg_launch_ms": pass_ms,
+                        "achieved": (32 << n) / (pass_ms / 1e3) / 1e9, "peak": peak,
+                        "frac": (32 << n) / (pass_ms / 1e3) / 1e9 / peak, "unit": "GB/s"}}
+    if not args.no_parity:
+        sv.reset()
+        sv.apply(ops).flush()
+        starts = spot_indices(n, seed=1)
+        got = np.concatenate([sv.amplitudes(s, w) for s, w in starts])
+        want = np.concatenate([orc.qft_closed_form(n, np.arange(s0, s0 + w)) for s0, w in starts])
+        row["parity"] = {"against": "closed form of the QFT of the prep product state (pinned to oracle/_ref at "
+                                    "n <= 20, tests/test_scale_parity_cpu.py)",
+                         "amplitudes_checked": int(len(got)), "max_abs_amplitude_diff": float(np.max(np.abs(got - want))),
+                         "norm_sq_diff": abs(sv.norm_sq() - 1.0), "tolerance": PARITY_TOL,
+                         "pass": bool(np.max(np.abs(got - want)) <= PARITY_TOL)}
     sv.close()
-    # C4: noisy TFIM, DM n=14 (synthetic calibration), wall time of the schedule
+    if have_ref and not args.no_cpu_baseline and not ref_state_fits(n):
+        ref = orc.Ref()
+        cores = ref.set_threads(cpu_threads())
+        h = ref.sv_new(n)
+        try:
+            k = 50
+            ms = ref.sv_run_timed(h, orc.list_to_ops(qops[:k]))
+        finally:
+            ref.sv_free(h)
+        row["cpu"] = {"value": k / (ms / 1e3), "unit": "gates/s", "cores": cores,
+                      "sample": f"first {k} ops of the QFT-30 circuit"}
+    out["qft30"] = row
+
+    # ---- C5: VQE n=28 energy evaluations (exact, 193 gates + 55 terms)
+    nv, layers = 28, 3
+    params = workloads.vqe_initial_params(nv, layers)
+    vlist = workloads.vqe_ansatz(nv, layers, params)
+    vops = abi.make_ops(vlist)
+    terms = workloads.tfim_hamiltonian(nv)
+    sv = abi.SV(nv, device=device)
+    for _ in range(2):
+        sv.reset()
+        sv.apply(vops)
+        e = float(sum(sv.expectations(terms)))
+        abi.jit_wait()
+    sv.synchronize()
+    reps = 5
+    abi.profile_begin(device, per_pass_events=True)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        sv.reset()
+        sv.apply(vops)
+        e = float(sum(sv.expectations(terms)))
+    dt = (time.perf_counter() - t0) / reps
+    p = abi.profile_end(device)
+    pass_ms = p["pass_ms"] / max(p["pass_launches"], 1)
+    row = {"evals_per_s": 1.0 / dt, "ms_per_eval": dt * 1e3, "energy": e, "terms": len(terms), "gates": len(vops),
+           "passes_per_eval": sv.stats()["passes"],
+           "roofline": {"bound": "hbm", "avg_launch_ms": pass_ms, "achieved": (32 << nv) / (pass_ms / 1e3) / 1e9,
+                        "peak": peak, "frac": (32 << nv) / (pass_ms / 1e3) / 1e9 / peak, "unit": "GB/s"}}
+    sv.close()
+    if have_ref and not ref_state_fits(nv):
+        ref = orc.Ref()
+        cores = ref.set_threads(cpu_threads())
+        h = ref.sv_new(nv)
+        try:
+            t0 = time.perf_counter()
+            ref.sv_run_timed(h, orc.list_to_ops(vlist))
+            e_ref = float(np.sum(ref.sv_expectations_h(h, nv, terms)))
+            cpu_s = time.perf_counter() - t0
+        finally:
+            ref.sv_free(h)
+        row["parity"] = {"against": "oracle/_ref energy (193 gates + 55 terms)", "energy_ref": e_ref,
+                         "abs_diff": abs(e - e_ref), "tolerance": PARITY_TOL, "pass": abs(e - e_ref) <= PARITY_TOL}
+        row["cpu"] = {"evals_per_s": 1.0 / cpu_s, "ms_per_eval": cpu_s * 1e3, "cores": cores,
+                      "sample": "one whole exact evaluation (ansatz + 55-term energy) on a fresh state"}
+    out["vqe28"] = row
+
+    # ---- C4: noisy density matrices (synthetic calibration, SURVEY.md §8d)
     from paper_2401_06861_b200 import naqs
 
+    def model_for(nd):
+        cal = {"name": "synthetic",
+               "qubits": [{"t1_us": 60.0, "t2_us": 40.0, "readout_p01": 0.02, "readout_p10": 0.02}] * nd,
+               "default_1q": {"error": 0.001, "duration_ns": 50.0}, "default_2q": {"error": 0.01, "duration_ns": 300.0}}
+        return naqs.load_calibration(json.dumps(cal))
+
+    def circuit(nd, op_list):
+        c = naqs.Circuit(nd)
+        for name, qs, ps in op_list:
+            c.add(name, qs, ps)
+        return c
+
+    # n = 12: the whole noisy TFIM (10 Trotter steps) on both engines, full rho compared
+    n12 = 12
+    t12 = list(workloads.tfim_trotter(n12, 1.0, steps=10))
+    c12, m12 = circuit(n12, t12), model_for(n12)
+    naqs.run_density(c12, m12)
+    abi.jit_wait()
+    t0 = time.perf_counter()
+    rho = naqs.run_density(c12, m12)
+    gpu12 = time.perf_counter() - t0
+    row = {"wall_s": gpu12, "gates": len(t12), "note": "end to end via naqs.run_density (rho copied out)"}
+    cpu_per_gate12 = None
+    if have_ref:
+        spec = orc.NoiseSpec(n12)
+        ref = orc.Ref()
+        cores = ref.set_threads(cpu_threads())
+        t0 = time.perf_counter()
+        rho_ref = ref.dm_run_noisy(n12, t12, spec)
+        cpu12 = time.perf_counter() - t0
+        cpu_per_gate12 = cpu12 / len(t12)
+        err = float(np.max(np.abs(rho - rho_ref)))
+        row["parity"] = {"against": "oracle/_ref dm_run_noisy, full rho (4^12 entries)", "max_abs_entry_diff": err,
+                         "tolerance": PARITY_TOL, "pass": err <= PARITY_TOL}
+        row["cpu"] = {"wall_s": cpu12, "cores": cores, "sample": "the whole noisy circuit (dm_run_noisy)"}
+    out["dm_noisy_tfim12"] = row
+
     nd = 14
-    cal = {"name": "synthetic", "qubits": [{"t1_us": 60.0, "t2_us": 40.0, "readout_p01": 0.02, "readout_p10": 0.02}] * nd,
-           "default_1q": {"error": 0.001, "duration_ns": 50.0}, "default_2q": {"error": 0.01, "duration_ns": 300.0}}
-    model = naqs.load_calibration(json.dumps(cal))
-    circ = naqs.Circuit(nd)
-    for name, qs, ps in workloads.tfim_trotter(nd, 1.0, steps=10):
-        circ.add(name, qs, ps)
+    model = model_for(nd)
+    circ = circuit(nd, workloads.tfim_trotter(nd, 1.0, steps=10))
     naqs.density_expectation(circ, "Z" + "I" * (nd - 1), model)  # warm: plan + queue kernels
     abi.jit_wait()
     naqs.density_expectation(circ, "Z" + "I" * (nd - 1), model)
     t0 = time.perf_counter()
     z = naqs.density_expectation(circ, "Z" + "I" * (nd - 1), model)
     dt = time.perf_counter() - t0
-    # C4: noisy QAOA-MaxCut ring (p = 2), same calibration, <Z0 Z1>
-    qc = naqs.Circuit(nd)
-    for name, qs, ps in workloads.qaoa_ring(nd, 2):
-        qc.add(name, qs, ps)
+    out["dm_noisy_tfim14"] = {
+        "wall_s": dt, "z0": z, "gates": len(circ),
+        "cpu": None if cpu_per_gate12 is None else {
+            "extrapolated_wall_s": cpu_per_gate12 * 16 * len(circ),
+            "sample": "EXTRAPOLATED: the measured n = 12 whole-circuit seconds per gate x 16 (4^n work) x the "
+                      "n = 14 gate count"},
+        "note": "end-to-end via naqs.density_expectation: attach_noise, superoperator compile, fused passes, "
+                "expectation"}
+    qc = circuit(nd, workloads.qaoa_ring(nd, 2))
     zz = "ZZ" + "I" * (nd - 2)
     naqs.density_expectation(qc, zz, model)
     abi.jit_wait()
@@ -318,47 +605,15 @@ def secondary_workloads(abi, workloads, device):
     out["dm_noisy_qaoa14"] = {"wall_s": time.perf_counter() - t0, "z0z1": zzq, "gates": len(qc),
                               "note": "QAOA-MaxCut ring p=2 (h; cx.rz.cx per edge; rx), end to end via "
                                       "naqs.density_expectation"}
-    # C4 upper end: n = 16 (4^16 entries = 69 GB; beyond the reference's
-    # 14-qubit guard, so GPU only)
     nd16 = 16
-    cal16 = dict(cal, qubits=cal["qubits"][:1] * nd16)
-    model16 = naqs.load_calibration(json.dumps(cal16))
-    circ16 = naqs.Circuit(nd16)
-    for name, qs, ps in workloads.tfim_trotter(nd16, 1.0, steps=10):
-        circ16.add(name, qs, ps)
+    circ16 = circuit(nd16, workloads.tfim_trotter(nd16, 1.0, steps=10))
+    model16 = model_for(nd16)
     naqs.density_expectation(circ16, "Z" + "I" * (nd16 - 1), model16, max_qubits=16)
     abi.jit_wait()
     t0 = time.perf_counter()
     z16 = naqs.density_expectation(circ16, "Z" + "I" * (nd16 - 1), model16, max_qubits=16)
     out["dm_noisy_tfim16"] = {"wall_s": time.perf_counter() - t0, "z0": z16, "cpu": None,
                               "note": "beyond the reference's 14-qubit guard: no CPU baseline"}
-    dm_cpu = dm_cpu_sample(workloads, nd)
-    out["dm_noisy_tfim14"] = {"wall_s": dt, "cpu": dm_cpu,
-                              "items": len(circ) * 3 + sum(1 for o in circ.ops() if len(o[1]) == 2),
-                              "z0": z, "note": "end-to-end via naqs.density_expectation: attach_noise, superoperator "
-                                               "compile, fused passes, expectation"}
-    # C5: VQE n=28 energy evaluations (exact, 193 gates + 55 terms)
-    nv, layers = 28, 3
-    params = workloads.vqe_initial_params(nv, layers)
-    vops = abi.make_ops(workloads.vqe_ansatz(nv, layers, params))
-    terms = workloads.tfim_hamiltonian(nv)
-    sv = abi.SV(nv, device=device)
-    sv.apply(vops)
-    e = float(sum(sv.expectations(terms)))
-    abi.jit_wait()
-    sv.reset()
-    sv.apply(vops)
-    e = float(sum(sv.expectations(terms)))
-    reps = 3
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        sv.reset()
-        sv.apply(vops)
-        e = float(sum(sv.expectations(terms)))
-    dt = (time.perf_counter() - t0) / reps
-    out["vqe28"] = {"evals_per_s": 1.0 / dt, "ms_per_eval": dt * 1e3, "energy": e, "terms": len(terms),
-                    "gates": len(vops)}
-    sv.close()
     # f1: batched Monte-Carlo trajectories (one launch) vs the reference's
     # sequential loop (acceptance 5 shape, and a 10-qubit noisy TFIM)
     out["trajectories"] = trajectory_workloads(workloads)
@@ -376,11 +631,10 @@ def tfim4_sweep(workloads):
     """C1: the n = 4 TFIM magnetization sweep (31 rows, ideal + noisy with
     example_5q.json), end to end: all rows' state vectors in one launch and all
     rows' noisy density matrices in another (naqs.batch_*), vs the reference's
-    own row loop on the host."""
+    own row loop on the host at 1 thread (its bench convention) and all threads."""
     import numpy as np
 
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle import Ref  # CPU baseline only
+    orc = oracle_mod()
     from paper_2401_06861_b200 import naqs
 
     cal = open(os.path.join(ROOT, "tests", "golden", "example_5q.json")).read()
@@ -394,44 +648,27 @@ def tfim4_sweep(workloads):
         rows = np.array(workloads.tfim_sweep_rows_batched(naqs, 4, model))
     gpu_s = (time.perf_counter() - t0) / reps
     res = {"rows": len(rows), "gpu_wall_s": gpu_s, "gates": 60671, "note": "SV ideal + DM noisy columns, shots = 0"}
-    if Ref.available():
-        ref = Ref()
-        threads = ref.set_threads(cpu_threads())
-        _, ideal, noisy, ms = ref.tfim_sweep(cal, 4)
-        res.update({"cpu_wall_s": ms / 1e3, "cpu_threads": threads,
+    if orc.Ref.available():
+        ref = orc.Ref()
+        all_threads = cpu_threads()
+        ref.set_threads(1)
+        _, ideal, noisy, ms1 = ref.tfim_sweep(cal, 4)
+        ref.set_threads(all_threads)
+        _, _, _, ms_all = ref.tfim_sweep(cal, 4)
+        res.update({"cpu_wall_s_1thread": ms1 / 1e3, "cpu_wall_s_all": ms_all / 1e3, "cpu_threads_all": all_threads,
                     "max_abs_diff_vs_cpu": float(max(np.max(np.abs(rows[:, 1] - ideal)),
                                                      np.max(np.abs(rows[:, 2] - noisy))))})
     return res
 
 
-def dm_cpu_sample(workloads, nd):
-    """The reference's noisy density-matrix run (dm_run_noisy, all host
-    threads) on a prefix of the same n = 14 TFIM circuit: seconds per source
-    gate, and that rate times the full circuit (an extrapolation, labelled)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle import NoiseSpec, Ref  # CPU baseline only
-
-    if not Ref.available():
-        return None
-    ops = list(workloads.tfim_trotter(nd, 1.0, steps=10))
-    k = 3  # one ZZ bond (cx, rz, cx): each noisy 2-qubit gate costs the reference ~10 s at n = 14
-    spec = NoiseSpec(nd, t1=60.0, t2=40.0, p01=0.02, p10=0.02, e1=0.001, d1=50.0, e2=0.01, d2=300.0)
-    ref = Ref()
-    threads = ref.set_threads(cpu_threads())
-    ms = ref.dm_time_noisy(nd, ops[:k], spec, 1)
-    per_gate = float(ms[0]) / 1e3 / k
-    return {"sample": f"first {k} of {len(ops)} gates (with their noise channels), reference dm_run_noisy, "
-                      f"{threads} threads", "s_per_gate": per_gate, "extrapolated_wall_s": per_gate * len(ops)}
-
-
 def trajectory_workloads(workloads):
     import numpy as np
 
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle import NoiseSpec, Ref  # CPU baseline only
+    orc = oracle_mod()
     from paper_2401_06861_b200 import naqs
 
     res = {}
+    NoiseSpec = orc.NoiseSpec
     cases = [("acc5_n3", 3, [("h", [0], []), ("cx", [0, 1], []), ("cx", [1, 2], []), ("rx", [0], [0.4]),
                              ("rz", [1], [0.9]), ("cx", [0, 2], [])], 10000, 10000,
               NoiseSpec(3, t1=60.0, t2=40.0, p01=0.0, p10=0.0, e1=0.02, d1=100.0, e2=0.02, d2=100.0)),
@@ -448,8 +685,8 @@ def trajectory_workloads(workloads):
         z = naqs.trajectory_expectations(c, obs, model, ntraj, 505)[:, 0]
         gpu_s = time.perf_counter() - t0
         row = {"trajectories": ntraj, "gpu_wall_s": gpu_s, "gpu_traj_per_s": ntraj / gpu_s, "z0_mean": float(z.mean())}
-        if Ref.available():
-            ms, zref = Ref().traj_time(n, ops, spec, ncpu, 505)
+        if orc.Ref.available():
+            ms, zref = orc.Ref().traj_time(n, ops, spec, ncpu, 505)
             row.update({"cpu_traj_per_s": ncpu / (ms / 1e3), "cpu_sample": f"first {ncpu} trajectories of the reference's "
                         "sequential run_trajectory loop (shared Rng) on the host",
                         "max_abs_diff_vs_cpu": float(np.max(np.abs(z[:ncpu] - zref)))})
@@ -476,27 +713,41 @@ def emit(obj):
     out.flush()
 
 
+def fresh_e2e(abi, sv, workloads, n, depth, seed, steps, term):
+    """e2e with a NEW random circuit every step: the planner, the pass
+    compiler and (for unseen pass structures) kernel specialisation run
+    inside the step; passes whose kernel is still compiling run on the
+    generic interpreter kernel meanwhile."""
+    circuits = [abi.make_ops(workloads.random_circuit(seed + 1000 + i, n, depth)) for i in range(steps)]
+    sv.synchronize()
+    t0 = time.perf_counter()
+    for c in circuits:
+        sv.apply(c)
+        sv.expectations(term)
+    dt = time.perf_counter() - t0
+    abi.jit_wait()
+    return {"value": steps * depth / dt, "unit": "gates/s", "steps": steps,
+            "note": "a different random circuit (seed+1000+i) each step: planning and JIT specialisation "
+                    "are inside the timed region"}
+
+
 def main():
-    claim_stdout()
     args = parse_args()
-    world, rank, local, dist = dist_setup(args)
+    maybe_self_launch(args)
+    claim_stdout()
     if args.impl == "reference":
-        rc = run_reference_arm(args, world, rank)
-        if dist is not None:
-            dist.destroy_process_group()
-        return rc
+        # no process group: ranks other than 0 exit without work
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        return run_reference_arm(args, world, int(os.environ.get("RANK", "0")))
+    world, rank, local, dist = dist_setup()
 
     from paper_2401_06861_b200 import abi, workloads
 
     if abi.device_count() < 1:
         raise SystemExit("bench.py: no CUDA device")
     dev = local
-    g = world.bit_length() - 1
-    if (1 << g) != world:
-        raise SystemExit("bench.py: the sharded state needs a power-of-two number of GPUs")
-    n_local, depth = args.qubits, args.depth
-    n = n_local + g  # weak scaling: 2^n_local amplitudes per GPU
-    ops_list = workloads.random_circuit(args.seed, n, depth)
+    n, n_local, g, seed, depth = workload(args, world)
+    ops_list = workloads.random_circuit(seed, n, depth)
     ops = abi.make_ops(ops_list)
     if world == 1:
         sv = abi.SV(n, device=dev, tile_qubits=args.tile, max_qubits=max(30, n))
@@ -511,16 +762,22 @@ def main():
                             tile_qubits=args.tile, max_qubits=n)
 
     clk = ClockSampler(dev).__enter__()
-    # warm-up: the first step plans the passes and queues their specialised
-    # kernels for compilation (jit.cpp); wait for them, then warm the rest
     # Warm-up: at least W steps, continued (up to 16) while steps still meet
     # pass structures that had to be compiled -- a sharded state carries its
     # qubit map from step to step and settles into a short cycle of layouts.
-    # All ranks take the same decision (the flushes are collective).
+    # All ranks take the same decision (the flushes are collective).  The
+    # first (cold) step starts from the identity qubit map and is timed alone.
     warm = 0
+    cold_ms = None
     while True:
         before = abi.jit_stats()["compiled"]
-        sv.apply(ops).flush()
+        if warm == 0:
+            sv.synchronize()
+            abi.profile_begin(dev, per_pass_events=False)
+            sv.apply(ops).flush()
+            cold_ms = abi.profile_end(dev)["region_ms"]
+        else:
+            sv.apply(ops).flush()
         abi.jit_wait()
         warm += 1
         fresh = abi.jit_stats()["compiled"] > before
@@ -535,6 +792,7 @@ def main():
     sv.synchronize()
     jit = abi.jit_stats()
     stats = sv.stats()
+    comm0 = sv.comm_stats() if world > 1 else None
 
     # ---- value: device time of K steps
     barrier(dist, local)
@@ -548,6 +806,7 @@ def main():
     clk.__exit__(None, None, None)
     barrier(dist, local)
     ms = max_over_ranks(dist, local, prof["region_ms"])
+    comm1 = sv.comm_stats() if world > 1 else None
     # one circuit on the whole (sharded) state; weak scaling: a gate on the
     # 2^(n_local+g)-amplitude state counts 2^g gate equivalents of n_local qubits
     gates_total = args.steps * depth * world
@@ -571,21 +830,26 @@ def main():
     t0 = time.perf_counter()
     lap = []
     for _ in range(args.steps):
-        sv.apply(ops)  # host op array -> planner -> pinned staging -> H2D
+        sv.apply(ops)  # host op array -> planner (plan cache) -> pinned staging -> H2D
         sv.expectations(e2e_term)  # D2H of the step's result
         lap.append(time.perf_counter())
     t_e2e = time.perf_counter() - t0
-    if os.environ.get("NQ_BENCH_LAPS") == "1":
-        print(f"rank {rank} e2e step ms:", [round((b - a) * 1e3, 2) for a, b in zip([t0] + lap[:-1], lap)],
-              file=sys.stderr)
     prof_e2e = abi.profile_end(dev)
     t_e2e = max_over_ranks(dist, local, t_e2e)
     laps_ms = sorted((b - a) * 1e3 for a, b in zip([t0] + lap[:-1], lap))
     e2e = {"value": gates_total / t_e2e, "unit": "gates/s",
            "h2d_bytes_per_step": int(prof_e2e["h2d_bytes"] / args.steps),
            "d2h_bytes_per_step": int(prof_e2e["d2h_bytes"] / args.steps),
-           "step_ms_median_rank0": laps_ms[len(laps_ms) // 2], "step_ms_max_rank0": laps_ms[-1]}
+           "step_ms_median_rank0": laps_ms[len(laps_ms) // 2], "step_ms_max_rank0": laps_ms[-1],
+           "plan": "same circuit every step: plan cache and specialised kernels are hits (see e2e_fresh)"}
+    e2e_fresh = None
+    if world == 1 and not args.no_fresh:
+        e2e_fresh = fresh_e2e(abi, sv, workloads, n, depth, seed, 3, e2e_term)
     jit_end = abi.jit_stats()
+
+    parity, cpu_base = None, None
+    if world == 1 and n <= 30 and not (args.no_parity and args.no_cpu_baseline):
+        parity, cpu_base = headline_parity_and_baseline(abi, sv, n, ops, ops_list, args)
 
     out = None
     if rank == 0:
@@ -602,17 +866,13 @@ def main():
             "vs_baseline": None,
             "dtype": "c128",
             "data": "synthetic",
-            "config": {"workload": f"random_circuit(Rng({args.seed})) n={n} depth={depth} "
-                                   f"(proj/tests/test_util.hpp generator)",
-                       "qubits": n, "depth": depth, "state_bytes": 16 << n,
-                       "parallelism": "single" if world == 1 else
-                       f"sharded x{world}: {g} global qubits; half-shard exchanges over NVLink peer memory, fused into the preceding pass",
-                       "local_qubits": n_local,
-                       "warmup_steps_run": warm,
-                       "unit_note": (f"gates/s of {n_local}-qubit gate equivalents: each gate on the {n}-qubit "
-                                     f"state counts {world} (2^{g}); whole-job aggregate over {world} GPU(s)"),
-                       "comm": sv.comm_stats() if world > 1 else None,
-                       "l2": "state (16 GiB) >> L2 (126 MB): every pass streams from HBM"},
+            "config": workload_config(args, world),
+            "warmup_steps_run": warm,
+            "cold_first_step_ms": cold_ms,
+            "comm": None if comm0 is None else {
+                "timed_exchanges": comm1["exchanges"] - comm0["exchanges"],
+                "timed_fused": comm1["fused"] - comm0["fused"],
+                "timed_bytes_sent": comm1["bytes_sent"] - comm0["bytes_sent"], "alt_buffer": comm1["alt_buffer"]},
             "hbm_gbs": step_gbs,
             "hbm_frac_step": step_gbs / peak,
             "passes_per_step": stats["passes"],
@@ -628,17 +888,18 @@ def main():
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
             "clocks": clk.summary(),
             "e2e": e2e,
+            "e2e_fresh": e2e_fresh,
         }
+        if parity is not None and not args.no_parity:
+            out["parity"] = parity
     sv.close()
     if rank == 0 and world == 1 and not args.no_secondary:
         try:
-            out["secondary"] = secondary_workloads(abi, workloads, dev)
+            out["secondary"] = secondary_workloads(abi, workloads, dev, args)
         except Exception as exc:  # secondary numbers never hide the headline
             out["secondary"] = {"error": repr(exc)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        res, why = cpu_reference_rate(n, ops_list, args.cpu_ops, 3)
-        out["cpu_baseline"] = (
-            {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")} if res else {"unavailable": why})
+        out["cpu_baseline"] = cpu_base if cpu_base is not None else {"unavailable": f"n={n} > 30 (reference guard)"}
     if rank == 0:
         emit(out)
     if dist is not None:

@@ -410,6 +410,33 @@ class Ref:
         self._chk(self.lib.ref_sv_run_timed(h, arr.ctypes.data, len(arr), C.byref(ms)))
         return ms.value
 
+    def sv_gather(self, h, idx) -> np.ndarray:
+        """Amplitudes at the given indices of a persistent reference state."""
+        ix = np.ascontiguousarray(idx, dtype=np.int64)
+        out = np.zeros(len(ix), dtype=np.complex128)
+        self.lib.ref_sv_gather.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+        self._chk(self.lib.ref_sv_gather(h, ix.ctypes.data, len(ix), out.ctypes.data))
+        return out
+
+    def sv_norm_sq_h(self, h) -> float:
+        v = C.c_double()
+        self.lib.ref_sv_norm_sq_h.argtypes = [C.c_void_p, _dp]
+        self._chk(self.lib.ref_sv_norm_sq_h(h, C.byref(v)))
+        return v.value
+
+    def sv_expectations_h(self, h, n, terms) -> np.ndarray:
+        letters = "".join(t[0] for t in terms).encode()
+        assert all(len(t[0]) == n for t in terms)
+        coeff = np.array([t[1] for t in terms], dtype=np.float64)
+        out = np.zeros(len(terms))
+        self.lib.ref_sv_expectations_h.argtypes = [C.c_void_p, C.c_char_p, _dp, C.c_int, _dp]
+        self._chk(self.lib.ref_sv_expectations_h(h, letters, _d(coeff), len(terms), _d(out)))
+        return out
+
+    def sv_reset_h(self, h):
+        self.lib.ref_sv_reset_h.argtypes = [C.c_void_p]
+        self._chk(self.lib.ref_sv_reset_h(h))
+
     def tfim_sweep(self, calib_json: str, n: int, t_max: float = 3.0, dt: float = 0.1, steps_per_unit: int = 100,
                    max_rows: int = 1000):
         """Reference magnetization sweep rows (no exact column): (t, ideal, noisy, wall ms)."""
@@ -443,3 +470,30 @@ class Ref:
                                              C.c_double(noise.e1), C.c_double(noise.d1), C.c_double(noise.e2),
                                              C.c_double(noise.d2), reps, _d(ms)))
         return ms
+
+
+def qft_closed_form(n: int, ys, prep_seed: int = 7) -> np.ndarray:
+    """Closed form of the C2 QFT workload (paper_2401_06861_b200/workloads.qft):
+    RY(theta_q) then RZ(phi_q) on every qubit of |0..0> (angles
+    Rng(prep_seed).uniform(-pi, pi), ry before rz per qubit), then the QFT in
+    the reference gate set with the final swaps.  The prep state is a product
+    psi(x) = prod_q psi_q(x_q) with psi_q = (cos(t/2) e^{-i p/2}, sin(t/2) e^{i p/2})
+    (proj/src/gates.cpp:61-106), so with x = sum_q x_q 2^q
+        out[y] = 2^{-n/2} sum_x psi(x) e^{2 pi i x y / 2^n}
+               = 2^{-n/2} prod_q (psi_q(0) + psi_q(1) e^{2 pi i (2^q y mod 2^n) / 2^n}),
+    O(n) per amplitude at any n (the reference's 2^n engine needs ~6 min for
+    the 2,220 ops at n = 30).  Pinned against oracle/_ref by
+    tests/test_scale_parity_cpu.py."""
+    u = Port().rng_double(prep_seed, 2 * n)
+    psi = []
+    for q in range(n):
+        th = -np.pi + 2 * np.pi * u[2 * q]
+        ph = -np.pi + 2 * np.pi * u[2 * q + 1]
+        psi.append((np.cos(th / 2) * np.exp(-0.5j * ph), np.sin(th / 2) * np.exp(0.5j * ph)))
+    ys = np.asarray(ys, dtype=np.int64)
+    N = 1 << n
+    acc = np.full(len(ys), 2.0 ** (-n / 2), dtype=np.complex128)
+    for q in range(n):
+        frac = ((ys << q) & (N - 1)).astype(np.float64) / N
+        acc *= psi[q][0] + psi[q][1] * np.exp(2j * np.pi * frac)
+    return acc

@@ -415,6 +415,37 @@ int ref_sv_run_timed(void* h, const RefOp* ops, int64_t nops, double* ms) {
     });
 }
 
+// Readers of a persistent state (parity at benchmark scale): selected
+// amplitudes (StateVector::amplitude), norm_sq and Pauli expectations of the
+// reference engine's own state, without copying 2^n amplitudes out.
+int ref_sv_gather(void* h, const int64_t* idx, int64_t count, double* out) {
+    return wrap([&] {
+        auto* s = static_cast<StateVector*>(h);
+        for (int64_t i = 0; i < count; ++i) {
+            const cplx a = s->amplitude(size_t(idx[i]));
+            out[2 * i] = a.real();
+            out[2 * i + 1] = a.imag();
+        }
+    });
+}
+
+int ref_sv_norm_sq_h(void* h, double* out) {
+    return wrap([&] { *out = static_cast<StateVector*>(h)->norm_sq(); });
+}
+
+int ref_sv_expectations_h(void* h, const char* letters, const double* coeff, int nt, double* out) {
+    return wrap([&] {
+        auto* s = static_cast<StateVector*>(h);
+        const size_t n = size_t(s->num_qubits());
+        for (int t = 0; t < nt; ++t)
+            out[t] = s->expectation(PauliString(std::string(letters + size_t(t) * n, n), coeff[t]));
+    });
+}
+
+int ref_sv_reset_h(void* h) {
+    return wrap([&] { static_cast<StateVector*>(h)->reset(); });
+}
+
 // The reference's Nelder-Mead (proj/src/neldermead.cpp) on a C callback:
 // trace_out (capacity max_evals) receives every objective value, best_out
 // the best point; returns 0 / 1 / 2 like the other entry points.

@@ -112,6 +112,8 @@ void launch_kraus_weights(const double2* a, int nbits, const int* qubits, int k,
                           const double2* dev_mats, double* scratch, double* out, cudaStream_t s);
 void launch_block_psum(const double2* a, const double* p, uint64_t n, uint64_t bs, double* out,
                        cudaStream_t s);
+void launch_block_isum(const double2* a, const double* p, uint64_t n, uint64_t bs, const int* kb,
+                       unsigned long long* isum, int* flags, cudaStream_t s);
 void launch_block_sweep(const double2* a, const double* p, uint64_t n, uint64_t bs, const int64_t* blk,
                         const double* cum0, const int64_t* ulo, const int64_t* uhi, const double* u,
                         int nb, uint64_t* idx_out, uint64_t* cnt_out, int64_t* npairs, cudaStream_t s);

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -35,6 +36,10 @@ __device__ __forceinline__ uint32_t ins0(uint32_t w, int b) {
 __device__ __forceinline__ uint64_t ins0_64(uint64_t w, int b) {
     return ((w >> b) << (b + 1)) | (w & ((uint64_t(1) << b) - 1u));
 }
+// |a|^2 exactly as std::norm on the host (proj/src/statevector.cpp:281):
+// re*re + im*im with each product rounded, no fused multiply-add, so device
+// probabilities equal the reference's bit for bit on the same amplitudes.
+__device__ __forceinline__ double prob_rn(double2 v) { return __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)); }
 __device__ __forceinline__ double2 ld_stream(const double2* p) {
     double2 v;
     asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
@@ -192,8 +197,7 @@ __global__ void __launch_bounds__(kThreads) k_dm_expect(const double2* __restric
 __global__ void k_probs(const double2* __restrict__ a, uint64_t n, double* __restrict__ p) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
-        const double2 v = a[i];
-        p[i] = fma(v.x, v.x, v.y * v.y);
+        p[i] = prob_rn(a[i]);
     }
 }
 
@@ -319,14 +323,64 @@ __global__ void k_block_psum(const double2* __restrict__ a, const double* __rest
     const uint64_t hi = min(n, lo + bs);
     double acc[1] = {0.0};
     for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        if (a) {
-            const double2 v = a[i];
-            acc[0] += fma(v.x, v.x, v.y * v.y);
-        } else {
-            acc[0] += p[i];
-        }
+        acc[0] += a ? prob_rn(a[i]) : p[i];
     }
     block_reduce_store<1>(acc, out, 1);
+}
+
+// Exact reproduction of the reference's sequential `cum += p[i]`
+// (proj/src/statevector.cpp:311-320) without a serial pass: while cum stays in
+// one binade [2^k, 2^(k+1)) every partial sum lies on the grid of ulp
+// 2^(k-52), so fl(cum + p) = cum + rint(p / ulp) * ulp exactly unless
+// p / ulp is a tie (x.5, where round-half-even depends on cum's last bit).
+// Integer increments are associative: this kernel sums rint(p * 2^(52-k))
+// over the block for the binade k the host guessed (kb[b]); the host
+// (sample.cpp) verifies the binade and that the block stays inside it, and
+// replays flagged blocks (ties, overflow, binade crossings) sequentially.
+__global__ void k_block_isum(const double2* __restrict__ a, const double* __restrict__ p, uint64_t n,
+                             uint64_t bs, const int* __restrict__ kb, unsigned long long* __restrict__ isum,
+                             int* __restrict__ flags) {
+    constexpr unsigned long long kSat = 1ull << 62;
+    const uint64_t lo = uint64_t(blockIdx.x) * bs;
+    const uint64_t hi = min(n, lo + bs);
+    const int k = kb[blockIdx.x];
+    __shared__ unsigned long long red[kThreads / 32];
+    __shared__ int bad_any;
+    if (threadIdx.x == 0) bad_any = 0;
+    __syncthreads();
+    if (k == INT_MIN) {
+        if (threadIdx.x == 0) {
+            isum[blockIdx.x] = 0;
+            flags[blockIdx.x] = 1;
+        }
+        return;
+    }
+    const double scale = ldexp(1.0, 52 - k);  // exact power of two (host keeps 52 - k <= 1000)
+    unsigned long long acc = 0;
+    int bad = 0;
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double pi = a ? prob_rn(a[i]) : p[i];
+        const double y = __dmul_rn(pi, scale);
+        if (!(y < 9007199254740992.0) || !(y >= 0.0)) {  // >= 2^53 (leaves the binade), NaN, negative
+            bad = 1;
+            continue;
+        }
+        const double f = floor(y);
+        if (y - f == 0.5) bad = 1;  // tie: rounding depends on cum's parity
+        acc = min(acc + (unsigned long long)rint(y), kSat);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = min(acc + __shfl_xor_sync(0xffffffffu, acc, o), kSat);
+    if (lane == 0) red[warp] = acc;
+    if (bad) bad_any = 1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < kThreads / 32; ++w) t = min(t + red[w], kSat);
+        isum[blockIdx.x] = t;
+        flags[blockIdx.x] = bad_any;
+    }
 }
 
 // One thread per block that owns uniforms: sequential cumulative sweep from
@@ -346,14 +400,8 @@ __global__ void k_block_sweep(const double2* __restrict__ a, const double* __res
     int64_t slot = ulo[t];
     uint64_t last_nz = UINT64_MAX;
     for (uint64_t i = lo; i < hi && next < end; ++i) {
-        double pi;
-        if (a) {
-            const double2 v = a[i];
-            pi = v.x * v.x + v.y * v.y;
-        } else {
-            pi = p[i];
-        }
-        cum += pi;
+        const double pi = a ? prob_rn(a[i]) : p[i];
+        cum = __dadd_rn(cum, pi);
         if (pi > 0.0) last_nz = i;
         uint64_t here = 0;
         while (next < end && u[next] < cum) {
@@ -370,13 +418,7 @@ __global__ void k_block_sweep(const double2* __restrict__ a, const double* __res
         // rounding between the host block prefix and this sweep: the remaining
         // uniforms belong to this block; give them to its last nonzero entry.
         for (uint64_t i = hi; i-- > lo;) {
-            double pi;
-            if (a) {
-                const double2 v = a[i];
-                pi = v.x * v.x + v.y * v.y;
-            } else {
-                pi = p[i];
-            }
+            const double pi = a ? prob_rn(a[i]) : p[i];
             if (pi > 0.0) {
                 last_nz = i;
                 break;
@@ -402,13 +444,7 @@ __global__ void k_last_nonzero(const double2* __restrict__ a, const double* __re
     if (threadIdx.x == 0) best = 0;
     __syncthreads();
     for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        double pi;
-        if (a) {
-            const double2 v = a[i];
-            pi = v.x * v.x + v.y * v.y;
-        } else {
-            pi = p[i];
-        }
+        const double pi = a ? prob_rn(a[i]) : p[i];
         if (pi > 0.0) atomicMax(&best, (unsigned long long)(i + 1));
     }
     __syncthreads();
@@ -610,6 +646,13 @@ void launch_block_psum(const double2* a, const double* p, uint64_t n, uint64_t b
                        cudaStream_t s) {
     const uint64_t nb = (n + bs - 1) / bs;
     k_block_psum<<<unsigned(nb), kThreads, 0, s>>>(a, p, n, bs, out);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void launch_block_isum(const double2* a, const double* p, uint64_t n, uint64_t bs, const int* kb,
+                       unsigned long long* isum, int* flags, cudaStream_t s) {
+    const uint64_t nb = (n + bs - 1) / bs;
+    k_block_isum<<<unsigned(nb), kThreads, 0, s>>>(a, p, n, bs, kb, isum, flags);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 

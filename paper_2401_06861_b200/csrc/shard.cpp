@@ -1010,27 +1010,38 @@ void shard_sample(State& s, const double* sorted_u, uint64_t shots, uint64_t* id
                   uint64_t* nout) {
     normalize_map(s);
     DeviceCtx& c = ctx_for(s.dev);
-    // this rank's probability mass; rank-ordered offsets
+    // approximate rank masses (binade guesses only), then the exact sequential
+    // cumulative handed from rank to rank: rank r walks its shard from the
+    // exact end of rank r - 1 (sample.cpp), so the ranks' ranges [start, end)
+    // tile [0, final) with no gap and every uniform has exactly one owner
     c.ensure_scratch(scratch_doubles_needed(s.count) + 64);
     launch_sumsq(s.d, s.count, c.d_scratch + 64, result_slot(c, 0), c.stream);
     double mass = 0.0;
     fetch(c, result_slot(c, 0), 1, &mass);
     const auto masses = allgather_doubles(s, {mass});
-    double start = 0.0;
-    for (int r = 0; r < s.rank; ++r) start += masses[size_t(r)];
+    double approx = 0.0;
+    for (int r = 0; r < s.rank; ++r) approx += masses[size_t(r)];
+    SeqCum sc;
+    seqcum_prepare(c, s.d, nullptr, s.count, approx, sc);
+    double start = 0.0, end = 0.0;
+    for (int r = 0; r < s.world; ++r) {
+        double mine = 0.0;
+        if (r == s.rank) mine = end = seqcum_walk(c, s.d, nullptr, sc, start);
+        const auto ends = allgather_doubles(s, {mine});
+        if (r < s.rank) start = ends[size_t(r)];
+    }
     int last_nz = -1;
     for (int r = 0; r < s.world; ++r)
         if (masses[size_t(r)] > 0.0) last_nz = r;
-    const double end = start + mass;
-    // uniforms owned by this rank: [start, end), the last nonzero rank also takes leftovers
+    // uniforms owned by this rank: [start, end); the last nonzero rank also takes leftovers
     uint64_t lo = uint64_t(std::lower_bound(sorted_u, sorted_u + shots, start) - sorted_u);
     uint64_t hi = (s.rank == last_nz) ? shots : uint64_t(std::lower_bound(sorted_u, sorted_u + shots, end) - sorted_u);
     if (s.rank > last_nz) lo = hi = 0;
     std::vector<uint64_t> li(std::max<uint64_t>(hi - lo, 1)), lc(std::max<uint64_t>(hi - lo, 1));
     uint64_t k = 0;
     if (hi > lo)
-        sample_sweep(c, s.d, nullptr, s.count, sorted_u + lo, hi - lo, li.data(), lc.data(), &k, start,
-                     s.rank == last_nz);
+        sample_assign(c, s.d, nullptr, sc, start, sorted_u + lo, hi - lo, li.data(), lc.data(), &k,
+                      s.rank == last_nz);
     // gather (index, count) pairs in rank order
     const auto ks = allgather_doubles(s, {double(k)});
     uint64_t maxk = 1;
@@ -1048,6 +1059,11 @@ void shard_sample(State& s, const double* sorted_u, uint64_t shots, uint64_t* id
             count_out[o] = uint64_t(all[size_t(r) * pack.size() + size_t(2 * i + 1)]);
             ++o;
         }
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < o; ++i) total += count_out[i];
+    if (total != shots)
+        throw NqError{NQ_ERR_INTERNAL, "sharded sampling assigned " + std::to_string(total) + " of " +
+                                           std::to_string(shots) + " shots"};
     *nout = o;
 }
 

@@ -110,12 +110,26 @@ void configure_caps(PlanOptions& p);
 double* result_slot(DeviceCtx& c, int i);
 void fetch(DeviceCtx& c, const double* dsrc, size_t count, double* host);
 
-// sampling (sample.cpp): either amplitudes `a` or probabilities `p` (one is null)
-// cum_start: cumulative probability before this array (sharded states);
-// leftovers: whether uniforms beyond the final cumulative are assigned here.
+// sampling (sample.cpp): either amplitudes `a` or probabilities `p` (one is
+// null).  The cumulative sum is the reference's sequential one, bit for bit.
+struct SeqCum {
+    uint64_t n = 0, bs = 0, nb = 0;
+    std::vector<double> bsum;                // approximate block sums (guesses only)
+    std::vector<int> kb;                     // guessed binade per block (INT_MIN: replay)
+    std::vector<unsigned long long> isum;    // integer increments in that binade
+    std::vector<int> flags;                  // tie / overflow inside the block
+    std::vector<double> ends;                // exact sequential cum at each block end
+    int64_t replayed = 0;                    // blocks replayed on the host
+};
+void seqcum_prepare(DeviceCtx& c, const double2* a, const double* p, uint64_t n, double approx_start, SeqCum& sc);
+// exact walk from the exact cumulative `start`; returns the final cumulative
+double seqcum_walk(DeviceCtx& c, const double2* a, const double* p, SeqCum& sc, double start);
+// leftovers: whether uniforms beyond the final cumulative are assigned here
+void sample_assign(DeviceCtx& c, const double2* a, const double* p, const SeqCum& sc, double start,
+                   const double* sorted_u, uint64_t shots, uint64_t* idx_out, uint64_t* count_out, uint64_t* nout,
+                   bool leftovers);
 void sample_sweep(DeviceCtx& c, const double2* a, const double* p, uint64_t n, const double* sorted_u,
-                  uint64_t shots, uint64_t* idx_out, uint64_t* count_out, uint64_t* nout, double cum_start = 0.0,
-                  bool leftovers = true);
+                  uint64_t shots, uint64_t* idx_out, uint64_t* count_out, uint64_t* nout);
 
 // multi-GPU (shard.cpp)
 void shard_free(State& s);
