@@ -141,6 +141,17 @@ nq_status nq_sv_set_amplitudes(nq_sv* s, uint64_t offset, uint64_t count, const 
 /* Device pointer to the (flushed) amplitude array, for zero-copy consumers
  * (sharded states: this rank's 2^(n-g) block, qubit map restored first). */
 nq_status nq_sv_device_ptr(nq_sv* s, void** out);
+/* Device probabilities |a_i|^2 (std::norm rounding) in a buffer owned by the
+ * state, valid until the state is next modified or destroyed (zero-copy
+ * replacement of probabilities(), proj/python/bindings.cpp:25-42; sharded
+ * states: this rank's block). */
+nq_status nq_sv_probabilities_device(nq_sv* s, double** out);
+/* Global index of this rank's first amplitude and the number it holds
+ * (0 and 2^n for single-device states). */
+nq_status nq_sv_local_range(const nq_sv* s, uint64_t* offset, uint64_t* count);
+/* CUDA device ordinal holding the state (for DLPack / CUDA-array consumers). */
+nq_status nq_sv_device(const nq_sv* s, int* device);
+nq_status nq_dm_device(const nq_dm* d, int* device);
 /* Planner/executor statistics of the last flush: passes, fused micro-ops,
  * source ops, kernel launches. */
 nq_status nq_sv_last_stats(const nq_sv* s, int64_t* passes, int64_t* microops,
@@ -152,6 +163,12 @@ nq_status nq_sv_synchronize(nq_sv* s);
 nq_status nq_dm_create(int num_qubits, const nq_opts* opts, nq_dm** out);
 nq_status nq_dm_destroy(nq_dm* d);
 nq_status nq_dm_clone(const nq_dm* d, nq_dm** out);
+/* Device pointer to row-major rho (rho[r * 2^n + c], densitymatrix.hpp:30),
+ * flushed and in amplitude order; valid until the state is modified. */
+nq_status nq_dm_device_ptr(nq_dm* d, void** out);
+/* Device probabilities max(0, Re rho_ii) / trace (DensityMatrix::probabilities,
+ * densitymatrix.cpp:221-232) in a state-owned buffer. */
+nq_status nq_dm_probabilities_device(nq_dm* d, double** out);
 nq_status nq_dm_reset(nq_dm* d);
 nq_status nq_dm_num_qubits(const nq_dm* d, int* out);
 /* apply(op) — densitymatrix.cpp:114-125: BARRIER and ID skipped, MEASURE rejected. */

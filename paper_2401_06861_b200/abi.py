@@ -117,6 +117,9 @@ SIGNATURES = {
     "nq_sv_get_amplitudes": ([_p, C.c_uint64, C.c_uint64, _dp], C.c_int),
     "nq_sv_set_amplitudes": ([_p, C.c_uint64, C.c_uint64, _dp], C.c_int),
     "nq_sv_device_ptr": ([_p, _pp], C.c_int),
+    "nq_sv_device": ([_p, C.POINTER(C.c_int)], C.c_int),
+    "nq_sv_probabilities_device": ([_p, C.POINTER(_dp)], C.c_int),
+    "nq_sv_local_range": ([_p, _u64p, _u64p], C.c_int),
     "nq_sv_last_stats": ([_p, _i64p, _i64p, _i64p, _i64p], C.c_int),
     "nq_sv_synchronize": ([_p], C.c_int),
     "nq_dm_create": ([C.c_int, C.POINTER(nq_opts), _pp], C.c_int),
@@ -133,6 +136,9 @@ SIGNATURES = {
     "nq_dm_hermiticity_residual": ([_p, _dp], C.c_int),
     "nq_dm_expectation_batch": ([_p, _u64p, _u64p, _i32p, _dp, C.c_int, _dp, _dp], C.c_int),
     "nq_dm_probabilities": ([_p, _dp], C.c_int),
+    "nq_dm_device_ptr": ([_p, _pp], C.c_int),
+    "nq_dm_device": ([_p, C.POINTER(C.c_int)], C.c_int),
+    "nq_dm_probabilities_device": ([_p, C.POINTER(_dp)], C.c_int),
     "nq_dm_get_entries": ([_p, C.c_uint64, C.c_uint64, _dp], C.c_int),
     "nq_dm_set_entries": ([_p, C.c_uint64, C.c_uint64, _dp], C.c_int),
     "nq_dm_last_stats": ([_p, _i64p, _i64p, _i64p, _i64p], C.c_int),
@@ -271,16 +277,30 @@ class SV:
         check(lib.nq_sv_get_amplitudes(self.h, offset, count, out.view(np.float64).ctypes.data_as(_dp)))
         return out
 
-    def device_view(self) -> "DeviceAmplitudes":
+    def _device(self) -> int:
+        d = C.c_int()
+        check(lib.nq_sv_device(self.h, C.byref(d)))
+        return d.value
+
+    def device_view(self) -> DeviceArray:
         """Zero-copy view of the (flushed) amplitudes in HBM:
-        an object with ``__cuda_array_interface__`` (complex128, 2^n; for a
-        sharded state this rank's 2^nloc block), e.g. ``torch.as_tensor(view,
-        device="cuda")`` or CuPy.  Valid until the state is modified or closed;
-        the state's queued work is synchronised first."""
+        complex128, 2^n (a sharded state: this rank's 2^nloc block, global
+        offset in ``.offset``).  The state's queued work is synchronised first."""
         p = C.c_void_p()
         check(lib.nq_sv_device_ptr(self.h, C.byref(p)))
         check(lib.nq_sv_synchronize(self.h))
-        return DeviceAmplitudes(p.value, self.local_count())
+        off, cnt = C.c_uint64(), C.c_uint64()
+        check(lib.nq_sv_local_range(self.h, C.byref(off), C.byref(cnt)))
+        return DeviceArray(p.value, (cnt.value,), "<c16", self._device(), self, off.value)
+
+    def device_probabilities(self) -> DeviceArray:
+        """|a_i|^2 on the device (no 2^n host copy), float64, in a buffer owned
+        by the state: valid until the state is next modified."""
+        p = C.POINTER(C.c_double)()
+        check(lib.nq_sv_probabilities_device(self.h, C.byref(p)))
+        off, cnt = C.c_uint64(), C.c_uint64()
+        check(lib.nq_sv_local_range(self.h, C.byref(off), C.byref(cnt)))
+        return DeviceArray(C.cast(p, C.c_void_p).value, (cnt.value,), "<f8", self._device(), self, off.value)
 
     def local_count(self) -> int:
         return 1 << self.n if getattr(self, "world", 1) == 1 else 1 << (self.n - (self.world.bit_length() - 1))
@@ -387,16 +407,101 @@ def shard_debug(n: int, world: int, ops, rebalance: bool = True):
     return out
 
 
-class DeviceAmplitudes:
-    """``__cuda_array_interface__`` (v3) over a device amplitude array."""
+class _DLDevice(C.Structure):
+    _fields_ = [("device_type", C.c_int32), ("device_id", C.c_int32)]
 
-    def __init__(self, ptr: int, count: int):
-        self.ptr, self.count = ptr, count
+
+class _DLDataType(C.Structure):
+    _fields_ = [("code", C.c_uint8), ("bits", C.c_uint8), ("lanes", C.c_uint16)]
+
+
+class _DLTensor(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("device", _DLDevice), ("ndim", C.c_int32), ("dtype", _DLDataType),
+                ("shape", C.POINTER(C.c_int64)), ("strides", C.POINTER(C.c_int64)), ("byte_offset", C.c_uint64)]
+
+
+_DLDeleter = C.CFUNCTYPE(None, C.c_void_p)
+
+
+class _DLManagedTensor(C.Structure):
+    _fields_ = [("dl_tensor", _DLTensor), ("manager_ctx", C.c_void_p), ("deleter", _DLDeleter)]
+
+
+_KDL_CUDA = 2
+_DL_CODES = {"<c16": (5, 128), "<f8": (2, 64)}  # kDLComplex / kDLFloat
+_dl_live = {}  # manager_ctx -> (managed tensor, shape array, owner): alive until the consumer's deleter
+
+
+@_DLDeleter
+def _dl_delete(ptr):
+    mt = _DLManagedTensor.from_address(ptr)
+    _dl_live.pop(mt.manager_ctx, None)
+
+
+_PyCapsule_Destructor = C.CFUNCTYPE(None, C.py_object)
+_capsule_new = C.pythonapi.PyCapsule_New
+_capsule_new.restype = C.py_object
+_capsule_new.argtypes = [C.c_void_p, C.c_char_p, _PyCapsule_Destructor]
+_capsule_is_valid = C.pythonapi.PyCapsule_IsValid
+_capsule_is_valid.restype = C.c_int
+_capsule_is_valid.argtypes = [C.py_object, C.c_char_p]
+_capsule_get_ptr = C.pythonapi.PyCapsule_GetPointer
+_capsule_get_ptr.restype = C.c_void_p
+_capsule_get_ptr.argtypes = [C.py_object, C.c_char_p]
+
+
+@_PyCapsule_Destructor
+def _dl_capsule_destructor(cap):
+    # never consumed (still named "dltensor"): release it ourselves
+    if _capsule_is_valid(cap, b"dltensor"):
+        _dl_delete(_capsule_get_ptr(cap, b"dltensor"))
+
+
+class DeviceArray:
+    """Zero-copy view of a device array owned by a state:
+    ``__cuda_array_interface__`` (v3) and DLPack (``__dlpack__`` /
+    ``__dlpack_device__``), e.g. ``torch.from_dlpack(view)`` or CuPy.  The
+    view keeps its owner alive; it is valid until the owner is modified,
+    flushed again or closed.  ``offset`` is the global index of element 0
+    (a sharded state's rank block starts at rank << n_local)."""
+
+    def __init__(self, ptr: int, shape, typestr: str, device: int, owner=None, offset: int = 0):
+        self.ptr, self.shape, self.typestr, self.device = ptr, tuple(shape), typestr, device
+        self.owner, self.offset = owner, offset
+
+    @property
+    def count(self) -> int:
+        c = 1
+        for d in self.shape:
+            c *= d
+        return c
 
     @property
     def __cuda_array_interface__(self):
-        return {"shape": (self.count,), "typestr": "<c16", "data": (self.ptr, False), "version": 3,
+        return {"shape": self.shape, "typestr": self.typestr, "data": (self.ptr, False), "version": 3,
                 "strides": None, "stream": None}
+
+    def __dlpack_device__(self):
+        return (_KDL_CUDA, self.device)
+
+    def __dlpack__(self, stream=None, max_version=None, dl_device=None, copy=None):
+        if copy:
+            raise BufferError("DeviceArray exports zero-copy views only")
+        # the owner's stream was synchronised when the view was made, so any
+        # consumer stream may read it without further ordering
+        shape = (C.c_int64 * len(self.shape))(*self.shape)
+        mt = _DLManagedTensor()
+        code, bits = _DL_CODES[self.typestr]
+        mt.dl_tensor = _DLTensor(C.c_void_p(self.ptr), _DLDevice(_KDL_CUDA, self.device), len(self.shape),
+                                 _DLDataType(code, bits, 1), shape, None, 0)
+        key = C.addressof(mt)
+        mt.manager_ctx = key
+        mt.deleter = _dl_delete
+        _dl_live[key] = (mt, shape, self)
+        return _capsule_new(key, b"dltensor", _dl_capsule_destructor)
+
+
+DeviceAmplitudes = DeviceArray  # round-1 name
 
 
 class DM:
@@ -452,6 +557,23 @@ class DM:
     def set_rho(self, rho):
         a = np.ascontiguousarray(np.asarray(rho, dtype=np.complex128).reshape(-1))
         check(lib.nq_dm_set_entries(self.h, 0, len(a), a.view(np.float64).ctypes.data_as(_dp)))
+
+    def _device(self) -> int:
+        d = C.c_int()
+        check(lib.nq_dm_device(self.h, C.byref(d)))
+        return d.value
+
+    def device_view(self) -> DeviceArray:
+        """Zero-copy view of row-major rho (2^n x 2^n complex128) in HBM."""
+        p = C.c_void_p()
+        check(lib.nq_dm_device_ptr(self.h, C.byref(p)))
+        d = 1 << self.n
+        return DeviceArray(p.value, (d, d), "<c16", self._device(), self)
+
+    def device_probabilities(self) -> DeviceArray:
+        p = C.POINTER(C.c_double)()
+        check(lib.nq_dm_probabilities_device(self.h, C.byref(p)))
+        return DeviceArray(C.cast(p, C.c_void_p).value, (1 << self.n,), "<f8", self._device(), self)
 
     def _scalar(self, fn) -> float:
         v = C.c_double()

@@ -206,6 +206,11 @@ void state_free(State& s) {
     if (!s.d) return;
     DeviceCtx& c = ctx_for(s.dev);
     cudaSetDevice(s.dev);
+    if (s.dprob) {
+        cudaFreeAsync(s.dprob, c.stream);
+        s.dprob = nullptr;
+        s.dprob_cap = 0;
+    }
     if (s.plain_alloc) {
         // peers may map this buffer: release the mappings (shard_free) first
         cudaStreamSynchronize(c.stream);
@@ -253,7 +258,7 @@ void trace_passes(const std::vector<PlannedPass>& passes, bool dm) {
 }
 
 void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStats& st, bool record = true,
-                std::atomic<void*>* memo = nullptr);
+                JitMemo* memo = nullptr);
 bool layout_is_identity(const State& s);
 
 // Fused-schedule cache: a flush whose queue (kinds, bits, controls,
@@ -267,7 +272,7 @@ struct PlanCacheEntry {
     std::vector<int> layout_out;
     // compiled kernel of each pass, remembered after its first specialised
     // launch (shared by copies of the entry; see jit_launch's memo)
-    std::shared_ptr<std::vector<std::atomic<void*>>> kern;
+    std::shared_ptr<std::vector<JitMemo>> kern;
 };
 
 std::vector<unsigned char> plan_key(const State& s, bool use_layout) {
@@ -298,35 +303,42 @@ void state_flush(State& s) {
         shard_flush(s);
         return;
     }
+    // entries are immutable once published: a hit copies the pointer under
+    // the lock and runs the passes after releasing it, so flushes of other
+    // states (and devices) are not serialised behind this one
     static std::mutex mu;
-    static std::deque<PlanCacheEntry> cache;  // most recent first
+    static std::deque<std::shared_ptr<const PlanCacheEntry>> cache;  // most recent first
     constexpr size_t kCacheEntries = 8;
     PlanStats st;
     const bool use_layout = int(s.layout.size()) == s.nbits && (s.popt.relabel || !layout_is_identity(s));
     std::vector<unsigned char> key = plan_key(s, use_layout);
+    std::shared_ptr<const PlanCacheEntry> hit;
     {
         std::lock_guard<std::mutex> lk(mu);
         for (auto it = cache.begin(); it != cache.end(); ++it) {
-            if (it->key != key) continue;
-            PlanCacheEntry e = *it;
+            if ((*it)->key != key) continue;
+            hit = *it;
             cache.erase(it);
-            cache.push_front(e);
-            if (use_layout) s.layout = e.layout_out;
-            s.queue.clear();
-            run_passes(s, e.passes, e.st, true, e.kern ? e.kern->data() : nullptr);
-            return;
+            cache.push_front(hit);
+            break;
         }
+    }
+    if (hit) {
+        if (use_layout) s.layout = hit->layout_out;
+        s.queue.clear();
+        run_passes(s, hit->passes, hit->st, true, hit->kern ? hit->kern->data() : nullptr);
+        return;
     }
     std::vector<PlannedPass> passes = plan_passes(s.queue, s.popt, &st, use_layout ? &s.layout : nullptr);
     s.queue.clear();
-    auto kern = std::make_shared<std::vector<std::atomic<void*>>>(passes.size());
-    for (auto& k : *kern) k.store(nullptr);
+    auto kern = std::make_shared<std::vector<JitMemo>>(passes.size());
+    auto entry = std::make_shared<const PlanCacheEntry>(PlanCacheEntry{std::move(key), std::move(passes), st, s.layout, kern});
     {
         std::lock_guard<std::mutex> lk(mu);
-        cache.push_front(PlanCacheEntry{std::move(key), passes, st, s.layout, kern});
+        cache.push_front(entry);
         if (cache.size() > kCacheEntries) cache.pop_back();
     }
-    run_passes(s, passes, st, true, kern->data());
+    run_passes(s, entry->passes, entry->st, true, kern->data());
 }
 
 bool layout_is_identity(const State& s) {
@@ -379,7 +391,7 @@ void state_flush_normal(State& s) {
 }
 
 void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStats& st, bool record,
-                std::atomic<void*>* memo) {
+                JitMemo* memo) {
     DeviceCtx& c = ctx_for(s.dev);
     CUDA_TRY(cudaSetDevice(s.dev));
     std::vector<size_t> offs;
@@ -892,6 +904,49 @@ nq_status nq_sv_device_ptr(nq_sv* h, void** out) {
     });
 }
 
+// Probabilities kept on the device for zero-copy consumers:
+// one state-owned buffer, refilled on every call.
+static double* device_prob_buffer(State& s, uint64_t len) {
+    DeviceCtx& c = ctx_for(s.dev);
+    if (s.dprob_cap < len) {
+        if (s.dprob) CUDA_TRY(cudaFreeAsync(s.dprob, c.stream));
+        s.dprob = nullptr;
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s.dprob), len * sizeof(double), c.stream));
+        s.dprob_cap = len;
+    }
+    return s.dprob;
+}
+
+nq_status nq_sv_probabilities_device(nq_sv* h, double** out) {
+    return guard([&] {
+        State& s = st(h);
+        state_flush_normal(s);
+        shard_normalize(s);
+        DeviceCtx& c = ctx_for(s.dev);
+        double* p = device_prob_buffer(s, s.count);
+        launch_probs(s.d, s.count, p, c.stream);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        *out = p;
+    });
+}
+
+nq_status nq_sv_device(const nq_sv* h, int* device) {
+    return guard([&] { *device = const_cast<nq_sv*>(h)->s.dev; });
+}
+
+nq_status nq_dm_device(const nq_dm* h, int* device) {
+    return guard([&] { *device = const_cast<nq_dm*>(h)->s.dev; });
+}
+
+nq_status nq_sv_local_range(const nq_sv* h, uint64_t* offset, uint64_t* count) {
+    return guard([&] {
+        const State& s = const_cast<nq_sv*>(h)->s;
+        *offset = uint64_t(s.rank) << s.nloc;
+        *count = s.count;
+    });
+}
+
 nq_status nq_sv_last_stats(const nq_sv* h, int64_t* passes, int64_t* microops, int64_t* source_ops,
                            int64_t* launches) {
     return guard([&] {
@@ -1145,6 +1200,31 @@ nq_status nq_dm_probabilities(nq_dm* h, double* host_out) {
         CUDA_TRY(cudaMemcpyAsync(host_out, p, dim * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
         CUDA_TRY(cudaFreeAsync(p, c.stream));
         CUDA_TRY(cudaStreamSynchronize(c.stream));
+    });
+}
+
+nq_status nq_dm_device_ptr(nq_dm* h, void** out) {
+    return guard([&] {
+        State& s = st(h);
+        state_flush_normal(s);  // row-major rho (the interleaved layout is undone)
+        CUDA_TRY(cudaSetDevice(s.dev));
+        CUDA_TRY(cudaStreamSynchronize(ctx_for(s.dev).stream));
+        *out = s.d;
+    });
+}
+
+nq_status nq_dm_probabilities_device(nq_dm* h, double** out) {
+    return guard([&] {
+        State& s = st(h);
+        const int il = dm_flush_for_reduction(s);
+        DeviceCtx& c = ctx_for(s.dev);
+        const uint64_t dim = uint64_t(1) << s.n;
+        c.ensure_scratch(scratch_doubles_needed(dim) + 64);
+        double* p = device_prob_buffer(s, dim);
+        launch_dm_probs(s.d, dim, p, c.d_scratch, c.stream, il);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        *out = p;
     });
 }
 

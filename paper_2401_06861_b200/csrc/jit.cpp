@@ -1134,13 +1134,15 @@ bool jit_xstore_ok(const PassHdr& h, const MOp* ops) {
 }
 
 bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,
-                uint64_t rankbase, cudaStream_t s, int device, const JitXStore* xs, std::atomic<void*>* memo) {
+                uint64_t rankbase, cudaStream_t s, int device, const JitXStore* xs, JitMemo* memo) {
     const JitMode mode = jit_mode();
     std::shared_ptr<Entry> e;
-    Entry* known = (memo && !xs) ? static_cast<Entry*>(memo->load(std::memory_order_acquire)) : nullptr;
-    if (known) {
-        // the JIT cache never drops entries: the remembered one stays valid
-        e = std::shared_ptr<Entry>(std::shared_ptr<Entry>{}, known);
+    if (memo && !xs) {
+        std::lock_guard<std::mutex> lk(memo->mu);
+        e = std::static_pointer_cast<Entry>(memo->entry);
+    }
+    if (e) {
+        // remembered for this pass record (owning reference)
     } else if (xs) {
         if (!jit_xstore_ok(h, ops)) throw NqError{NQ_ERR_INTERNAL, "exchange pass cannot be specialised"};
         e = acquire(jit_source(h, ops, pool, true), device, JitMode::Sync);
@@ -1149,7 +1151,10 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
         if (mode == JitMode::Off || h.m < 8 || h.m > 12) return false;
         if (mode == JitMode::Auto && h.nloc < 18) return false;  // interpreter is fine for small states
         e = acquire(jit_source(h, ops, pool), device, mode);
-        if (e && memo) memo->store(e.get(), std::memory_order_release);
+        if (e && memo && e->state.load() == 1) {
+            std::lock_guard<std::mutex> lk(memo->mu);
+            memo->entry = e;
+        }
     }
     if (!e) return false;
     Jit& J = jit();

@@ -8,6 +8,8 @@
 
 #include <atomic>
 #include <cstdint>
+#include <memory>
+#include <mutex>
 #include <string>
 
 namespace nqe {
@@ -57,12 +59,17 @@ bool jit_xstore_ok(const PassHdr& h, const MOp* ops);
 // compilation otherwise, or compiling inline under NQ_JIT=sync).  Returns
 // false when the caller must run the interpreter kernel instead.
 // With xs: compiled synchronously if needed; throws when it cannot run.
-// memo (optional, in-place passes only): an opaque handle of the compiled
-// kernel remembered by the caller for this exact pass record (plan cache):
-// when set, the source is not regenerated and looked up again.
+// memo (optional, in-place passes only): the compiled kernel remembered by
+// the caller for this exact pass record (plan cache): when set, the source is
+// not regenerated and looked up again.  It holds a reference to the JIT
+// entry, so the entry outlives any later eviction from the JIT cache.
+struct JitMemo {
+    std::mutex mu;
+    std::shared_ptr<void> entry;
+};
 bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,
                 uint64_t rankbase, cudaStream_t s, int device, const JitXStore* xs = nullptr,
-                std::atomic<void*>* memo = nullptr);
+                JitMemo* memo = nullptr);
 
 // Expectation batch kernel specialised to the batch's term structure: source,
 // and launch (plus the per-term final sums into out[0..nt)); false when the

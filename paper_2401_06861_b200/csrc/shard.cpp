@@ -133,7 +133,7 @@ struct ShardComm {
     struct SegPlan {
         std::vector<PlannedPass> passes;
         PlanStats st;
-        std::shared_ptr<std::vector<std::atomic<void*>>> kern;
+        std::shared_ptr<std::vector<JitMemo>> kern;
     };
     std::deque<std::pair<std::vector<unsigned char>, std::shared_ptr<SegPlan>>> seg_cache;  // acts_key -> ops moved per exchange
     double* d_flag = nullptr;  // 1-element buffer for the stream barrier
@@ -370,7 +370,7 @@ void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vecto
     po.relabel = layout != nullptr;
     PlanStats st;
     std::vector<PlannedPass> passes;
-    std::shared_ptr<std::vector<std::atomic<void*>>> kern;
+    std::shared_ptr<std::vector<JitMemo>> kern;
     if (layout == nullptr) {
         ShardComm& sc = *s.comm;
         std::vector<unsigned char> key = segment_key(po, ops);
@@ -386,8 +386,7 @@ void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vecto
             auto sp = std::make_shared<ShardComm::SegPlan>();
             sp->passes = passes;
             sp->st = st;
-            sp->kern = std::make_shared<std::vector<std::atomic<void*>>>(passes.size());
-            for (auto& k : *sp->kern) k.store(nullptr);
+            sp->kern = std::make_shared<std::vector<JitMemo>>(passes.size());
             kern = sp->kern;
             sc.seg_cache.emplace_front(std::move(key), std::move(sp));
             if (sc.seg_cache.size() > 16) sc.seg_cache.pop_back();

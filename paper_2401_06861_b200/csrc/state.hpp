@@ -97,6 +97,10 @@ struct State {
     // single-device state vectors: logical qubit -> physical bit after the
     // relabelling passes (identity otherwise); readouts normalise it
     std::vector<int> layout;
+    // device probabilities for zero-copy consumers (nq_*_probabilities_device):
+    // owned by the state, valid until it is next modified or destroyed
+    double* dprob = nullptr;
+    uint64_t dprob_cap = 0;
 };
 
 void sv_expect_raw(State& s, const uint64_t* flip, const uint64_t* signs, int nterms, std::vector<cplx>& totals);
