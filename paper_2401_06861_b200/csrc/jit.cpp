@@ -238,6 +238,13 @@ bool warplocal_enabled() {
     return on;
 }
 
+// Per-thread phase accumulators for unit-modulus diagonal tables (see the
+// generator).  NQ_JIT_PHASEACC=0 disables them (A/B).
+bool accumulate_phases() {
+    static const bool on = env_int("NQ_JIT_PHASEACC", 1) != 0;
+    return on;
+}
+
 bool diag_runtime_skip() {
     static const bool on = env_int("NQ_DIAG_SKIP", 0) != 0;
     return on;
@@ -638,14 +645,81 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
         return o.str();
     };
     bool full_barrier_done = false;
+    // Diagonal phase accumulators (unit-modulus tables, e.g. every phase of a
+    // state-vector circuit): a diagonal factor that depends on no register
+    // slot is uniform over the thread's amplitudes (ug); one that depends on
+    // register slot t only is ug-part x (a phase on the amplitudes whose slot
+    // t bit is 1), accumulated per thread in ph<t>.  A table on two slots
+    // t, u splits into those parts plus an interaction factor applied to the
+    // 4 amplitudes with both bits set.  Diagonals commute with each other, so
+    // the accumulated phases are applied only before an operator that does
+    // not commute with them (a non-diagonal op on the slot, a relayout, the
+    // store): one complex multiply per amplitude for all of them (Gray-code
+    // walk over the 16 registers) instead of one per amplitude per table.
     bool ug_pending = false;
+    bool ph_pending[4] = {false, false, false, false};
+    auto ph_name = [](int t) { return "ph" + std::to_string(t); };
+    // apply ph<t> to the registers with slot bit t set (no ug)
+    auto flush_ph = [&](unsigned mask) {
+        for (int t = 0; t < 4; ++t) {
+            if (!((mask >> t) & 1u) || !ph_pending[t]) continue;
+            for (int l = 0; l < E; ++l)
+                if ((l >> t) & 1) s << "    a[" << l << "] = cmul(" << ph_name(t) << ", a[" << l << "]);\n";
+            ph_pending[t] = false;
+        }
+    };
+    // everything pending: ug and every ph<t>, one multiply per amplitude
     auto flush_ug = [&] {
-        if (!ug_pending) return;
-        s << "    if (!is_one(ug)) {\n";
-        for (int l = 0; l < E; ++l) s << "      a[" << l << "] = cmul(ug, a[" << l << "]);\n";
+        unsigned pm = 0;
+        for (int t = 0; t < 4; ++t)
+            if (ph_pending[t]) pm |= 1u << t;
+        if (!ug_pending && !pm) return;
+        if (!pm) {
+            s << "    if (!is_one(ug)) {\n";
+            for (int l = 0; l < E; ++l) s << "      a[" << l << "] = cmul(ug, a[" << l << "]);\n";
+            s << "    }\n";
+            ug_pending = false;
+            return;
+        }
+        // Gray-code order over the pending slots: consecutive registers differ
+        // in one pending bit, so the running factor takes one multiply (by
+        // ph<t> or its conjugate = inverse) per step
+        std::vector<int> pb;
+        for (int t = 0; t < 4; ++t)
+            if ((pm >> t) & 1u) pb.push_back(t);
+        const int np = int(pb.size());
+        s << "    { double2 pr = " << (ug_pending ? "ug" : "make_double2(1.0, 0.0)") << ";\n";
+        unsigned prev = 0;
+        for (int i = 0; i < (1 << np); ++i) {
+            const unsigned gi = unsigned(i) ^ (unsigned(i) >> 1);
+            unsigned sel = 0;  // register bits of the pending slots
+            for (int j = 0; j < np; ++j)
+                if ((gi >> j) & 1u) sel |= 1u << pb[size_t(j)];
+            if (i > 0) {
+                const unsigned ch = gi ^ prev;
+                const int t = pb[size_t(__builtin_ctz(ch))];
+                if (gi & ch) s << "      pr = cmul(pr, " << ph_name(t) << ");\n";
+                else s << "      pr = cmul(pr, cconj(" << ph_name(t) << "));\n";
+            }
+            prev = gi;
+            for (int l = 0; l < E; ++l)
+                if ((unsigned(l) & pm) == sel) s << "      a[" << l << "] = cmul(pr, a[" << l << "]);\n";
+        }
         s << "    }\n";
         ug_pending = false;
+        for (int t = 0; t < 4; ++t) ph_pending[t] = false;
     };
+    auto ph_mul = [&](int t, const std::string& f) {
+        if (ph_pending[t]) s << "      " << ph_name(t) << " = cmul(" << ph_name(t) << ", " << f << ");\n";
+        else s << "      " << ph_name(t) << " = " << f << ";\n";
+        ph_pending[t] = true;
+    };
+    auto ug_mul = [&](const std::string& f) {
+        if (ug_pending) s << "      ug = cmul(ug, " << f << ");\n";
+        else s << "      ug = " << f << ";\n";
+        ug_pending = true;
+    };
+    if (accumulate_phases()) s << "    double2 ph0, ph1, ph2, ph3;\n    (void)ph0; (void)ph1; (void)ph2; (void)ph3;\n";
     for (int i = 1; i < h.nops; ++i) {
         const MOp& op = ops[i];
         const int li = lay_of_op[size_t(i)];
@@ -680,6 +754,11 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
             break;
         }
         case MOP_DENSE: {
+            {
+                unsigned sl = 0;
+                for (int j = 0; j < op.k; ++j) sl |= 1u << op.pos[j];
+                flush_ph(sl);
+            }
             bool real = true;
             size_t generic = 0;  // entries that are neither zero, real nor pure imaginary
             const size_t nent = size_t(1) << (2 * op.k);
@@ -720,6 +799,17 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
         }
         case MOP_SWAP: {
             const int j0 = op.pos[0], j1 = op.pos[1];
+            if (ph_pending[j0] || ph_pending[j1]) {
+                // the registers trade places: so do their pending phases
+                if (ph_pending[j0] && ph_pending[j1])
+                    s << "    { const double2 t_ = " << ph_name(j0) << "; " << ph_name(j0) << " = " << ph_name(j1) << "; "
+                      << ph_name(j1) << " = t_; }\n";
+                else if (ph_pending[j0])
+                    s << "    " << ph_name(j1) << " = " << ph_name(j0) << ";\n";
+                else
+                    s << "    " << ph_name(j0) << " = " << ph_name(j1) << ";\n";
+                std::swap(ph_pending[j0], ph_pending[j1]);
+            }
             if (use_px && (dirty & ((1u << j0) | (1u << j1)))) {
                 // SWAP(j0, j1) . X^px = X^swap(px) . SWAP(j0, j1)
                 s << "    px = (px & ~" << ((1u << j0) | (1u << j1)) << "u) | (" << px_bit(j0) << " << " << j1 << ") | ("
@@ -731,6 +821,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
             break;
         }
         case MOP_DEPOL:
+            flush_ph(0xFu);
             if (use_px) commit(0xFu);
             if (op.k == 2) {
                 const int a0 = std::min(op.pos[0], op.pos[1]), a1 = std::max(op.pos[0], op.pos[1]);
@@ -744,6 +835,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
             }
             break;
         case MOP_XPERM: {
+            flush_ph(1u << op.pos[0]);
             unsigned cmL = 0, cmT = 0;
             for (int p = 0; p < m; ++p) {
                 if (!((op.cmask_tile >> p) & 1u)) continue;
@@ -802,6 +894,38 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
             unsigned dslots = 0;
             for (int t = 0; t < 4; ++t)
                 if (slotc[t]) dslots |= 1u << t;
+            const int nds = __builtin_popcount(dslots);
+            bool unit = true;
+            for (int gi = 0; gi < (1 << op.k) && unit; ++gi) unit = std::abs(std::norm(tab[gi]) - 1.0) < 1e-14;
+            if (accumulate_phases() && unit && nds >= 1 && nds <= 2 && !(use_px && (dirty & dslots))) {
+                const unsigned regmask = slotc[0] | slotc[1] | slotc[2] | slotc[3];
+                // table entries with none of the register bits set: exactly 1 for every g?
+                bool one0 = true;
+                for (int gi = 0; gi < (1 << op.k) && one0; ++gi)
+                    if ((unsigned(gi) & regmask) == 0u) one0 = tab[gi] == cplx(1.0, 0.0);
+                std::vector<int> ts;
+                for (int t = 0; t < 4; ++t)
+                    if ((dslots >> t) & 1u) ts.push_back(t);
+                if (!one0) {
+                    s << "      const double2 f00 = lds(D);\n      const double2 c00 = cconj(f00);\n";
+                    ug_mul("f00");
+                }
+                for (int t : ts) {
+                    s << "      const double2 fs" << t << " = lds(D + " << slotc[t] << "u);\n";
+                    ph_mul(t, one0 ? "fs" + std::to_string(t) : "cmul(fs" + std::to_string(t) + ", c00)");
+                }
+                if (nds == 2) {
+                    // interaction part on the registers with both slot bits set
+                    const int t = ts[0], u = ts[1];
+                    s << "      double2 fr = cmul(lds(D + " << (slotc[t] | slotc[u]) << "u), cconj(cmul(fs" << t << ", fs" << u
+                      << ")));\n";
+                    if (!one0) s << "      fr = cmul(fr, f00);\n";
+                    for (int l = 0; l < E; ++l)
+                        if (((l >> t) & 1) && ((l >> u) & 1)) s << "      a[" << l << "] = cmul(fr, a[" << l << "]);\n";
+                }
+                s << "    }\n";
+                break;
+            }
             if (anyreg && use_px && (dirty & dslots)) {
                 // table entries selected through the pending permutation
                 std::ostringstream gx;
