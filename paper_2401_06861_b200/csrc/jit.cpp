@@ -9,12 +9,17 @@
 // (shared memory), so re-running the same circuit structure with new angles
 // (VQE, Trotter sweeps, repeated benchmark steps) reuses the compiled kernel.
 //
-// Memory pipeline of the generated kernel: the next tile is prefetched into
-// one of two shared-memory buffers with cp.async (16-byte LDGSTS, natural
-// order, fully coalesced) while the current tile is computed from registers;
-// the current tile's buffer doubles as the relayout scratch.  The buffer
-// addressing uses a per-pass linear swizzle chosen so that every register
-// layout of the pass (and the natural order) is bank-conflict free.
+// Memory pipeline of the generated pass kernel: each thread streams its 16
+// amplitudes of the tile straight into registers in the first register
+// layout (128-bit ld.global.cs), computes, relayouts through one shared-memory
+// tile buffer, and streams the results out of registers (st.global.cs).
+// Residency (4 CTAs x 128 threads x 128 registers per SM) hides the load
+// latency.  Measured and removed (round 1, profiles/r01b_*): a cp.async
+// double buffer, bulk (TMA) staging, L2 bulk prefetch and warp-local
+// relayouts were all slower, because the extra shared memory halves the
+// resident CTAs.  The relayout buffer addressing uses a per-pass linear
+// swizzle chosen so that every register layout of the pass is bank-conflict
+// free.
 //
 // Compilation is asynchronous: the first time a structure is seen the
 // interpreter runs it while worker threads compile; later flushes use the
@@ -224,20 +229,6 @@ bool px_enabled() {
     return on;
 }
 
-// Warp-local relayouts (opt-in, NQ_JIT_WARPLOCAL=1): when a pass leaves at
-// least as many tile bits out of every register set as there are warp bits,
-// those bits become the warp index in every layout, so each warp only ever
-// exchanges amplitudes with itself through shared memory and the relayout
-// barriers are __syncwarp instead of __syncthreads (warps drift apart and
-// overlap their load, compute and store phases).  Measured slower on B200
-// (random-30 4044 -> 3750 gates/s, VQE-28 18.1 -> 24 ms, QFT-30 96 -> 105-110
-// ms): the warp bits must be tiles bits no register set uses, which pushes
-// the lanes onto higher tile bits (less coalesced per instruction).
-bool warplocal_enabled() {
-    static const bool on = env_int("NQ_JIT_WARPLOCAL", 0) != 0;
-    return on;
-}
-
 // Per-thread phase accumulators for unit-modulus diagonal tables (see the
 // generator).  NQ_JIT_PHASEACC=0 disables them (A/B).
 bool accumulate_phases() {
@@ -248,15 +239,6 @@ bool accumulate_phases() {
 bool diag_runtime_skip() {
     static const bool on = env_int("NQ_DIAG_SKIP", 0) != 0;
     return on;
-}
-
-const JitKnobs& jit_knobs() {
-    // Measured on B200 (random circuit, n = 30): direct loads with a 128-register
-    // cap (512 threads / SM) beat the cp.async double buffer, whose extra 32-64 KB
-    // of shared memory halves the resident CTAs.  -1 = auto (512 / threads).
-    static const JitKnobs k{env_int("NQ_JIT_PREFETCH", 0) != 0, env_int("NQ_JIT_MINB", -1), env_int("NQ_JIT_TMA", 0) != 0,
-                            env_int("NQ_JIT_L2PF", 0)};
-    return k;
 }
 
 // Dense k <= 2 operator with structural zeros (Liouville superoperators of
@@ -353,8 +335,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
     std::vector<int> qst(h.qst, h.qst + m);  // store positions (a permutation of q: relabelled pass)
     const bool relabel = qst != q;
     // Hermitian (mirror) pass: tile / rest bits pair as physical (2q, 2q+1)
-    const JitKnobs& kn0 = jit_knobs();
-    bool mirror = (h.flags & PASS_MIRROR) && !kn0.prefetch && !xstore;
+    bool mirror = (h.flags & PASS_MIRROR) && !xstore;
     std::vector<int> tpair(size_t(m), -1), rpair(rest.size(), -1);
     for (int i = 0; i < m && mirror; ++i)
         for (int j = 0; j < m; ++j)
@@ -366,9 +347,6 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
     for (int x : rpair) mirror = mirror && x >= 0;
     std::vector<int> qmir(static_cast<size_t>(m));
     for (int i = 0; i < m && mirror; ++i) qmir[size_t(i)] = qst[size_t(tpair[size_t(i)])];
-    // bulk-copy staging needs the 16 contiguous low amplitudes as tile bits 0-3
-    bool use_tma = kn0.tma && !kn0.prefetch && !mirror && m >= 8 && !xstore;
-    for (int b = 0; b < 4 && use_tma; ++b) use_tma = q[size_t(b)] == b;
     auto mirror_rest_expr = [&](const std::string& r) {
         std::ostringstream o;
         o << "0ull";
@@ -397,40 +375,6 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
     const bool extra_relayout = relabel && lays.size() == 1;
     if (extra_relayout) mirror = false;  // (full tiles then; the mirror store path expects the last layout)
     Layout LS = by_store(lays.back());
-    // warp-local relayouts (see warplocal_enabled)
-    bool warp_local = false;
-    {
-        const int nwb = logT - 5;  // warp-index bits of the thread id
-        bool ok = warplocal_enabled() && !mirror && !kn0.prefetch && !use_tma && nwb >= 1 && lays.size() >= 2;
-        for (int i = 1; i < h.nops && ok; ++i) ok = !(ops[i].type == MOP_DENSE && ops[i].k >= 4);
-        unsigned used = 0;
-        for (const auto& L : lays)
-            for (int j = 0; j < L.r; ++j) used |= 1u << L.rp[j];
-        std::vector<int> fr;
-        for (int b = m - 1; b >= 0 && int(fr.size()) < nwb; --b)
-            if (!((used >> b) & 1u)) fr.push_back(b);
-        ok = ok && int(fr.size()) == nwb;
-        if (ok) {
-            std::reverse(fr.begin(), fr.end());
-            auto force = [&](Layout L) {
-                std::vector<int> rest_bits;
-                for (int b : L.nonr)
-                    if (std::find(fr.begin(), fr.end(), b) == fr.end()) rest_bits.push_back(b);
-                L.nonr = rest_bits;
-                L.nonr.insert(L.nonr.end(), fr.begin(), fr.end());
-                return L;
-            };
-            std::vector<Layout> wl;
-            for (const auto& L : lays) wl.push_back(force(L));
-            // (the lanes may move to higher tile bits: every thread's registers
-            // still cover whole 256-byte runs, and L2 merges the sectors)
-            if (ok) {
-                lays = wl;
-                LS = force(LS);
-                warp_local = true;
-            }
-        }
-    }
     std::vector<Layout> sw_lays = lays;
     if (extra_relayout) sw_lays.push_back(LS);
     const Swizzle sw = choose_swizzle(sw_lays, m);
@@ -452,12 +396,11 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
         return o.str();
     };
 
-    const JitKnobs& kn = jit_knobs();
     std::ostringstream s;
     s << "#include \"pass_ops.cuh\"\n"
       << "extern \"C\" __global__ void __launch_bounds__(" << T;
     // 8 amplitudes per thread need ~half the registers: aim for 768 threads/SM
-    const int minb = kn.min_blocks >= 0 ? kn.min_blocks : std::max(1, (E == 8 ? 768 : 512) / T);
+    const int minb = std::max(1, (E == 8 ? 768 : 512) / T);
     if (minb > 0) s << ", " << minb;
     s << ")\n"
       << "nqjit(double2* __restrict__ st, const double2* __restrict__ gpool, unsigned long long rankbase,"
@@ -466,17 +409,9 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
       << "  using namespace nq;\n"
       << "  extern __shared__ __align__(16) unsigned char smem[];\n"
       << "  double2* buf0 = reinterpret_cast<double2*>(smem);\n"
-      << "  double2* buf1 = buf0 + " << ((kn.prefetch || use_tma) ? SIZE : 0) << ";\n"
-      << "  double2* pool = buf1 + " << SIZE << ";\n"
+      << "  double2* pool = buf0 + " << SIZE << ";\n"
       << "  const unsigned tid = threadIdx.x;\n"
       << "  for (unsigned i = tid; i < " << h.pool_n << "u; i += " << T << "u) pool[i] = gpool[i];\n";
-    // natural-order prefetch: element e = tid + j*T
-    {
-        std::vector<int> lowbits;
-        for (int b = 0; b < logT; ++b) lowbits.push_back(b);
-        s << "  const unsigned long long poff = " << state_off("tid", lowbits, q) << ";\n";
-        s << "  const unsigned psw = " << swz_expr("tid", sw) << ";\n";
-    }
     for (size_t k = 0; k < lays.size(); ++k) {
         s << "  const unsigned tb" << k << " = " << deposit_expr("tid", lays[k].nonr, false) << ";\n";
         s << "  const unsigned sw" << k << " = " << swz_expr("tb" + std::to_string(k), sw) << ";\n";
@@ -494,84 +429,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
             s << "  const unsigned long long toff_mir = "
               << state_off("tb" + std::to_string(lays.size() - 1), LN.nonr, qmir) << ";\n";
     }
-    // prefetch helper (inline lambda-free: a macro-like block emitted twice)
-    auto prefetch = [&](const std::string& rexpr, const std::string& bufname, const std::string& indent) {
-        s << indent << "{ const unsigned long long pb = " << deposit_expr("(unsigned long long)(" + rexpr + ")", rest, true)
-          << " + poff;\n";
-        for (int j = 0; j < E; ++j) {
-            const unsigned e = unsigned(j) * unsigned(T);
-            unsigned long long go = 0;
-            for (int b = 0; b < m; ++b)
-                if ((e >> b) & 1u) go |= 1ull << q[size_t(b)];
-            s << indent << "  cp_async16(" << bufname << " + (psw ^ " << sw.apply(e) << "u), st + pb + " << hex64(go)
-              << ");\n";
-        }
-        s << indent << "}\n";
-    };
-    if (use_tma) {
-        // warp 0 stages the next tile with bulk copies of 256-byte chunks (the
-        // 16 contiguous low amplitudes) onto an mbarrier while every warp
-        // computes the current one
-        const int nch = SIZE / 16;
-        std::vector<int> qhi(q.begin() + 4, q.end());
-        s << "  __shared__ __align__(8) unsigned long long mbar[2];\n"
-          << "  if (tid == 0) { mbar_init(&mbar[0], 1); mbar_init(&mbar[1], 1); mbar_fence_init(); }\n"
-          << "  __syncthreads();\n";
-        auto issue = [&](const std::string& rexpr, const std::string& bufname, const std::string& bar,
-                         const std::string& ind) {
-            s << ind << "if (tid < 32u) {\n"
-              << ind << "  const double2* src = st + (" << deposit_expr("(unsigned long long)(" + rexpr + ")", rest, true)
-              << ");\n"
-              << ind << "  if (tid == 0) mbar_expect_tx(" << bar << ", " << SIZE * 16 << "u);\n"
-              << ind << "  for (unsigned c = tid; c < " << nch << "u; c += 32u)\n"
-              << ind << "    bulk_g2s(" << bufname << " + c * 16u, src + (" << deposit_expr("(unsigned long long)c", qhi, true)
-              << "), 256u, " << bar << ");\n"
-              << ind << "}\n";
-        };
-        s << "  long long r = blockIdx.x;\n"
-          << "  if (r < ntiles) {\n";
-        issue("r", "buf0", "&mbar[0]", "    ");
-        s << "  }\n"
-          << "  for (int it = 0; r < ntiles; r += gridDim.x, ++it) {\n"
-          << "    double2* cur = (it & 1) ? buf1 : buf0;\n"
-          << "    double2* nxt = (it & 1) ? buf0 : buf1;\n"
-          << "    const long long rn = r + gridDim.x;\n"
-          << "    if (rn < ntiles) {\n"
-          << "      fence_proxy_async();\n";
-        issue("rn", "nxt", "&mbar[(it + 1) & 1]", "      ");
-        s << "    }\n"
-          << "    mbar_wait(&mbar[it & 1], (unsigned)(it >> 1) & 1u);\n"
-          << "    const unsigned long long base = " << deposit_expr("(unsigned long long)r", rest, true) << ";\n"
-          << "    const unsigned long long full = rankbase | base;\n"
-          << "    (void)full;\n"
-          << "    double2 a[" << E << "];\n"
-          << "    double2 ug = make_double2(1.0, 0.0);\n"
-          << "    (void)ug;\n";
-        for (int l = 0; l < E; ++l) s << "    a[" << l << "] = cur[tb0 | " << L0.rconst(l) << "u];\n";
-    } else if (kn.prefetch && !xstore) {
-        s << "  long long r = blockIdx.x;\n"
-          << "  if (r < ntiles) {\n";
-        prefetch("r", "buf0", "    ");
-        s << "  }\n  cp_async_commit();\n"
-          << "  __syncthreads();\n"
-          << "  for (int it = 0; r < ntiles; r += gridDim.x, ++it) {\n"
-          << "    double2* cur = (it & 1) ? buf1 : buf0;\n"
-          << "    double2* nxt = (it & 1) ? buf0 : buf1;\n"
-          << "    const long long rn = r + gridDim.x;\n"
-          << "    if (rn < ntiles) {\n";
-        prefetch("rn", "nxt", "      ");
-        s << "    }\n"
-          << "    cp_async_commit();\n"
-          << "    cp_async_wait<1>();\n"
-          << "    __syncthreads();\n"
-          << "    const unsigned long long base = " << deposit_expr("(unsigned long long)r", rest, true) << ";\n"
-          << "    const unsigned long long full = rankbase | base;\n"
-          << "    (void)full;\n"
-          << "    double2 a[" << E << "];\n"
-          << "    double2 ug = make_double2(1.0, 0.0);\n"
-          << "    (void)ug;\n";
-        for (int l = 0; l < E; ++l) s << "    a[" << l << "] = cur[sw0 ^ " << sw.apply(L0.rconst(l)) << "u];\n";
-    } else {
+    {
         // direct streaming loads into the first register layout; one buffer
         s << "  const unsigned long long toff_ld = " << state_off("tb0", L0.nonr, q) << ";\n"
           << "  __syncthreads();\n"
@@ -599,19 +457,6 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
           << "    { const double2* src = st + base + toff_ld;\n";
         for (int l = 0; l < E; ++l) s << "      a[" << l << "] = ld_stream(src + " << hex64(reg_off(L0, l, q)) << ");\n";
         s << "    }\n";
-        // L2 prefetch of a later tile (bulk, 256-byte chunks of the 16
-        // contiguous low amplitudes): its loads then hit L2 while this one computes
-        bool l2pf = kn.l2pf > 0 && !mirror && !xstore && m >= 8;
-        for (int b = 0; b < 4 && l2pf; ++b) l2pf = q[size_t(b)] == b;
-        if (l2pf) {
-            const int nch = SIZE / 16;
-            std::vector<int> qhi(q.begin() + 4, q.end());
-            s << "    { const long long rn = r + " << kn.l2pf << "ll * gridDim.x;\n"
-              << "      if (rn < ntiles" << (nch < T ? " && tid < " + std::to_string(nch) + "u" : "") << ")\n"
-              << "        prefetch_l2_bulk(st + (" << deposit_expr("(unsigned long long)rn", rest, true) << ") + ("
-              << deposit_expr("(unsigned long long)tid", qhi, true) << "), 256u);\n"
-              << "    }\n";
-        }
     }
     // pending-permutation state (see px_enabled): dirty = register slots
     // whose px bit may be set at this point of the program
@@ -733,8 +578,8 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
             // warp-local: intra-warp exchange; a relabelled pass still needs one
             // full barrier after every warp has consumed its loads (its stores
             // hit addresses other warps load), taken at the first relayout
-            const char* bar1 = warp_local ? "__syncwarp()" : "__syncthreads()";
-            const char* bar2 = (warp_local && !(relabel && !full_barrier_done)) ? "__syncwarp()" : "__syncthreads()";
+            const char* bar1 = "__syncthreads()";
+            const char* bar2 = "__syncthreads()";
             full_barrier_done = true;
             s << "    " << bar1 << ";\n";
             if (use_px && dirty) {
@@ -1050,9 +895,8 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
         s << "    }\n";
     }
     s << ""
-      << (warp_local ? "    __syncwarp();\n" : "    __syncthreads();\n")
+      << "    __syncthreads();\n"
       << "  }\n";
-    if (kn.prefetch && !xstore) s << "  cp_async_wait<0>();\n";
     s << "}\n";
     return s.str();
 }
@@ -1283,7 +1127,7 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
     if (!e) return false;
     Jit& J = jit();
     const int T = (1 << h.m) / (1 << ops[0].k);
-    const size_t smem = (size_t((jit_knobs().prefetch || jit_knobs().tma) ? 2 : 1) << h.m) * 16 + size_t(h.pool_n) * 16;
+    const size_t smem = (size_t(1) << h.m) * 16 + size_t(h.pool_n) * 16;
     const int occ = occupancy(*e, device, T, smem);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);

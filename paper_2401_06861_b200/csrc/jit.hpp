@@ -25,16 +25,6 @@ struct JitStats {
 
 JitMode jit_mode();
 
-// Code-generation knobs (environment, read once): NQ_JIT_PREFETCH=0|1 selects
-// direct loads vs a cp.async double-buffered prefetch of the next tile;
-// NQ_JIT_MINB=k adds __launch_bounds__ min-blocks k (register cap).
-struct JitKnobs {
-    bool prefetch;
-    int min_blocks;
-    bool tma;  // NQ_JIT_TMA=1: next tile staged by bulk (TMA) copies on an mbarrier
-    int l2pf;  // NQ_JIT_L2PF=k: bulk L2 prefetch of the tile k iterations ahead (0 = off)
-};
-const JitKnobs& jit_knobs();
 
 // CUDA source of the kernel specialised to one pass record.  xstore: the
 // exchange-store variant (sharded states, see JitXStore).
