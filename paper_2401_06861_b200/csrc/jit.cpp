@@ -412,27 +412,22 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
       << "  double2* pool = buf0 + " << SIZE << ";\n"
       << "  const unsigned tid = threadIdx.x;\n"
       << "  for (unsigned i = tid; i < " << h.pool_n << "u; i += " << T << "u) pool[i] = gpool[i];\n";
-    for (size_t k = 0; k < lays.size(); ++k) {
-        s << "  const unsigned tb" << k << " = " << deposit_expr("tid", lays[k].nonr, false) << ";\n";
-        s << "  const unsigned sw" << k << " = " << swz_expr("tb" + std::to_string(k), sw) << ";\n";
-    }
+    // Per-layout thread constants (tile-bit pattern tb<k> and swizzled
+    // offset sw<k>) are defined inside the tile loop where layout k becomes
+    // active: short live ranges, so the 16 amplitudes keep the registers.
+    // (tidv is tid made opaque to the optimiser once per tile, so these are
+    // recomputed per tile -- a few integer ops -- instead of being hoisted out
+    // of the loop, where 16 addresses per layout would spill to local memory)
+    auto def_layout = [&](size_t k) {
+        s << "    const unsigned tb" << k << " = " << deposit_expr("tidv", lays[k].nonr, false) << ";\n";
+        s << "    const unsigned sw" << k << " = " << swz_expr("tb" + std::to_string(k), sw) << ";\n";
+        s << "    (void)sw" << k << ";\n";
+    };
     const Layout& L0 = lays.front();
     const Layout& LN = lays.back();
-    if (extra_relayout) {
-        s << "  const unsigned tbS = " << deposit_expr("tid", LS.nonr, false) << ";\n";
-        s << "  const unsigned swS = " << swz_expr("tbS", sw) << ";\n";
-        s << "  const unsigned long long toff_st = " << state_off("tbS", LS.nonr, qst) << ";\n";
-    } else {
-        s << "  const unsigned long long toff_st = "
-          << state_off("tb" + std::to_string(lays.size() - 1), LN.nonr, qst) << ";\n";
-        if (mirror)
-            s << "  const unsigned long long toff_mir = "
-              << state_off("tb" + std::to_string(lays.size() - 1), LN.nonr, qmir) << ";\n";
-    }
     {
         // direct streaming loads into the first register layout; one buffer
-        s << "  const unsigned long long toff_ld = " << state_off("tb0", L0.nonr, q) << ";\n"
-          << "  __syncthreads();\n"
+        s << "  __syncthreads();\n"
           << "  for (long long r = blockIdx.x; r < ntiles; r += gridDim.x) {\n";
         if (mirror) {
             // Hermitian pass: only canonical tiles (r <= mirror(r)) are read
@@ -454,7 +449,10 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
           << "    double2 a[" << E << "];\n"
           << "    double2 ug = make_double2(1.0, 0.0);\n"
           << "    (void)ug;\n"
-          << "    { const double2* src = st + base + toff_ld;\n";
+          << "    unsigned tidv = tid;\n"
+          << "    asm volatile(\"\" : \"+r\"(tidv));\n";
+        def_layout(0);
+        s << "    { const double2* src = st + base + (" << state_off("tb0", L0.nonr, q) << ");\n";
         for (int l = 0; l < E; ++l) s << "      a[" << l << "] = ld_stream(src + " << hex64(reg_off(L0, l, q)) << ");\n";
         s << "    }\n";
     }
@@ -489,7 +487,6 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
                 o << " | ((unsigned long long)" << px_bit(b) << " << " << pos[size_t(A.rp[b])] << ")";
         return o.str();
     };
-    bool full_barrier_done = false;
     // Diagonal phase accumulators (unit-modulus tables, e.g. every phase of a
     // state-vector circuit): a diagonal factor that depends on no register
     // slot is uniform over the thread's amplitudes (ug); one that depends on
@@ -575,12 +572,8 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
         case MOP_LAYOUT: {
             const Layout& A = lays[size_t(li - 1)];
             flush_ug();
-            // warp-local: intra-warp exchange; a relabelled pass still needs one
-            // full barrier after every warp has consumed its loads (its stores
-            // hit addresses other warps load), taken at the first relayout
             const char* bar1 = "__syncthreads()";
             const char* bar2 = "__syncthreads()";
-            full_barrier_done = true;
             s << "    " << bar1 << ";\n";
             if (use_px && dirty) {
                 s << "    {\n";
@@ -594,6 +587,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
                     s << "    cur[sw" << (li - 1) << " ^ " << sw.apply(A.rconst(l)) << "u] = a[" << l << "];\n";
             }
             s << "    " << bar2 << ";\n";
+            def_layout(size_t(li));
             for (int l = 0; l < E; ++l)
                 s << "    a[" << l << "] = cur[sw" << li << " ^ " << sw.apply(L.rconst(l)) << "u];\n";
             break;
@@ -863,12 +857,19 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
                 s << "    cur[" << swN << " ^ " << sw.apply(LN.rconst(l)) << "u] = a[" << l << "];\n";
         }
         s << "    __syncthreads();\n";
+        s << "    const unsigned tbS = " << deposit_expr("tidv", LS.nonr, false) << ";\n";
+        s << "    const unsigned swS = " << swz_expr("tbS", sw) << ";\n";
         for (int l = 0; l < E; ++l) s << "    a[" << l << "] = cur[swS ^ " << sw.apply(LS.rconst(l)) << "u];\n";
     }
     const Layout& LST = extra_relayout ? LS : LN;
     // pending permutation: register l holds the amplitude of index l ^ px
     const std::string pxo = (use_px && dirty) ? " ^ pxo" : "";
     if (use_px && dirty) s << "    const unsigned long long pxo = " << px_state_xor(LST, qst) << ";\n";
+    {
+        const std::string tbl = extra_relayout ? "tbS" : "tb" + std::to_string(lays.size() - 1);
+        s << "    const unsigned long long toff_st = " << state_off(tbl, LST.nonr, qst) << ";\n";
+        if (mirror) s << "    const unsigned long long toff_mir = " << state_off(tbl, LN.nonr, qmir) << ";\n";
+    }
     if (xstore) {
         // exchange store (sharded states): element o whose bit v (xmask)
         // differs from this rank's bit (xval) goes to the partner's buffer at
