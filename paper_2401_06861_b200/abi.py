@@ -438,16 +438,19 @@ def _dl_delete(ptr):
     _dl_live.pop(mt.manager_ctx, None)
 
 
-_PyCapsule_Destructor = C.CFUNCTYPE(None, C.py_object)
+# the destructor receives the dying capsule as a raw pointer: wrapping it in a
+# py_object would take a new reference to an object at refcount 0 (resurrect
+# it) and crash when that reference is dropped
+_PyCapsule_Destructor = C.CFUNCTYPE(None, C.c_void_p)
 _capsule_new = C.pythonapi.PyCapsule_New
 _capsule_new.restype = C.py_object
 _capsule_new.argtypes = [C.c_void_p, C.c_char_p, _PyCapsule_Destructor]
 _capsule_is_valid = C.pythonapi.PyCapsule_IsValid
 _capsule_is_valid.restype = C.c_int
-_capsule_is_valid.argtypes = [C.py_object, C.c_char_p]
+_capsule_is_valid.argtypes = [C.c_void_p, C.c_char_p]
 _capsule_get_ptr = C.pythonapi.PyCapsule_GetPointer
 _capsule_get_ptr.restype = C.c_void_p
-_capsule_get_ptr.argtypes = [C.py_object, C.c_char_p]
+_capsule_get_ptr.argtypes = [C.c_void_p, C.c_char_p]
 
 
 @_PyCapsule_Destructor

@@ -99,3 +99,36 @@ def test_pass_kernels_compile_with_nvrtc_including_exchange_stores():
         xsrc, xok = abi.jit_debug(24, ops, idx, xstore=True)
         assert xok == 1, xsrc[-2000:]
         assert "xout_r + (o ^ xmask)" in xsrc and "rr = " in xsrc
+
+
+def test_dlpack_capsule_lifecycle_without_a_device():
+    """The DLPack export path without touching device memory:
+    an unconsumed capsule releases its managed tensor when it dies, and a
+    consumed one ("used_dltensor", as torch / CuPy rename it) is released by
+    the consumer calling the tensor's deleter exactly once."""
+    import ctypes as C
+    import gc
+
+    view = abi.DeviceArray(0x1000, (8,), "<c16", 0)
+    for _ in range(3):  # unconsumed: the capsule destructor frees it
+        cap = view.__dlpack__()
+        assert len(abi._dl_live) == 1
+        del cap
+        gc.collect()
+        assert len(abi._dl_live) == 0
+    cap = view.__dlpack__()
+    get = C.pythonapi.PyCapsule_GetPointer
+    get.restype, get.argtypes = C.c_void_p, [C.py_object, C.c_char_p]
+    ptr = get(cap, b"dltensor")
+    mt = abi._DLManagedTensor.from_address(ptr)
+    assert mt.dl_tensor.data == 0x1000 and mt.dl_tensor.ndim == 1 and mt.dl_tensor.shape[0] == 8
+    assert (mt.dl_tensor.dtype.code, mt.dl_tensor.dtype.bits) == (5, 128)
+    rename = C.pythonapi.PyCapsule_SetName
+    rename.restype, rename.argtypes = C.c_int, [C.py_object, C.c_char_p]
+    used = C.c_char_p(b"used_dltensor")
+    assert rename(cap, used) == 0
+    del cap
+    gc.collect()
+    assert len(abi._dl_live) == 1  # consumed: the consumer owns it now
+    mt.deleter(ptr)
+    assert len(abi._dl_live) == 0
