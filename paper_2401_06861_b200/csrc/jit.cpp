@@ -255,16 +255,19 @@ bool diag_runtime_skip() {
 // entry from shared memory (as the d2 template does) to spare registers.
 std::string sparse_dense(const MOp& op, const cplx* u, int E, const std::string& P) {
     const int d = 1 << op.k;
-    enum Cls { Z, R, I, C };
+    // O / M: exactly +1 / -1 (pivot-normalised rows, planner.cpp): an addition
+    enum Cls { Z, R, I, C, O, M };
     auto cls = [&](int e) {
         const cplx v = u[e];
         if (v == cplx(0.0, 0.0)) return Z;
+        if (v == cplx(1.0, 0.0)) return O;
+        if (v == cplx(-1.0, 0.0)) return M;
         if (v.imag() == 0.0) return R;
         if (v.real() == 0.0) return I;
         return C;
     };
     int nnz = 0;
-    for (int e = 0; e < d * d; ++e) nnz += cls(e) != Z;
+    for (int e = 0; e < d * d; ++e) nnz += cls(e) != Z && cls(e) != O && cls(e) != M;
     const bool hoist = nnz <= 8;
     auto load = [&](int e) {
         std::ostringstream o;
@@ -275,7 +278,7 @@ std::string sparse_dense(const MOp& op, const cplx* u, int E, const std::string&
     s << "    {\n";
     if (hoist)
         for (int e = 0; e < d * d; ++e) {
-            if (cls(e) == Z) continue;
+            if (cls(e) == Z || cls(e) == O || cls(e) == M) continue;
             s << "      const " << (cls(e) == C ? "double2" : "double") << " u" << e << " = " << load(e) << ";\n";
         }
     unsigned smask = 0;
@@ -294,10 +297,26 @@ std::string sparse_dense(const MOp& op, const cplx* u, int E, const std::string&
         for (int r = 0; r < d; ++r) {
             const std::string dst = "a[" + std::to_string(idx(r)) + "]";
             bool first = true;
-            for (int c = 0; c < d; ++c) {
+            // +-1 terms first: they seed the accumulator (a copy / negation the
+            // next fma takes as its addend), later ones are additions
+            std::vector<int> order;
+            for (int c = 0; c < d; ++c)
+                if (cls(r * d + c) == O || cls(r * d + c) == M) order.push_back(c);
+            for (int c = 0; c < d; ++c)
+                if (!(cls(r * d + c) == O || cls(r * d + c) == M)) order.push_back(c);
+            for (int c : order) {
                 const int e = r * d + c;
                 const Cls k = cls(e);
                 if (k == Z) continue;
+                if (k == O || k == M) {
+                    const std::string xn = "x" + std::to_string(c);
+                    const char* sg = k == O ? "" : "-";
+                    if (first) s << "        " << dst << " = make_double2(" << sg << xn << ".x, " << sg << xn << ".y);\n";
+                    else s << "        " << dst << ".x " << (k == O ? "+" : "-") << "= " << xn << ".x; " << dst << ".y "
+                           << (k == O ? "+" : "-") << "= " << xn << ".y;\n";
+                    first = false;
+                    continue;
+                }
                 const std::string un = hoist ? "u" + std::to_string(e) : "(" + load(e) + ")";
                 const std::string xn = "x" + std::to_string(c);
                 s << "        ";
@@ -375,6 +394,24 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
     const bool extra_relayout = relabel && lays.size() == 1;
     if (extra_relayout) mirror = false;  // (full tiles then; the mirror store path expects the last layout)
     Layout LS = by_store(lays.back());
+    if (extra_relayout) {
+        // the extra relayout is free to pick the store layout's register bits:
+        // the tile bits with the highest store positions, so the lanes of a
+        // warp span the lowest ones (fully coalesced 512-byte stores) even when
+        // the program's only layout holds low store bits in registers
+        std::vector<int> bits(static_cast<size_t>(m));
+        for (int b = 0; b < m; ++b) bits[size_t(b)] = b;
+        std::stable_sort(bits.begin(), bits.end(), [&](int x, int y) { return qst[size_t(x)] > qst[size_t(y)]; });
+        unsigned rm = 0;
+        for (int j = 0; j < LS.r; ++j) rm |= 1u << bits[size_t(j)];
+        int j = 0;
+        for (int b = 0; b < m; ++b)
+            if ((rm >> b) & 1u) LS.rp[j++] = b;
+        LS.nonr.clear();
+        for (int b = 0; b < m; ++b)
+            if (!((rm >> b) & 1u)) LS.nonr.push_back(b);
+        LS = by_store(LS);
+    }
     std::vector<Layout> sw_lays = lays;
     if (extra_relayout) sw_lays.push_back(LS);
     const Swizzle sw = choose_swizzle(sw_lays, m);
@@ -453,7 +490,19 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
           << "    asm volatile(\"\" : \"+r\"(tidv));\n";
         def_layout(0);
         s << "    { const double2* src = st + base + (" << state_off("tb0", L0.nonr, q) << ");\n";
-        for (int l = 0; l < E; ++l) s << "      a[" << l << "] = ld_stream(src + " << hex64(reg_off(L0, l, q)) << ");\n";
+        // a register slot on physical bit 0: its amplitude pairs are adjacent,
+        // one 256-bit load each (full 32-byte sectors per lane)
+        int j0 = -1;
+        for (int j = 0; j < L0.r; ++j)
+            if (q[size_t(L0.rp[j])] == 0) j0 = j;
+        for (int l = 0; l < E; ++l) {
+            if (j0 < 0) {
+                s << "      a[" << l << "] = ld_stream(src + " << hex64(reg_off(L0, l, q)) << ");\n";
+            } else if (!((l >> j0) & 1)) {
+                s << "      ld_stream2(src + " << hex64(reg_off(L0, l, q)) << ", a[" << l << "], a[" << (l | (1 << j0))
+                  << "]);\n";
+            }
+        }
         s << "    }\n";
     }
     // pending-permutation state (see px_enabled): dirty = register slots
@@ -598,18 +647,19 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
                 for (int j = 0; j < op.k; ++j) sl |= 1u << op.pos[j];
                 flush_ph(sl);
             }
-            bool real = true;
+            bool real = true, special = false;
             size_t generic = 0;  // entries that are neither zero, real nor pure imaginary
             const size_t nent = size_t(1) << (2 * op.k);
             for (size_t i = 0; i < nent; ++i) {
                 const cplx v = pool[op.mat + i];
                 real = real && v.imag() == 0.0;
                 generic += v.real() != 0.0 && v.imag() != 0.0;
+                special = special || v == cplx(0.0, 0.0) || v == cplx(1.0, 0.0) || v == cplx(-1.0, 0.0);
             }
             const char* R = real ? ", true" : "";
             unsigned slots = 0;
             for (int j = 0; j < op.k; ++j) slots |= 1u << op.pos[j];
-            const bool sparse = op.k <= 2 && !real && generic < nent;
+            const bool sparse = op.k <= 2 && (special || (!real && generic < nent));
             if (use_px && (dirty & slots)) {
                 if (op.k == 1 && !sparse) {
                     s << "    d1f<" << E << ", " << int(op.pos[0]) << R << ">(a, " << P << ", " << px_bit(op.pos[0])
@@ -880,9 +930,19 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
               << "; st_stream(((o ^ xval) & xmask) ? xout_r + (o ^ xmask) : xout_l + o, a[" << l << "]); }\n";
         s << "    }\n";
     } else {
+        // register slot stored to physical bit 0 (and not pending in px):
+        // adjacent pairs, one 256-bit store each
+        int j0 = -1;
+        for (int j = 0; j < LST.r; ++j)
+            if (qst[size_t(LST.rp[j])] == 0 && !(use_px && ((dirty >> j) & 1u))) j0 = j;
         s << "    { double2* dst = st + base + toff_st;\n";
-        for (int l = 0; l < E; ++l)
-            s << "      st_stream(dst + (" << hex64(reg_off(LST, l, qst)) << pxo << "), a[" << l << "]);\n";
+        for (int l = 0; l < E; ++l) {
+            if (j0 < 0)
+                s << "      st_stream(dst + (" << hex64(reg_off(LST, l, qst)) << pxo << "), a[" << l << "]);\n";
+            else if (!((l >> j0) & 1))
+                s << "      st_stream2(dst + (" << hex64(reg_off(LST, l, qst)) << pxo << "), a[" << l << "], a["
+                  << (l | (1 << j0)) << "]);\n";
+        }
         s << "    }\n";
     }
     if (mirror) {

@@ -9,6 +9,10 @@
 // registers; operator matrices are read from shared memory at the point of use.
 #pragma once
 
+#ifdef NQ_EMU
+#include "jit_emu.hpp"
+#endif
+
 namespace nq {
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -21,6 +25,7 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ bool is_one(double2 f) { return f.x == 1.0 && f.y == 0.0; }
 
+#ifndef NQ_EMU
 __device__ __forceinline__ double2 ld_stream(const double2* p) {
     double2 v;
     asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
@@ -28,6 +33,17 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
 }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) {
     asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+// 256-bit streaming pair access (LDG/STG.E.ENL2.256, sm_100): two amplitudes
+// adjacent in memory (a register slot on physical bit 0) in one 32-byte sector
+__device__ __forceinline__ void ld_stream2(const double2* p, double2& a, double2& b) {
+    asm volatile("ld.global.cs.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+                 : "l"(p));
+}
+__device__ __forceinline__ void st_stream2(double2* p, double2 a, double2 b) {
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+                 : "memory");
 }
 // Shared-memory load the compiler may not hoist: matrices are re-read (one
 // broadcast LDS per entry) instead of occupying registers.
@@ -51,6 +67,21 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+#else
+// Host emulation of the memory primitives (tests/jit_emu.py runs generated
+// pass kernels on CPU threads against the oracle; NQ_EMU builds only).
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return *p; }
+__device__ __forceinline__ void st_stream(double2* p, double2 v) { *p = v; }
+__device__ __forceinline__ void ld_stream2(const double2* p, double2& a, double2& b) {
+    a = p[0];
+    b = p[1];
+}
+__device__ __forceinline__ void st_stream2(double2* p, double2 a, double2 b) {
+    p[0] = a;
+    p[1] = b;
+}
+__device__ __forceinline__ double2 lds(const double2* p) { return *p; }
+#endif
 
 // a <- diag factor f, skipping exact ones (d0 = 1 diagonals touch half the amplitudes)
 __device__ __forceinline__ double2 dmul(double2 a, double2 f) { return is_one(f) ? a : cmul(f, a); }

@@ -595,6 +595,11 @@ class PassBuilder {
             break;
         }
         if (idx < 0) return false;
+        // pending (not yet emitted) work on the controls sits between the two
+        // P as well: it commutes with P only when diagonal (a dense group on
+        // a control, e.g. CX(c,t) U3(c) CX(c,t), blocks the cancellation)
+        for (const auto& g : pend_)
+            if ((g.mask() & ctrl) && !g.diag) return false;
         // pending groups involving t must be diagonal; conjugate and merge them
         std::vector<size_t> on_t;
         uint64_t uni = 0;
@@ -776,6 +781,15 @@ bool mat_is_real(const std::vector<cplx>& pool, uint32_t off, size_t n) {
     return true;
 }
 
+// NQ_NORM_DENSE=0 keeps 1-qubit dense matrices as fused (A/B).
+bool normalise_dense_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("NQ_NORM_DENSE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void hoist_global_phase(std::vector<PlannedPass>& passes) {
     PlannedPass* cp = nullptr;
     const MOp* carrier = nullptr;
@@ -803,6 +817,31 @@ void hoist_global_phase(std::vector<PlannedPass>& passes) {
             for (size_t i = 1; i < (size_t(1) << op.k); ++i) p.pool[op.mat + i] *= inv;
             p.pool[op.mat] = cplx(1.0, 0.0);
             phase *= f;
+        }
+    }
+    // Pivot normalisation of 1-qubit dense operators (state-vector passes:
+    // a Hermitian mirror pass needs every intermediate state Hermitian, so
+    // density-matrix flushes with mirror passes keep their matrices).  Row 0
+    // is divided by its larger entry p, so that entry is an exact 1, and the
+    // other row by the same p; p joins the hoisted scalar.  The pass compiler
+    // turns the exact 1 into an addition: out0 = x0 + a x1 costs 2 FP64 per
+    // component instead of 4 (complex: 12 instead of 16 per amplitude pair;
+    // RX / RY / H-like matrices, whose diagonal also becomes exactly +-1:
+    // 4 instead of 8).  |p| >= 1/sqrt(2) for unitaries, so the scalar product
+    // stays far from underflow.
+    bool mirror_flush = false;
+    for (const auto& p : passes) mirror_flush = mirror_flush || (p.flags & PASS_MIRROR);
+    if (!mirror_flush && normalise_dense_enabled()) {
+        for (auto& p : passes) {
+            for (const auto& op : p.ops) {
+                if (op.type != MOP_DENSE || op.k != 1 || op.cmask_tile || op.cmask_glob || &op == carrier) continue;
+                cplx* u = &p.pool[op.mat];
+                const cplx piv = std::abs(u[0]) >= std::abs(u[1]) ? u[0] : u[1];
+                const double ap = std::abs(piv);
+                if (!(ap > 0.25 && ap < 4.0) || piv == cplx(1.0, 0.0)) continue;
+                for (int e = 0; e < 4; ++e) u[e] = (u[e] == piv) ? cplx(1.0, 0.0) : u[e] / piv;
+                phase *= piv;
+            }
         }
     }
     if (phase == cplx(1.0, 0.0)) return;
@@ -1233,20 +1272,40 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
                     newpos[size_t(x)] = pos;
                     used[size_t(pos)] = 1;
                 };
-                // 1) chosen qubits: home if home is a low bit, then stay if already low
-                for (int x : q)
-                    if (((chosen >> x) & 1) && x < lb) place(x, x);
-                for (int x : q)
-                    if (((chosen >> x) & 1) && newpos[size_t(x)] < 0 && l2p[size_t(x)] < lb &&
-                        !used[size_t(l2p[size_t(x)])])
-                        place(x, l2p[size_t(x)]);
-                for (int x : q) {
-                    if (!((chosen >> x) & 1) || newpos[size_t(x)] >= 0) continue;
-                    for (int pbit = 0; pbit < lb; ++pbit)
-                        if (!used[size_t(pbit)]) {
-                            place(x, pbit);
-                            break;
-                        }
+                // 1) chosen qubits.  Those held in registers by the pass's last
+                //    layout take the highest low bits, so the warp's lanes (its
+                //    thread bits, ordered by store position) span the lowest
+                //    physical bits and the stores stay fully coalesced; within
+                //    each group: home if home is free, then stay, then any.
+                //    (A pass with a single layout stores through an extra
+                //    relayout whose register bits the pass compiler picks.)
+                uint64_t regq = 0;
+                int nlay = 0;
+                for (const auto& o : p.ops) nlay += o.type == MOP_LAYOUT;
+                for (auto it = p.ops.rbegin(); it != p.ops.rend() && nlay > 1; ++it)
+                    if (it->type == MOP_LAYOUT) {
+                        for (int j = 0; j < it->k; ++j) regq |= bit(q[size_t(it->pos[j])]);
+                        break;
+                    }
+                int nthr = 0;
+                for (int x : q) nthr += ((chosen >> x) & 1) && !((regq >> x) & 1);
+                for (int grp = 0; grp < 2; ++grp) {
+                    const int lo = grp == 0 ? 0 : nthr, hi = grp == 0 ? nthr : lb;
+                    auto member = [&](int x) { return ((chosen >> x) & 1) && (((regq >> x) & 1) != 0) == (grp == 1); };
+                    for (int x : q)
+                        if (member(x) && x >= lo && x < hi && !used[size_t(x)]) place(x, x);
+                    for (int x : q)
+                        if (member(x) && newpos[size_t(x)] < 0 && l2p[size_t(x)] >= lo && l2p[size_t(x)] < hi &&
+                            !used[size_t(l2p[size_t(x)])])
+                            place(x, l2p[size_t(x)]);
+                    for (int x : q) {
+                        if (!member(x) || newpos[size_t(x)] >= 0) continue;
+                        for (int pbit = lo; pbit < hi; ++pbit)
+                            if (!used[size_t(pbit)]) {
+                                place(x, pbit);
+                                break;
+                            }
+                    }
                 }
                 // 2) the others: home when it is a free high bit of this tile, else any free high bit
                 auto in_tile = [&](int pos) { return std::find(phys_set.begin(), phys_set.end(), pos) != phys_set.end(); };

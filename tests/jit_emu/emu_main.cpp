@@ -1,0 +1,36 @@
+// Runner for generated pass kernels on the host (see jit_emu.hpp).  The
+// generated sources are concatenated after this file with their entry points
+// renamed nqjit_<i>; emu_run(i, ...) launches pass i as one CTA of T threads
+// whose grid-stride loop covers every tile.
+#include "pass_ops.cuh"
+
+#include <thread>
+#include <vector>
+
+thread_local EmuDim threadIdx;
+thread_local EmuDim blockIdx;
+EmuDim gridDim{1, 1, 1};
+EmuDim blockDim{1, 1, 1};
+std::barrier<>* emu_barrier = nullptr;
+alignas(16) unsigned char smem[1 << 20];
+
+typedef void (*emu_kernel)(double2*, const double2*, unsigned long long, long long, double2*, double2*,
+                           unsigned long long, unsigned long long, int);
+extern emu_kernel emu_table[];
+
+extern "C" int emu_run(int pass, double* state, const double* pool, long long ntiles, int threads) {
+    std::barrier<> bar(threads);
+    emu_barrier = &bar;
+    blockDim.x = unsigned(threads);
+    std::vector<std::thread> ts;
+    for (int t = 0; t < threads; ++t)
+        ts.emplace_back([=] {
+            threadIdx = EmuDim{unsigned(t), 0, 0};
+            blockIdx = EmuDim{0, 0, 0};
+            emu_table[pass](reinterpret_cast<double2*>(state), reinterpret_cast<const double2*>(pool), 0ull, ntiles,
+                            nullptr, nullptr, 0ull, 0ull, 0);
+        });
+    for (auto& t : ts) t.join();
+    emu_barrier = nullptr;
+    return 0;
+}

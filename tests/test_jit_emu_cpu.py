@@ -1,0 +1,68 @@
+"""The pass-kernel generator (csrc/jit.cpp) checked on the host: the
+generated sources of every planned pass are compiled with g++ against
+pass_ops.cuh (NQ_EMU) and executed on CPU threads (tests/jit_emu.py), then
+compared with the oracle.  Covers what the GPU tests cover for the code
+generator -- register layouts and relayouts, relabelled stores, 256-bit pair
+accesses, pending register permutations (px on and off), phase accumulators,
+pivot-normalised matrices -- without a GPU, so generator changes are caught
+by the CPU suite."""
+import os
+import subprocess
+import sys
+import textwrap
+
+import numpy as np
+import pytest
+
+import jit_emu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _perm_circuit(prng, n):
+    kinds = [("cx", 2, 0), ("cx", 2, 0), ("ccx", 3, 0), ("swap", 2, 0), ("x", 1, 0), ("y", 1, 0), ("ry", 1, 1),
+             ("u3", 1, 3), ("h", 1, 0), ("t", 1, 0), ("rz", 1, 1), ("cz", 2, 0), ("s", 1, 0)]
+    circ = []
+    for _ in range(300):
+        k, ar, npar = kinds[int(prng.integers(len(kinds)))]
+        qs = [int(q) for q in prng.choice(n, size=ar, replace=False)]
+        circ.append((k, qs, [float(v) for v in prng.uniform(-3, 3, size=npar)]))
+    for _ in range(2):
+        circ += [("cx", [i, i + 1], []) for i in range(n - 1)] + [("ry", [q], [0.1 * q + 0.3]) for q in range(n)]
+    return circ
+
+
+@pytest.mark.parametrize("n,tile,seed", [(12, 8, 1), (13, 9, 5), (14, 11, 7)])
+def test_generated_kernels_random_circuits(port, n, tile, seed):
+    ops = port.random_circuit(seed, n, 250)
+    got = jit_emu.run(n, ops, tile)
+    assert np.max(np.abs(got - port.sv_run(n, ops))) <= 1e-12
+
+
+@pytest.mark.parametrize("n,tile,seed", [(12, 8, 11), (13, 10, 12)])
+def test_generated_kernels_permutation_heavy(port, n, tile, seed):
+    circ = _perm_circuit(np.random.default_rng(seed), n)
+    got = jit_emu.run(n, circ, tile)
+    assert np.max(np.abs(got - port.sv_run(n, circ))) <= 1e-12
+
+
+def test_generated_kernels_without_pending_permutations():
+    # NQ_JIT_PX is read once per process by the generator: run in a child
+    code = textwrap.dedent(f"""
+        import sys
+        sys.path[:0] = [{ROOT!r}, {os.path.join(ROOT, 'oracle')!r}, {os.path.join(ROOT, 'tests')!r}]
+        import numpy as np
+        from oracle import Port
+        import jit_emu
+        from test_jit_emu_cpu import _perm_circuit
+        port = Port()
+        worst = 0.0
+        for n, tile, seed in [(12, 8, 11), (13, 9, 3)]:
+            circ = _perm_circuit(np.random.default_rng(seed), n)
+            worst = max(worst, float(np.max(np.abs(jit_emu.run(n, circ, tile) - port.sv_run(n, circ)))))
+        print("WORST", worst)
+        assert worst <= 1e-12, worst
+    """)
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, NQ_JIT_PX="0"), capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-2000:])

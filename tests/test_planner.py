@@ -170,3 +170,47 @@ def test_plan_rejects_bad_ops():
         abi.plan_debug(4, [("cx", [0, 4])])
     with pytest.raises(abi.ContractError):
         abi.plan_debug(4, [("measure", [0])])
+
+
+def test_cancelled_permutation_pairs_respect_dense_work_on_controls(port):
+    """P U P with U dense on a control of P does not cancel (regression: the
+    sandwich check once only looked at pending work on the target;
+    CX(c,t) U3(c) CX(c,t) was folded into U3(c))."""
+    n = 5
+    circ = [("h", [2], []), ("cx", [0, 2], []), ("u3", [0], [-0.6, -2.75, 1.79]), ("cx", [0, 2], []),
+            ("ccx", [0, 1, 3], []), ("ry", [1], [0.7]), ("ccx", [0, 1, 3], [])]
+    a0 = np.zeros(1 << n, dtype=complex)
+    a0[0] = 1
+    for tile in (3, 4, 5):
+        passes = plan_format.decode(abi.plan_debug(n, circ, tile_qubits=tile))
+        np.testing.assert_allclose(run_plan(n, passes, a0), port.sv_run(n, circ), atol=1e-12, rtol=0)
+
+
+@pytest.mark.parametrize("block", range(4))
+def test_plan_fuzz_against_oracle(port, block):
+    """Seeded random plans (uniform gate mix and permutation-heavy mixes,
+    random qubit counts and tile sizes, with and without relabelling) emulated
+    against the oracle."""
+    from oracle import ops_to_list
+
+    kinds = [("cx", 2, 0), ("cx", 2, 0), ("ccx", 3, 0), ("swap", 2, 0), ("x", 1, 0), ("y", 1, 0), ("ry", 1, 1),
+             ("u3", 1, 3), ("h", 1, 0), ("t", 1, 0), ("rz", 1, 1), ("cz", 2, 0), ("s", 1, 0)]
+    for seed in range(block * 25, block * 25 + 25):
+        rng = np.random.default_rng(1000 + seed)
+        n = int(rng.integers(5, 10))
+        tile = int(rng.integers(3, min(n, 8) + 1))
+        if seed % 2:
+            circ = []
+            for _ in range(150):
+                k, ar, npar = kinds[int(rng.integers(len(kinds)))]
+                qs = [int(q) for q in rng.choice(n, size=ar, replace=False)]
+                circ.append((k, qs, [float(v) for v in rng.uniform(-3, 3, size=npar)]))
+        else:
+            circ = [tuple(x) for x in ops_to_list(port.random_circuit(seed, n, 150))]
+        a0 = np.zeros(1 << n, dtype=complex)
+        a0[0] = 1
+        want = port.sv_run(n, circ)
+        for relabel in (False, True):
+            passes = plan_format.decode(abi.plan_debug(n, circ, tile_qubits=tile, relabel=relabel))
+            err = np.max(np.abs(run_plan(n, passes, a0) - want))
+            assert err <= 1e-10, (seed, n, tile, relabel, err)
