@@ -442,15 +442,12 @@ def _dl_delete(ptr):
 # py_object would take a new reference to an object at refcount 0 (resurrect
 # it) and crash when that reference is dropped
 _PyCapsule_Destructor = C.CFUNCTYPE(None, C.c_void_p)
-_capsule_new = C.pythonapi.PyCapsule_New
-_capsule_new.restype = C.py_object
-_capsule_new.argtypes = [C.c_void_p, C.c_char_p, _PyCapsule_Destructor]
-_capsule_is_valid = C.pythonapi.PyCapsule_IsValid
-_capsule_is_valid.restype = C.c_int
-_capsule_is_valid.argtypes = [C.c_void_p, C.c_char_p]
-_capsule_get_ptr = C.pythonapi.PyCapsule_GetPointer
-_capsule_get_ptr.restype = C.c_void_p
-_capsule_get_ptr.argtypes = [C.c_void_p, C.c_char_p]
+# private prototypes: C.pythonapi caches one function object per symbol and
+# other libraries (torch among them) re-declare argtypes on the shared ones
+_capsule_new = C.PYFUNCTYPE(C.py_object, C.c_void_p, C.c_char_p, _PyCapsule_Destructor)(
+    ("PyCapsule_New", C.pythonapi))
+_capsule_is_valid = C.PYFUNCTYPE(C.c_int, C.c_void_p, C.c_char_p)(("PyCapsule_IsValid", C.pythonapi))
+_capsule_get_ptr = C.PYFUNCTYPE(C.c_void_p, C.c_void_p, C.c_char_p)(("PyCapsule_GetPointer", C.pythonapi))
 
 
 @_PyCapsule_Destructor

@@ -624,6 +624,10 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
             const char* bar1 = "__syncthreads()";
             const char* bar2 = "__syncthreads()";
             s << "    " << bar1 << ";\n";
+            // (the pending permutation is XOR-ed into the store addresses: a
+            // quarter-warp may then hit colliding bank groups -- random-30
+            // pass 2: 71 M conflicts -- but committing it to the registers
+            // instead measured no faster: that pass is FP64-bound)
             if (use_px && dirty) {
                 s << "    {\n";
                 px_smem_xor(A);
@@ -642,6 +646,42 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
             break;
         }
         case MOP_DENSE: {
+            if (op.k == 1 && accumulate_phases() && ph_pending[op.pos[0]] &&
+                !(use_px && ((dirty >> op.pos[0]) & 1u))) {
+                // N with two exact 1s (planner.cpp: pivot-normalised unitary)
+                // after a pending phase p on its slot: N diag(1, p) is folded
+                // at run time instead of multiplying p into 8 amplitudes:
+                //   [[1, a], [b, 1]] diag(1, p) = diag(1, p) [[1, a p], [b p*, 1]]
+                //   [[a, 1], [1, b]] diag(1, p) = p diag(1, p*) [[a p*, 1], [1, b p]]
+                const cplx* u = pool + op.mat;
+                const bool nd = u[0] == cplx(1.0, 0.0) && u[3] == cplx(1.0, 0.0);
+                const bool no = u[1] == cplx(1.0, 0.0) && u[2] == cplx(1.0, 0.0);
+                if (nd || no) {
+                    const int t = op.pos[0];
+                    const std::string ph = ph_name(t);
+                    s << "    {\n";
+                    if (nd) {
+                        s << "      const double2 na = cmul(lds(" << P << " + 1), " << ph << ");\n"
+                          << "      const double2 nb = cmul(lds(" << P << " + 2), cconj(" << ph << "));\n";
+                    } else {
+                        s << "      const double2 na = cmul(lds(" << P << "), cconj(" << ph << "));\n"
+                          << "      const double2 nb = cmul(lds(" << P << " + 3), " << ph << ");\n";
+                        ug_mul(ph);
+                        s << "      " << ph << " = cconj(" << ph << ");\n";
+                    }
+                    for (int l = 0; l < E; ++l) {
+                        if ((l >> t) & 1) continue;
+                        const int hi = l | (1 << t);
+                        s << "      { const double2 x0 = a[" << l << "]; const double2 x1 = a[" << hi << "];\n";
+                        if (nd)
+                            s << "        a[" << l << "] = cfma(na, x1, x0); a[" << hi << "] = cfma(nb, x0, x1); }\n";
+                        else
+                            s << "        a[" << l << "] = cfma(na, x0, x1); a[" << hi << "] = cfma(nb, x1, x0); }\n";
+                    }
+                    s << "    }\n";
+                    break;
+                }
+            }
             {
                 unsigned sl = 0;
                 for (int j = 0; j < op.k; ++j) sl |= 1u << op.pos[j];

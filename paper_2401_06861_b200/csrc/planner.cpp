@@ -781,14 +781,16 @@ bool mat_is_real(const std::vector<cplx>& pool, uint32_t off, size_t n) {
     return true;
 }
 
-// NQ_NORM_DENSE=0 keeps 1-qubit dense matrices as fused (A/B).
-bool normalise_dense_enabled() {
-    static const bool on = [] {
+// NQ_NORM_DENSE=0 keeps 1-qubit dense matrices as fused, 1 normalises rows
+// only, 2 (default) also splits off the unit phase (A/B).
+int normalise_dense_mode() {
+    static const int v = [] {
         const char* e = std::getenv("NQ_NORM_DENSE");
-        return !(e && e[0] == '0');
+        return e ? std::atoi(e) : 2;
     }();
-    return on;
+    return v;
 }
+bool normalise_dense_enabled() { return normalise_dense_mode() > 0; }
 
 void hoist_global_phase(std::vector<PlannedPass>& passes) {
     PlannedPass* cp = nullptr;
@@ -829,21 +831,62 @@ void hoist_global_phase(std::vector<PlannedPass>& passes) {
     // RX / RY / H-like matrices, whose diagonal also becomes exactly +-1:
     // 4 instead of 8).  |p| >= 1/sqrt(2) for unitaries, so the scalar product
     // stays far from underflow.
+    //
+    // Unitaries whose normalised second row is not already +-1 on its
+    // diagonal are further split as U = p * diag(1, d) * N with N having two
+    // exact 1s ([[1, a], [b, 1]], or [[a, 1], [1, b]] when row 0's larger
+    // entry is off the diagonal) and |d| = 1: N costs 8 FP64 per amplitude
+    // pair, and the phase d follows as a 1-bit diagonal micro-op, which the
+    // pass compiler accumulates per thread and folds into the next N on the
+    // same register slot at run time (jit.cpp) instead of multiplying it in.
     bool mirror_flush = false;
     for (const auto& p : passes) mirror_flush = mirror_flush || (p.flags & PASS_MIRROR);
+    const size_t cpi = size_t(cp - passes.data());
+    const size_t coi0 = size_t(carrier - cp->ops.data());  // the carrier's index before insertions
+    size_t coi = coi0;
     if (!mirror_flush && normalise_dense_enabled()) {
-        for (auto& p : passes) {
-            for (const auto& op : p.ops) {
-                if (op.type != MOP_DENSE || op.k != 1 || op.cmask_tile || op.cmask_glob || &op == carrier) continue;
-                cplx* u = &p.pool[op.mat];
-                const cplx piv = std::abs(u[0]) >= std::abs(u[1]) ? u[0] : u[1];
+        for (size_t pi = 0; pi < passes.size(); ++pi) {
+            PlannedPass& p = passes[pi];
+            std::vector<MOp> out;
+            out.reserve(p.ops.size() + 8);
+            const MOp* lay = nullptr;
+            for (size_t oi = 0; oi < p.ops.size(); ++oi) {
+                const MOp op = p.ops[oi];
+                if (pi == cpi && oi == coi0) coi = out.size();
+                out.push_back(op);
+                if (op.type == MOP_LAYOUT) lay = &p.ops[oi];
+                if (op.type != MOP_DENSE || op.k != 1 || op.cmask_tile || op.cmask_glob || (pi == cpi && oi == coi0))
+                    continue;
+                cplx u[4] = {p.pool[op.mat], p.pool[op.mat + 1], p.pool[op.mat + 2], p.pool[op.mat + 3]};
+                const bool diag_form = std::abs(u[0]) >= std::abs(u[1]);
+                const cplx piv = diag_form ? u[0] : u[1];
                 const double ap = std::abs(piv);
-                if (!(ap > 0.25 && ap < 4.0) || piv == cplx(1.0, 0.0)) continue;
+                if (!(ap > 0.25 && ap < 4.0)) continue;
                 for (int e = 0; e < 4; ++e) u[e] = (u[e] == piv) ? cplx(1.0, 0.0) : u[e] / piv;
                 phase *= piv;
+                // row 1's entry under row 0's pivot: d (diag form: u11, off form: u10)
+                const int de = diag_form ? 3 : 2;
+                const cplx d = u[de];
+                const bool unit = std::abs(std::abs(d) - 1.0) < 1e-13;
+                if (normalise_dense_mode() >= 2 && unit && lay && d != cplx(1.0, 0.0) && d != cplx(-1.0, 0.0)) {
+                    u[2 + (de == 3 ? 0 : 1)] /= d;
+                    u[de] = cplx(1.0, 0.0);
+                    MOp dg{};
+                    dg.type = MOP_DIAG;
+                    dg.k = 1;
+                    dg.pos[0] = lay->pos[op.pos[0]];  // the dense op's register slot as a tile bit
+                    dg.mat = uint32_t(p.pool.size());
+                    p.pool.push_back(cplx(1.0, 0.0));
+                    p.pool.push_back(d);
+                    out.push_back(dg);
+                }
+                for (int e = 0; e < 4; ++e) p.pool[op.mat + e] = u[e];
             }
+            p.ops = std::move(out);
         }
     }
+    carrier = &passes[cpi].ops[coi];
+    cp = &passes[cpi];
     if (phase == cplx(1.0, 0.0)) return;
     const size_t n = size_t(1) << (2 * carrier->k);
     for (size_t i = 0; i < n; ++i) cp->pool[carrier->mat + i] *= phase;

@@ -66,3 +66,16 @@ def test_generated_kernels_without_pending_permutations():
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, NQ_JIT_PX="0"), capture_output=True,
                        text=True, timeout=900)
     assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-2000:])
+
+
+@pytest.mark.parametrize("n,tile", [(12, 8), (14, 10)])
+def test_generated_kernels_qft_and_vqe_shapes(port, n, tile):
+    """The two secondary benchmark shapes (bench.py): QFT (pure-phase
+    controlled tables, per-thread phase accumulation, pivot-normalised
+    rotations folding a pending phase) and the VQE ansatz (RY/RZ layers and
+    CX ladders, relayout-heavy)."""
+    from paper_2401_06861_b200 import workloads
+
+    for circ in (workloads.qft(n), workloads.vqe_ansatz(n, 3, workloads.vqe_initial_params(n, 3))):
+        got = jit_emu.run(n, circ, tile)
+        assert np.max(np.abs(got - port.sv_run(n, circ))) <= 1e-12
