@@ -10,6 +10,8 @@
 #include "engine.hpp"
 #include "jit.hpp"
 #include "kernels.hpp"
+#include "knobs.hpp"
+#include "nvtx.hpp"
 #include "lower.hpp"
 #include "state.hpp"
 
@@ -99,10 +101,7 @@ void DeviceCtx::stage(const unsigned char* src, size_t bytes) {
 // Hermitian (mirror) passes for density matrices, in the interleaved layout
 // (NQ_DM_MIRROR=0 disables).  Noisy TFIM-14: 134.8 -> 82.0 ms.
 bool dm_mirror_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("NQ_DM_MIRROR");
-        return !(e && e[0] == '0');
-    }();
+    static const bool on = ab_knob("NQ_DM_MIRROR", 1) != 0;
     return on;
 }
 
@@ -110,19 +109,13 @@ bool dm_mirror_enabled() {
 // the low pairs).  Off by default: noisy TFIM-14 planned 52 instead of 55
 // passes but ran slower (88.5 vs 81.9 ms).
 bool dm_relabel_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("NQ_DM_RELABEL");
-        return e && e[0] == '1';
-    }();
+    static const bool on = ab_knob("NQ_DM_RELABEL", 0) == 1;
     return on;
 }
 
 void set_initial_layout(State& s) {
     for (int b = 0; b < s.nbits; ++b) s.layout[size_t(b)] = b;
-    static const bool interleave = [] {
-        const char* e = std::getenv("NQ_DM_INTERLEAVE");
-        return e && e[0] == '1';
-    }();
+    static const bool interleave = ab_knob("NQ_DM_INTERLEAVE", 0) == 1;
     s.popt.dm_mirror_n = 0;
     if (s.dm) s.popt.relabel = s.popt.relabel && dm_mirror_enabled() && dm_relabel_enabled();
     if (!s.dm || !(interleave || dm_mirror_enabled()) || s.nloc <= s.popt.tile_bits) return;
@@ -158,25 +151,15 @@ void state_init(State& s, int n, bool dm, const nq_opts* opts) {
     s.popt.tile_bits = o.tile_qubits > 0 ? std::min(o.tile_qubits, kMaxTileBits) : 11;
     s.popt.low_bits = 4;
     // relabelling stores for state vectors (NQ_RELABEL=0 disables)
-    {
-        const char* e = std::getenv("NQ_RELABEL");
-        s.popt.relabel = !(e && e[0] == '0');  // density matrices: only with the Hermitian layout (below)
-    }
+    s.popt.relabel = ab_knob("NQ_RELABEL", 1) != 0;  // density matrices: only with the Hermitian layout (below)
     s.popt.stage_sched = !dm;
     s.layout.resize(size_t(s.nbits));
     set_initial_layout(s);
-    // A/B knobs (read per state): NQ_LOW_BITS for state vectors, NQ_TILE_DM /
-    // NQ_LOW_BITS_DM for density matrices
-    if (!dm) {
-        if (const char* e = std::getenv("NQ_LOW_BITS")) s.popt.low_bits = std::max(0, std::min(std::atoi(e), 7));
-        if (const char* e = std::getenv("NQ_TILE_SV"); e && o.tile_qubits <= 0)
-            s.popt.tile_bits = std::max(4, std::min(std::atoi(e), kMaxTileBits));
-    }
-    if (dm) {
-        if (const char* e = std::getenv("NQ_TILE_DM"); e && o.tile_qubits <= 0)
-            s.popt.tile_bits = std::max(4, std::min(std::atoi(e), kMaxTileBits));
-        if (const char* e = std::getenv("NQ_LOW_BITS_DM")) s.popt.low_bits = std::max(0, std::min(std::atoi(e), 4));
-    }
+    // tile size options (read per state), A/B low-bit counts
+    if (const int t = env_option(dm ? "NQ_TILE_DM" : "NQ_TILE_SV", 0); t > 0 && o.tile_qubits <= 0)
+        s.popt.tile_bits = std::max(4, std::min(t, kMaxTileBits));
+    s.popt.low_bits = dm ? std::max(0, std::min(ab_knob("NQ_LOW_BITS_DM", 4), 4))
+                         : std::max(0, std::min(ab_knob("NQ_LOW_BITS", 4), 7));
     s.popt.fuse = o.fuse != 0;
     configure_caps(s.popt);
     DeviceCtx& c = ctx_for(dev);
@@ -195,10 +178,7 @@ void configure_caps(PlanOptions& p) {
         p.max_ops_per_pass = 192;
         p.max_pool_per_pass = 1536;
     }
-    static const int cap = [] {
-        const char* e = std::getenv("NQ_MAX_OPS");
-        return e ? std::atoi(e) : 0;
-    }();
+    static const int cap = ab_knob("NQ_MAX_OPS", 0);
     if (cap > 0) p.max_ops_per_pass = cap;  // A/B measurements
 }
 
@@ -404,8 +384,10 @@ void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStat
     }
     if (buf.empty()) return;
     if (plan_trace()) trace_passes(passes, s.dm);
+    NvtxRange flush_range("nq.passes", int64_t(passes.size()));
     c.stage(buf.data(), buf.size());
     for (size_t i = 0; i < passes.size(); ++i) {
+        NvtxRange pass_range("nq.pass", int64_t(i));
         PassHdr h;
         std::memcpy(&h, buf.data() + offs[i], sizeof(h));
         std::pair<cudaEvent_t, cudaEvent_t>* ev = c.prof_pass ? prof_slot(c) : nullptr;

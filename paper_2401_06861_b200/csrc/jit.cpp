@@ -27,6 +27,7 @@
 #include "jit.hpp"
 
 #include "kernels.hpp"
+#include "knobs.hpp"
 #include "state.hpp"
 
 #include <cuda_runtime.h>
@@ -92,11 +93,6 @@ JitMode mode_from_env() {
     if (s == "off" || s == "0") return JitMode::Off;
     if (s == "sync") return JitMode::Sync;
     return JitMode::Auto;
-}
-
-int env_int(const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e ? std::atoi(e) : dflt;
 }
 
 std::string hex64(unsigned long long v) {
@@ -225,19 +221,19 @@ std::string swz_expr(const std::string& x, const Swizzle& sw) {
 // sparse k <= 2 operators, depolarizing maps) first apply the pending bits
 // they touch.
 bool px_enabled() {
-    static const bool on = env_int("NQ_JIT_PX", 1) != 0;
+    static const bool on = env_option("NQ_JIT_PX", 1) != 0;
     return on;
 }
 
 // Per-thread phase accumulators for unit-modulus diagonal tables (see the
 // generator).  NQ_JIT_PHASEACC=0 disables them (A/B).
 bool accumulate_phases() {
-    static const bool on = env_int("NQ_JIT_PHASEACC", 1) != 0;
+    static const bool on = ab_knob("NQ_JIT_PHASEACC", 1) != 0;
     return on;
 }
 
 bool diag_runtime_skip() {
-    static const bool on = env_int("NQ_DIAG_SKIP", 0) != 0;
+    static const bool on = ab_knob("NQ_DIAG_SKIP", 0) != 0;
     return on;
 }
 

@@ -23,6 +23,7 @@
 //  Micro-ops are kept in state-bit form and mapped to tile positions when the
 //  pass is closed, so the pass caps apply to the fused (post-fusion) program.
 #include "engine.hpp"
+#include "knobs.hpp"
 
 #include <algorithm>
 #include <functional>
@@ -656,38 +657,26 @@ class PassBuilder {
 // cost more (8.08 ms/pass) than the partially coalesced accesses (7.43 ms/pass),
 // whose DRAM traffic stays exactly algorithmic (L2 merges the sectors).
 bool coalesce_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("NQ_COALESCE");
-        return e && e[0] == '1';
-    }();
+    static const bool on = ab_knob("NQ_COALESCE", 0) == 1;
     return on;
 }
 
 // Tile bits that must not be register bits of the load / store layouts
 // (NQ_COALESCE_MASK, default tile bits 0-4).
 uint32_t coalesce_mask() {
-    static const uint32_t v = [] {
-        const char* e = std::getenv("NQ_COALESCE_MASK");
-        return e ? uint32_t(std::strtoul(e, nullptr, 0)) : 0x1Fu;
-    }();
+    static const uint32_t v = uint32_t(ab_knob("NQ_COALESCE_MASK", 0x1F));
     return v;
 }
 
 // NQ_STAGE_SCHED=0 keeps each pass program in source order (A/B).
 bool stage_sched_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("NQ_STAGE_SCHED");
-        return !(e && e[0] == '0');
-    }();
+    static const bool on = ab_knob("NQ_STAGE_SCHED", 1) != 0;
     return on;
 }
 
 // NQ_REGBITS=3|4 overrides PlanOptions::reg_bits (A/B measurements).
 int reg_bits_env(int dflt) {
-    static const int v = [] {
-        const char* e = std::getenv("NQ_REGBITS");
-        return e ? std::atoi(e) : 0;
-    }();
+    static const int v = ab_knob("NQ_REGBITS", 0);
     return (v == 3 || v == 4) ? v : dflt;
 }
 
@@ -784,10 +773,7 @@ bool mat_is_real(const std::vector<cplx>& pool, uint32_t off, size_t n) {
 // NQ_NORM_DENSE=0 keeps 1-qubit dense matrices as fused, 1 normalises rows
 // only, 2 (default) also splits off the unit phase (A/B).
 int normalise_dense_mode() {
-    static const int v = [] {
-        const char* e = std::getenv("NQ_NORM_DENSE");
-        return e ? std::atoi(e) : 2;
-    }();
+    static const int v = ab_knob("NQ_NORM_DENSE", 2);
     return v;
 }
 bool normalise_dense_enabled() { return normalise_dense_mode() > 0; }
@@ -1046,10 +1032,7 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
     };
     // Off by default: on the BASELINE workloads (random-30, QFT-30, TFIM-28,
     // VQE-28) it found no plan with fewer passes than the plain greedy.
-    static const bool seeds_env = [] {
-        const char* e = std::getenv("NQ_PLAN_SEEDS");
-        return e && e[0] == '1';
-    }();
+    static const bool seeds_env = ab_knob("NQ_PLAN_SEEDS", 0) == 1;
     const bool multi_seed = seeds_env && opt.fuse && nloc > m;
     // first position at which each logical bit is a non-diagonal target in `list`
     auto next_use = [&](const std::vector<const EOp*>& list) {

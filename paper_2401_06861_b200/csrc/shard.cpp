@@ -20,6 +20,8 @@
 // through nq_shard_debug().
 #include "jit.hpp"
 #include "kernels.hpp"
+#include "knobs.hpp"
+#include "nvtx.hpp"
 #include "lower.hpp"
 #include "state.hpp"
 
@@ -59,6 +61,7 @@ struct NcclApi {
     decltype(&::ncclAllReduce) AllReduce = nullptr;
     decltype(&::ncclBroadcast) Broadcast = nullptr;
     decltype(&::ncclGetErrorString) GetErrorString = nullptr;
+    decltype(&::ncclCommGetAsyncError) CommGetAsyncError = nullptr;
 };
 
 NcclApi& nccl() {
@@ -88,6 +91,7 @@ NcclApi& nccl() {
         NQ_SYM(AllReduce, "ncclAllReduce");
         NQ_SYM(Broadcast, "ncclBroadcast");
         NQ_SYM(GetErrorString, "ncclGetErrorString");
+        NQ_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
 #undef NQ_SYM
     });
     if (!api.CommInitRank) throw NqError{NQ_ERR_NCCL, "NCCL unavailable: " + err};
@@ -113,6 +117,17 @@ NcclApi& nccl() {
         if (nccl_try_r_ != ncclSuccess)                                                                \
             throw NqError{NQ_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(nccl_try_r_)}; \
     } while (0)
+
+// Errors NCCL reports asynchronously (a peer failed, a network/NVLink fault)
+// surface here instead of as a later hang: checked after every exchange and
+// sharded flush.
+void check_async(ncclComm_t comm) {
+    ncclResult_t st = ncclSuccess;
+    if (!comm || !nccl().CommGetAsyncError) return;
+    NCCL_TRY(nccl().CommGetAsyncError(comm, &st));
+    if (st != ncclSuccess && st != ncclInProgress)
+        throw NqError{NQ_ERR_NCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(st)};
+}
 
 struct ShardComm {
     ncclComm_t comm = nullptr;
@@ -245,10 +260,7 @@ int choose_victim(const std::vector<EOp>& ops, size_t from, const std::vector<in
 // carried qubit map cycle through many layouts (uncompiled pass structures):
 // N = 4 with 33 local qubits 661 -> 1012, but with 30 local 9050 -> 4779.
 bool shard_cyclic_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("NQ_SHARD_CYCLIC");
-        return e && e[0] == '1';
-    }();
+    static const bool on = ab_knob("NQ_SHARD_CYCLIC", 0) == 1;
     return on;
 }
 
@@ -410,6 +422,7 @@ void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vecto
     PhaseTimer pl("launches", s.rank);
     const uint64_t rankbase = uint64_t(s.rank) << s.nloc;
     for (size_t i = 0; i < passes.size(); ++i) {
+        NvtxRange pass_range("nq.pass", int64_t(i));
         PassHdr h;
         std::memcpy(&h, buf.data() + offs[i], sizeof(h));
         std::pair<cudaEvent_t, cudaEvent_t>* ev = c.prof_pass ? prof_slot(c) : nullptr;
@@ -446,6 +459,7 @@ void stream_barrier(ShardComm& sc, DeviceCtx& c) {
 
 void run_exchange(State& s, DeviceCtx& c, int g, int v) {
     ShardComm& sc = *s.comm;
+    NvtxRange range("nq.exchange", g);
     if (s.rank == 0 && std::getenv("NQ_SHARD_TRACE")) std::fprintf(stderr, "[shard] exchange g=%d v=%d\n", g, v);
     const int j = g - s.nloc;
     const int partner = s.rank ^ (1 << j);
@@ -462,6 +476,7 @@ void run_exchange(State& s, DeviceCtx& c, int g, int v) {
         CUDA_TRY(cudaGetLastError());
         sc.bytes += int64_t(half) * 16;
         ++sc.exchanges;
+        check_async(sc.comm);
         return;
     }
     for (uint64_t k0 = 0; k0 < half; k0 += sc.chunk) {
@@ -476,6 +491,7 @@ void run_exchange(State& s, DeviceCtx& c, int g, int v) {
     }
     CUDA_TRY(cudaGetLastError());
     ++sc.exchanges;
+    check_async(sc.comm);
 }
 
 // After a pass fused with the exchange (g, v): every rank wrote its output
@@ -485,6 +501,7 @@ void run_exchange(State& s, DeviceCtx& c, int g, int v) {
 // no barrier is needed before such a pass).
 void fused_exchange_done(State& s, DeviceCtx& c, int g, int v) {
     ShardComm& sc = *s.comm;
+    NvtxRange range("nq.exchange.fused", g);
     if (s.rank == 0 && std::getenv("NQ_SHARD_TRACE"))
         std::fprintf(stderr, "[shard] exchange g=%d v=%d (fused into the pass)\n", g, v);
     std::swap(s.d, sc.alt);
@@ -494,6 +511,7 @@ void fused_exchange_done(State& s, DeviceCtx& c, int g, int v) {
     sc.bytes += int64_t(s.count / 2) * 16;
     ++sc.exchanges;
     ++sc.fused;
+    check_async(sc.comm);
 }
 
 // Relabelling passes permute local physical bits inside a segment; the later
@@ -502,10 +520,7 @@ void fused_exchange_done(State& s, DeviceCtx& c, int g, int v) {
 // NQ_SHARD_RELABEL_RESTORE=0: keep a segment's final relabelling (composed
 // into the qubit map) instead of restoring it inside the segment.
 bool shard_relabel_restore() {
-    static const bool on = [] {
-        const char* e = std::getenv("NQ_SHARD_RELABEL_RESTORE");
-        return !(e && e[0] == '0');
-    }();
+    static const bool on = ab_knob("NQ_SHARD_RELABEL_RESTORE", 1) != 0;
     return on;
 }
 
@@ -532,10 +547,7 @@ EOp remap(const EOp& e, const std::vector<int>& perm) {
 // (N = 4) 10 -> 9 passes per step, 33 qubits (N = 8) 11 -> 9.
 // NQ_SHARD_REBALANCE=0 disables it.
 bool shard_rebalance_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("NQ_SHARD_REBALANCE");
-        return !(e && e[0] == '0');
-    }();
+    static const bool on = ab_knob("NQ_SHARD_REBALANCE", 1) != 0;
     return on;
 }
 
@@ -798,14 +810,27 @@ std::vector<double2*> map_peers(State& s, double2* mine_ptr, bool want) {
     return peer;
 }
 
+// Every rank plans its own flushes, so the options that shape plans and
+// exchanges (knobs.hpp) must be identical on all ranks, or their collectives
+// diverge: compare a hash of them at creation.
+void check_env_agreement(State& s) {
+    const std::string fp = plan_env_fingerprint();
+    uint64_t h = 1469598103934665603ull;  // FNV-1a
+    for (unsigned char ch : fp) h = (h ^ ch) * 1099511628211ull;
+    const auto all = allgather_doubles(s, {double(h >> 32), double(h & 0xffffffffu)});
+    for (int r = 0; r < s.world; ++r)
+        if (all[size_t(2 * r)] != all[0] || all[size_t(2 * r + 1)] != all[1])
+            throw NqError{NQ_ERR_CONTRACT, "sharded state: rank " + std::to_string(r) + " and rank 0 run with "
+                                               "different NQ_* options (this rank: '" + fp + "'); every rank "
+                                               "must see the same environment"};
+}
+
 bool fused_exchange_wanted() {
-    const char* e = std::getenv("NQ_FUSED_EXCHANGE");
-    return !(e && e[0] == '0');
+    return env_option("NQ_FUSED_EXCHANGE", 1) != 0;
 }
 
 void setup_peer_exchange(State& s, ShardComm& sc, DeviceCtx& c) {
-    const char* mode = std::getenv("NQ_EXCHANGE");
-    const bool want = !(mode && std::string(mode) == "nccl");
+    const bool want = env_option_str("NQ_EXCHANGE") != "nccl";
     sc.peer = map_peers(s, s.d, want);
     if (sc.peer.empty()) return;
     // a second copy of the shard for fused exchanges, when it fits with room
@@ -870,6 +895,7 @@ void shard_reset(State& s) {
 
 void shard_flush(State& s) {
     PhaseTimer pt("flush", s.rank);
+    NvtxRange range("nq.shard_flush", s.rank);
     ShardComm& sc = *s.comm;
     std::vector<EOp> ops;
     ops.swap(s.queue);
@@ -888,10 +914,7 @@ void shard_flush(State& s) {
     // flush needs few or no exchanges and runs the same physical program
     // every time (its specialised kernels are reused).  NQ_SHARD_RESTORE=1
     // restores the identity map at the end of every flush instead.
-    static const bool restore = [] {
-        const char* e = std::getenv("NQ_SHARD_RESTORE");
-        return e && e[0] == '1';
-    }();
+    static const bool restore = ab_knob("NQ_SHARD_RESTORE", 0) == 1;
     if (restore) {
         std::vector<Action> back = schedule_identity(sc.l2p, sc.p2l, s.nloc, s.n);
         acts.insert(acts.end(), back.begin(), back.end());
@@ -900,15 +923,13 @@ void shard_flush(State& s) {
     // Measured at N = 4 (random circuit, 2^30 per GPU): 9 instead of 10 passes
     // per step, but the composed qubit map keeps drifting for several flushes,
     // so repeated circuits keep meeting uncompiled pass structures.
-    static const bool relabel = [] {
-        const char* e = std::getenv("NQ_SHARD_RELABEL");
-        return e && e[0] == '1';
-    }();
+    static const bool relabel = ab_knob("NQ_SHARD_RELABEL", 0) == 1;
     if (shard_rebalance_enabled() && !(relabel && !restore)) {
         PhaseTimer pr("rebalance", s.rank);
         rebalance(acts, s.popt, s.n, &sc.rebalance_cache);
     }
     execute(s, acts, relabel && !restore);
+    check_async(sc.comm);
 }
 
 double shard_norm_sq(State& s) {
@@ -1200,6 +1221,7 @@ nq_status nq_sv_create_sharded(int n, int rank, int world, const unsigned char u
         CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&sc->d_flag), sizeof(double)));
         CUDA_TRY(cudaMemset(sc->d_flag, 0, sizeof(double)));
         s.comm = sc.release();
+        check_env_agreement(s);
         setup_peer_exchange(s, *s.comm, c);
         CUDA_TRY(cudaStreamSynchronize(c.stream));
         *out = h.release();

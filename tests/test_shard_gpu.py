@@ -16,8 +16,9 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _rank_main(rank, world, uid, n, seed, outdir, fused=True):
+def _rank_main(rank, world, uid, n, seed, outdir, fused=True, exchange="p2p"):
     os.environ["NQ_FUSED_EXCHANGE"] = "1" if fused else "0"
+    os.environ["NQ_EXCHANGE"] = exchange
     sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
     from oracle import Port
     from paper_2401_06861_b200 import abi as A
@@ -52,17 +53,21 @@ def _rank_main(rank, world, uid, n, seed, outdir, fused=True):
              coeff=np.array([t[1] for t in terms]))
 
 
-@pytest.mark.parametrize("n,world,fused", [(14, 2, True), (20, 2, True), (20, 2, False), (22, 4, True),
-                                           (22, 4, False)])
-def test_sharded_gpus(port, tmp_path, n, world, fused):
+@pytest.mark.parametrize("n,world,fused,exchange", [(14, 2, True, "p2p"), (20, 2, True, "p2p"),
+                                                    (20, 2, False, "p2p"), (20, 2, False, "nccl"),
+                                                    (22, 4, True, "p2p"), (22, 4, False, "p2p"),
+                                                    (22, 4, False, "nccl")])
+def test_sharded_gpus(port, tmp_path, n, world, fused, exchange):
     """Sharded run == oracle (amplitudes, norm, expectations, sampling), with
     exchanges fused into the preceding pass (out-of-place exchange stores into
-    the partner's second buffer) or as standalone peer-memory swaps."""
+    the partner's second buffer), as standalone peer-memory swaps, or through
+    the NCCL send/recv fallback (NQ_EXCHANGE=nccl: pack, send/recv through
+    bounce buffers, unpack -- the path taken when CUDA IPC is unavailable)."""
     if abi.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     seed = 808 + n
     uid = abi.comm_unique_id()
-    mp.start_processes(_rank_main, args=(world, uid, n, seed, str(tmp_path), fused), nprocs=world,
+    mp.start_processes(_rank_main, args=(world, uid, n, seed, str(tmp_path), fused, exchange), nprocs=world,
                        start_method="spawn")
     ops = port.random_circuit(seed, n, 300)
     want = port.sv_run(n, ops)
@@ -83,3 +88,32 @@ def test_sharded_gpus(port, tmp_path, n, world, fused):
         dense = np.zeros(1 << n, dtype=np.uint64)
         dense[d["idx"].astype(np.int64)] = d["cnt"]
         assert np.array_equal(dense, port.sample_distribution(np.abs(want) ** 2, 4000, 99))
+
+
+def _env_rank(rank, world, uid, outdir):
+    # rank 1 plans with a different tile size: the ranks' flushes would diverge
+    if rank == 1:
+        os.environ["NQ_TILE_SV"] = "10"
+    sys.path[:0] = [ROOT]
+    from paper_2401_06861_b200 import abi as A
+
+    try:
+        A.SV.sharded(16, rank, world, uid, device=rank)
+        msg = "created"
+    except A.ContractError as e:
+        msg = str(e)
+    with open(os.path.join(outdir, f"env{rank}.txt"), "w") as f:
+        f.write(msg)
+
+
+def test_ranks_must_share_the_environment(tmp_path):
+    """Every rank plans its own flushes, so creation fails on every rank (a
+    contract error, not a later collective hang) when the plan-shaping NQ_*
+    options differ between ranks."""
+    if abi.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    uid = abi.comm_unique_id()
+    mp.start_processes(_env_rank, args=(2, uid, str(tmp_path)), nprocs=2, start_method="spawn")
+    for r in range(2):
+        msg = (tmp_path / f"env{r}.txt").read_text()
+        assert "different NQ_* options" in msg, msg
