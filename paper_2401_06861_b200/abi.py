@@ -664,11 +664,15 @@ def jit_stats() -> dict:
     return dict(zip(("compiled", "failed", "misses", "launches"), (x.value for x in v)))
 
 
-def jit_debug(n: int, ops, pass_index: int, tile_qubits: int = 0, compile: bool = True, xstore: bool = False):
+def jit_debug(n: int, ops, pass_index: int, tile_qubits: int = 0, compile: bool = True, xstore: bool = False,
+              segment: bool = False):
+    """Generated source of one planned pass (and whether NVRTC compiles it):
+    as a single-device state plans it, or as a sharded segment (`segment`:
+    no relabelling stores); `xstore`: the exchange-store form."""
     arr = ops if isinstance(ops, np.ndarray) else make_ops(ops)
     size = C.c_int64()
     ok = C.c_int()
-    xs = 2 if xstore else 0
+    xs = (2 if xstore else 0) | (4 if segment else 0)
     check(lib.nq_jit_debug(n, arr.ctypes.data, len(arr), tile_qubits, pass_index, xs, None, 0, C.byref(size),
                            C.byref(ok)))
     buf = C.create_string_buffer(size.value + (1 << 16))

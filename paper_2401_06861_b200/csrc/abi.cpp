@@ -1369,12 +1369,14 @@ nq_status nq_jit_debug(int n, const nq_op* ops, int64_t count, int tile_qubits, 
         PlanOptions p;
         p.nbits = n;
         p.nloc = n;
-        p.tile_bits = tile_qubits > 0 ? std::min(tile_qubits, kMaxTileBits) : 12;
-        p.relabel = true;  // as single-device state vectors plan
+        p.tile_bits = tile_qubits > 0 ? std::min(tile_qubits, kMaxTileBits) : 11;  // the state default (state_init)
+        // as single-device state vectors plan; compile & 4: as a sharded
+        // segment plans (no relabelling, no carried layout)
+        p.relabel = (compile & 4) == 0;
         configure_caps(p);
         std::vector<int> layout(static_cast<size_t>(n));
         for (int b = 0; b < n; ++b) layout[size_t(b)] = b;
-        auto passes = plan_passes(q, p, nullptr, &layout);
+        auto passes = plan_passes(q, p, nullptr, (compile & 4) ? nullptr : &layout);
         if (pass_index < 0 || pass_index >= int(passes.size())) throw NqError{NQ_ERR_CONTRACT, "no such pass"};
         std::vector<size_t> offs;
         auto bytes = serialize_passes(passes, n, &offs);
@@ -1406,7 +1408,7 @@ nq_status nq_plan_debug(int n, const nq_op* ops, int64_t count, int tile_qubits,
         PlanOptions p;
         p.nbits = n;
         p.nloc = n;
-        p.tile_bits = tile_qubits > 0 ? std::min(tile_qubits, kMaxTileBits) : 12;
+        p.tile_bits = tile_qubits > 0 ? std::min(tile_qubits, kMaxTileBits) : 11;  // the state default (state_init)
         p.fuse = (fuse & 1) != 0;
         p.relabel = (fuse & 2) != 0;  // bit 1: relabelling stores (single-device state vectors)
         configure_caps(p);

@@ -41,6 +41,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <dlfcn.h>
 #include <execinfo.h>
 #include <csignal>
 #include <unistd.h>
@@ -60,6 +61,67 @@ namespace {
 const char* kPassOpsSrc =
 #include "pass_ops_src.inc"
     ;
+
+// NVRTC is bound at first use from the toolkit this library was built with
+// (NQ_NVRTC_PATH, the Makefile's CUDA_HOME), not through the soname: a process
+// that imported torch first already has torch's own, older libnvrtc.so.12
+// loaded, and that one rejects the pass kernels' 256-bit global accesses for
+// sm_100a.  Loaded RTLD_LOCAL, so the two copies do not interfere.  If only an
+// NVRTC older than 12.9 can be found, the kernels fall back to 128-bit pairs.
+struct NvrtcApi {
+    decltype(&::nvrtcCreateProgram) CreateProgram = nullptr;
+    decltype(&::nvrtcCompileProgram) CompileProgram = nullptr;
+    decltype(&::nvrtcDestroyProgram) DestroyProgram = nullptr;
+    decltype(&::nvrtcGetCUBIN) GetCUBIN = nullptr;
+    decltype(&::nvrtcGetCUBINSize) GetCUBINSize = nullptr;
+    decltype(&::nvrtcGetProgramLog) GetProgramLog = nullptr;
+    decltype(&::nvrtcGetProgramLogSize) GetProgramLogSize = nullptr;
+    decltype(&::nvrtcVersion) Version = nullptr;
+    bool wide = true;  // 256-bit global accesses supported
+    std::string where;
+};
+
+#ifndef NQ_NVRTC_PATH
+#define NQ_NVRTC_PATH "/usr/local/cuda/lib64/libnvrtc.so.12"
+#endif
+
+NvrtcApi& nvrtc() {
+    static NvrtcApi api = [] {
+        NvrtcApi a;
+        void* h = dlopen(NQ_NVRTC_PATH, RTLD_NOW | RTLD_LOCAL);
+        a.where = NQ_NVRTC_PATH;
+        if (!h) {
+            h = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+            a.where = "libnvrtc.so.12";
+        }
+        if (!h) throw NqError{NQ_ERR_CUDA, std::string("NVRTC unavailable: ") + (dlerror() ? dlerror() : "")};
+#define NQ_SYM(field, name) a.field = reinterpret_cast<decltype(a.field)>(dlsym(h, name))
+        NQ_SYM(CreateProgram, "nvrtcCreateProgram");
+        NQ_SYM(CompileProgram, "nvrtcCompileProgram");
+        NQ_SYM(DestroyProgram, "nvrtcDestroyProgram");
+        NQ_SYM(GetCUBIN, "nvrtcGetCUBIN");
+        NQ_SYM(GetCUBINSize, "nvrtcGetCUBINSize");
+        NQ_SYM(GetProgramLog, "nvrtcGetProgramLog");
+        NQ_SYM(GetProgramLogSize, "nvrtcGetProgramLogSize");
+        NQ_SYM(Version, "nvrtcVersion");
+#undef NQ_SYM
+        if (!a.CreateProgram || !a.CompileProgram || !a.GetCUBIN || !a.Version)
+            throw NqError{NQ_ERR_CUDA, "NVRTC at " + a.where + " lacks required entry points"};
+        int major = 0, minor = 0;
+        a.Version(&major, &minor);
+        a.wide = major > 12 || (major == 12 && minor >= 9);
+        return a;
+    }();
+    return api;
+}
+
+#define nvrtcCreateProgram nvrtc().CreateProgram
+#define nvrtcCompileProgram nvrtc().CompileProgram
+#define nvrtcDestroyProgram nvrtc().DestroyProgram
+#define nvrtcGetCUBIN nvrtc().GetCUBIN
+#define nvrtcGetCUBINSize nvrtc().GetCUBINSize
+#define nvrtcGetProgramLog nvrtc().GetProgramLog
+#define nvrtcGetProgramLogSize nvrtc().GetProgramLogSize
 
 struct Entry {
     std::atomic<int> state{0};  // 0 pending, 1 ready, 2 failed
@@ -1000,7 +1062,15 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
 
 namespace {
 
-const char* kNvrtcOpts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"};
+// options of every pass / expectation compile (4th: 128-bit pairs when the
+// bound NVRTC predates 256-bit global accesses on sm_100a)
+const char* const* nvrtc_opts(int* n) {
+    static const char* wide[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"};
+    static const char* narrow[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DNQ_NO_V4"};
+    const bool w = nvrtc().wide;
+    *n = w ? 3 : 4;
+    return w ? wide : narrow;
+}
 
 bool compile_entry(const std::string& src, Entry& e, int device) {
     if (const char* dir = std::getenv("NQ_JIT_DUMP")) {  // debugging: keep every generated source
@@ -1018,7 +1088,9 @@ bool compile_entry(const std::string& src, Entry& e, int device) {
         e.log = "nvrtcCreateProgram failed";
         return false;
     }
-    const nvrtcResult rc = nvrtcCompileProgram(prog, 3, kNvrtcOpts);
+    int nopt_ = 0;
+    const char* const* opts_ = nvrtc_opts(&nopt_);
+    const nvrtcResult rc = nvrtcCompileProgram(prog, nopt_, opts_);
     size_t logn = 0;
     nvrtcGetProgramLogSize(prog, &logn);
     if (logn > 1) {
@@ -1112,7 +1184,9 @@ void nvrtc_warm() {
     nvrtcProgram prog;
     const char* src = "extern \"C\" __global__ void nqwarm() {}";
     if (nvrtcCreateProgram(&prog, src, "warm.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return;
-    nvrtcCompileProgram(prog, 3, kNvrtcOpts);
+    int nopt_ = 0;
+    const char* const* opts_ = nvrtc_opts(&nopt_);
+    nvrtcCompileProgram(prog, nopt_, opts_);
     nvrtcDestroyProgram(&prog);
 }
 
@@ -1147,6 +1221,7 @@ std::shared_ptr<Entry> acquire(const std::string& src, int device, JitMode mode)
                 lk.lock();
                 if (ok) ++J.stats.compiled;
                 else ++J.stats.failed;
+                J.cv.notify_all();  // other threads waiting on this entry
             } else {
                 if (J.exiting) return nullptr;
                 J.device = device;
@@ -1167,6 +1242,11 @@ std::shared_ptr<Entry> acquire(const std::string& src, int device, JitMode mode)
         } else {
             e = it->second;
         }
+    }
+    if (mode == JitMode::Sync) {
+        // queued or compiling in the background: wait for the worker
+        std::unique_lock<std::mutex> lk(J.mu);
+        J.cv.wait(lk, [&] { return e->state.load() != 0 || J.exiting; });
     }
     if (e->state.load() != 1) {
         ++J.stats.misses;
@@ -1210,8 +1290,19 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
         // remembered for this pass record (owning reference)
     } else if (xs) {
         if (!jit_xstore_ok(h, ops)) throw NqError{NQ_ERR_INTERNAL, "exchange pass cannot be specialised"};
-        e = acquire(jit_source(h, ops, pool, true), device, JitMode::Sync);
-        if (!e) throw NqError{NQ_ERR_INTERNAL, "exchange pass kernel failed to compile"};
+        const std::string src = jit_source(h, ops, pool, true);
+        e = acquire(src, device, JitMode::Sync);
+        if (!e) {
+            std::string log;
+            {
+                Jit& J = jit();
+                std::lock_guard<std::mutex> lk(J.mu);
+                auto it = J.cache.find(src);
+                if (it != J.cache.end()) log = it->second->log;
+            }
+            if (log.size() > 1500) log = log.substr(log.size() - 1500);
+            throw NqError{NQ_ERR_INTERNAL, "exchange pass kernel failed to compile: " + log};
+        }
     } else {
         if (mode == JitMode::Off || h.m < 8 || h.m > 12) return false;
         if (mode == JitMode::Auto && h.nloc < 18) return false;  // interpreter is fine for small states
@@ -1507,7 +1598,9 @@ bool jit_compile_only(const std::string& src, std::string* log) {
     const char* hdrs[1] = {kPassOpsSrc};
     const char* names[1] = {"pass_ops.cuh"};
     if (nvrtcCreateProgram(&prog, src.c_str(), "nqjit.cu", 1, hdrs, names) != NVRTC_SUCCESS) return false;
-    const nvrtcResult rc = nvrtcCompileProgram(prog, 3, kNvrtcOpts);
+    int nopt_ = 0;
+    const char* const* opts_ = nvrtc_opts(&nopt_);
+    const nvrtcResult rc = nvrtcCompileProgram(prog, nopt_, opts_);
     size_t logn = 0;
     nvrtcGetProgramLogSize(prog, &logn);
     if (log && logn > 1) {

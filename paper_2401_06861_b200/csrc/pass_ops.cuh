@@ -36,14 +36,25 @@ __device__ __forceinline__ void st_stream(double2* p, double2 v) {
 }
 // 256-bit streaming pair access (LDG/STG.E.ENL2.256, sm_100): two amplitudes
 // adjacent in memory (a register slot on physical bit 0) in one 32-byte sector
+// (NQ_NO_V4: two 128-bit accesses, for an NVRTC older than 12.9)
 __device__ __forceinline__ void ld_stream2(const double2* p, double2& a, double2& b) {
+#ifdef NQ_NO_V4
+    a = ld_stream(p);
+    b = ld_stream(p + 1);
+#else
     asm volatile("ld.global.cs.v4.f64 {%0, %1, %2, %3}, [%4];"
                  : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
                  : "l"(p));
+#endif
 }
 __device__ __forceinline__ void st_stream2(double2* p, double2 a, double2 b) {
+#ifdef NQ_NO_V4
+    st_stream(p, a);
+    st_stream(p + 1, b);
+#else
     asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
                  : "memory");
+#endif
 }
 // Shared-memory load the compiler may not hoist: matrices are re-read (one
 // broadcast LDS per entry) instead of occupying registers.

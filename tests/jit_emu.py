@@ -24,18 +24,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CSRC = os.path.join(ROOT, "paper_2401_06861_b200", "csrc")
 EMU = os.path.join(ROOT, "tests", "jit_emu")
 _CACHE = os.path.join(tempfile.gettempdir(), "nq_jit_emu")
+# "address" / "thread": build the emulated kernels with that g++ sanitizer (the
+# process must preload its runtime; tests/test_jit_emu_cpu.py runs a child)
+SANITIZE = os.environ.get("NQ_EMU_SANITIZE", "")
 
 
-def sources(n: int, ops: np.ndarray, tile: int):
+def sources(n: int, ops: np.ndarray, tile: int, count: int):
     out = []
-    i = 0
-    while True:
-        try:
-            src, _ = abi.jit_debug(n, ops, i, tile_qubits=tile, compile=False)
-        except Exception:  # noqa: BLE001 - "no such pass" ends the list
-            break
+    for i in range(count):
+        src, _ = abi.jit_debug(n, ops, i, tile_qubits=tile, compile=False)
         out.append(src.split("/* NVRTC LOG")[0])
-        i += 1
     return out
 
 
@@ -44,21 +42,24 @@ def build(srcs) -> C.CDLL:
     body = [open(os.path.join(EMU, "emu_main.cpp")).read()]
     for i, s in enumerate(srcs):
         s = s.replace('#include "pass_ops.cuh"', "")
+        s = s.replace("extern __shared__ __align__(16) unsigned char smem[];", "unsigned char* const smem = emu_smem;")
         s = re.sub(r"\bnqjit\(", f"nqjit_{i}(", s, count=1)
         body.append(s)
     body.append("emu_kernel emu_table[] = {" + ", ".join(f"nqjit_{i}" for i in range(len(srcs))) + "};\n")
     code = "\n".join(body)
-    key = hashlib.sha1((code + open(os.path.join(CSRC, "pass_ops.cuh")).read()).encode()).hexdigest()[:16]
+    san = ["-fsanitize=" + SANITIZE, "-fno-omit-frame-pointer", "-g"] if SANITIZE else []
+    key = hashlib.sha1((code + open(os.path.join(CSRC, "pass_ops.cuh")).read() + " ".join(san)).encode()
+                       ).hexdigest()[:16]
     so = os.path.join(_CACHE, f"emu_{key}.so")
     if not os.path.exists(so):
         cpp = so[:-3] + ".cpp"
         with open(cpp, "w") as f:
             f.write(code)
         subprocess.run(["g++", "-std=c++20", "-O1", "-shared", "-fPIC", "-pthread", "-Wno-unknown-pragmas",
-                        "-DNQ_EMU", "-I", CSRC, "-I", EMU, "-o", so + ".tmp", cpp], check=True)
+                        "-DNQ_EMU", *san, "-I", CSRC, "-I", EMU, "-o", so + ".tmp", cpp], check=True)
         os.replace(so + ".tmp", so)
     lib = C.CDLL(so)
-    lib.emu_run.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int]
+    lib.emu_run.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int, C.c_longlong]
     return lib
 
 
@@ -68,7 +69,7 @@ def run(n: int, ops, tile: int, state: np.ndarray | None = None) -> np.ndarray:
     logical (reference) order."""
     arr = ops if isinstance(ops, np.ndarray) else abi.make_ops(ops)
     passes = plan_format.decode(abi.plan_debug(n, arr, tile_qubits=tile, relabel=True))
-    srcs = sources(n, arr, tile)
+    srcs = sources(n, arr, tile, len(passes))
     assert len(srcs) == len(passes), (len(srcs), len(passes))
     lib = build(srcs)
     st = np.zeros(1 << n, dtype=np.complex128) if state is None else np.array(state, dtype=np.complex128)
@@ -80,7 +81,8 @@ def run(n: int, ops, tile: int, state: np.ndarray | None = None) -> np.ndarray:
         threads = (1 << p.m) // e
         ntiles = 1 << (n - p.m)
         pool = np.ascontiguousarray(p.pool, dtype=np.complex128)
-        lib.emu_run(i, st.ctypes.data, pool.ctypes.data, ntiles, threads)
+        smem = (1 << p.m) * 16 + len(pool) * 16  # as jit_launch sizes it
+        lib.emu_run(i, st.ctypes.data, pool.ctypes.data, ntiles, threads, smem)
         qst = p.qst if p.qst else p.q
         move = dict(zip(p.q, qst))
         l2p = [move.get(x, x) for x in l2p]

@@ -4,6 +4,7 @@
 // whose grid-stride loop covers every tile.
 #include "pass_ops.cuh"
 
+#include <new>
 #include <thread>
 #include <vector>
 
@@ -12,13 +13,17 @@ thread_local EmuDim blockIdx;
 EmuDim gridDim{1, 1, 1};
 EmuDim blockDim{1, 1, 1};
 std::barrier<>* emu_barrier = nullptr;
-alignas(16) unsigned char smem[1 << 20];
+// the CTA's dynamic shared memory, allocated per launch at exactly the size
+// the launch would request (so an address sanitizer build sees overruns)
+unsigned char* emu_smem = nullptr;
 
 typedef void (*emu_kernel)(double2*, const double2*, unsigned long long, long long, double2*, double2*,
                            unsigned long long, unsigned long long, int);
 extern emu_kernel emu_table[];
 
-extern "C" int emu_run(int pass, double* state, const double* pool, long long ntiles, int threads) {
+extern "C" int emu_run(int pass, double* state, const double* pool, long long ntiles, int threads,
+                       long long smem_bytes) {
+    emu_smem = static_cast<unsigned char*>(::operator new[](size_t(smem_bytes), std::align_val_t(16)));
     std::barrier<> bar(threads);
     emu_barrier = &bar;
     blockDim.x = unsigned(threads);
@@ -32,5 +37,7 @@ extern "C" int emu_run(int pass, double* state, const double* pool, long long nt
         });
     for (auto& t : ts) t.join();
     emu_barrier = nullptr;
+    ::operator delete[](emu_smem, std::align_val_t(16));
+    emu_smem = nullptr;
     return 0;
 }

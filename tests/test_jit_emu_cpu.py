@@ -79,3 +79,43 @@ def test_generated_kernels_qft_and_vqe_shapes(port, n, tile):
     for circ in (workloads.qft(n), workloads.vqe_ansatz(n, 3, workloads.vqe_initial_params(n, 3))):
         got = jit_emu.run(n, circ, tile)
         assert np.max(np.abs(got - port.sv_run(n, circ))) <= 1e-12
+
+
+@pytest.mark.parametrize("sanitizer", ["address", "thread"])
+def test_generated_kernels_under_sanitizers(sanitizer):
+    """The memcheck / racecheck substitute (compute-sanitizer is not available
+    on the GPU pool): the generated pass kernels are emulated with g++'s
+    AddressSanitizer (shared memory allocated at exactly the launch's size, the
+    state and matrix pool as exact heap blocks: any out-of-bounds access
+    aborts) and ThreadSanitizer (the CTA's threads are real threads
+    synchronised by __syncthreads barriers: a missing barrier around a
+    relayout is a reported data race)."""
+    import shutil
+
+    rt = subprocess.run(["g++", f"-print-file-name=lib{'a' if sanitizer == 'address' else 't'}san.so"],
+                        capture_output=True, text=True).stdout.strip()
+    if not rt or not os.path.isabs(rt) or shutil.which("g++") is None:
+        pytest.skip("sanitizer runtime not available")
+    code = textwrap.dedent(f"""
+        import sys
+        sys.path[:0] = [{ROOT!r}, {os.path.join(ROOT, 'oracle')!r}, {os.path.join(ROOT, 'tests')!r}]
+        import numpy as np
+        from oracle import Port
+        import jit_emu
+        from test_jit_emu_cpu import _perm_circuit
+        from paper_2401_06861_b200 import workloads
+        port = Port()
+        worst = 0.0
+        cases = [(11, 8, port.random_circuit(3, 11, 120)), (11, 9, _perm_circuit(np.random.default_rng(4), 11)),
+                 (10, 8, workloads.qft(10))]
+        for n, tile, circ in cases:
+            worst = max(worst, float(np.max(np.abs(jit_emu.run(n, circ, tile) - port.sv_run(n, circ)))))
+        assert worst <= 1e-12, worst
+        print("EMU_OK", worst)
+    """)
+    env = dict(os.environ, NQ_EMU_SANITIZE=sanitizer, LD_PRELOAD=rt, PYTHONMALLOC="malloc",
+               ASAN_OPTIONS="detect_leaks=0:abort_on_error=1", TSAN_OPTIONS="halt_on_error=1:report_signal_unsafe=0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=1200)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "EMU_OK" in out, out[-6000:]
+    assert "ERROR: AddressSanitizer" not in out and "WARNING: ThreadSanitizer" not in out, out[-6000:]
