@@ -439,6 +439,22 @@ def headline_parity_and_baseline(abi, sv, n, ops_arr, ops_list, args):
     return parity, base
 
 
+def dm_pass_roofline(run):
+    """Per-launch HBM roofline of the density-matrix passes of one end-to-end
+    call (a separate, profiled repetition: CUDA events around every pass).
+    Algorithmic bytes per launch from the library: 32 * 4^n for a plain pass,
+    24 * 4^n for a Hermitian mirror pass (reads the canonical half only)."""
+    abi.profile_begin(0, per_pass_events=True)
+    run()
+    p = abi.profile_end(0)
+    peak, _ = measured_peaks()
+    launches = max(p["pass_launches"], 1)
+    ms = p["pass_ms"] / launches
+    achieved = p["pass_bytes"] / launches / (ms / 1e3) / 1e9
+    return {"bound": "hbm", "avg_launch_ms": ms, "launches": p["pass_launches"],
+            "bytes_per_launch": p["pass_bytes"] / launches, "achieved": achieved, "peak": peak,
+            "frac": achieved / peak, "unit": "GB/s", "pass_share_of_region": p["pass_ms"] / max(p["region_ms"], 1e-9)}
+
 def secondary_workloads(abi, workloads, device, args):
     """The other BASELINE.json configurations, each with its parity check."""
     import numpy as np
@@ -589,6 +605,7 @@ def secondary_workloads(abi, workloads, device, args):
     dt = time.perf_counter() - t0
     out["dm_noisy_tfim14"] = {
         "wall_s": dt, "z0": z, "gates": len(circ),
+        "roofline": dm_pass_roofline(lambda: naqs.density_expectation(circ, "Z" + "I" * (nd - 1), model)),
         "cpu": None if cpu_per_gate12 is None else {
             "extrapolated_wall_s": cpu_per_gate12 * 16 * len(circ),
             "sample": "EXTRAPOLATED: the measured n = 12 whole-circuit seconds per gate x 16 (4^n work) x the "
@@ -613,6 +630,8 @@ def secondary_workloads(abi, workloads, device, args):
     t0 = time.perf_counter()
     z16 = naqs.density_expectation(circ16, "Z" + "I" * (nd16 - 1), model16, max_qubits=16)
     out["dm_noisy_tfim16"] = {"wall_s": time.perf_counter() - t0, "z0": z16, "cpu": None,
+                              "roofline": dm_pass_roofline(lambda: naqs.density_expectation(
+                                  circ16, "Z" + "I" * (nd16 - 1), model16, max_qubits=16)),
                               "note": "beyond the reference's 14-qubit guard: no CPU baseline"}
     # f1: batched Monte-Carlo trajectories (one launch) vs the reference's
     # sequential loop (acceptance 5 shape, and a 10-qubit noisy TFIM)

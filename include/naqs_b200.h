@@ -273,7 +273,8 @@ typedef struct nq_profile {
     double region_ms;        /* device time between begin and end: CUDA events on the device stream */
     double pass_ms;          /* summed device time of the fused-pass kernel launches in the region  */
     int64_t pass_launches;
-    double pass_bytes;       /* algorithmic bytes of those launches: 32 * 2^nloc each (read+write)  */
+    double pass_bytes;       /* algorithmic bytes of those launches: 32 * 2^nloc each (read+write), */
+                             /* 24 * 2^nloc for Hermitian DM mirror passes (half the reads)         */
     int64_t kernel_launches; /* every kernel this library launched in the region                     */
     int64_t h2d_bytes;       /* bytes this library copied host->device in the region                 */
     int64_t d2h_bytes;       /* bytes copied device->host                                            */

@@ -399,7 +399,10 @@ void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStat
             launch_pass(s.d, c.d_ops + offs[i], h, 0, c.stream,
                         reinterpret_cast<const MOp*>(rec + h.op_off)[0].k);
         if (ev) CUDA_TRY(cudaEventRecord(ev->second, c.stream));
-        if (c.prof) c.prof_pass_bytes += 32.0 * double(s.count);
+        // algorithmic bytes: read + write every element; a Hermitian mirror
+        // pass reads only the canonical half (self-mirror tiles are a
+        // 2^-(rest bits / 2) fraction: ignored) and writes everything
+        if (c.prof) c.prof_pass_bytes += ((h.flags & PASS_MIRROR) ? 24.0 : 32.0) * double(s.count);
     }
     CUDA_TRY(cudaGetLastError());
 }
