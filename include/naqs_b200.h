@@ -256,9 +256,12 @@ nq_status nq_sv_create_sharded(int num_qubits, int rank, int world, const unsign
                                const nq_opts* opts, nq_sv** out);
 /* Number of global-qubit exchanges performed so far and bytes sent. */
 nq_status nq_sv_comm_stats(const nq_sv* s, int64_t* exchanges, int64_t* bytes_sent);
-/* Of those exchanges, how many were fused into the preceding pass (the pass
- * wrote its output out of place, the moved half straight into the partner's
- * second buffer over NVLink), and whether this rank holds that second buffer. */
+/* Of those exchanges, how many were fused into the preceding pass, and how:
+ * *has_alt_buffer = 1: the pass writes out of place, the moved half straight
+ * into the partner's second buffer over NVLink; 2: no second copy fits
+ * (e.g. 2^33 amplitudes per GPU): staged -- kept half in place, moved half
+ * chunk by chunk through a staging ring that a pusher kernel copies into the
+ * partner's state as both ranks finish each chunk; 0: standalone swaps. */
 nq_status nq_sv_comm_fused(const nq_sv* s, int64_t* fused, int* has_alt_buffer);
 /* Host-side schedule of a sharded flush (no device, no NCCL): the segments of
  * local work and the global<->local exchanges `ops` would produce on `world`

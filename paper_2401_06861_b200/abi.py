@@ -369,7 +369,8 @@ class SV:
         check(lib.nq_sv_comm_stats(self.h, C.byref(a), C.byref(b)))
         f, alt = C.c_int64(), C.c_int()
         check(lib.nq_sv_comm_fused(self.h, C.byref(f), C.byref(alt)))
-        return {"exchanges": a.value, "bytes_sent": b.value, "fused": f.value, "alt_buffer": bool(alt.value)}
+        return {"exchanges": a.value, "bytes_sent": b.value, "fused": f.value, "alt_buffer": alt.value == 1,
+                "staged": alt.value == 2}
 
 
 def comm_unique_id() -> bytes:
@@ -665,14 +666,15 @@ def jit_stats() -> dict:
 
 
 def jit_debug(n: int, ops, pass_index: int, tile_qubits: int = 0, compile: bool = True, xstore: bool = False,
-              segment: bool = False):
+              segment: bool = False, staged: str = ""):
     """Generated source of one planned pass (and whether NVRTC compiles it):
     as a single-device state plans it, or as a sharded segment (`segment`:
-    no relabelling stores); `xstore`: the exchange-store form."""
+    no relabelling stores); `xstore`: the exchange-store form; `staged`
+    ("rest" / "tile": where the exchanged bit lies): the staged form."""
     arr = ops if isinstance(ops, np.ndarray) else make_ops(ops)
     size = C.c_int64()
     ok = C.c_int()
-    xs = (2 if xstore else 0) | (4 if segment else 0)
+    xs = (2 if xstore else 0) | (4 if segment else 0) | {"": 0, "rest": 8, "tile": 24}[staged]
     check(lib.nq_jit_debug(n, arr.ctypes.data, len(arr), tile_qubits, pass_index, xs, None, 0, C.byref(size),
                            C.byref(ok)))
     buf = C.create_string_buffer(size.value + (1 << 16))

@@ -1386,8 +1386,23 @@ nq_status nq_jit_debug(int n, const nq_op* ops, int64_t count, int tile_qubits, 
         const unsigned char* rec = bytes.data() + offs[size_t(pass_index)];
         PassHdr h;
         std::memcpy(&h, rec, sizeof(h));
+        // compile & 8: the staged exchange-store form (16 chunks, exchanged
+        // bit v = the top rest bit, or with compile & 16 a tile bit)
+        JitXStore xs;
+        if (compile & 8) {
+            const int vpos = (compile & 16) ? h.q[std::min(2, h.m - 1)] : h.rest[h.nrest - 1];
+            xs.staged = true;
+            xs.xmask = uint64_t(1) << vpos;
+            xs.xrot = 0;
+            for (int j = 0; j < h.nrest; ++j)
+                if (h.rest[j] == vpos) xs.xrot = j;
+            xs.cshift = std::max(1, h.nrest - 4);
+            xs.chunk_bits = jit_stage_chunk_bits(h, xs.xrot, xs.cshift);
+            xs.pushers = 16;
+        }
         std::string src = jit_source(h, reinterpret_cast<const MOp*>(rec + h.op_off),
-                                     reinterpret_cast<const cplx*>(rec + h.pool_off), (compile & 2) != 0);
+                                     reinterpret_cast<const cplx*>(rec + h.pool_off), (compile & 10) != 0,
+                                     (compile & 8) ? &xs : nullptr);
         std::string log;
         if (compiled_ok) *compiled_ok = (compile & 1) ? int(jit_compile_only(src, &log)) : -1;
         if (!log.empty()) src += "\n/* NVRTC LOG\n" + log + "\n*/\n";

@@ -401,7 +401,23 @@ std::string sparse_dense(const MOp& op, const cplx* u, int E, const std::string&
     return s.str();
 }
 
-std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool xstore) {
+uint64_t jit_stage_chunk_bits(const PassHdr& h, int xrot, int cshift) {
+    // rotated counter rr: r bit 0 -> rest position xrot, r bit j >= 1 -> rest
+    // position j - 1 below xrot + 1, j above (see the exchange passes' rr)
+    uint64_t bits = 0;
+    for (int j = std::max(cshift, 1); j < h.nrest; ++j) bits |= uint64_t(1) << h.rest[j <= xrot ? j - 1 : j];
+    return bits;
+}
+
+std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool xstore, const JitXStore* stage) {
+    const bool staged = xstore && stage && stage->staged;
+    // staged exchange: compressed position of physical bit p in a staging
+    // slot (-1: a removed bit -- a chunk bit or the exchanged bit v)
+    const uint64_t holes = staged ? (stage->chunk_bits | stage->xmask) : 0;
+    auto cpos = [&](int p) {
+        if ((holes >> p) & 1) return -1;
+        return p - __builtin_popcountll(holes & ((uint64_t(1) << p) - 1));
+    };
     const int m = h.m;
     const int SIZE = 1 << m;
     const int E = 1 << ops[0].k;  // ops[0] is the load layout: 3 or 4 register bits
@@ -500,7 +516,8 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
     s << ")\n"
       << "nqjit(double2* __restrict__ st, const double2* __restrict__ gpool, unsigned long long rankbase,"
          " long long ntiles, double2* xout_l, double2* xout_r, unsigned long long xmask, unsigned long long xval,"
-         " int xrot) {\n"
+         " int xrot" << (staged ? ", unsigned* pdone, const unsigned* qdone, unsigned long long slot_elems" : "")
+      << ") {\n"
       << "  using namespace nq;\n"
       << "  extern __shared__ __align__(16) unsigned char smem[];\n"
       << "  double2* buf0 = reinterpret_cast<double2*>(smem);\n"
@@ -522,8 +539,25 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
     const Layout& LN = lays.back();
     {
         // direct streaming loads into the first register layout; one buffer
-        s << "  __syncthreads();\n"
-          << "  for (long long r = blockIdx.x; r < ntiles; r += gridDim.x) {\n";
+        s << "  __syncthreads();\n";
+        if (staged)
+            s << "  unsigned ck_cur = 0xffffffffu, ck_n = 0u;  // chunk of the tiles in flight, tiles stored in it\n";
+        s << "  for (long long r = blockIdx.x; r < ntiles; r += gridDim.x) {\n";
+        if (staged) {
+            // entering a new chunk: publish the tiles stored in the previous
+            // one (fenced), then wait until its staging slot is free again
+            s << "    { const unsigned ck = (unsigned)((unsigned long long)r >> " << stage->cshift << ");\n"
+              << "      if (ck != ck_cur) {\n"
+              << "        if (ck_n) { __threadfence(); __syncthreads(); if (tid == 0) atomicAdd(pdone + ck_cur, ck_n); }\n"
+              << "        ck_cur = ck; ck_n = 0u;\n"
+              << "        if (ck >= " << stage->slots << "u) {\n"
+              << "          if (tid == 0) while (ld_acquire_u32(qdone + ck - " << stage->slots << "u) < " << stage->pushers
+              << "u) {}\n"
+              << "          __syncthreads();\n"
+              << "        }\n"
+              << "      }\n"
+              << "    }\n";
+        }
         if (mirror) {
             // Hermitian pass: only canonical tiles (r <= mirror(r)) are read
             s << "    const long long rstar = (long long)(" << mirror_rest_expr("(unsigned long long)r") << ");\n"
@@ -1018,7 +1052,41 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
         s << "    const unsigned long long toff_st = " << state_off(tbl, LST.nonr, qst) << ";\n";
         if (mirror) s << "    const unsigned long long toff_mir = " << state_off(tbl, LN.nonr, qmir) << ";\n";
     }
-    if (xstore) {
+    if (staged) {
+        // staged exchange store: kept elements in place, outgoing ones into
+        // the staging slot at their compressed physical index
+        std::vector<int> qc(qst.size());
+        for (size_t i = 0; i < qst.size(); ++i) qc[i] = cpos(qst[i]);
+        std::ostringstream sb;
+        sb << "0ull";
+        for (size_t j = 0; j < rest.size(); ++j)
+            if (cpos(rest[j]) >= 0) sb << " | (((rr >> " << j << ") & 1ull) << " << cpos(rest[j]) << ")";
+        std::ostringstream tc;
+        tc << "0ull";
+        for (int b : LST.nonr)
+            if (qc[size_t(b)] >= 0) tc << " | ((unsigned long long)((" << (extra_relayout ? "tbS" : "tb" + std::to_string(lays.size() - 1))
+                                       << " >> " << b << ") & 1u) << " << qc[size_t(b)] << ")";
+        std::ostringstream pc;
+        pc << "0ull";
+        for (int b = 0; b < LST.r && use_px && dirty; ++b)
+            if (((dirty >> b) & 1u) && qc[size_t(LST.rp[b])] >= 0)
+                pc << " | ((unsigned long long)" << px_bit(b) << " << " << qc[size_t(LST.rp[b])] << ")";
+        auto creg = [&](int l) {
+            unsigned long long c = 0;
+            for (int j = 0; j < LST.r; ++j)
+                if (((l >> j) & 1) && qc[size_t(LST.rp[j])] >= 0) c |= 1ull << qc[size_t(LST.rp[j])];
+            return c;
+        };
+        s << "    { const unsigned long long ob = base + toff_st;\n"
+          << "      double2* const sg = xout_r + (unsigned long long)(ck_cur % " << stage->slots << "u) * slot_elems + ("
+          << sb.str() << ") + (" << tc.str() << ");\n";
+        if (use_px && dirty) s << "      const unsigned long long pxc = " << pc.str() << ";\n";
+        for (int l = 0; l < E; ++l)
+            s << "      { const unsigned long long o = ob + (" << hex64(reg_off(LST, l, qst)) << pxo << ")"
+              << "; st_stream(((o ^ xval) & xmask) ? sg + (" << hex64(creg(l)) << (use_px && dirty ? " ^ pxc" : "")
+              << ") : st + o, a[" << l << "]); }\n";
+        s << "    }\n";
+    } else if (xstore) {
         // exchange store (sharded states): element o whose bit v (xmask)
         // differs from this rank's bit (xval) goes to the partner's buffer at
         // o ^ xmask, the rest to the local output buffer (out of place)
@@ -1054,8 +1122,10 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
         s << "    }\n";
     }
     s << ""
-      << "    __syncthreads();\n"
-      << "  }\n";
+      << "    __syncthreads();\n";
+    if (staged) s << "    ++ck_n;\n";
+    s << "  }\n";
+    if (staged) s << "  if (ck_n) { __threadfence(); __syncthreads(); if (tid == 0) atomicAdd(pdone + ck_cur, ck_n); }\n";
     s << "}\n";
     return s.str();
 }
@@ -1290,7 +1360,7 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
         // remembered for this pass record (owning reference)
     } else if (xs) {
         if (!jit_xstore_ok(h, ops)) throw NqError{NQ_ERR_INTERNAL, "exchange pass cannot be specialised"};
-        const std::string src = jit_source(h, ops, pool, true);
+        const std::string src = jit_source(h, ops, pool, true, xs);
         e = acquire(src, device, JitMode::Sync);
         if (!e) {
             std::string log;
@@ -1319,7 +1389,10 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
     const int occ = occupancy(*e, device, T, smem);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    const long long grid = std::min<long long>(h.ntiles, (long long)sms * occ);
+    // a staged exchange leaves SMs to its pusher kernel: the whole pass grid
+    // must stay co-resident with it (its CTAs wait on the pusher's progress)
+    const int pass_sms = (xs && xs->staged) ? std::max(1, sms - xs->reserve_sms) : sms;
+    const long long grid = std::min<long long>(h.ntiles, (long long)pass_sms * occ);
     const double2* gpool = reinterpret_cast<const double2*>(dev_rec + h.pool_off);
     unsigned long long rb = rankbase;
     long long nt = h.ntiles;
@@ -1327,7 +1400,10 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
     double2* xr = xs ? xs->out_remote : nullptr;
     unsigned long long xm = xs ? xs->xmask : 0ull, xv = xs ? xs->xval : 0ull;
     int xrot = xs ? xs->xrot : 0;
-    void* args[] = {&state, &gpool, &rb, &nt, &xl, &xr, &xm, &xv, &xrot};
+    unsigned* pdone = xs ? xs->pass_done : nullptr;
+    const unsigned* qdone = xs ? xs->push_done : nullptr;
+    unsigned long long slot_elems = xs ? xs->slot_elems : 0ull;
+    void* args[] = {&state, &gpool, &rb, &nt, &xl, &xr, &xm, &xv, &xrot, &pdone, &qdone, &slot_elems};
     if (cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(unsigned(grid)), dim3(unsigned(T)), args, smem,
                          s) != cudaSuccess) {
         cudaGetLastError();

@@ -28,7 +28,9 @@ JitMode jit_mode();
 
 // CUDA source of the kernel specialised to one pass record.  xstore: the
 // exchange-store variant (sharded states, see JitXStore).
-std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool xstore = false);
+struct JitXStore;
+std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool xstore = false,
+                       const JitXStore* stage = nullptr);
 
 // A pass fused with a global<->local qubit exchange (shard.cpp): the pass
 // reads the state in place and writes out of place; element o of its output
@@ -40,7 +42,28 @@ struct JitXStore {
     double2* out_remote = nullptr;
     uint64_t xmask = 0, xval = 0;
     int xrot = 0;
+    // Staged form, for shards too large for a second copy (shard.cpp): the
+    // kept half is stored in place (out_local = the state) and the outgoing
+    // half into this rank's staging ring (out_remote) of `slots` slots of
+    // slot_elems, from which a pusher kernel on `pushers` reserved SMs copies
+    // it into the partner's state once the partner has consumed that chunk.
+    // Chunk of tile counter r: r >> cshift; an outgoing element o lands at
+    // slot (chunk % slots), index compress(o) = o with the physical bits
+    // chunk_bits | xmask removed (physical order kept: coalesced both ways).
+    // pass_done[c] counts the tiles this rank stored in chunk c; a tile of
+    // chunk c >= slots first waits for push_done[c - slots] == pushers.
+    bool staged = false;
+    int cshift = 0, slots = 2;
+    uint64_t chunk_bits = 0;
+    uint64_t slot_elems = 0;
+    unsigned* pass_done = nullptr;
+    const unsigned* push_done = nullptr;
+    unsigned pushers = 0;
+    int reserve_sms = 0;  // SMs left to the pusher (the pass grid avoids them)
 };
+// Physical positions of the chunk bits of a staged exchange pass: the rest
+// positions the top (nrest - cshift) bits of the rotated tile counter drive.
+uint64_t jit_stage_chunk_bits(const PassHdr& h, int xrot, int cshift);
 // Whether a pass can run as an exchange-store kernel (deterministic: every
 // rank decides alike from the same pass record).
 bool jit_xstore_ok(const PassHdr& h, const MOp* ops);

@@ -56,6 +56,13 @@ __device__ __forceinline__ void st_stream2(double2* p, double2 a, double2 b) {
                  : "memory");
 #endif
 }
+// Acquire load of a 32-bit counter (staged exchanges: another kernel, or the
+// partner GPU over NVLink, increments it)
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 // Shared-memory load the compiler may not hoist: matrices are re-read (one
 // broadcast LDS per entry) instead of occupying registers.
 __device__ __forceinline__ double2 lds(const double2* p) {

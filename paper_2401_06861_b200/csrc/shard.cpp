@@ -142,6 +142,19 @@ struct ShardComm {
     double2* alt = nullptr;
     std::vector<double2*> peer_alt;
     int64_t fused = 0;
+    // staged fused exchanges (no room for `alt`, e.g. 2^33 amplitudes per
+    // GPU): a ring of `stage_slots` staging slots for the outgoing half,
+    // per-chunk counters (pass_done[kMaxChunks], push_done[kMaxChunks]) mapped
+    // into the partner, and a side stream for the pusher kernel
+    static constexpr int kMaxChunks = 256;
+    double2* stage = nullptr;
+    uint64_t stage_slot_elems = 0;
+    int stage_slots = 2, stage_chunks = 0;
+    unsigned* sync = nullptr;
+    std::vector<unsigned*> peer_sync;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_go = nullptr, ev_pushed = nullptr;
+    int64_t staged = 0;
     std::unordered_map<uint64_t, std::vector<int>> rebalance_cache;  // see rebalance()
     // planned segments of recent flushes (repeated circuits replan nothing and
     // reuse their kernels): key = segment ops incl. matrices + plan options
@@ -344,6 +357,8 @@ __attribute__((unused)) uint64_t ins_bit(uint64_t k, int v, uint64_t val) {
 struct FuseX {
     int v = 0;           // local physical bit exchanged with the global bit
     uint64_t mybit = 0;  // this rank's value of that global bit
+    int partner = 0;
+    bool staged = false;  // staged form: in place + staging ring + pusher
     double2* out_local = nullptr;
     double2* out_remote = nullptr;
     bool done = false;   // set when the segment's last pass carried the exchange
@@ -374,6 +389,67 @@ std::vector<unsigned char> segment_key(const PlanOptions& o, const std::vector<E
         if (!e.mat.empty()) put(e.mat.data(), e.mat.size() * sizeof(cplx));
     }
     return k;
+}
+
+void stream_barrier(ShardComm& sc, DeviceCtx& c);
+
+// A pass fused with an exchange when no second copy of the shard fits: the
+// pass (on the SMs the pusher leaves free) stores the kept half in place and
+// the outgoing half chunk by chunk into the staging ring; the pusher kernel
+// (side stream) copies each chunk into the partner's state as soon as both
+// ranks have stored that chunk, so NVLink traffic overlaps the pass.
+void launch_staged_exchange(State& s, DeviceCtx& c, const PassHdr& h, const MOp* mops, const cplx* pool,
+                            const unsigned char* dev_rec, uint64_t rankbase, JitXStore xs, const FuseX& fx) {
+    ShardComm& sc = *s.comm;
+    constexpr int kPushers = 16;  // SMs (one CTA each) driving the NVLink copies
+    const int chunks = sc.stage_chunks;
+    int cb = 0;
+    while ((1 << cb) < chunks) ++cb;
+    const int cshift = h.nrest - cb;
+    if (cshift < 1) throw NqError{NQ_ERR_INTERNAL, "staged exchange: too few tiles for the chunk count"};
+    xs.staged = true;
+    xs.cshift = cshift;
+    xs.slots = sc.stage_slots;
+    xs.chunk_bits = jit_stage_chunk_bits(h, xs.xrot, cshift);
+    xs.slot_elems = s.count / 2 / uint64_t(chunks);
+    xs.pass_done = sc.sync;
+    xs.push_done = sc.sync + ShardComm::kMaxChunks;
+    xs.pushers = kPushers;
+    xs.reserve_sms = kPushers;
+    if (xs.slot_elems != sc.stage_slot_elems) throw NqError{NQ_ERR_INTERNAL, "staged exchange: slot size mismatch"};
+    // pusher: holes = chunk bits (source: bit of the chunk number) and v
+    StagePush sp;
+    sp.chunks = chunks;
+    sp.slots = sc.stage_slots;
+    sp.tiles_per_chunk = unsigned(1u << cshift);
+    sp.slot_elems = xs.slot_elems;
+    sp.vval = fx.mybit;  // the partner's copy of this element has v = this rank's bit
+    {
+        // chunk number bit i = tile counter bit cshift + i -> physical position
+        std::vector<std::pair<int, int>> holes;
+        for (int i = 0; i < cb; ++i) {
+            const int j = cshift + i;
+            holes.push_back({h.rest[j <= xs.xrot ? j - 1 : j], i});
+        }
+        holes.push_back({fx.v, -1});
+        std::sort(holes.begin(), holes.end());
+        sp.nholes = int(holes.size());
+        for (size_t k = 0; k < holes.size(); ++k) {
+            sp.hole_pos[k] = holes[k].first;
+            sp.hole_src[k] = holes[k].second;
+        }
+    }
+    // zero the counters on every rank before any rank's pusher reads them
+    CUDA_TRY(cudaMemsetAsync(sc.sync, 0, sizeof(unsigned) * 2 * ShardComm::kMaxChunks, c.stream));
+    stream_barrier(sc, c);
+    CUDA_TRY(cudaEventRecord(sc.ev_go, c.stream));
+    CUDA_TRY(cudaStreamWaitEvent(sc.side, sc.ev_go, 0));
+    launch_stage_push(sc.stage, sc.peer[size_t(fx.partner)], sc.sync, sc.peer_sync[size_t(fx.partner)],
+                      sc.sync + ShardComm::kMaxChunks, sp, kPushers, sc.side);
+    jit_launch(s.d, dev_rec, h, mops, pool, rankbase, c.stream, s.dev, &xs);
+    CUDA_TRY(cudaEventRecord(sc.ev_pushed, sc.side));
+    CUDA_TRY(cudaStreamWaitEvent(c.stream, sc.ev_pushed, 0));
+    CUDA_TRY(cudaGetLastError());
 }
 
 void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vector<int>* layout = nullptr,
@@ -436,8 +512,13 @@ void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vecto
             xs.xmask = uint64_t(1) << fx->v;
             xs.xval = fx->mybit << fx->v;
             xs.xrot = rest_pos(h, fx->v);
-            jit_launch(s.d, c.d_ops + offs[i], h, mops, reinterpret_cast<const cplx*>(rec + h.pool_off), rankbase,
-                       c.stream, s.dev, &xs);
+            if (fx->staged) {
+                launch_staged_exchange(s, c, h, mops, reinterpret_cast<const cplx*>(rec + h.pool_off), c.d_ops + offs[i],
+                                       rankbase, xs, *fx);
+            } else {
+                jit_launch(s.d, c.d_ops + offs[i], h, mops, reinterpret_cast<const cplx*>(rec + h.pool_off), rankbase,
+                           c.stream, s.dev, &xs);
+            }
             fx->done = true;
         } else if (!jit_launch(s.d, c.d_ops + offs[i], h, mops,
                         reinterpret_cast<const cplx*>(rec + h.pool_off), rankbase, c.stream, s.dev, nullptr,
@@ -499,13 +580,17 @@ void run_exchange(State& s, DeviceCtx& c, int g, int v) {
 // rank from reading its new state before its partner's stores have landed
 // (and, as no rank touches its old buffer again before the next exchange,
 // no barrier is needed before such a pass).
-void fused_exchange_done(State& s, DeviceCtx& c, int g, int v) {
+void fused_exchange_done(State& s, DeviceCtx& c, int g, int v, bool staged = false) {
     ShardComm& sc = *s.comm;
     NvtxRange range("nq.exchange.fused", g);
     if (s.rank == 0 && std::getenv("NQ_SHARD_TRACE"))
         std::fprintf(stderr, "[shard] exchange g=%d v=%d (fused into the pass)\n", g, v);
-    std::swap(s.d, sc.alt);
-    std::swap(sc.peer, sc.peer_alt);
+    if (staged) {
+        ++sc.staged;  // in place: the partner's pusher wrote into this state
+    } else {
+        std::swap(s.d, sc.alt);
+        std::swap(sc.peer, sc.peer_alt);
+    }
     stream_barrier(sc, c);
     CUDA_TRY(cudaGetLastError());
     sc.bytes += int64_t(s.count / 2) * 16;
@@ -680,7 +765,7 @@ void execute(State& s, const std::vector<Action>& acts, bool relabel = false) {
         if (a.kind == Action::Segment) {
             if (!relabel) {
                 const bool next_x = ai + 1 < acts.size() && acts[ai + 1].kind == Action::Exchange;
-                if (next_x && scx.alt) {
+                if (next_x && (scx.alt || scx.stage)) {
                     // fuse the exchange into the segment's last pass
                     const Action& x = acts[ai + 1];
                     const int j = x.gbit - s.nloc;
@@ -688,11 +773,13 @@ void execute(State& s, const std::vector<Action>& acts, bool relabel = false) {
                     FuseX fx;
                     fx.v = x.vbit;
                     fx.mybit = uint64_t((s.rank >> j) & 1);
-                    fx.out_local = scx.alt;
-                    fx.out_remote = scx.peer_alt[size_t(partner)];
+                    fx.partner = partner;
+                    fx.staged = scx.alt == nullptr;
+                    fx.out_local = fx.staged ? s.d : scx.alt;
+                    fx.out_remote = fx.staged ? scx.stage : scx.peer_alt[size_t(partner)];
                     run_segment(s, c, a.ops, nullptr, &fx);
                     if (fx.done) {
-                        fused_exchange_done(s, c, x.gbit, x.vbit);
+                        fused_exchange_done(s, c, x.gbit, x.vbit, fx.staged);
                         ++ai;
                     }
                     continue;
@@ -825,8 +912,24 @@ void check_env_agreement(State& s) {
                                                "must see the same environment"};
 }
 
+void free_staging(ShardComm& sc) {
+    for (unsigned* p : sc.peer_sync)
+        if (p) cudaIpcCloseMemHandle(p);
+    sc.peer_sync.clear();
+    if (sc.stage) cudaFree(sc.stage);
+    if (sc.sync) cudaFree(sc.sync);
+    if (sc.side) cudaStreamDestroy(sc.side);
+    if (sc.ev_go) cudaEventDestroy(sc.ev_go);
+    if (sc.ev_pushed) cudaEventDestroy(sc.ev_pushed);
+    sc.stage = nullptr;
+    sc.sync = nullptr;
+    sc.side = nullptr;
+    sc.ev_go = sc.ev_pushed = nullptr;
+    sc.stage_chunks = 0;
+}
+
 bool fused_exchange_wanted() {
-    return env_option("NQ_FUSED_EXCHANGE", 1) != 0;
+    return env_option_str("NQ_FUSED_EXCHANGE") != "0";
 }
 
 void setup_peer_exchange(State& s, ShardComm& sc, DeviceCtx& c) {
@@ -850,6 +953,42 @@ void setup_peer_exchange(State& s, ShardComm& sc, DeviceCtx& c) {
     if (sc.peer_alt.empty() && sc.alt) {
         cudaFree(sc.alt);
         sc.alt = nullptr;
+    }
+    // staged fused exchanges when no second copy fits (or when forced by
+    // NQ_FUSED_EXCHANGE=staged): 64 chunks (fewer for small shards: a chunk
+    // spans at least 2 tiles of the largest pass tile, 2^12), 2 slots of
+    // half a chunk each -- 2 GiB at 2^33 amplitudes per GPU
+    const std::string fxm = env_option_str("NQ_FUSED_EXCHANGE");
+    const bool want_staged = fused_exchange_wanted() && (fxm == "staged" || !sc.alt);
+    if (want_staged) {
+        if (sc.alt) {  // forced: release the second copy
+            for (double2* p : sc.peer_alt)
+                if (p) cudaIpcCloseMemHandle(p);
+            sc.peer_alt.clear();
+            cudaFree(sc.alt);
+            sc.alt = nullptr;
+        }
+        int chunks = 64;
+        while (chunks > 2 && (uint64_t(chunks) << 13) > s.count) chunks /= 2;
+        sc.stage_chunks = chunks;
+        sc.stage_slot_elems = s.count / 2 / uint64_t(chunks);
+        bool ok = (uint64_t(chunks) << 13) <= s.count &&
+                  cudaMalloc(reinterpret_cast<void**>(&sc.stage),
+                             size_t(sc.stage_slots) * sc.stage_slot_elems * sizeof(double2)) == cudaSuccess &&
+                  cudaMalloc(reinterpret_cast<void**>(&sc.sync), sizeof(unsigned) * 2 * ShardComm::kMaxChunks) ==
+                      cudaSuccess &&
+                  cudaMemset(sc.sync, 0, sizeof(unsigned) * 2 * ShardComm::kMaxChunks) == cudaSuccess &&
+                  cudaStreamCreateWithFlags(&sc.side, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&sc.ev_go, cudaEventDisableTiming) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&sc.ev_pushed, cudaEventDisableTiming) == cudaSuccess;
+        cudaGetLastError();
+        std::vector<double2*> ps = map_peers(s, reinterpret_cast<double2*>(sc.sync), ok);
+        ok = !ps.empty();
+        if (ok) {
+            for (double2* p : ps) sc.peer_sync.push_back(reinterpret_cast<unsigned*>(p));
+        } else {
+            free_staging(sc);
+        }
     }
     (void)c;
 }
@@ -883,6 +1022,7 @@ void shard_free(State& s) {
     for (double2* p : sc->peer_alt)
         if (p) cudaIpcCloseMemHandle(p);
     if (sc->alt) cudaFree(sc->alt);
+    free_staging(*sc);
     if (sc->comm) ncclCommDestroy(sc->comm);
     delete sc;
     s.comm = nullptr;
@@ -1240,7 +1380,7 @@ nq_status nq_sv_comm_fused(const nq_sv* h, int64_t* fused, int* has_alt_buffer) 
     return guard([&] {
         const State& s = h->s;
         if (fused) *fused = s.comm ? s.comm->fused : 0;
-        if (has_alt_buffer) *has_alt_buffer = (s.comm && s.comm->alt) ? 1 : 0;
+        if (has_alt_buffer) *has_alt_buffer = !s.comm ? 0 : s.comm->alt ? 1 : s.comm->stage ? 2 : 0;
     });
 }
 

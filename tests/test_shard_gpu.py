@@ -16,8 +16,8 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _rank_main(rank, world, uid, n, seed, outdir, fused=True, exchange="p2p"):
-    os.environ["NQ_FUSED_EXCHANGE"] = "1" if fused else "0"
+def _rank_main(rank, world, uid, n, seed, outdir, fused="1", exchange="p2p"):
+    os.environ["NQ_FUSED_EXCHANGE"] = fused
     os.environ["NQ_EXCHANGE"] = exchange
     sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
     from oracle import Port
@@ -48,19 +48,21 @@ def _rank_main(rank, world, uid, n, seed, outdir, fused=True, exchange="p2p"):
     stats = sv.comm_stats()
     np.savez(os.path.join(outdir, f"r{rank}.npz"), norm=norm, ex=ex, idx=idx, cnt=cnt, amps=amps, probs=probs,
              psi=psi, after=after,
-             exchanges=stats["exchanges"], fused=stats["fused"], alt=stats["alt_buffer"],
+             exchanges=stats["exchanges"], fused=stats["fused"], alt=stats["alt_buffer"], staged=stats["staged"],
              letters=np.array([t[0] for t in terms]),
              coeff=np.array([t[1] for t in terms]))
 
 
-@pytest.mark.parametrize("n,world,fused,exchange", [(14, 2, True, "p2p"), (20, 2, True, "p2p"),
-                                                    (20, 2, False, "p2p"), (20, 2, False, "nccl"),
-                                                    (22, 4, True, "p2p"), (22, 4, False, "p2p"),
-                                                    (22, 4, False, "nccl")])
+@pytest.mark.parametrize("n,world,fused,exchange", [(14, 2, "1", "p2p"), (20, 2, "1", "p2p"),
+                                                    (20, 2, "staged", "p2p"), (21, 2, "staged", "p2p"),
+                                                    (20, 2, "0", "p2p"), (20, 2, "0", "nccl"),
+                                                    (22, 4, "1", "p2p"), (22, 4, "staged", "p2p"),
+                                                    (22, 4, "0", "p2p"), (22, 4, "0", "nccl")])
 def test_sharded_gpus(port, tmp_path, n, world, fused, exchange):
     """Sharded run == oracle (amplitudes, norm, expectations, sampling), with
     exchanges fused into the preceding pass (out-of-place exchange stores into
-    the partner's second buffer), as standalone peer-memory swaps, or through
+    the partner's second buffer, or staged: in place + staging ring + pusher
+    kernel, the form used when no second copy fits), as standalone peer-memory swaps, or through
     the NCCL send/recv fallback (NQ_EXCHANGE=nccl: pack, send/recv through
     bounce buffers, unpack -- the path taken when CUDA IPC is unavailable)."""
     if abi.device_count() < world:
@@ -74,8 +76,10 @@ def test_sharded_gpus(port, tmp_path, n, world, fused, exchange):
     for r in range(world):
         d = np.load(tmp_path / f"r{r}.npz")
         assert int(d["exchanges"]) > 0
-        if fused:
+        if fused == "1":
             assert bool(d["alt"]) and int(d["fused"]) > 0
+        elif fused == "staged":
+            assert bool(d["staged"]) and not bool(d["alt"]) and int(d["fused"]) > 0
         else:
             assert int(d["fused"]) == 0
         np.testing.assert_allclose(d["amps"], want, atol=1e-10, rtol=0)
