@@ -69,15 +69,30 @@ __device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
     return v;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void __launch_bounds__(256) k_stage_push(const double2* __restrict__ stage, double2* __restrict__ peer,
                                                     const unsigned* my_done, const unsigned* peer_done,
                                                     unsigned* push_done, StagePush sp) {
     for (int c = 0; c < sp.chunks; ++c) {
-        if (threadIdx.x == 0) {
-            while (ld_acq(my_done + c) < sp.tiles_per_chunk) {
-            }
-            while (ld_acq(peer_done + c) < sp.tiles_per_chunk) {
-            }
+        if (threadIdx.x == 0 && ld_acq(push_done + sp.err_index) == 0u) {
+            // bounded waits (60 s): a stalled partner is recorded and reported
+            // by the host, not hung on (no further waits once recorded)
+            const unsigned long long t0 = gtimer();
+            while (ld_acq(my_done + c) < sp.tiles_per_chunk)
+                if (gtimer() - t0 > 60000000000ull) {
+                    atomicMax(push_done + sp.err_index, 0x10000u + unsigned(c));
+                    break;
+                }
+            while (ld_acq(peer_done + c) < sp.tiles_per_chunk)
+                if (gtimer() - t0 > 60000000000ull) {
+                    atomicMax(push_done + sp.err_index, 0x20000u + unsigned(c));
+                    break;
+                }
         }
         __syncthreads();
         // index bits contributed by the chunk number and v: fixed per chunk
@@ -138,6 +153,14 @@ void launch_swap_peer(double2* mine, double2* peer, int v, uint64_t mval, uint64
     if (k1 <= k0) return;
     k_swap_peer<<<148 * 8, 256, 0, s>>>(mine, peer, v, mval, pval, k0, k1);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void preload_stage_push() {
+    // see jit_xstore_prepare: kernels that spin on each other must both be
+    // loaded before either is launched (CUDA lazy loading)
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(&k_stage_push));
+    cudaGetLastError();
 }
 
 void launch_stage_push(const double2* stage, double2* peer, const unsigned* my_done, const unsigned* peer_done,

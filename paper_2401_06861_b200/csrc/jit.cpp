@@ -401,6 +401,10 @@ std::string sparse_dense(const MOp& op, const cplx* u, int E, const std::string&
     return s.str();
 }
 
+// Bounded waits of a staged exchange (pass kernel and pusher): a stall is
+// recorded in the sync buffer and reported by the host instead of hanging.
+constexpr unsigned long long kStageWatchdogNs = 60000000000ull;
+
 uint64_t jit_stage_chunk_bits(const PassHdr& h, int xrot, int cshift) {
     // rotated counter rr: r bit 0 -> rest position xrot, r bit j >= 1 -> rest
     // position j - 1 below xrot + 1, j above (see the exchange passes' rr)
@@ -551,8 +555,9 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
               << "        if (ck_n) { __threadfence(); __syncthreads(); if (tid == 0) atomicAdd(pdone + ck_cur, ck_n); }\n"
               << "        ck_cur = ck; ck_n = 0u;\n"
               << "        if (ck >= " << stage->slots << "u) {\n"
-              << "          if (tid == 0) while (ld_acquire_u32(qdone + ck - " << stage->slots << "u) < " << stage->pushers
-              << "u) {}\n"
+              << "          if (tid == 0 && ld_acquire_u32(pdone + " << 2 * 256 << ") == 0u && !wait_at_least(qdone + ck - "
+              << stage->slots << "u, " << stage->pushers << "u, " << kStageWatchdogNs
+              << "ull)) atomicMax(pdone + " << 2 * 256 << ", 0x100u + ck);  // watchdog\n"
               << "          __syncthreads();\n"
               << "        }\n"
               << "      }\n"
@@ -1346,6 +1351,20 @@ bool jit_xstore_ok(const PassHdr& h, const MOp* ops) {
     if (h.flags & PASS_MIRROR) return false;
     (void)ops;
     return true;
+}
+
+void jit_xstore_prepare(const PassHdr& h, const MOp* ops, const cplx* pool, int device, const JitXStore* xs) {
+    if (!jit_xstore_ok(h, ops)) throw NqError{NQ_ERR_INTERNAL, "exchange pass cannot be specialised"};
+    std::shared_ptr<Entry> e = acquire(jit_source(h, ops, pool, true, xs), device, JitMode::Sync);
+    // load it into this device's context now: with lazy loading, a first
+    // launch next to a kernel that spins on it (the staged pusher) could wait
+    // for that kernel to finish -- a deadlock
+    if (e) {
+        cudaFuncAttributes fa;
+        cudaSetDevice(device);
+        cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(e->kern));
+        cudaGetLastError();
+    }
 }
 
 bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,

@@ -112,9 +112,11 @@ struct StagePush {
     uint64_t slot_elems = 0;
     uint64_t vval = 0;
     int nholes = 0;
+    int err_index = 0;  // push_done[err_index]: watchdog record (0 = fine)
     int hole_pos[24] = {};
     int hole_src[24] = {};
 };
+void preload_stage_push();
 void launch_stage_push(const double2* stage, double2* peer, const unsigned* my_done, const unsigned* peer_done,
                        unsigned* push_done, const StagePush& sp, int ctas, cudaStream_t s);
 

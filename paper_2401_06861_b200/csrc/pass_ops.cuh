@@ -63,6 +63,21 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// Nanosecond clock (watchdogs of the staged exchange waits)
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// Bounded wait until *p >= want (acquire): false after `ns` without progress
+// (the caller records the failure instead of hanging the device)
+__device__ __forceinline__ bool wait_at_least(const unsigned* p, unsigned want, unsigned long long ns) {
+    if (ld_acquire_u32(p) >= want) return true;
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_u32(p) < want)
+        if (globaltimer_ns() - t0 > ns) return false;
+    return true;
+}
 // Shared-memory load the compiler may not hoist: matrices are re-read (one
 // broadcast LDS per entry) instead of occupying registers.
 __device__ __forceinline__ double2 lds(const double2* p) {

@@ -424,6 +424,7 @@ void launch_staged_exchange(State& s, DeviceCtx& c, const PassHdr& h, const MOp*
     sp.tiles_per_chunk = unsigned(1u << cshift);
     sp.slot_elems = xs.slot_elems;
     sp.vval = fx.mybit;  // the partner's copy of this element has v = this rank's bit
+    sp.err_index = ShardComm::kMaxChunks;  // push_done[kMaxChunks] = sync[2 * kMaxChunks]
     {
         // chunk number bit i = tile counter bit cshift + i -> physical position
         std::vector<std::pair<int, int>> holes;
@@ -439,14 +440,25 @@ void launch_staged_exchange(State& s, DeviceCtx& c, const PassHdr& h, const MOp*
             sp.hole_src[k] = holes[k].second;
         }
     }
-    // zero the counters on every rank before any rank's pusher reads them
-    CUDA_TRY(cudaMemsetAsync(sc.sync, 0, sizeof(unsigned) * 2 * ShardComm::kMaxChunks, c.stream));
+    if (std::getenv("NQ_SHARD_TRACE")) {
+        std::string hs;
+        for (int k = 0; k < sp.nholes; ++k) hs += " " + std::to_string(sp.hole_pos[k]) + ":" + std::to_string(sp.hole_src[k]);
+        std::fprintf(stderr, "[shard] rank %d staged exchange v=%d partner=%d m=%d nrest=%d ntiles=%lld cshift=%d "
+                     "chunks=%d slot=%llu xrot=%d holes%s\n", s.rank, fx.v, fx.partner, h.m, h.nrest,
+                     (long long)h.ntiles, cshift, chunks, (unsigned long long)xs.slot_elems, xs.xrot, hs.c_str());
+    }
+    // kernel compiled before the ranks meet (a rank still compiling would
+    // stall its partner's pusher), counters zeroed on every rank before any
+    // rank's pusher reads them
+    jit_xstore_prepare(h, mops, pool, s.dev, &xs);
+    preload_stage_push();
+    CUDA_TRY(cudaMemsetAsync(sc.sync, 0, sizeof(unsigned) * (2 * ShardComm::kMaxChunks + 4), c.stream));
     stream_barrier(sc, c);
     CUDA_TRY(cudaEventRecord(sc.ev_go, c.stream));
     CUDA_TRY(cudaStreamWaitEvent(sc.side, sc.ev_go, 0));
+    jit_launch(s.d, dev_rec, h, mops, pool, rankbase, c.stream, s.dev, &xs);
     launch_stage_push(sc.stage, sc.peer[size_t(fx.partner)], sc.sync, sc.peer_sync[size_t(fx.partner)],
                       sc.sync + ShardComm::kMaxChunks, sp, kPushers, sc.side);
-    jit_launch(s.d, dev_rec, h, mops, pool, rankbase, c.stream, s.dev, &xs);
     CUDA_TRY(cudaEventRecord(sc.ev_pushed, sc.side));
     CUDA_TRY(cudaStreamWaitEvent(c.stream, sc.ev_pushed, 0));
     CUDA_TRY(cudaGetLastError());
@@ -587,6 +599,33 @@ void fused_exchange_done(State& s, DeviceCtx& c, int g, int v, bool staged = fal
         std::fprintf(stderr, "[shard] exchange g=%d v=%d (fused into the pass)\n", g, v);
     if (staged) {
         ++sc.staged;  // in place: the partner's pusher wrote into this state
+        // watchdog record of the bounded waits (pass kernel / pusher)
+        unsigned err = 0;
+        CUDA_TRY(cudaMemcpyAsync(&err, sc.sync + 2 * ShardComm::kMaxChunks, sizeof err, cudaMemcpyDeviceToHost,
+                                 c.stream));
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        if (err) {
+            std::vector<unsigned> cnt(2 * size_t(sc.stage_chunks));
+            cudaMemcpy(cnt.data(), sc.sync, sc.stage_chunks * sizeof(unsigned), cudaMemcpyDeviceToHost);
+            cudaMemcpy(cnt.data() + sc.stage_chunks, sc.sync + ShardComm::kMaxChunks,
+                       sc.stage_chunks * sizeof(unsigned), cudaMemcpyDeviceToHost);
+            std::string d;
+            for (int i = 0; i < sc.stage_chunks; ++i)
+                d += " " + std::to_string(cnt[size_t(i)]) + "/" + std::to_string(cnt[size_t(sc.stage_chunks + i)]);
+            // the partner's counters as this rank sees them through the mapping
+            std::vector<unsigned> pc(size_t(sc.stage_chunks), 0u);
+            for (size_t r = 0; r < sc.peer_sync.size(); ++r)
+                if (sc.peer_sync[r]) {
+                    cudaMemcpy(pc.data(), sc.peer_sync[r], pc.size() * sizeof(unsigned), cudaMemcpyDeviceToHost);
+                    d += " | peer " + std::to_string(r) + ":";
+                    for (int i = 0; i < std::min(8, sc.stage_chunks); ++i) d += " " + std::to_string(pc[size_t(i)]);
+                }
+            cudaGetLastError();
+            char head[96];
+            std::snprintf(head, sizeof head, "staged exchange stalled (rank %d, record 0x%x); pass/push per chunk:",
+                          s.rank, err);
+            throw NqError{NQ_ERR_INTERNAL, head + d};
+        }
     } else {
         std::swap(s.d, sc.alt);
         std::swap(sc.peer, sc.peer_alt);
@@ -975,9 +1014,11 @@ void setup_peer_exchange(State& s, ShardComm& sc, DeviceCtx& c) {
         bool ok = (uint64_t(chunks) << 13) <= s.count &&
                   cudaMalloc(reinterpret_cast<void**>(&sc.stage),
                              size_t(sc.stage_slots) * sc.stage_slot_elems * sizeof(double2)) == cudaSuccess &&
-                  cudaMalloc(reinterpret_cast<void**>(&sc.sync), sizeof(unsigned) * 2 * ShardComm::kMaxChunks) ==
-                      cudaSuccess &&
-                  cudaMemset(sc.sync, 0, sizeof(unsigned) * 2 * ShardComm::kMaxChunks) == cudaSuccess &&
+                  // 2 MiB: a small cudaMalloc may share an IPC-able block with
+                  // others, and a peer's mapping of the handle then starts at
+                  // that block's base, not at this buffer
+                  cudaMalloc(reinterpret_cast<void**>(&sc.sync), size_t(2) << 20) == cudaSuccess &&
+                  cudaMemset(sc.sync, 0, sizeof(unsigned) * (2 * ShardComm::kMaxChunks + 4)) == cudaSuccess &&
                   cudaStreamCreateWithFlags(&sc.side, cudaStreamNonBlocking) == cudaSuccess &&
                   cudaEventCreateWithFlags(&sc.ev_go, cudaEventDisableTiming) == cudaSuccess &&
                   cudaEventCreateWithFlags(&sc.ev_pushed, cudaEventDisableTiming) == cudaSuccess;
