@@ -520,13 +520,52 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
     s << ")\n"
       << "nqjit(double2* __restrict__ st, const double2* __restrict__ gpool, unsigned long long rankbase,"
          " long long ntiles, double2* xout_l, double2* xout_r, unsigned long long xmask, unsigned long long xval,"
-         " int xrot" << (staged ? ", unsigned* pdone, const unsigned* qdone, unsigned long long slot_elems" : "")
+         " int xrot" << (staged ? ", unsigned* pdone, const unsigned* qdone, unsigned long long slot_elems,"
+                                  " double2* xpeer, const unsigned* xpeer_done, unsigned npass" : "")
       << ") {\n"
       << "  using namespace nq;\n"
       << "  extern __shared__ __align__(16) unsigned char smem[];\n"
       << "  double2* buf0 = reinterpret_cast<double2*>(smem);\n"
       << "  double2* pool = buf0 + " << SIZE << ";\n"
-      << "  const unsigned tid = threadIdx.x;\n"
+      << "  const unsigned tid = threadIdx.x;\n";
+    if (staged) {
+        // staged exchange: CTAs >= npass are the pusher (cooperative launch:
+        // the whole grid is co-resident, so the waits cannot deadlock)
+        const int cb = h.nrest - stage->cshift;
+        // slot index k -> partner index: k deposited into the kept bit runs
+        // (between the holes), plus the chunk number's bits at the chunk-bit
+        // holes and v = this rank's bit (xval: the partner keeps v = mybit)
+        std::vector<int> hp;
+        for (int p = 0; p < 64; ++p)
+            if ((holes >> p) & 1) hp.push_back(p);
+        std::ostringstream ex;
+        ex << "(xval & xmask)";
+        int src_bit = 0, prev = 0;  // k bits consumed, next kept position
+        for (size_t j = 0; j <= hp.size(); ++j) {
+            const int end = j < hp.size() ? hp[j] : 63;  // kept run [prev, end)
+            if (end > prev)
+                ex << " | (((k >> " << src_bit << ") & " << hex64((end - prev >= 64) ? ~0ull : ((1ull << (end - prev)) - 1))
+                   << ") << " << prev << ")";
+            src_bit += end - prev;
+            prev = end + 1;
+        }
+        // chunk number bit i -> its hole position
+        std::ostringstream cx;
+        cx << "0ull";
+        for (int i = 0; i < cb; ++i) {
+            const int j = stage->cshift + i;
+            cx << " | (((unsigned long long)c >> " << i << ") & 1ull) << " << rest[size_t(j <= stage->xrot ? j - 1 : j)];
+        }
+        s << "  if (blockIdx.x >= npass) {\n"
+          << "    stage_push_role<16>(blockIdx.x - npass, gridDim.x - npass, xout_r, xpeer, pdone, xpeer_done, pdone + 256, "
+             "pdone + 512, " << (1 << cb) << ", " << stage->slots << ", " << (1u << stage->cshift) << "u, slot_elems, "
+          << kStageWatchdogNs << "ull,\n"
+          << "      [=] (unsigned long long k, int c) -> unsigned long long { return " << ex.str() << " | "
+          << cx.str() << "; });\n"
+          << "    return;\n"
+          << "  }\n";
+    }
+    s << ""
       << "  for (unsigned i = tid; i < " << h.pool_n << "u; i += " << T << "u) pool[i] = gpool[i];\n";
     // Per-layout thread constants (tile-bit pattern tb<k> and swizzled
     // offset sw<k>) are defined inside the tile loop where layout k becomes
@@ -546,7 +585,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
         s << "  __syncthreads();\n";
         if (staged)
             s << "  unsigned ck_cur = 0xffffffffu, ck_n = 0u;  // chunk of the tiles in flight, tiles stored in it\n";
-        s << "  for (long long r = blockIdx.x; r < ntiles; r += gridDim.x) {\n";
+        s << "  for (long long r = blockIdx.x; r < ntiles; r += " << (staged ? "npass" : "gridDim.x") << ") {\n";
         if (staged) {
             // entering a new chunk: publish the tiles stored in the previous
             // one (fenced), then wait until its staging slot is free again
@@ -1408,10 +1447,15 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
     const int occ = occupancy(*e, device, T, smem);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    // a staged exchange leaves SMs to its pusher kernel: the whole pass grid
-    // must stay co-resident with it (its CTAs wait on the pusher's progress)
-    const int pass_sms = (xs && xs->staged) ? std::max(1, sms - xs->reserve_sms) : sms;
-    const long long grid = std::min<long long>(h.ntiles, (long long)pass_sms * occ);
+    // a staged exchange: the last `pushers` CTAs of a co-resident
+    // (cooperative) grid are the pusher, the others the pass
+    const bool staged = xs && xs->staged;
+    const long long pushers = staged ? xs->pushers : 0;
+    const long long grid =
+        std::min<long long>(h.ntiles, std::max<long long>(1, (long long)sms * occ - pushers)) + pushers;
+    unsigned npass = unsigned(grid - pushers);
+    double2* xpeer = staged ? xs->peer : nullptr;
+    const unsigned* xpeer_done = staged ? xs->peer_done : nullptr;
     const double2* gpool = reinterpret_cast<const double2*>(dev_rec + h.pool_off);
     unsigned long long rb = rankbase;
     long long nt = h.ntiles;
@@ -1422,9 +1466,14 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
     unsigned* pdone = xs ? xs->pass_done : nullptr;
     const unsigned* qdone = xs ? xs->push_done : nullptr;
     unsigned long long slot_elems = xs ? xs->slot_elems : 0ull;
-    void* args[] = {&state, &gpool, &rb, &nt, &xl, &xr, &xm, &xv, &xrot, &pdone, &qdone, &slot_elems};
-    if (cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(unsigned(grid)), dim3(unsigned(T)), args, smem,
-                         s) != cudaSuccess) {
+    void* args[] = {&state, &gpool, &rb, &nt, &xl, &xr, &xm, &xv, &xrot, &pdone, &qdone, &slot_elems, &xpeer, &xpeer_done,
+                    &npass};
+    const cudaError_t lrc =
+        staged ? cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(e->kern), dim3(unsigned(grid)),
+                                             dim3(unsigned(T)), args, smem, s)
+               : cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(unsigned(grid)), dim3(unsigned(T)), args,
+                                  smem, s);
+    if (lrc != cudaSuccess) {
         cudaGetLastError();
         if (xs) throw NqError{NQ_ERR_CUDA, "exchange pass kernel launch failed"};
         return false;

@@ -45,8 +45,8 @@ struct JitXStore {
     // Staged form, for shards too large for a second copy (shard.cpp): the
     // kept half is stored in place (out_local = the state) and the outgoing
     // half into this rank's staging ring (out_remote) of `slots` slots of
-    // slot_elems, from which a pusher kernel on `pushers` reserved SMs copies
-    // it into the partner's state once the partner has consumed that chunk.
+    // slot_elems, from which the grid's last `pushers` CTAs copy it into the
+    // partner's state once the partner has consumed that chunk.
     // Chunk of tile counter r: r >> cshift; an outgoing element o lands at
     // slot (chunk % slots), index compress(o) = o with the physical bits
     // chunk_bits | xmask removed (physical order kept: coalesced both ways).
@@ -58,8 +58,9 @@ struct JitXStore {
     uint64_t slot_elems = 0;
     unsigned* pass_done = nullptr;
     const unsigned* push_done = nullptr;
-    unsigned pushers = 0;
-    int reserve_sms = 0;  // SMs left to the pusher (the pass grid avoids them)
+    unsigned pushers = 0;  // pusher CTAs appended to the pass grid (cooperative launch)
+    double2* peer = nullptr;            // the partner's state (peer memory)
+    const unsigned* peer_done = nullptr;  // the partner's pass_done counters
 };
 // Physical positions of the chunk bits of a staged exchange pass: the rest
 // positions the top (nrest - cshift) bits of the rotated tile counter drive.

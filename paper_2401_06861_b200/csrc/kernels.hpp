@@ -103,22 +103,6 @@ void launch_half_unpack(double2* st, const double2* buf, uint64_t k0, uint64_t l
 // mine[ins(k, v, mval)] <-> peer[ins(k, v, pval)] for k in [k0, k1) (peer: IPC-mapped)
 void launch_swap_peer(double2* mine, double2* peer, int v, uint64_t mval, uint64_t pval, uint64_t k0, uint64_t k1,
                       cudaStream_t s);
-// Staged exchange pusher (shard.cpp): chunk c's staging slot -> partner state,
-// slot index expanded by inserting hole j (ascending position hole_pos[j]) with
-// chunk bit hole_src[j] of c, or vval where hole_src[j] < 0.
-struct StagePush {
-    int chunks = 0, slots = 2;
-    unsigned tiles_per_chunk = 0;
-    uint64_t slot_elems = 0;
-    uint64_t vval = 0;
-    int nholes = 0;
-    int err_index = 0;  // push_done[err_index]: watchdog record (0 = fine)
-    int hole_pos[24] = {};
-    int hole_src[24] = {};
-};
-void preload_stage_push();
-void launch_stage_push(const double2* stage, double2* peer, const unsigned* my_done, const unsigned* peer_done,
-                       unsigned* push_done, const StagePush& sp, int ctas, cudaStream_t s);
 
 void launch_probs(const double2* a, uint64_t n, double* p, cudaStream_t s);
 void launch_dm_probs(const double2* rho, uint64_t dim, double* p, double* scratch, cudaStream_t s, int il = 0);

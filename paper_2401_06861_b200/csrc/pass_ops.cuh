@@ -78,6 +78,53 @@ __device__ __forceinline__ bool wait_at_least(const unsigned* p, unsigned want, 
         if (globaltimer_ns() - t0 > ns) return false;
     return true;
 }
+// Pusher role of a staged exchange pass (shard.cpp, jit.cpp): the last CTAs
+// of the (cooperatively launched, so co-resident) grid.  Chunk by chunk, once
+// this rank and the partner have stored every tile of the chunk (pass_done
+// counters; the partner's read over NVLink, so the partner has consumed its
+// own copy of those positions), the chunk's staging slot is copied into the
+// partner's state: slot index k expands to the physical index with the holes
+// re-inserted (Expand: generated per pass, the hole positions are constants;
+// the chunk's own bits and v come in through `fixed`), so consecutive k are
+// consecutive addresses on both sides.  Waits are bounded: a stall is
+// recorded in *err and reported by the host.
+template <int U, class Expand>
+__device__ __forceinline__ void stage_push_role(unsigned pid, unsigned npush, const double2* stage, double2* peer,
+                                                const unsigned* my_done, const unsigned* peer_done,
+                                                unsigned* push_done, unsigned* err, int chunks, int slots,
+                                                unsigned tpc, unsigned long long slot_elems,
+                                                unsigned long long watchdog_ns, Expand expand) {
+    const unsigned tid = threadIdx.x, nt = blockDim.x;
+    const unsigned long long stride = (unsigned long long)npush * nt;
+    for (int c = 0; c < chunks; ++c) {
+        if (tid == 0 && ld_acquire_u32(err) == 0u) {
+            if (!wait_at_least(my_done + c, tpc, watchdog_ns)) atomicMax(err, 0x10000u + unsigned(c));
+            else if (!wait_at_least(peer_done + c, tpc, watchdog_ns)) atomicMax(err, 0x20000u + unsigned(c));
+        }
+        __syncthreads();
+        const double2* src = stage + (unsigned long long)(c % slots) * slot_elems;
+        // U loads in flight per thread: the copy is bound by local-read
+        // latency x bytes in flight unless that exceeds what NVLink takes
+        for (unsigned long long k0 = (unsigned long long)pid * nt + tid; k0 < slot_elems; k0 += U * stride) {
+            double2 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const unsigned long long k = k0 + (unsigned long long)u * stride;
+                if (k < slot_elems) x[u] = ld_stream(src + k);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const unsigned long long k = k0 + (unsigned long long)u * stride;
+                if (k < slot_elems) st_stream(peer + expand(k, c), x[u]);
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence_system();
+            atomicAdd(push_done + c, 1u);
+        }
+    }
+}
 // Shared-memory load the compiler may not hoist: matrices are re-read (one
 // broadcast LDS per entry) instead of occupying registers.
 __device__ __forceinline__ double2 lds(const double2* p) {

@@ -145,15 +145,13 @@ struct ShardComm {
     // staged fused exchanges (no room for `alt`, e.g. 2^33 amplitudes per
     // GPU): a ring of `stage_slots` staging slots for the outgoing half,
     // per-chunk counters (pass_done[kMaxChunks], push_done[kMaxChunks]) mapped
-    // into the partner, and a side stream for the pusher kernel
+    // into the partner, and the pusher's descriptor
     static constexpr int kMaxChunks = 256;
     double2* stage = nullptr;
     uint64_t stage_slot_elems = 0;
-    int stage_slots = 2, stage_chunks = 0;
+    int stage_slots = 4, stage_chunks = 0;
     unsigned* sync = nullptr;
     std::vector<unsigned*> peer_sync;
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev_go = nullptr, ev_pushed = nullptr;
     int64_t staged = 0;
     std::unordered_map<uint64_t, std::vector<int>> rebalance_cache;  // see rebalance()
     // planned segments of recent flushes (repeated circuits replan nothing and
@@ -393,15 +391,17 @@ std::vector<unsigned char> segment_key(const PlanOptions& o, const std::vector<E
 
 void stream_barrier(ShardComm& sc, DeviceCtx& c);
 
-// A pass fused with an exchange when no second copy of the shard fits: the
-// pass (on the SMs the pusher leaves free) stores the kept half in place and
-// the outgoing half chunk by chunk into the staging ring; the pusher kernel
-// (side stream) copies each chunk into the partner's state as soon as both
-// ranks have stored that chunk, so NVLink traffic overlaps the pass.
+// A pass fused with an exchange when no second copy of the shard fits: one
+// cooperative grid whose pass CTAs store the kept half in place and the
+// outgoing half chunk by chunk into the staging ring, while its last CTAs
+// (the pusher) copy each chunk into the partner's state as soon as both
+// ranks have stored it -- NVLink traffic overlaps the pass.
 void launch_staged_exchange(State& s, DeviceCtx& c, const PassHdr& h, const MOp* mops, const cplx* pool,
                             const unsigned char* dev_rec, uint64_t rankbase, JitXStore xs, const FuseX& fx) {
     ShardComm& sc = *s.comm;
-    constexpr int kPushers = 16;  // SMs (one CTA each) driving the NVLink copies
+    // pusher CTAs appended to the pass grid (one co-resident cooperative
+    // launch): enough bytes in flight to keep NVLink busy
+    static const unsigned kPushers = unsigned(ab_knob("NQ_STAGE_PUSHERS", 224));
     const int chunks = sc.stage_chunks;
     int cb = 0;
     while ((1 << cb) < chunks) ++cb;
@@ -415,18 +415,14 @@ void launch_staged_exchange(State& s, DeviceCtx& c, const PassHdr& h, const MOp*
     xs.pass_done = sc.sync;
     xs.push_done = sc.sync + ShardComm::kMaxChunks;
     xs.pushers = kPushers;
-    xs.reserve_sms = kPushers;
+    xs.peer = sc.peer[size_t(fx.partner)];
+    xs.peer_done = sc.peer_sync[size_t(fx.partner)];
     if (xs.slot_elems != sc.stage_slot_elems) throw NqError{NQ_ERR_INTERNAL, "staged exchange: slot size mismatch"};
-    // pusher: holes = chunk bits (source: bit of the chunk number) and v
-    StagePush sp;
-    sp.chunks = chunks;
-    sp.slots = sc.stage_slots;
-    sp.tiles_per_chunk = unsigned(1u << cshift);
-    sp.slot_elems = xs.slot_elems;
-    sp.vval = fx.mybit;  // the partner's copy of this element has v = this rank's bit
-    sp.err_index = ShardComm::kMaxChunks;  // push_done[kMaxChunks] = sync[2 * kMaxChunks]
+    // pusher descriptor (sync words 598..647): [vval, nholes, pos[24], src[24]];
+    // holes = the chunk bits (source: a bit of the chunk number) and v, whose
+    // value on the partner's side is this rank's bit
+    unsigned desc[50] = {};
     {
-        // chunk number bit i = tile counter bit cshift + i -> physical position
         std::vector<std::pair<int, int>> holes;
         for (int i = 0; i < cb; ++i) {
             const int j = cshift + i;
@@ -434,33 +430,29 @@ void launch_staged_exchange(State& s, DeviceCtx& c, const PassHdr& h, const MOp*
         }
         holes.push_back({fx.v, -1});
         std::sort(holes.begin(), holes.end());
-        sp.nholes = int(holes.size());
+        desc[0] = unsigned(fx.mybit);
+        desc[1] = unsigned(holes.size());
         for (size_t k = 0; k < holes.size(); ++k) {
-            sp.hole_pos[k] = holes[k].first;
-            sp.hole_src[k] = holes[k].second;
+            desc[2 + k] = unsigned(holes[k].first);
+            desc[26 + k] = unsigned(holes[k].second);
         }
     }
     if (std::getenv("NQ_SHARD_TRACE")) {
         std::string hs;
-        for (int k = 0; k < sp.nholes; ++k) hs += " " + std::to_string(sp.hole_pos[k]) + ":" + std::to_string(sp.hole_src[k]);
+        for (unsigned k = 0; k < desc[1]; ++k) hs += " " + std::to_string(desc[2 + k]) + ":" + std::to_string(int(desc[26 + k]));
         std::fprintf(stderr, "[shard] rank %d staged exchange v=%d partner=%d m=%d nrest=%d ntiles=%lld cshift=%d "
                      "chunks=%d slot=%llu xrot=%d holes%s\n", s.rank, fx.v, fx.partner, h.m, h.nrest,
                      (long long)h.ntiles, cshift, chunks, (unsigned long long)xs.slot_elems, xs.xrot, hs.c_str());
     }
-    // kernel compiled before the ranks meet (a rank still compiling would
-    // stall its partner's pusher), counters zeroed on every rank before any
-    // rank's pusher reads them
+    // kernel compiled and loaded before the ranks meet (a rank still
+    // compiling would stall its partner), counters zeroed on every rank
+    // before any rank's pusher reads them
     jit_xstore_prepare(h, mops, pool, s.dev, &xs);
-    preload_stage_push();
-    CUDA_TRY(cudaMemsetAsync(sc.sync, 0, sizeof(unsigned) * (2 * ShardComm::kMaxChunks + 4), c.stream));
+    CUDA_TRY(cudaMemsetAsync(sc.sync, 0, sizeof(unsigned) * (2 * ShardComm::kMaxChunks + 16), c.stream));
+    CUDA_TRY(cudaMemcpyAsync(sc.sync + 598, desc, sizeof desc, cudaMemcpyHostToDevice, c.stream));
+    CUDA_TRY(cudaStreamSynchronize(c.stream));  // desc is a host stack array
     stream_barrier(sc, c);
-    CUDA_TRY(cudaEventRecord(sc.ev_go, c.stream));
-    CUDA_TRY(cudaStreamWaitEvent(sc.side, sc.ev_go, 0));
     jit_launch(s.d, dev_rec, h, mops, pool, rankbase, c.stream, s.dev, &xs);
-    launch_stage_push(sc.stage, sc.peer[size_t(fx.partner)], sc.sync, sc.peer_sync[size_t(fx.partner)],
-                      sc.sync + ShardComm::kMaxChunks, sp, kPushers, sc.side);
-    CUDA_TRY(cudaEventRecord(sc.ev_pushed, sc.side));
-    CUDA_TRY(cudaStreamWaitEvent(c.stream, sc.ev_pushed, 0));
     CUDA_TRY(cudaGetLastError());
 }
 
@@ -957,13 +949,8 @@ void free_staging(ShardComm& sc) {
     sc.peer_sync.clear();
     if (sc.stage) cudaFree(sc.stage);
     if (sc.sync) cudaFree(sc.sync);
-    if (sc.side) cudaStreamDestroy(sc.side);
-    if (sc.ev_go) cudaEventDestroy(sc.ev_go);
-    if (sc.ev_pushed) cudaEventDestroy(sc.ev_pushed);
     sc.stage = nullptr;
     sc.sync = nullptr;
-    sc.side = nullptr;
-    sc.ev_go = sc.ev_pushed = nullptr;
     sc.stage_chunks = 0;
 }
 
@@ -995,8 +982,8 @@ void setup_peer_exchange(State& s, ShardComm& sc, DeviceCtx& c) {
     }
     // staged fused exchanges when no second copy fits (or when forced by
     // NQ_FUSED_EXCHANGE=staged): 64 chunks (fewer for small shards: a chunk
-    // spans at least 2 tiles of the largest pass tile, 2^12), 2 slots of
-    // half a chunk each -- 2 GiB at 2^33 amplitudes per GPU
+    // spans at least 2 tiles of the largest pass tile, 2^12), 4 slots of
+    // half a chunk each -- 4 GiB at 2^33 amplitudes per GPU
     const std::string fxm = env_option_str("NQ_FUSED_EXCHANGE");
     const bool want_staged = fused_exchange_wanted() && (fxm == "staged" || !sc.alt);
     if (want_staged) {
@@ -1007,7 +994,8 @@ void setup_peer_exchange(State& s, ShardComm& sc, DeviceCtx& c) {
             cudaFree(sc.alt);
             sc.alt = nullptr;
         }
-        int chunks = 64;
+        sc.stage_slots = ab_knob("NQ_STAGE_SLOTS", 4);
+        int chunks = ab_knob("NQ_STAGE_CHUNKS", 64);
         while (chunks > 2 && (uint64_t(chunks) << 13) > s.count) chunks /= 2;
         sc.stage_chunks = chunks;
         sc.stage_slot_elems = s.count / 2 / uint64_t(chunks);
@@ -1018,10 +1006,7 @@ void setup_peer_exchange(State& s, ShardComm& sc, DeviceCtx& c) {
                   // others, and a peer's mapping of the handle then starts at
                   // that block's base, not at this buffer
                   cudaMalloc(reinterpret_cast<void**>(&sc.sync), size_t(2) << 20) == cudaSuccess &&
-                  cudaMemset(sc.sync, 0, sizeof(unsigned) * (2 * ShardComm::kMaxChunks + 4)) == cudaSuccess &&
-                  cudaStreamCreateWithFlags(&sc.side, cudaStreamNonBlocking) == cudaSuccess &&
-                  cudaEventCreateWithFlags(&sc.ev_go, cudaEventDisableTiming) == cudaSuccess &&
-                  cudaEventCreateWithFlags(&sc.ev_pushed, cudaEventDisableTiming) == cudaSuccess;
+                  cudaMemset(sc.sync, 0, sizeof(unsigned) * (2 * ShardComm::kMaxChunks + 16)) == cudaSuccess;
         cudaGetLastError();
         std::vector<double2*> ps = map_peers(s, reinterpret_cast<double2*>(sc.sync), ok);
         ok = !ps.empty();
