@@ -444,6 +444,8 @@ def dm_pass_roofline(run):
     call (a separate, profiled repetition: CUDA events around every pass).
     Algorithmic bytes per launch from the library: 32 * 4^n for a plain pass,
     24 * 4^n for a Hermitian mirror pass (reads the canonical half only)."""
+    from paper_2401_06861_b200 import abi
+
     abi.profile_begin(0, per_pass_events=True)
     run()
     p = abi.profile_end(0)

@@ -1085,6 +1085,21 @@ void shard_flush(State& s) {
         std::vector<Action> back = schedule_identity(sc.l2p, sc.p2l, s.nloc, s.n);
         acts.insert(acts.end(), back.begin(), back.end());
     }
+    // Tail exchange: a flush that repeats the previous one is predicted to be
+    // followed by itself.  If that next flush would open with an exchange (its
+    // first op needs a qubit this flush leaves global), the exchange runs now
+    // as this flush's last action, where it fuses into the final pass, instead
+    // of as a standalone swap at the start of the next flush (nothing precedes
+    // it there to fuse with).  The map is valid either way; only the moment
+    // of the swap moves.
+    if (repeat && !restore && !acts.empty() && acts.back().kind == Action::Segment && (sc.alt || sc.stage)) {
+        std::vector<int> l2 = sc.l2p, p2 = sc.p2l;
+        const std::vector<Action> nxt = schedule(ops, l2, p2, s.nloc, false);
+        if (!nxt.empty() && nxt.front().kind == Action::Exchange) {
+            acts.push_back(nxt.front());
+            swap_map(sc.l2p, sc.p2l, nxt.front().gbit, nxt.front().vbit);
+        }
+    }
     // Relabelling passes inside the segments: off unless NQ_SHARD_RELABEL=1.
     // Measured at N = 4 (random circuit, 2^30 per GPU): 9 instead of 10 passes
     // per step, but the composed qubit map keeps drifting for several flushes,

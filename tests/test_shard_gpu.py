@@ -121,3 +121,39 @@ def test_ranks_must_share_the_environment(tmp_path):
     for r in range(2):
         msg = (tmp_path / f"env{r}.txt").read_text()
         assert "different NQ_* options" in msg, msg
+
+
+def _repeat_rank(rank, world, uid, n, seed, outdir, fused):
+    os.environ["NQ_FUSED_EXCHANGE"] = fused
+    sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
+    from oracle import Port
+    from paper_2401_06861_b200 import abi as A
+
+    ops = Port().random_circuit(seed, n, 200)
+    sv = A.SV.sharded(n, rank, world, uid, device=rank)
+    for _ in range(4):  # the same circuit flushed again and again (benchmark / iterative shape)
+        sv.apply(ops)
+        sv.norm_sq()
+    stats = sv.comm_stats()
+    np.savez(os.path.join(outdir, f"rep{rank}.npz"), amps=sv.amplitudes(), exchanges=stats["exchanges"],
+             fused=stats["fused"])
+
+
+@pytest.mark.parametrize("n,world,fused", [(20, 2, "1"), (20, 2, "staged"), (22, 4, "staged"), (22, 4, "0")])
+def test_sharded_repeated_flushes(port, tmp_path, n, world, fused):
+    """Repeated flushes of one circuit carry the qubit map from flush to flush
+    and move the next flush's opening exchange to the end of the current one
+    (where it fuses into the last pass): the state after four repetitions
+    equals the oracle's."""
+    if abi.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    seed = 909 + n
+    uid = abi.comm_unique_id()
+    mp.start_processes(_repeat_rank, args=(world, uid, n, seed, str(tmp_path), fused), nprocs=world,
+                       start_method="spawn")
+    ops = port.random_circuit(seed, n, 200)
+    want = port.sv_run(n, np.concatenate([ops] * 4))
+    for r in range(world):
+        d = np.load(tmp_path / f"rep{r}.npz")
+        np.testing.assert_allclose(d["amps"], want, atol=1e-10, rtol=0)
+        assert int(d["exchanges"]) > 0
