@@ -73,7 +73,7 @@ def parse_args():
     ap.add_argument("--no-fresh", action="store_true", help="skip the e2e_fresh leg")
     ap.add_argument("--ref-chunk", type=int, default=12,
                     help="reference arm: ops per step (steps walk the circuit in chunks of this many ops)")
-    ap.add_argument("--single-thread-ops", type=int, default=8,
+    ap.add_argument("--single-thread-ops", type=int, default=50,
                     help="ops of the single-thread reference sample (proj/src/bench.cpp convention)")
     return ap.parse_args()
 

@@ -647,6 +647,9 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
     unsigned dirty = 0;
     if (use_px) s << "    unsigned px = 0u;\n";
     auto px_bit = [](int b) { return "((px >> " + std::to_string(b) + ") & 1u)"; };
+    // tile bits the pending permutation's conditions depend on (px varies
+    // across the threads that differ in them)
+    unsigned px_ctl = 0;
     auto commit = [&](unsigned mask) {
         const unsigned m = dirty & mask;
         for (int b = 0; b < 4; ++b)
@@ -760,10 +763,22 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
             const char* bar1 = "__syncthreads()";
             const char* bar2 = "__syncthreads()";
             s << "    " << bar1 << ";\n";
-            // (the pending permutation is XOR-ed into the store addresses: a
-            // quarter-warp may then hit colliding bank groups -- random-30
-            // pass 2: 71 M conflicts -- but committing it to the registers
-            // instead measured no faster: that pass is FP64-bound)
+            // A pending permutation that varies across the 8 lanes of a
+            // quarter-warp (its conditions read the layout's 3 lowest thread
+            // bits) scatters their 128-bit stores over colliding bank groups
+            // when XOR-ed into the addresses (VQE-28: 69 M / 136 M store
+            // conflicts in two passes, random-30 pass 2: 71 M).  Committing it
+            // to the registers first (predicated swaps) removes them (1.3 M /
+            // 4.2 M) but measured slower overall (VQE-28 13.10 -> 13.30 ms,
+            // random-30 43.88 -> 44.05 ms): those passes are bound by their
+            // relayout count and FP64 work, not by the conflicts.  A/B switch.
+            static const bool commit_lanes = ab_knob("NQ_PX_COMMIT_LANES", 0) != 0;
+            unsigned lanes8 = 0;
+            for (size_t t = 0; t < A.nonr.size() && t < 3; ++t) lanes8 |= 1u << A.nonr[t];
+            if (commit_lanes && use_px && dirty && (px_ctl & lanes8)) {
+                commit(dirty);
+                px_ctl = 0;
+            }
             if (use_px && dirty) {
                 s << "    {\n";
                 px_smem_xor(A);
@@ -771,6 +786,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
                     s << "    cur[sw" << (li - 1) << " ^ " << sw.apply(A.rconst(l)) << "u ^ kx] = a[" << l << "];\n";
                 s << "    }\n    px = 0u;\n";
                 dirty = 0;
+                px_ctl = 0;
             } else {
                 for (int l = 0; l < E; ++l)
                     s << "    cur[sw" << (li - 1) << " ^ " << sw.apply(A.rconst(l)) << "u] = a[" << l << "];\n";
@@ -916,6 +932,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
                 // controls outside the registers: record the X, move nothing
                 s << "    px ^= (" << cond << " ? 1u : 0u) << " << int(op.pos[0]) << ";\n";
                 dirty |= 1u << op.pos[0];
+                px_ctl |= cmT;
                 break;
             }
             const bool trivial = op.cmask_glob == 0 && cmT == 0;
@@ -998,22 +1015,22 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
                 for (int t = 0; t < 4; ++t)
                     if (((dirty & dslots) >> t) & 1u) gx << " | (" << px_bit(t) << " * " << slotc[t] << "u)";
                 s << "      const unsigned gx = " << gx.str() << ";\n";
-                std::map<unsigned, int> fidx;
-                std::ostringstream body;
+                // each distinct entry loaded right before the amplitudes it
+                // multiplies: one factor live at a time (preloading all 16
+                // next to the 16 amplitudes spilled registers)
+                std::map<unsigned, std::vector<int>> users;
                 for (int l = 0; l < E; ++l) {
                     unsigned c = 0;
                     for (int t = 0; t < 4; ++t)
                         if ((l >> t) & 1) c |= slotc[t];
-                    auto it = fidx.find(c);
-                    if (it == fidx.end()) {
-                        const int id = int(fidx.size());
-                        fidx[c] = id;
-                        s << "      const double2 f" << id << " = lds(D + (" << c << "u ^ gx));\n";
-                        it = fidx.find(c);
-                    }
-                    body << "      a[" << l << "] = cmul(f" << it->second << ", a[" << l << "]);\n";
+                    users[c].push_back(l);
                 }
-                s << body.str() << "    }\n";
+                for (const auto& [c, ls] : users) {
+                    s << "      { const double2 f = lds(D + (" << c << "u ^ gx));\n";
+                    for (int l : ls) s << "        a[" << l << "] = cmul(f, a[" << l << "]);\n";
+                    s << "      }\n";
+                }
+                s << "    }\n";
                 break;
             }
             if (!anyreg) {
@@ -1024,11 +1041,10 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
                 ug_pending = true;
             } else {
                 const unsigned regmask = slotc[0] | slotc[1] | slotc[2] | slotc[3];
-                // one shared-memory load per distinct table entry, then a plain
-                // complex multiply per amplitude (exact ones skipped at compile time)
-                std::map<unsigned, int> fidx;
-                std::ostringstream body;
-                std::vector<std::ostringstream> skip_body(16);
+                // one shared-memory load per distinct table entry, right before
+                // the complex multiplies of the amplitudes it scales (exact ones
+                // skipped at compile time); one factor live at a time
+                std::map<unsigned, std::vector<int>> users;
                 for (int l = 0; l < E; ++l) {
                     unsigned c = 0;
                     for (int t = 0; t < 4; ++t)
@@ -1038,26 +1054,18 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
                         if ((unsigned(gi) & regmask) != c) continue;
                         all_one = tab[gi] == cplx(1.0, 0.0);
                     }
-                    if (all_one) continue;
-                    auto it = fidx.find(c);
-                    if (it == fidx.end()) {
-                        const int id = int(fidx.size());
-                        fidx[c] = id;
-                        s << "      const double2 f" << id << " = lds(D + " << c << "u);\n";
-                        it = fidx.find(c);
-                    }
-                    skip_body[size_t(it->second)] << "      a[" << l << "] = cmul(f" << it->second << ", a[" << l << "]);\n";
-                    body << "      a[" << l << "] = cmul(f" << it->second << ", a[" << l << "]);\n";
+                    if (!all_one) users[c].push_back(l);
                 }
-                if (diag_runtime_skip()) {
-                    // factors that depend on thread / tile bits are often exactly 1
-                    // for a whole warp: test once per distinct factor
-                    for (size_t f = 0; f < fidx.size(); ++f)
-                        s << "      if (!is_one(f" << f << ")) {\n" << skip_body[f].str() << "      }\n";
-                    s << "    }\n";
-                } else {
-                    s << body.str() << "    }\n";
+                for (const auto& [c, ls] : users) {
+                    s << "      { const double2 f = lds(D + " << c << "u);\n";
+                    // factors that depend on thread / tile bits are often exactly
+                    // 1 for a whole warp: optionally tested once per factor
+                    if (diag_runtime_skip()) s << "        if (!is_one(f)) {\n";
+                    for (int l : ls) s << "        a[" << l << "] = cmul(f, a[" << l << "]);\n";
+                    if (diag_runtime_skip()) s << "        }\n";
+                    s << "      }\n";
                 }
+                s << "    }\n";
             }
             break;
         }
