@@ -666,15 +666,16 @@ def jit_stats() -> dict:
 
 
 def jit_debug(n: int, ops, pass_index: int, tile_qubits: int = 0, compile: bool = True, xstore: bool = False,
-              segment: bool = False, staged: str = ""):
+              segment: bool = False, staged: str = "", zterms: bool = False):
     """Generated source of one planned pass (and whether NVRTC compiles it):
     as a single-device state plans it, or as a sharded segment (`segment`:
     no relabelling stores); `xstore`: the exchange-store form; `staged`
-    ("rest" / "tile": where the exchanged bit lies): the staged form."""
+    ("rest" / "tile": where the exchanged bit lies): the staged form;
+    `zterms`: with a fused Z-term expectation epilogue."""
     arr = ops if isinstance(ops, np.ndarray) else make_ops(ops)
     size = C.c_int64()
     ok = C.c_int()
-    xs = (2 if xstore else 0) | (4 if segment else 0) | {"": 0, "rest": 8, "tile": 24}[staged]
+    xs = (2 if xstore else 0) | (4 if segment else 0) | {"": 0, "rest": 8, "tile": 24}[staged] | (32 if zterms else 0)
     check(lib.nq_jit_debug(n, arr.ctypes.data, len(arr), tile_qubits, pass_index, xs, None, 0, C.byref(size),
                            C.byref(ok)))
     buf = C.create_string_buffer(size.value + (1 << 16))

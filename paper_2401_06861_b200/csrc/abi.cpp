@@ -238,7 +238,7 @@ void trace_passes(const std::vector<PlannedPass>& passes, bool dm) {
 }
 
 void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStats& st, bool record = true,
-                JitMemo* memo = nullptr);
+                JitMemo* memo = nullptr, FlushEpilogue* fe = nullptr);
 bool layout_is_identity(const State& s);
 
 // Fused-schedule cache: a flush whose queue (kinds, bits, controls,
@@ -277,7 +277,17 @@ std::vector<unsigned char> plan_key(const State& s, bool use_layout) {
     return k;
 }
 
-void state_flush(State& s) {
+// logical sign masks -> physical bits of the state's current layout
+void epilogue_masks(const State& s, const FlushEpilogue& fe, uint64_t* out) {
+    for (int t = 0; t < fe.nterms; ++t) {
+        uint64_t g = 0;
+        for (int q = 0; q < s.n; ++q)
+            if ((fe.signs[t] >> q) & 1) g |= uint64_t(1) << (s.layout.empty() ? q : s.layout[size_t(q)]);
+        out[t] = g;
+    }
+}
+
+void state_flush(State& s, FlushEpilogue* fe) {
     if (s.queue.empty()) return;
     if (s.world > 1) {
         shard_flush(s);
@@ -306,7 +316,7 @@ void state_flush(State& s) {
     if (hit) {
         if (use_layout) s.layout = hit->layout_out;
         s.queue.clear();
-        run_passes(s, hit->passes, hit->st, true, hit->kern ? hit->kern->data() : nullptr);
+        run_passes(s, hit->passes, hit->st, true, hit->kern ? hit->kern->data() : nullptr, fe);
         return;
     }
     std::vector<PlannedPass> passes = plan_passes(s.queue, s.popt, &st, use_layout ? &s.layout : nullptr);
@@ -318,7 +328,7 @@ void state_flush(State& s) {
         cache.push_front(entry);
         if (cache.size() > kCacheEntries) cache.pop_back();
     }
-    run_passes(s, entry->passes, entry->st, true, kern->data());
+    run_passes(s, entry->passes, entry->st, true, kern->data(), fe);
 }
 
 bool layout_is_identity(const State& s) {
@@ -371,7 +381,7 @@ void state_flush_normal(State& s) {
 }
 
 void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStats& st, bool record,
-                JitMemo* memo) {
+                JitMemo* memo, FlushEpilogue* fe) {
     DeviceCtx& c = ctx_for(s.dev);
     CUDA_TRY(cudaSetDevice(s.dev));
     std::vector<size_t> offs;
@@ -393,7 +403,24 @@ void run_passes(State& s, const std::vector<PlannedPass>& passes, const PlanStat
         std::pair<cudaEvent_t, cudaEvent_t>* ev = c.prof_pass ? prof_slot(c) : nullptr;
         if (ev) CUDA_TRY(cudaEventRecord(ev->first, c.stream));
         const unsigned char* rec = buf.data() + offs[i];
-        if (!jit_launch(s.d, c.d_ops + offs[i], h, reinterpret_cast<const MOp*>(rec + h.op_off),
+        // the flush's last pass may carry Z-type expectation terms (the
+        // layout is already the post-flush one: masks in its physical bits)
+        JitEpilogue epi;
+        JitEpilogue* ep = nullptr;
+        if (fe && fe->nterms > 0 && fe->nterms <= 8 && i + 1 == passes.size() && !s.dm) {
+            epi.nterms = fe->nterms;
+            epilogue_masks(s, *fe, epi.signs);
+            c.ensure_scratch(size_t(4096) * kMaxExpTerms + 64);
+            epi.part = c.d_scratch + 64;
+            ep = &epi;
+        }
+        if (ep && jit_launch(s.d, c.d_ops + offs[i], h, reinterpret_cast<const MOp*>(rec + h.op_off),
+                             reinterpret_cast<const cplx*>(rec + h.pool_off), 0, c.stream, s.dev, nullptr, nullptr,
+                             ep)) {
+            launch_expect_final(epi.part, epi.grid, epi.nterms, c.d_scratch, c.stream);
+            fe->fused = true;
+            fe->dev_sums = c.d_scratch;
+        } else if (!jit_launch(s.d, c.d_ops + offs[i], h, reinterpret_cast<const MOp*>(rec + h.op_off),
                         reinterpret_cast<const cplx*>(rec + h.pool_off), 0, c.stream, s.dev, nullptr,
                         memo ? memo + i : nullptr))
             launch_pass(s.d, c.d_ops + offs[i], h, 0, c.stream,
@@ -623,7 +650,23 @@ nq_status nq_sv_expectation_batch(nq_sv* h, const uint64_t* flip, const uint64_t
         for (int t = 0; t < nterms; ++t)
             if ((flip[t] & ~lim) || (signs[t] & ~lim))
                 throw NqError{NQ_ERR_CONTRACT, "Pauli mask exceeds the state's qubit count"};
-        state_flush(s);
+        // a pending flush whose result is read only as Z-type terms computes
+        // them in its last pass (one state read saved)
+        bool diag_only = nterms >= 1 && nterms <= 8 && s.world == 1 && !s.dm && !s.queue.empty();
+        for (int t = 0; t < nterms && diag_only; ++t) diag_only = flip[t] == 0;
+        FlushEpilogue fe;
+        if (diag_only) {
+            fe.nterms = nterms;
+            fe.signs = signs;
+        }
+        state_flush(s, diag_only ? &fe : nullptr);
+        if (fe.fused) {
+            DeviceCtx& c = ctx_for(s.dev);
+            std::vector<double> sums(static_cast<size_t>(nterms));
+            fetch(c, fe.dev_sums, size_t(nterms), sums.data());
+            for (int t = 0; t < nterms; ++t) out[t] = coeff[t] * (cplx(sums[size_t(t)], 0.0) * kIPow[ny[t] & 3]).real();
+            return;
+        }
         if (s.world > 1) {
             shard_expectation(s, flip, signs, ny, coeff, nterms, out);
             return;
@@ -1400,9 +1443,16 @@ nq_status nq_jit_debug(int n, const nq_op* ops, int64_t count, int tile_qubits, 
             xs.chunk_bits = jit_stage_chunk_bits(h, xs.xrot, xs.cshift);
             xs.pushers = 16;
         }
+        // compile & 32: with a fused Z-term epilogue (Z on physical bits 0,
+        // n-1 and 0+1)
+        JitEpilogue epi;
+        epi.nterms = 3;
+        epi.signs[0] = 1;
+        epi.signs[1] = uint64_t(1) << (n - 1);
+        epi.signs[2] = 3;
         std::string src = jit_source(h, reinterpret_cast<const MOp*>(rec + h.op_off),
                                      reinterpret_cast<const cplx*>(rec + h.pool_off), (compile & 10) != 0,
-                                     (compile & 8) ? &xs : nullptr);
+                                     (compile & 8) ? &xs : nullptr, (compile & 32) ? &epi : nullptr);
         std::string log;
         if (compiled_ok) *compiled_ok = (compile & 1) ? int(jit_compile_only(src, &log)) : -1;
         if (!log.empty()) src += "\n/* NVRTC LOG\n" + log + "\n*/\n";

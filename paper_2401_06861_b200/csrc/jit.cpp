@@ -413,7 +413,9 @@ uint64_t jit_stage_chunk_bits(const PassHdr& h, int xrot, int cshift) {
     return bits;
 }
 
-std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool xstore, const JitXStore* stage) {
+std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool xstore, const JitXStore* stage,
+                       const JitEpilogue* epi) {
+    const int nep = (epi && !xstore && !(h.flags & PASS_MIRROR)) ? epi->nterms : 0;
     const bool staged = xstore && stage && stage->staged;
     // staged exchange: compressed position of physical bit p in a staging
     // slot (-1: a removed bit -- a chunk bit or the exchanged bit v)
@@ -522,7 +524,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
          " long long ntiles, double2* xout_l, double2* xout_r, unsigned long long xmask, unsigned long long xval,"
          " int xrot" << (staged ? ", unsigned* pdone, const unsigned* qdone, unsigned long long slot_elems,"
                                   " double2* xpeer, const unsigned* xpeer_done, unsigned npass" : "")
-      << ") {\n"
+      << (nep ? ", double* __restrict__ epart" : "") << ") {\n"
       << "  using namespace nq;\n"
       << "  extern __shared__ __align__(16) unsigned char smem[];\n"
       << "  double2* buf0 = reinterpret_cast<double2*>(smem);\n"
@@ -585,6 +587,7 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
         s << "  __syncthreads();\n";
         if (staged)
             s << "  unsigned ck_cur = 0xffffffffu, ck_n = 0u;  // chunk of the tiles in flight, tiles stored in it\n";
+        for (int k = 0; k < nep; ++k) s << "  double ep" << k << " = 0.0;  // fused <Z> term " << k << "\n";
         s << "  for (long long r = blockIdx.x; r < ntiles; r += " << (staged ? "npass" : "gridDim.x") << ") {\n";
         if (staged) {
             // entering a new chunk: publish the tiles stored in the previous
@@ -1162,6 +1165,26 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
                   << (l | (1 << j0)) << "]);\n";
         }
         s << "    }\n";
+        if (nep) {
+            // fused Z-type terms: the sign of amplitude l is the parity of its
+            // store index under the term's mask = a per-thread part (tile and
+            // rest bits, pending permutation) x a compile-time part (register l)
+            s << "    { const unsigned long long oe = (base + toff_st)" << (use_px && dirty ? " ^ pxo" : "") << ";\n";
+            for (int l = 0; l < E; ++l)
+                s << "      const double p" << l << " = fma(a[" << l << "].x, a[" << l << "].x, a[" << l << "].y * a[" << l
+                  << "].y);\n";
+            for (int k = 0; k < nep; ++k) {
+                const uint64_t M = epi->signs[k];
+                std::ostringstream pos, neg;
+                pos << "0.0";
+                neg << "0.0";
+                for (int l = 0; l < E; ++l)
+                    ((__builtin_popcountll(reg_off(LST, l, qst) & M) & 1) ? neg : pos) << " + p" << l;
+                s << "      { const double d = (" << pos.str() << ") - (" << neg.str() << ");\n"
+                  << "        ep" << k << " += (__popcll(oe & " << hex64(M) << ") & 1) ? -d : d; }\n";
+            }
+            s << "    }\n";
+        }
     }
     if (mirror) {
         // the mirror tile holds the conjugate transpose: element e of tile r is
@@ -1178,6 +1201,22 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
     if (staged) s << "    ++ck_n;\n";
     s << "  }\n";
     if (staged) s << "  if (ck_n) { __threadfence(); __syncthreads(); if (tid == 0) atomicAdd(pdone + ck_cur, ck_n); }\n";
+    if (nep) {
+        // fixed-order CTA reduction of the fused terms: warp shuffles, then
+        // warp 0 sums the warps' values in order (buf0 is free after the loop)
+        s << "  {\n"
+          << "    double* red = reinterpret_cast<double*>(buf0);\n";
+        for (int k = 0; k < nep; ++k)
+            s << "    for (int o = 16; o > 0; o >>= 1) ep" << k << " += __shfl_down_sync(0xffffffffu, ep" << k << ", o);\n"
+              << "    if ((tid & 31u) == 0u) red[" << k << " * " << (T / 32) << " + (tid >> 5)] = ep" << k << ";\n";
+        s << "    __syncthreads();\n"
+          << "    if (tid < " << nep << "u) {\n"
+          << "      double t = 0.0;\n"
+          << "      for (int w = 0; w < " << (T / 32) << "; ++w) t += red[tid * " << (T / 32) << " + w];\n"
+          << "      epart[(unsigned long long)blockIdx.x * " << kMaxExpTerms << " + tid] = t;\n"
+          << "    }\n"
+          << "  }\n";
+    }
     s << "}\n";
     return s.str();
 }
@@ -1415,10 +1454,11 @@ void jit_xstore_prepare(const PassHdr& h, const MOp* ops, const cplx* pool, int 
 }
 
 bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,
-                uint64_t rankbase, cudaStream_t s, int device, const JitXStore* xs, JitMemo* memo) {
+                uint64_t rankbase, cudaStream_t s, int device, const JitXStore* xs, JitMemo* memo, JitEpilogue* epi) {
+    if (epi && (xs || (h.flags & PASS_MIRROR) || epi->nterms < 1)) epi = nullptr;
     const JitMode mode = jit_mode();
     std::shared_ptr<Entry> e;
-    if (memo && !xs) {
+    if (memo && !xs && !epi) {
         std::lock_guard<std::mutex> lk(memo->mu);
         e = std::static_pointer_cast<Entry>(memo->entry);
     }
@@ -1442,8 +1482,8 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
     } else {
         if (mode == JitMode::Off || h.m < 8 || h.m > 12) return false;
         if (mode == JitMode::Auto && h.nloc < 18) return false;  // interpreter is fine for small states
-        e = acquire(jit_source(h, ops, pool), device, mode);
-        if (e && memo && e->state.load() == 1) {
+        e = acquire(jit_source(h, ops, pool, false, nullptr, epi), device, mode);
+        if (e && memo && !epi && e->state.load() == 1) {
             std::lock_guard<std::mutex> lk(memo->mu);
             memo->entry = e;
         }
@@ -1474,8 +1514,12 @@ bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, 
     unsigned* pdone = xs ? xs->pass_done : nullptr;
     const unsigned* qdone = xs ? xs->push_done : nullptr;
     unsigned long long slot_elems = xs ? xs->slot_elems : 0ull;
-    void* args[] = {&state, &gpool, &rb, &nt, &xl, &xr, &xm, &xv, &xrot, &pdone, &qdone, &slot_elems, &xpeer, &xpeer_done,
-                    &npass};
+    double* epart = epi ? epi->part : nullptr;
+    void* args_ep[] = {&state, &gpool, &rb, &nt, &xl, &xr, &xm, &xv, &xrot, &epart};
+    void* args_x[] = {&state, &gpool, &rb, &nt, &xl, &xr, &xm, &xv, &xrot, &pdone, &qdone, &slot_elems, &xpeer,
+                      &xpeer_done, &npass};
+    void** args = epi ? args_ep : args_x;
+    if (epi) epi->grid = int(grid);
     const cudaError_t lrc =
         staged ? cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(e->kern), dim3(unsigned(grid)),
                                              dim3(unsigned(T)), args, smem, s)

@@ -29,8 +29,19 @@ JitMode jit_mode();
 // CUDA source of the kernel specialised to one pass record.  xstore: the
 // exchange-store variant (sharded states, see JitXStore).
 struct JitXStore;
+// Diagonal (Z-type) expectation terms fused into a pass's stores (the last
+// pass of a flush whose result is read as <Z...> terms): the sum over the
+// pass's output of |a|^2 (-1)^popcount(o & signs[k]), o the physical index an
+// amplitude is stored to; one partial per CTA at part[b * kMaxExpTerms + k]
+// (fixed order: the sum is deterministic), `grid` set by the launch.
+struct JitEpilogue {
+    int nterms = 0;
+    uint64_t signs[8] = {};
+    double* part = nullptr;
+    int grid = 0;
+};
 std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool xstore = false,
-                       const JitXStore* stage = nullptr);
+                       const JitXStore* stage = nullptr, const JitEpilogue* epi = nullptr);
 
 // A pass fused with a global<->local qubit exchange (shard.cpp): the pass
 // reads the state in place and writes out of place; element o of its output
@@ -86,7 +97,7 @@ struct JitMemo {
 };
 bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,
                 uint64_t rankbase, cudaStream_t s, int device, const JitXStore* xs = nullptr,
-                JitMemo* memo = nullptr);
+                JitMemo* memo = nullptr, JitEpilogue* epi = nullptr);
 
 // Expectation batch kernel specialised to the batch's term structure: source,
 // and launch (plus the per-term final sums into out[0..nt)); false when the

@@ -107,7 +107,17 @@ void sv_expect_raw(State& s, const uint64_t* flip, const uint64_t* signs, int nt
 
 void state_init(State& s, int n, bool dm, const nq_opts* opts);
 void state_free(State& s);
-void state_flush(State& s);
+// Z-type expectation terms a flush may compute in its last pass (fused
+// epilogue): signs in logical qubits in, per-term sums on the device out
+// (fused = false when the last pass could not carry them, e.g. its kernel is
+// not compiled yet: the caller then reads the state separately)
+struct FlushEpilogue {
+    int nterms = 0;
+    const uint64_t* signs = nullptr;
+    bool fused = false;
+    double* dev_sums = nullptr;
+};
+void state_flush(State& s, FlushEpilogue* fe = nullptr);
 // flush, then restore the identity layout (amplitude-order readouts)
 void state_flush_normal(State& s);
 void configure_caps(PlanOptions& p);

@@ -95,3 +95,48 @@ def test_specialised_kernels_match_oracle(px):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
     assert "WORST" in r.stdout
+
+
+FUSED_Z = textwrap.dedent(
+    """
+    import sys
+    sys.path[:0] = [{root!r}, {oracle!r}]
+    import numpy as np
+    from oracle import Port
+    from paper_2401_06861_b200 import abi
+    port = Port()
+    worst = 0.0
+    for n, seed in [(19, 3), (20, 8), (22, 13)]:
+        ops = port.random_circuit(seed, n, 150)
+        terms = [("Z" + "I" * (n - 1), 1.0), ("I" * (n - 1) + "Z", -0.5),
+                 ("ZZ" + "I" * (n - 3) + "Z", 0.25), ("I" * 5 + "Z" + "I" * (n - 6), 2.0)]
+        sv = abi.SV(n)
+        for rep in range(3):  # the repeated circuit: carried layout, cached plan
+            abi.profile_begin(0, per_pass_events=False)
+            sv.apply(ops)
+            fused = sv.expectations(terms)  # flush + terms in its last pass
+            prof = abi.profile_end(0)
+            passes = sv.stats()["launches"]
+            assert prof["kernel_launches"] == passes + 1, (prof, passes)  # passes + the final fixed-order sum
+            again = sv.expectations(terms)  # nothing queued: the standalone reduction
+            amps = sv.amplitudes()
+            for (letters, coeff), g, h in zip(terms, fused, again):
+                ref = port.expectation(amps, letters, coeff)
+                worst = max(worst, abs(g - ref), abs(h - ref))
+        sv.close()
+    print("WORST", worst)
+    assert worst <= 1e-10, worst
+    """
+)
+
+
+def test_z_terms_fused_into_the_last_pass():
+    """A flush whose result is read as Z-type terms computes them in the
+    epilogue of its last pass (one state read saved; the e2e benchmark's
+    <Z0>): same values as the standalone reduction and the oracle, and no
+    separate reduction kernel (launches = passes + 1 fixed-order final sum)."""
+    env = dict(os.environ, NQ_JIT="sync")
+    code = FUSED_Z.format(root=ROOT, oracle=os.path.join(ROOT, "oracle"))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
+    assert "WORST" in r.stdout
