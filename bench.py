@@ -73,6 +73,7 @@ def parse_args():
     ap.add_argument("--no-fresh", action="store_true", help="skip the e2e_fresh leg")
     ap.add_argument("--ref-chunk", type=int, default=12,
                     help="reference arm: ops per step (steps walk the circuit in chunks of this many ops)")
+    ap.add_argument("--c1-sweep-only", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--single-thread-ops", type=int, default=50,
                     help="ops of the single-thread reference sample (proj/src/bench.cpp convention)")
     return ap.parse_args()
@@ -638,7 +639,7 @@ def secondary_workloads(abi, workloads, device, args):
     # f1: batched Monte-Carlo trajectories (one launch) vs the reference's
     # sequential loop (acceptance 5 shape, and a 10-qubit noisy TFIM)
     out["trajectories"] = trajectory_workloads(workloads)
-    out["tfim4_sweep"] = tfim4_sweep(workloads)
+    out["tfim4_sweep"] = tfim4_sweep_isolated()
     return out
 
 
@@ -680,6 +681,18 @@ def tfim4_sweep(workloads):
                     "max_abs_diff_vs_cpu": float(max(np.max(np.abs(rows[:, 1] - ideal)),
                                                      np.max(np.abs(rows[:, 2] - noisy))))})
     return res
+
+
+def tfim4_sweep_isolated():
+    """tfim4_sweep in a fresh process: its host side (60 k gate records built
+    through the Python API) measured 4-6x slower inside the benchmark process
+    after the 16 GiB workloads than in a clean one (0.11 s)."""
+    try:
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--c1-sweep-only"], capture_output=True,
+                           text=True, timeout=600)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001 - reported, not fatal
+        return {"error": repr(e)}
 
 
 def trajectory_workloads(workloads):
@@ -754,6 +767,11 @@ def fresh_e2e(abi, sv, workloads, n, depth, seed, steps, term):
 
 def main():
     args = parse_args()
+    if args.c1_sweep_only:
+        from paper_2401_06861_b200 import workloads
+
+        print(json.dumps(tfim4_sweep(workloads)), flush=True)
+        return 0
     maybe_self_launch(args)
     claim_stdout()
     if args.impl == "reference":

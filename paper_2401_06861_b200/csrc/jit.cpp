@@ -1439,18 +1439,22 @@ bool jit_xstore_ok(const PassHdr& h, const MOp* ops) {
     return true;
 }
 
-void jit_xstore_prepare(const PassHdr& h, const MOp* ops, const cplx* pool, int device, const JitXStore* xs) {
+int jit_xstore_prepare(const PassHdr& h, const MOp* ops, const cplx* pool, int device, const JitXStore* xs) {
     if (!jit_xstore_ok(h, ops)) throw NqError{NQ_ERR_INTERNAL, "exchange pass cannot be specialised"};
     std::shared_ptr<Entry> e = acquire(jit_source(h, ops, pool, true, xs), device, JitMode::Sync);
+    if (!e) throw NqError{NQ_ERR_INTERNAL, "exchange pass kernel failed to compile"};
     // load it into this device's context now: with lazy loading, a first
     // launch next to a kernel that spins on it (the staged pusher) could wait
     // for that kernel to finish -- a deadlock
-    if (e) {
-        cudaFuncAttributes fa;
-        cudaSetDevice(device);
-        cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(e->kern));
-        cudaGetLastError();
-    }
+    cudaFuncAttributes fa;
+    cudaSetDevice(device);
+    cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(e->kern));
+    cudaGetLastError();
+    const int T = (1 << h.m) / (1 << ops[0].k);
+    const size_t smem = (size_t(1) << h.m) * 16 + size_t(h.pool_n) * 16;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    return sms * occupancy(*e, device, T, smem);
 }
 
 bool jit_launch(double2* state, const unsigned char* dev_rec, const PassHdr& h, const MOp* ops, const cplx* pool,

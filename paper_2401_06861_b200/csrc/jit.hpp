@@ -77,8 +77,9 @@ struct JitXStore {
 // positions the top (nrest - cshift) bits of the rotated tile counter drive.
 uint64_t jit_stage_chunk_bits(const PassHdr& h, int xrot, int cshift);
 // Compile (synchronously) the exchange-store kernel of a pass ahead of its
-// launch, so that ranks meet at the exchange with their kernels ready.
-void jit_xstore_prepare(const PassHdr& h, const MOp* ops, const cplx* pool, int device, const JitXStore* xs);
+// launch, so that ranks meet at the exchange with their kernels ready; the
+// number of its CTAs that can be co-resident on the device.
+int jit_xstore_prepare(const PassHdr& h, const MOp* ops, const cplx* pool, int device, const JitXStore* xs);
 // Whether a pass can run as an exchange-store kernel (deterministic: every
 // rank decides alike from the same pass record).
 bool jit_xstore_ok(const PassHdr& h, const MOp* ops);

@@ -396,7 +396,7 @@ void stream_barrier(ShardComm& sc, DeviceCtx& c);
 // outgoing half chunk by chunk into the staging ring, while its last CTAs
 // (the pusher) copy each chunk into the partner's state as soon as both
 // ranks have stored it -- NVLink traffic overlaps the pass.
-void launch_staged_exchange(State& s, DeviceCtx& c, const PassHdr& h, const MOp* mops, const cplx* pool,
+bool launch_staged_exchange(State& s, DeviceCtx& c, const PassHdr& h, const MOp* mops, const cplx* pool,
                             const unsigned char* dev_rec, uint64_t rankbase, JitXStore xs, const FuseX& fx) {
     ShardComm& sc = *s.comm;
     // pusher CTAs appended to the pass grid (one co-resident cooperative
@@ -447,13 +447,16 @@ void launch_staged_exchange(State& s, DeviceCtx& c, const PassHdr& h, const MOp*
     // kernel compiled and loaded before the ranks meet (a rank still
     // compiling would stall its partner), counters zeroed on every rank
     // before any rank's pusher reads them
-    jit_xstore_prepare(h, mops, pool, s.dev, &xs);
+    // the grid (pass CTAs + pushers) must be co-resident with room for the
+    // pass: every rank decides alike (same pass, same device type)
+    if (jit_xstore_prepare(h, mops, pool, s.dev, &xs) < int(kPushers) + 148) return false;
     CUDA_TRY(cudaMemsetAsync(sc.sync, 0, sizeof(unsigned) * (2 * ShardComm::kMaxChunks + 16), c.stream));
     CUDA_TRY(cudaMemcpyAsync(sc.sync + 598, desc, sizeof desc, cudaMemcpyHostToDevice, c.stream));
     CUDA_TRY(cudaStreamSynchronize(c.stream));  // desc is a host stack array
     stream_barrier(sc, c);
     jit_launch(s.d, dev_rec, h, mops, pool, rankbase, c.stream, s.dev, &xs);
     CUDA_TRY(cudaGetLastError());
+    return true;
 }
 
 void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vector<int>* layout = nullptr,
@@ -517,13 +520,17 @@ void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vecto
             xs.xval = fx->mybit << fx->v;
             xs.xrot = rest_pos(h, fx->v);
             if (fx->staged) {
-                launch_staged_exchange(s, c, h, mops, reinterpret_cast<const cplx*>(rec + h.pool_off), c.d_ops + offs[i],
-                                       rankbase, xs, *fx);
+                fx->done = launch_staged_exchange(s, c, h, mops, reinterpret_cast<const cplx*>(rec + h.pool_off),
+                                                  c.d_ops + offs[i], rankbase, xs, *fx);
+                if (!fx->done && !jit_launch(s.d, c.d_ops + offs[i], h, mops,
+                                             reinterpret_cast<const cplx*>(rec + h.pool_off), rankbase, c.stream,
+                                             s.dev, nullptr, kern ? kern->data() + i : nullptr))
+                    launch_pass(s.d, c.d_ops + offs[i], h, rankbase, c.stream, mops[0].k);
             } else {
                 jit_launch(s.d, c.d_ops + offs[i], h, mops, reinterpret_cast<const cplx*>(rec + h.pool_off), rankbase,
                            c.stream, s.dev, &xs);
+                fx->done = true;
             }
-            fx->done = true;
         } else if (!jit_launch(s.d, c.d_ops + offs[i], h, mops,
                         reinterpret_cast<const cplx*>(rec + h.pool_off), rankbase, c.stream, s.dev, nullptr,
                         kern ? kern->data() + i : nullptr))
