@@ -1204,15 +1204,20 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
     if (nep) {
         // fixed-order CTA reduction of the fused terms: warp shuffles, then
         // warp 0 sums the warps' values in order (buf0 is free after the loop)
+        // (a CTA narrower than a warp -- small tiles -- is one partial warp)
+        const int WL = std::min(32, T), NW = std::max(1, T / 32);
+        const std::string wmask = T >= 32 ? "0xffffffffu" : std::to_string((1u << T) - 1u) + "u";
         s << "  {\n"
           << "    double* red = reinterpret_cast<double*>(buf0);\n";
         for (int k = 0; k < nep; ++k)
-            s << "    for (int o = 16; o > 0; o >>= 1) ep" << k << " += __shfl_down_sync(0xffffffffu, ep" << k << ", o);\n"
-              << "    if ((tid & 31u) == 0u) red[" << k << " * " << (T / 32) << " + (tid >> 5)] = ep" << k << ";\n";
+            s << "    for (int o = " << WL / 2 << "; o > 0; o >>= 1) ep" << k << " += __shfl_down_sync(" << wmask << ", ep"
+              << k << ", o);\n"
+              << "    if ((tid & " << (WL - 1) << "u) == 0u) red[" << k << " * " << NW << " + tid / " << WL << "u] = ep" << k
+              << ";\n";
         s << "    __syncthreads();\n"
           << "    if (tid < " << nep << "u) {\n"
           << "      double t = 0.0;\n"
-          << "      for (int w = 0; w < " << (T / 32) << "; ++w) t += red[tid * " << (T / 32) << " + w];\n"
+          << "      for (int w = 0; w < " << NW << "; ++w) t += red[tid * " << NW << " + w];\n"
           << "      epart[(unsigned long long)blockIdx.x * " << kMaxExpTerms << " + tid] = t;\n"
           << "    }\n"
           << "  }\n";

@@ -29,10 +29,12 @@ _CACHE = os.path.join(tempfile.gettempdir(), "nq_jit_emu")
 SANITIZE = os.environ.get("NQ_EMU_SANITIZE", "")
 
 
-def sources(n: int, ops: np.ndarray, tile: int, count: int):
+def sources(n: int, ops: np.ndarray, tile: int, count: int, zterms: bool = False):
+    """Generated pass sources; with `zterms` the last one carries the fused
+    Z-term epilogue of jit_debug (physical masks: bit 0, bit n-1, bits 0+1)."""
     out = []
     for i in range(count):
-        src, _ = abi.jit_debug(n, ops, i, tile_qubits=tile, compile=False)
+        src, _ = abi.jit_debug(n, ops, i, tile_qubits=tile, compile=False, zterms=zterms and i == count - 1)
         out.append(src.split("/* NVRTC LOG")[0])
     return out
 
@@ -43,7 +45,15 @@ def build(srcs) -> C.CDLL:
     for i, s in enumerate(srcs):
         s = s.replace('#include "pass_ops.cuh"', "")
         s = s.replace("extern __shared__ __align__(16) unsigned char smem[];", "unsigned char* const smem = emu_smem;")
-        s = re.sub(r"\bnqjit\(", f"nqjit_{i}(", s, count=1)
+        if "double* __restrict__ epart" in s:
+            # epilogue kernel: called through a wrapper with the emulator's
+            # partial-sum buffer as its extra parameter
+            s = re.sub(r"\bnqjit\(", f"nqjit_{i}_ep(", s, count=1)
+            s += (f"\nvoid nqjit_{i}(double2* st, const double2* gp, unsigned long long rb, long long nt, double2* xl,"
+                  f" double2* xr, unsigned long long xm, unsigned long long xv, int xrot) {{"
+                  f" nqjit_{i}_ep(st, gp, rb, nt, xl, xr, xm, xv, xrot, emu_epart); }}\n")
+        else:
+            s = re.sub(r"\bnqjit\(", f"nqjit_{i}(", s, count=1)
         body.append(s)
     body.append("emu_kernel emu_table[] = {" + ", ".join(f"nqjit_{i}" for i in range(len(srcs))) + "};\n")
     code = "\n".join(body)
@@ -60,18 +70,23 @@ def build(srcs) -> C.CDLL:
         os.replace(so + ".tmp", so)
     lib = C.CDLL(so)
     lib.emu_run.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int, C.c_longlong]
+    lib.emu_set_epart.argtypes = [C.c_void_p]
     return lib
 
 
-def run(n: int, ops, tile: int, state: np.ndarray | None = None) -> np.ndarray:
+def run(n: int, ops, tile: int, state: np.ndarray | None = None, zterms: bool = False):
     """Apply `ops` (nq_op records or tuples) to `state` (default |0..0>) by
     emulating the generated kernel of every planned pass; returns the state in
-    logical (reference) order."""
+    logical (reference) order.  With `zterms` the last pass also runs the
+    fused Z-term epilogue (physical masks bit 0, bit n-1, bits 0+1) and the
+    result is (state, epilogue sums, final physical-order state)."""
     arr = ops if isinstance(ops, np.ndarray) else abi.make_ops(ops)
     passes = plan_format.decode(abi.plan_debug(n, arr, tile_qubits=tile, relabel=True))
-    srcs = sources(n, arr, tile, len(passes))
+    srcs = sources(n, arr, tile, len(passes), zterms=zterms)
     assert len(srcs) == len(passes), (len(srcs), len(passes))
     lib = build(srcs)
+    part = np.zeros(64, dtype=np.float64)
+    lib.emu_set_epart(part.ctypes.data)
     st = np.zeros(1 << n, dtype=np.complex128) if state is None else np.array(state, dtype=np.complex128)
     if state is None:
         st[0] = 1.0
@@ -90,4 +105,6 @@ def run(n: int, ops, tile: int, state: np.ndarray | None = None) -> np.ndarray:
     phys = np.zeros_like(idx)
     for x in range(n):
         phys |= ((idx >> x) & 1) << l2p[x]
+    if zterms:
+        return st[phys], part[:3].copy(), st
     return st[phys]

@@ -16,6 +16,10 @@ std::barrier<>* emu_barrier = nullptr;
 // the CTA's dynamic shared memory, allocated per launch at exactly the size
 // the launch would request (so an address sanitizer build sees overruns)
 unsigned char* emu_smem = nullptr;
+double emu_shfl[1024];
+// partial sums of a fused-expectation epilogue (tests/jit_emu.py run(zterms=...))
+double* emu_epart = nullptr;
+extern "C" void emu_set_epart(double* p) { emu_epart = p; }
 
 typedef void (*emu_kernel)(double2*, const double2*, unsigned long long, long long, double2*, double2*,
                            unsigned long long, unsigned long long, int);

@@ -31,3 +31,17 @@ extern EmuDim gridDim;
 extern EmuDim blockDim;
 extern std::barrier<>* emu_barrier;
 inline void __syncthreads() { emu_barrier->arrive_and_wait(); }
+inline int __popcll(unsigned long long v) { return __builtin_popcountll(v); }
+
+// Warp shuffles for the fused-expectation epilogue: every thread of the CTA
+// calls them uniformly there, so a CTA-wide exchange through a shared array
+// (two barriers) emulates the warp-synchronous shuffle.
+extern double emu_shfl[1024];
+inline double __shfl_down_sync(unsigned, double v, int o) {
+    const unsigned t = threadIdx.x;
+    emu_shfl[t] = v;
+    __syncthreads();
+    const double r = ((t & 31u) + unsigned(o) < 32u && t + unsigned(o) < blockDim.x) ? emu_shfl[t + unsigned(o)] : v;
+    __syncthreads();
+    return r;
+}

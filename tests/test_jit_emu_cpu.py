@@ -119,3 +119,19 @@ def test_generated_kernels_under_sanitizers(sanitizer):
     out = r.stdout + r.stderr
     assert r.returncode == 0 and "EMU_OK" in out, out[-6000:]
     assert "ERROR: AddressSanitizer" not in out and "WARNING: ThreadSanitizer" not in out, out[-6000:]
+
+
+@pytest.mark.parametrize("n,tile,seed", [(12, 8, 21), (13, 10, 22)])
+def test_fused_z_epilogue(port, n, tile, seed):
+    """The fused Z-term epilogue of a flush's last pass (sign = per-thread
+    parity of the store index x compile-time register parity, with pending
+    permutations): its sums equal sum_o |a_o|^2 (-1)^popcount(o & M) over the
+    stored physical state, and the state itself is unchanged."""
+    for circ in (port.random_circuit(seed, n, 200), _perm_circuit(np.random.default_rng(seed), n)):
+        got, sums, phys_state = jit_emu.run(n, circ, tile, zterms=True)
+        assert np.max(np.abs(got - port.sv_run(n, circ))) <= 1e-12
+        p = np.abs(phys_state) ** 2
+        o = np.arange(1 << n, dtype=np.int64)
+        for k, mask in enumerate([1, 1 << (n - 1), 3]):
+            sign = 1 - 2 * (np.array([bin(x).count("1") for x in (o & mask)]) & 1)
+            assert abs(sums[k] - float(np.sum(p * sign))) <= 1e-12, (k, sums[k], float(np.sum(p * sign)))
