@@ -40,7 +40,7 @@ std::string plan_env_fingerprint() {
 #ifndef NQ_AB_KNOBS
         // A/B switches are ignored by this build, so they cannot diverge
         static const char* const honoured[] = {"NQ_JIT", "NQ_JIT_PX", "NQ_TILE_SV", "NQ_TILE_DM", "NQ_EXCHANGE",
-                                               "NQ_FUSED_EXCHANGE"};
+                                               "NQ_FUSED_EXCHANGE", "NQ_COMM"};
         if (std::none_of(std::begin(honoured), std::end(honoured), [&](const char* d) { return name == d; }))
             continue;
 #endif

@@ -9,6 +9,9 @@
 //   NQ_EXCHANGE=nccl        sharded exchanges through NCCL send/recv instead of
 //                           CUDA-IPC peer memory
 //   NQ_FUSED_EXCHANGE=0     no exchange fused into the preceding pass
+//                           (=staged: the staged form even when a second copy fits)
+//   NQ_COMM=host            sharded ranks coordinate through host shared memory
+//                           instead of NCCL (ranks may share one GPU: tests)
 //   NQ_NCCL_LIB             libnccl.so.2 to bind when none is loaded yet
 // Diagnostics (no effect on plans or results):
 //   NQ_PLAN_TRACE, NQ_SHARD_TRACE, NQ_SHARD_TIMING, NQ_JIT_DUMP,

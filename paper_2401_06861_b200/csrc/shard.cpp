@@ -26,7 +26,10 @@
 #include "state.hpp"
 
 #include <dlfcn.h>
+#include <fcntl.h>
 #include <nccl.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -37,7 +40,9 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <random>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -129,8 +134,92 @@ void check_async(ncclComm_t comm) {
         throw NqError{NQ_ERR_NCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(st)};
 }
 
+// ---- host-coordinated ranks (NQ_COMM=host) -----------------------------------
+// Ranks that are processes on one node -- possibly sharing ONE GPU, which is
+// how the sharded parity tests run on a single-GPU box -- coordinate through
+// a POSIX shared-memory block (a counting barrier, the CUDA-IPC handles of a
+// per-rank collective buffer) instead of NCCL.  Collectives are then
+// host-synchronous copies through those buffers; exchanges still go through
+// peer memory.  Staged exchanges are off in this mode: two ranks' cooperative
+// grids cannot be co-resident on one shared GPU.
+struct HostShm {
+    std::atomic<uint64_t> arrived;
+    std::atomic<uint64_t> generation;
+    cudaIpcMemHandle_t coll[64];
+};
+
+struct HostGroup {
+    std::string name;
+    HostShm* shm = nullptr;
+    int world = 1, rank = 0;
+    double* coll = nullptr;  // this rank's collective buffer
+    size_t coll_cap = 0;     // doubles
+    std::vector<double*> peer_coll;
+
+    void barrier() const {
+        const uint64_t g = shm->generation.load();
+        if (shm->arrived.fetch_add(1) + 1 == uint64_t(world)) {
+            shm->arrived.store(0);
+            shm->generation.fetch_add(1);
+            return;
+        }
+        const auto t0 = std::chrono::steady_clock::now();
+        while (shm->generation.load() == g) {
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+                throw NqError{NQ_ERR_INTERNAL, "host-coordinated ranks: barrier timed out (a rank stopped)"};
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
+    }
+    double* buf(int r) const { return r == rank ? coll : peer_coll[size_t(r)]; }
+};
+
+bool host_comm_requested() { return env_option_str("NQ_COMM") == "host"; }
+
+HostGroup* host_group_create(const unsigned char uid[128], int rank, int world) {
+    auto g = std::make_unique<HostGroup>();
+    g->world = world;
+    g->rank = rank;
+    char hex[33];
+    for (int i = 0; i < 16; ++i) std::snprintf(hex + 2 * i, 3, "%02x", uid[i]);
+    g->name = std::string("/naqs_b200_") + hex;
+    const int fd = shm_open(g->name.c_str(), O_CREAT | O_RDWR, 0600);
+    if (fd < 0) throw NqError{NQ_ERR_INTERNAL, "host-coordinated ranks: shm_open failed"};
+    if (ftruncate(fd, sizeof(HostShm)) != 0) {
+        close(fd);
+        throw NqError{NQ_ERR_INTERNAL, "host-coordinated ranks: ftruncate failed"};
+    }
+    void* p = mmap(nullptr, sizeof(HostShm), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) throw NqError{NQ_ERR_INTERNAL, "host-coordinated ranks: mmap failed"};
+    g->shm = static_cast<HostShm*>(p);  // zero-filled by ftruncate
+    g->coll_cap = size_t(1) << 23;     // 64 MiB of doubles per rank
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&g->coll), g->coll_cap * sizeof(double)));
+    CUDA_TRY(cudaIpcGetMemHandle(&g->shm->coll[rank], g->coll));
+    g->barrier();
+    g->peer_coll.assign(size_t(world), nullptr);
+    for (int r = 0; r < world; ++r) {
+        if (r == rank) continue;
+        void* q = nullptr;
+        CUDA_TRY(cudaIpcOpenMemHandle(&q, g->shm->coll[r], cudaIpcMemLazyEnablePeerAccess));
+        g->peer_coll[size_t(r)] = static_cast<double*>(q);
+    }
+    g->barrier();
+    return g.release();
+}
+
+void host_group_free(HostGroup* g) {
+    if (!g) return;
+    for (double* q : g->peer_coll)
+        if (q) cudaIpcCloseMemHandle(q);
+    if (g->coll) cudaFree(g->coll);
+    if (g->rank == 0) shm_unlink(g->name.c_str());
+    munmap(g->shm, sizeof(HostShm));
+    delete g;
+}
+
 struct ShardComm {
     ncclComm_t comm = nullptr;
+    HostGroup* hg = nullptr;  // NQ_COMM=host: no NCCL communicator
     std::vector<EOp> prev_ops;  // the previous flush (logical), for repeat prediction
     // peer-memory exchange: every rank's state mapped into this process (CUDA
     // IPC over NVLink); empty when unavailable or NQ_EXCHANGE=nccl
@@ -546,6 +635,11 @@ void run_segment(State& s, DeviceCtx& c, const std::vector<EOp>& ops, std::vecto
 // rank's stream has reached it, so no rank touches a peer's state while that
 // peer's earlier kernels may still be running (and vice versa afterwards).
 void stream_barrier(ShardComm& sc, DeviceCtx& c) {
+    if (sc.hg) {
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        sc.hg->barrier();
+        return;
+    }
     NCCL_TRY(ncclAllReduce(sc.d_flag, sc.d_flag, 1, ncclDouble, ncclSum, sc.comm, c.stream));
 }
 
@@ -571,6 +665,7 @@ void run_exchange(State& s, DeviceCtx& c, int g, int v) {
         check_async(sc.comm);
         return;
     }
+    if (sc.hg) throw NqError{NQ_ERR_INTERNAL, "host-coordinated ranks need CUDA-IPC peer memory for exchanges"};
     for (uint64_t k0 = 0; k0 < half; k0 += sc.chunk) {
         const uint64_t len = std::min(sc.chunk, half - k0);
         launch_half_pack(s.d, sc.sendbuf, k0, len, v, 1 - mybit, c.stream);
@@ -889,9 +984,20 @@ std::vector<double> allgather_doubles(State& s, const std::vector<double>& mine)
         sc.gather_cap = cap;
     }
     double* d = sc.gather;
+    std::vector<double> all(size_t(s.world) * k);
+    if (sc.hg) {
+        // (a pageable H2D cudaMemcpy may return before the data lands: copy
+        // on the stream and wait for it before the peers may read)
+        CUDA_TRY(cudaMemcpyAsync(sc.hg->coll, mine.data(), k * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        sc.hg->barrier();
+        for (int r = 0; r < s.world; ++r)
+            CUDA_TRY(cudaMemcpy(all.data() + size_t(r) * k, sc.hg->buf(r), k * sizeof(double), cudaMemcpyDeviceToHost));
+        sc.hg->barrier();
+        return all;
+    }
     CUDA_TRY(cudaMemcpyAsync(d, mine.data(), k * sizeof(double), cudaMemcpyHostToDevice, c.stream));
     NCCL_TRY(ncclAllGather(d, d + k, k, ncclDouble, sc.comm, c.stream));
-    std::vector<double> all(size_t(s.world) * k);
     CUDA_TRY(cudaMemcpyAsync(all.data(), d + k, all.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     CUDA_TRY(cudaStreamSynchronize(c.stream));
     return all;
@@ -902,8 +1008,11 @@ std::vector<double> allgather_doubles(State& s, const std::vector<double>& mine)
 // any rank) returns an empty vector everywhere.
 std::vector<double2*> map_peers(State& s, double2* mine_ptr, bool want) {
     cudaIpcMemHandle_t mine{};
-    bool ok = want && mine_ptr && cudaIpcGetMemHandle(&mine, mine_ptr) == cudaSuccess;
+    cudaError_t gerr = cudaSuccess;
+    bool ok = want && mine_ptr && (gerr = cudaIpcGetMemHandle(&mine, mine_ptr)) == cudaSuccess;
     cudaGetLastError();
+    if (std::getenv("NQ_SHARD_TRACE") && want && mine_ptr && gerr != cudaSuccess)
+        std::fprintf(stderr, "[shard] rank %d: cudaIpcGetMemHandle: %s\n", s.rank, cudaGetErrorString(gerr));
     // all-gather the 64-byte handles as doubles (8 per handle) + an ok flag
     constexpr size_t kW = sizeof(cudaIpcMemHandle_t) / sizeof(double) + 1;
     std::vector<double> buf(kW, 0.0);
@@ -917,8 +1026,12 @@ std::vector<double2*> map_peers(State& s, double2* mine_ptr, bool want) {
         cudaIpcMemHandle_t h;
         std::memcpy(&h, all.data() + size_t(r) * kW, sizeof(h));
         void* p = nullptr;
-        if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        const cudaError_t oerr = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (oerr != cudaSuccess) {
             cudaGetLastError();
+            if (std::getenv("NQ_SHARD_TRACE"))
+                std::fprintf(stderr, "[shard] rank %d: cudaIpcOpenMemHandle(rank %d): %s\n", s.rank, r,
+                             cudaGetErrorString(oerr));
             ok = false;
             break;
         }
@@ -992,7 +1105,7 @@ void setup_peer_exchange(State& s, ShardComm& sc, DeviceCtx& c) {
     // spans at least 2 tiles of the largest pass tile, 2^12), 4 slots of
     // half a chunk each -- 4 GiB at 2^33 amplitudes per GPU
     const std::string fxm = env_option_str("NQ_FUSED_EXCHANGE");
-    const bool want_staged = fused_exchange_wanted() && (fxm == "staged" || !sc.alt);
+    const bool want_staged = fused_exchange_wanted() && (fxm == "staged" || !sc.alt) && !sc.hg;
     if (want_staged) {
         if (sc.alt) {  // forced: release the second copy
             for (double2* p : sc.peer_alt)
@@ -1057,6 +1170,7 @@ void shard_free(State& s) {
     if (sc->alt) cudaFree(sc->alt);
     free_staging(*sc);
     if (sc->comm) ncclCommDestroy(sc->comm);
+    host_group_free(sc->hg);
     delete sc;
     s.comm = nullptr;
 }
@@ -1290,6 +1404,20 @@ void shard_probabilities(State& s, double* host_out) {
         CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&sc.bcast), chunk * sizeof(double)));
         sc.bcast_cap = chunk;
     }
+    if (sc.hg) {
+        const uint64_t hc = std::min<uint64_t>(chunk, sc.hg->coll_cap);
+        for (int r = 0; r < s.world; ++r)
+            for (uint64_t off = 0; off < s.count; off += hc) {
+                const uint64_t len = std::min(hc, s.count - off);
+                if (r == s.rank) launch_probs(s.d + off, len, sc.hg->coll, c.stream);
+                CUDA_TRY(cudaStreamSynchronize(c.stream));
+                sc.hg->barrier();
+                CUDA_TRY(cudaMemcpy(host_out + (uint64_t(r) << s.nloc) + off, sc.hg->buf(r), len * sizeof(double),
+                                    cudaMemcpyDeviceToHost));
+                sc.hg->barrier();
+            }
+        return;
+    }
     for (int r = 0; r < s.world; ++r) {
         for (uint64_t off = 0; off < s.count; off += chunk) {
             const uint64_t len = std::min(chunk, s.count - off);
@@ -1331,7 +1459,29 @@ void shard_get_amplitudes(State& s, uint64_t offset, uint64_t count, double* hos
         CUDA_TRY(cudaMemcpyAsync(d + (a - offset), s.d + (a - mine_lo), (b - a) * sizeof(double2),
                                  cudaMemcpyDeviceToDevice, c.stream));
     // exactly one rank contributes each element: the sum with zeros is exact
-    if (count) NCCL_TRY(ncclAllReduce(d, d, size_t(count) * 2, ncclDouble, ncclSum, s.comm->comm, c.stream));
+    if (count && s.comm->hg) {
+        HostGroup& hg = *s.comm->hg;
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        const uint64_t total = count * 2, hc = hg.coll_cap;
+        std::vector<double> part(std::min<uint64_t>(total, hc)), acc(part.size());
+        double* dd = reinterpret_cast<double*>(d);
+        for (uint64_t off = 0; off < total; off += hc) {
+            const uint64_t len = std::min(hc, total - off);
+            CUDA_TRY(cudaMemcpyAsync(hg.coll, dd + off, len * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+            CUDA_TRY(cudaStreamSynchronize(c.stream));
+            hg.barrier();
+            std::fill(acc.begin(), acc.begin() + long(len), 0.0);
+            for (int r = 0; r < s.world; ++r) {
+                CUDA_TRY(cudaMemcpy(part.data(), hg.buf(r), len * sizeof(double), cudaMemcpyDeviceToHost));
+                for (uint64_t i = 0; i < len; ++i) acc[i] += part[i];
+            }
+            hg.barrier();
+            CUDA_TRY(cudaMemcpyAsync(dd + off, acc.data(), len * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+            CUDA_TRY(cudaStreamSynchronize(c.stream));
+        }
+    } else if (count) {
+        NCCL_TRY(ncclAllReduce(d, d, size_t(count) * 2, ncclDouble, ncclSum, s.comm->comm, c.stream));
+    }
     if (count)
         CUDA_TRY(cudaMemcpyAsync(host_out, d, count * sizeof(double2), cudaMemcpyDeviceToHost, c.stream));
     CUDA_TRY(cudaFreeAsync(d, c.stream));
@@ -1346,6 +1496,15 @@ extern "C" {
 
 nq_status nq_comm_unique_id(unsigned char out[128]) {
     return guard([&] {
+        if (host_comm_requested()) {
+            // host-coordinated ranks: the id only names the shared-memory block
+            std::random_device rd;
+            for (int i = 0; i < 128; i += 4) {
+                const unsigned v = rd();
+                std::memcpy(out + i, &v, 4);
+            }
+            return;
+        }
         ncclUniqueId id;
         NCCL_TRY(ncclGetUniqueId(&id));
         static_assert(sizeof(id) == 128, "ncclUniqueId size");
@@ -1403,9 +1562,13 @@ nq_status nq_sv_create_sharded(int n, int rank, int world, const unsigned char u
         sc->chunk = std::min<uint64_t>(s.count / 2, uint64_t(1) << 26);
         CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&sc->sendbuf), sc->chunk * sizeof(double2)));
         CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&sc->recvbuf), sc->chunk * sizeof(double2)));
-        ncclUniqueId id;
-        std::memcpy(&id, uid, 128);
-        NCCL_TRY(ncclCommInitRank(&sc->comm, world, id, rank));
+        if (host_comm_requested()) {
+            sc->hg = host_group_create(uid, rank, world);
+        } else {
+            ncclUniqueId id;
+            std::memcpy(&id, uid, 128);
+            NCCL_TRY(ncclCommInitRank(&sc->comm, world, id, rank));
+        }
         CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&sc->d_flag), sizeof(double)));
         CUDA_TRY(cudaMemset(sc->d_flag, 0, sizeof(double)));
         s.comm = sc.release();

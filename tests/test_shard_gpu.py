@@ -1,7 +1,11 @@
-"""Sharded state vector over 2 GPUs (NCCL) against the oracle.
+"""Sharded state vector against the oracle.
 
-Needs >= 2 visible GPUs (gpurun --gpus 2); skipped otherwise.  Each rank is a
-process owning one GPU; the NCCL unique id is created in the parent.
+Each rank is a process; the communicator id is created in the parent.  With
+>= world visible GPUs every rank owns one GPU and the ranks talk NCCL; on a
+box with fewer GPUs the same cases run with every rank on GPU 0 and
+NQ_COMM=host (ranks coordinate through host shared memory; exchanges still go
+through CUDA-IPC peer memory), except the forms that need one GPU per rank
+(staged exchanges: two ranks' cooperative grids cannot share a GPU; NCCL).
 """
 import os
 import sys
@@ -16,16 +20,49 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _rank_main(rank, world, uid, n, seed, outdir, fused="1", exchange="p2p"):
+def _uid(shared):
+    """The communicator id, made the way the ranks will use it (NQ_COMM is
+    read when the id is made: an NCCL id, or random bytes naming the
+    shared-memory block)."""
+    old = os.environ.get("NQ_COMM")
+    if shared:
+        os.environ["NQ_COMM"] = "host"
+    try:
+        return abi.comm_unique_id()
+    finally:
+        if old is None:
+            os.environ.pop("NQ_COMM", None)
+        else:
+            os.environ["NQ_COMM"] = old
+
+
+def _mode(world, fused="1", exchange="p2p"):
+    """(shared_gpu, skip reason): one GPU per rank when there are enough,
+    else every rank on GPU 0 with host coordination."""
+    if abi.device_count() >= world:
+        return False, None
+    if fused == "staged" or exchange == "nccl":
+        return True, f"needs {world} GPUs ({fused} / {exchange})"
+    return True, None
+
+
+def _setup_rank(rank, shared):
+    if shared:
+        os.environ["NQ_COMM"] = "host"
+    return 0 if shared else rank
+
+
+def _rank_main(rank, world, uid, n, seed, outdir, fused="1", exchange="p2p", shared=False):
     os.environ["NQ_FUSED_EXCHANGE"] = fused
     os.environ["NQ_EXCHANGE"] = exchange
+    dev = _setup_rank(rank, shared)
     sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
     from oracle import Port
     from paper_2401_06861_b200 import abi as A
 
     port = Port()
     ops = port.random_circuit(seed, n, 300)
-    sv = A.SV.sharded(n, rank, world, uid, device=rank)
+    sv = A.SV.sharded(n, rank, world, uid, device=dev)
     sv.apply(ops)
     norm = sv.norm_sq()
     rng = np.random.default_rng(seed)
@@ -65,11 +102,12 @@ def test_sharded_gpus(port, tmp_path, n, world, fused, exchange):
     kernel, the form used when no second copy fits), as standalone peer-memory swaps, or through
     the NCCL send/recv fallback (NQ_EXCHANGE=nccl: pack, send/recv through
     bounce buffers, unpack -- the path taken when CUDA IPC is unavailable)."""
-    if abi.device_count() < world:
-        pytest.skip(f"needs {world} GPUs")
+    shared, why = _mode(world, fused, exchange)
+    if why:
+        pytest.skip(why)
     seed = 808 + n
-    uid = abi.comm_unique_id()
-    mp.start_processes(_rank_main, args=(world, uid, n, seed, str(tmp_path), fused, exchange), nprocs=world,
+    uid = _uid(shared)
+    mp.start_processes(_rank_main, args=(world, uid, n, seed, str(tmp_path), fused, exchange, shared), nprocs=world,
                        start_method="spawn")
     ops = port.random_circuit(seed, n, 300)
     want = port.sv_run(n, ops)
@@ -77,7 +115,7 @@ def test_sharded_gpus(port, tmp_path, n, world, fused, exchange):
         d = np.load(tmp_path / f"r{r}.npz")
         assert int(d["exchanges"]) > 0
         if fused == "1":
-            assert bool(d["alt"]) and int(d["fused"]) > 0
+            assert bool(d["alt"]) and int(d["fused"]) > 0, (d["alt"], d["fused"])
         elif fused == "staged":
             assert bool(d["staged"]) and not bool(d["alt"]) and int(d["fused"]) > 0
         else:
@@ -94,15 +132,16 @@ def test_sharded_gpus(port, tmp_path, n, world, fused, exchange):
         assert np.array_equal(dense, port.sample_distribution(np.abs(want) ** 2, 4000, 99))
 
 
-def _env_rank(rank, world, uid, outdir):
+def _env_rank(rank, world, uid, outdir, shared=False):
     # rank 1 plans with a different tile size: the ranks' flushes would diverge
+    dev = _setup_rank(rank, shared)
     if rank == 1:
         os.environ["NQ_TILE_SV"] = "10"
     sys.path[:0] = [ROOT]
     from paper_2401_06861_b200 import abi as A
 
     try:
-        A.SV.sharded(16, rank, world, uid, device=rank)
+        A.SV.sharded(16, rank, world, uid, device=dev)
         msg = "created"
     except A.ContractError as e:
         msg = str(e)
@@ -114,23 +153,23 @@ def test_ranks_must_share_the_environment(tmp_path):
     """Every rank plans its own flushes, so creation fails on every rank (a
     contract error, not a later collective hang) when the plan-shaping NQ_*
     options differ between ranks."""
-    if abi.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
-    uid = abi.comm_unique_id()
-    mp.start_processes(_env_rank, args=(2, uid, str(tmp_path)), nprocs=2, start_method="spawn")
+    shared, _ = _mode(2)
+    uid = _uid(shared)
+    mp.start_processes(_env_rank, args=(2, uid, str(tmp_path), shared), nprocs=2, start_method="spawn")
     for r in range(2):
         msg = (tmp_path / f"env{r}.txt").read_text()
         assert "different NQ_* options" in msg, msg
 
 
-def _repeat_rank(rank, world, uid, n, seed, outdir, fused):
+def _repeat_rank(rank, world, uid, n, seed, outdir, fused, shared=False):
     os.environ["NQ_FUSED_EXCHANGE"] = fused
+    dev = _setup_rank(rank, shared)
     sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
     from oracle import Port
     from paper_2401_06861_b200 import abi as A
 
     ops = Port().random_circuit(seed, n, 200)
-    sv = A.SV.sharded(n, rank, world, uid, device=rank)
+    sv = A.SV.sharded(n, rank, world, uid, device=dev)
     for _ in range(4):  # the same circuit flushed again and again (benchmark / iterative shape)
         sv.apply(ops)
         sv.norm_sq()
@@ -145,11 +184,12 @@ def test_sharded_repeated_flushes(port, tmp_path, n, world, fused):
     and move the next flush's opening exchange to the end of the current one
     (where it fuses into the last pass): the state after four repetitions
     equals the oracle's."""
-    if abi.device_count() < world:
-        pytest.skip(f"needs {world} GPUs")
+    shared, why = _mode(world, fused)
+    if why:
+        pytest.skip(why)
     seed = 909 + n
-    uid = abi.comm_unique_id()
-    mp.start_processes(_repeat_rank, args=(world, uid, n, seed, str(tmp_path), fused), nprocs=world,
+    uid = _uid(shared)
+    mp.start_processes(_repeat_rank, args=(world, uid, n, seed, str(tmp_path), fused, shared), nprocs=world,
                        start_method="spawn")
     ops = port.random_circuit(seed, n, 200)
     want = port.sv_run(n, np.concatenate([ops] * 4))
