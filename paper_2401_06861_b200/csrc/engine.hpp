@@ -64,6 +64,9 @@ struct PassHdr {
     int8_t qst[16];     // tile bit i is stored to state bit qst[i] (a permutation of q:
                         // the pass relabels qubits among its tile bits for free)
     int32_t flags;      // PASS_MIRROR: Hermitian pass (density matrix, interleaved layout)
+    int8_t lab[16];     // the content stored from tile bit i carries the logical qubit
+                        // label of tile bit lab[i] (identity unless SWAP micro-ops were
+                        // folded into qst; host-side bookkeeping, kernels ignore it)
     int32_t pad_[3];
 };
 // The pass maps Hermitian matrices to Hermitian matrices and its tile and rest
@@ -117,6 +120,7 @@ struct PlanOptions {
 struct PlannedPass {
     std::vector<int> q;     // tile bits (physical, ascending) at load
     std::vector<int> qst;   // physical store bit of tile bit i (empty: same as q)
+    std::vector<int> lab;   // see PassHdr::lab (empty: identity)
     int32_t flags = 0;
     std::vector<MOp> ops;
     std::vector<cplx> pool;

@@ -880,6 +880,52 @@ void hoist_global_phase(std::vector<PlannedPass>& passes) {
 
 }  // namespace
 
+// SWAP micro-ops at the end of a relabelling pass move no data in registers
+// that anything later in the pass reads: they are folded into the store
+// permutation instead (the data of tile bit i is stored where tile bit j's
+// would have gone, and vice versa).  A pass left without any arithmetic (the
+// bit reversal closing a QFT) then loads in a layout with its 4 highest tile
+// bits in registers, so its loads are as coalesced as its stores (it had
+// held the swapped low bits in registers).  The logical->physical map is
+// unchanged: SWAP(a, b) o store == store with the two positions exchanged.
+void absorb_trailing_swaps(PlannedPass& p) {
+    if (p.ops.empty() || p.ops[0].type != MOP_LAYOUT) return;
+    int last = -1;  // last op that is neither a layout nor a swap
+    for (size_t i = 0; i < p.ops.size(); ++i)
+        if (p.ops[i].type != MOP_LAYOUT && p.ops[i].type != MOP_SWAP) last = int(i);
+    int last_layout = 0;
+    for (size_t i = 0; i < p.ops.size(); ++i)
+        if (p.ops[i].type == MOP_LAYOUT) last_layout = int(i);
+    // with arithmetic left, only swaps after the final layout (the store
+    // layout stays the one the relabelling chose)
+    const int from = last < 0 ? 0 : std::max(last, last_layout);
+    std::vector<std::pair<int, int>> tb;  // swapped tile bits, program order
+    const MOp* lay = nullptr;
+    for (size_t i = 0; i < p.ops.size(); ++i) {
+        const MOp& o = p.ops[i];
+        if (o.type == MOP_LAYOUT) lay = &o;
+        else if (o.type == MOP_SWAP && int(i) > from && lay) tb.push_back({lay->pos[o.pos[0]], lay->pos[o.pos[1]]});
+    }
+    if (tb.empty()) return;
+    p.lab.resize(p.q.size());
+    for (size_t i = 0; i < p.lab.size(); ++i) p.lab[i] = int(i);
+    for (size_t k = tb.size(); k-- > 0;) {
+        std::swap(p.qst[size_t(tb[k].first)], p.qst[size_t(tb[k].second)]);
+        std::swap(p.lab[size_t(tb[k].first)], p.lab[size_t(tb[k].second)]);
+    }
+    std::vector<MOp> keep;
+    if (last < 0) {
+        MOp l = p.ops[0];
+        const int m = int(p.q.size());
+        for (int j = 0; j < l.k; ++j) l.pos[j] = int8_t(m - l.k + j);
+        keep.push_back(l);
+    } else {
+        for (size_t i = 0; i < p.ops.size(); ++i)
+            if (!(p.ops[i].type == MOP_SWAP && int(i) > from)) keep.push_back(p.ops[i]);
+    }
+    p.ops.swap(keep);
+}
+
 std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanOptions& opt,
                                      PlanStats* stats, std::vector<int>* map) {
     const std::vector<EOp> ops = opt.fuse ? cancel_perm_sandwiches(ops_in) : ops_in;
@@ -1353,6 +1399,7 @@ std::vector<PlannedPass> plan_passes(const std::vector<EOp>& ops_in, const PlanO
             }
             p.qst.resize(q.size());
             for (size_t i = 0; i < q.size(); ++i) p.qst[i] = l2p[size_t(q[i])];
+            if (relabel && !(p.flags & PASS_MIRROR)) absorb_trailing_swaps(p);
             passes.push_back(std::move(p));
         }
         remaining.swap(next);
@@ -1382,6 +1429,7 @@ std::vector<unsigned char> serialize_passes(const std::vector<PlannedPass>& pass
         for (size_t i = 0; i < p.q.size(); ++i) {
             h.q[i] = int8_t(p.q[i]);
             h.qst[i] = int8_t(p.qst.empty() ? p.q[i] : p.qst[i]);
+            h.lab[i] = int8_t(p.lab.empty() ? int(i) : p.lab[i]);
         }
         h.flags = p.flags;
         int nr = 0;

@@ -13,11 +13,11 @@ from typing import List
 import numpy as np
 
 MOP_NAMES = {0: "dense", 1: "diag", 2: "xperm", 3: "swap", 4: "depol", 5: "layout"}
-HDR_FMT = "<iiiiqIIII16b56b16biiii"
+HDR_FMT = "<iiiiqIIII16b56b16bi16b3i"
 HDR_SIZE = struct.calcsize(HDR_FMT)
 MOP_FMT = "<BB8bHII4xQ"
 MOP_SIZE = struct.calcsize(MOP_FMT)
-assert HDR_SIZE == 144 and MOP_SIZE == 32
+assert HDR_SIZE == 160 and MOP_SIZE == 32
 
 
 @dataclass
@@ -39,6 +39,7 @@ class Pass:
     q: List[int]
     rest: List[int]
     qst: List[int] = field(default_factory=list)  # store position of tile bit i (relabelling pass)
+    lab: List[int] = field(default_factory=list)  # stored content of tile bit i carries tile bit lab[i]'s label
     ops: List[MicroOp] = field(default_factory=list)
     pool: np.ndarray = None
 
@@ -52,7 +53,8 @@ def decode(buf: bytes) -> List[Pass]:
         q = list(f[9:9 + 16])[:m]
         rest = list(f[25:25 + 56])[:nrest]
         qst = list(f[81:81 + 16])[:m]
-        p = Pass(m=m, nloc=nloc, ntiles=ntiles, q=q, rest=rest, qst=qst)
+        lab = list(f[98:98 + 16])[:m]
+        p = Pass(m=m, nloc=nloc, ntiles=ntiles, q=q, rest=rest, qst=qst, lab=lab)
         for i in range(nops):
             f2 = struct.unpack_from(MOP_FMT, buf, at + op_off + i * MOP_SIZE)
             t, k = f2[0], f2[1]

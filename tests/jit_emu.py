@@ -99,7 +99,9 @@ def run(n: int, ops, tile: int, state: np.ndarray | None = None, zterms: bool = 
         smem = (1 << p.m) * 16 + len(pool) * 16  # as jit_launch sizes it
         lib.emu_run(i, st.ctypes.data, pool.ctypes.data, ntiles, threads, smem)
         qst = p.qst if p.qst else p.q
-        move = dict(zip(p.q, qst))
+        lab = p.lab if p.lab else list(range(p.m))
+        # the logical qubit at load bit q[lab[i]] ends at store bit qst[i]
+        move = {p.q[lab[i]]: qst[i] for i in range(p.m)}
         l2p = [move.get(x, x) for x in l2p]
     idx = np.arange(1 << n, dtype=np.int64)
     phys = np.zeros_like(idx)

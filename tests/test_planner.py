@@ -36,9 +36,10 @@ def run_plan(n, passes, amps):
         qst = p.qst if p.qst else p.q
         assert sorted(qst) == sorted(p.q)
         offs_st = np.array([deposit(e, qst) for e in range(size)], dtype=np.int64)
+        lab = p.lab if p.lab else list(range(p.m))
         new = list(p2l)
         for i in range(p.m):
-            new[qst[i]] = p2l[p.q[i]]
+            new[qst[i]] = p2l[p.q[lab[i]]]
         p2l = new
         assert p.ops[0].type == "layout"
         for r in range(p.ntiles):
