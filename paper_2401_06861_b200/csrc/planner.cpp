@@ -347,7 +347,12 @@ class PassBuilder {
                     if (std::find(tried.begin(), tried.end(), r) != tried.end()) continue;
                     tried.push_back(r);
                     const int ran = simulate(r, np, done);
-                    if (ran > best_ran) {
+                    // the first set is the load layout: on a tie, the one with
+                    // fewer of the 5 lowest tile bits (the lowest physical bits)
+                    // in registers, so a warp's lanes load contiguous amplitudes
+                    const bool coalesce_tie = !have && ran == best_ran &&
+                                              popcount64(r & 0x1Fu) < popcount64(best & 0x1Fu);
+                    if (ran > best_ran || coalesce_tie) {
                         best_ran = ran;
                         best = r;
                     }
@@ -429,7 +434,13 @@ class PassBuilder {
         // memory instead.
         const uint32_t lane_bits = m >= 9 ? coalesce_mask() : 0u;
         const uint32_t top = fill(0);
-        if (coalesce_ && (lay & lane_bits)) p.ops.push_back(layout_op(top));
+        // Always when the first stage holds all 4 lowest tile bits: each lane
+        // would then load its own 256-byte run (the warp's requests touch 32
+        // lines; the L2 re-serves up to 1.75x the sectors: QFT-30 pass 0).
+        static const int full_low = ab_knob("NQ_COALESCE_FULL_LOW", 1);
+        if ((coalesce_ && (lay & lane_bits)) ||
+            (full_low > 0 && m >= 9 && popcount64(lay & 0xFu) >= (full_low == 1 ? 4 : 3)))
+            p.ops.push_back(layout_op(top));
         p.ops.push_back(layout_op(lay));
         for (size_t i = 0; i < live.size(); ++i) {
             if (stage_of[i] != lay) {
