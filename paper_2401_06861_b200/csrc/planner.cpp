@@ -434,12 +434,14 @@ class PassBuilder {
         // memory instead.
         const uint32_t lane_bits = m >= 9 ? coalesce_mask() : 0u;
         const uint32_t top = fill(0);
-        // Always when the first stage holds all 4 lowest tile bits: each lane
-        // would then load its own 256-byte run (the warp's requests touch 32
-        // lines; the L2 re-serves up to 1.75x the sectors: QFT-30 pass 0).
-        static const int full_low = ab_knob("NQ_COALESCE_FULL_LOW", 1);
+        // Always when the first stage holds 3 or 4 of the 4 lowest tile bits:
+        // each lane would then load its own 128-256-byte run (the warp's
+        // requests touch 16-32 lines; the L2 re-serves up to 1.75x the
+        // sectors: QFT-30 pass 0).
+        // (A/B: NQ_COALESCE_FULL_LOW = 1/2/3 for >= 4/3/2 of the lowest 4)
+        static const int full_low = ab_knob("NQ_COALESCE_FULL_LOW", 2);
         if ((coalesce_ && (lay & lane_bits)) ||
-            (full_low > 0 && m >= 9 && popcount64(lay & 0xFu) >= (full_low == 1 ? 4 : 3)))
+            (full_low > 0 && m >= 9 && popcount64(lay & 0xFu) >= 5 - full_low))
             p.ops.push_back(layout_op(top));
         p.ops.push_back(layout_op(lay));
         for (size_t i = 0; i < live.size(); ++i) {
