@@ -516,8 +516,20 @@ std::string jit_source(const PassHdr& h, const MOp* ops, const cplx* pool, bool 
     std::ostringstream s;
     s << "#include \"pass_ops.cuh\"\n"
       << "extern \"C\" __global__ void __launch_bounds__(" << T;
-    // 8 amplitudes per thread need ~half the registers: aim for 768 threads/SM
-    const int minb = std::max(1, (E == 8 ? 768 : 512) / T);
+    // 8 amplitudes per thread need ~half the registers: aim for 768 threads/SM.
+    // Passes with >= 45 arithmetic micro-ops (QFT's phase-table passes) run
+    // 3 CTAs/SM of up to 168 registers instead of 4 of 128: their schedules
+    // keep more loads and table factors in flight without spilling.
+    // Measured (A/B NQ_HEAVY_OPS): QFT-30 73.7 -> 70.8 ms at thresholds 40-50
+    // (72.3 at 60); random-30 and VQE-28 unchanged; 2 CTAs/SM for >= 60 ops
+    // (NQ_HEAVY2_OPS) slower.
+    static const int heavy_ops = ab_knob("NQ_HEAVY_OPS", 45);
+    static const int heavy2_ops = ab_knob("NQ_HEAVY2_OPS", 0);  // (2 CTAs/SM, up to 255 registers)
+    int narith = 0;
+    for (int i = 0; i < h.nops; ++i) narith += ops[i].type == MOP_DENSE || ops[i].type == MOP_DIAG;
+    const int minb = (heavy2_ops > 0 && E == 16 && narith >= heavy2_ops) ? std::max(1, 256 / T)
+                     : (heavy_ops > 0 && E == 16 && narith >= heavy_ops) ? std::max(1, 384 / T)
+                                                                          : std::max(1, (E == 8 ? 768 : 512) / T);
     if (minb > 0) s << ", " << minb;
     s << ")\n"
       << "nqjit(double2* __restrict__ st, const double2* __restrict__ gpool, unsigned long long rankbase,"
