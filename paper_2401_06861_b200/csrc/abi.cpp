@@ -302,6 +302,7 @@ void state_flush(State& s, FlushEpilogue* fe) {
     PlanStats st;
     const bool use_layout = int(s.layout.size()) == s.nbits && (s.popt.relabel || !layout_is_identity(s));
     std::vector<unsigned char> key = plan_key(s, use_layout);
+    const std::vector<int> pre_layout = s.layout;  // (a second plan starts from the same map)
     std::shared_ptr<const PlanCacheEntry> hit;
     {
         std::lock_guard<std::mutex> lk(mu);
@@ -320,6 +321,29 @@ void state_flush(State& s, FlushEpilogue* fe) {
         return;
     }
     std::vector<PlannedPass> passes = plan_passes(s.queue, s.popt, &st, use_layout ? &s.layout : nullptr);
+    // A second plan with 5 low bits on lanes (32 contiguous amplitudes per
+    // warp access instead of 16) is taken when it needs no more passes and no
+    // more relayouts: VQE-28 12.87 -> 12.48 ms; random-30 and QFT-30 then
+    // need more passes and keep the 4-bit plan (A/B switch NQ_TRY_LOW5).
+    static const bool try_low5 = ab_knob("NQ_TRY_LOW5", 1) != 0;
+    if (try_low5 && !s.dm && s.world == 1 && s.popt.low_bits == 4 && s.nloc >= 20 && s.popt.relabel && use_layout) {
+        PlanOptions o5 = s.popt;
+        o5.low_bits = 5;
+        std::vector<int> lay5 = pre_layout;
+        PlanStats st5;
+        std::vector<PlannedPass> p5 = plan_passes(s.queue, o5, &st5, &lay5);
+        auto layouts = [](const std::vector<PlannedPass>& ps) {
+            size_t k = 0;
+            for (const auto& p : ps)
+                for (const auto& o : p.ops) k += o.type == MOP_LAYOUT;
+            return k;
+        };
+        if (p5.size() == passes.size() && layouts(p5) <= layouts(passes)) {
+            passes.swap(p5);
+            st = st5;
+            s.layout = lay5;
+        }
+    }
     s.queue.clear();
     auto kern = std::make_shared<std::vector<JitMemo>>(passes.size());
     auto entry = std::make_shared<const PlanCacheEntry>(PlanCacheEntry{std::move(key), std::move(passes), st, s.layout, kern});
@@ -1479,6 +1503,7 @@ nq_status nq_plan_debug(int n, const nq_op* ops, int64_t count, int tile_qubits,
         p.tile_bits = tile_qubits > 0 ? std::min(tile_qubits, kMaxTileBits) : 11;  // the state default (state_init)
         p.fuse = (fuse & 1) != 0;
         p.relabel = (fuse & 2) != 0;  // bit 1: relabelling stores (single-device state vectors)
+        if (fuse >> 4) p.low_bits = (fuse >> 4) & 7;  // bits 4-6: low-bit count (planner experiments)
         configure_caps(p);
         PlanStats stt;
         std::vector<int> layout(static_cast<size_t>(n));
