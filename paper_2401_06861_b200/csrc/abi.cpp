@@ -158,7 +158,8 @@ void state_init(State& s, int n, bool dm, const nq_opts* opts) {
     // tile size options (read per state), A/B low-bit counts
     if (const int t = env_option(dm ? "NQ_TILE_DM" : "NQ_TILE_SV", 0); t > 0 && o.tile_qubits <= 0)
         s.popt.tile_bits = std::max(4, std::min(t, kMaxTileBits));
-    s.popt.low_bits = dm ? std::max(0, std::min(ab_knob("NQ_LOW_BITS_DM", 4), 4))
+    // (density matrices: an even count -- the Hermitian layout pairs bits)
+    s.popt.low_bits = dm ? (std::max(0, std::min(ab_knob("NQ_LOW_BITS_DM", 4), 4)) & ~1)
                          : std::max(0, std::min(ab_knob("NQ_LOW_BITS", 4), 7));
     s.popt.fuse = o.fuse != 0;
     configure_caps(s.popt);
